@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""Outer-sync throughput bench (BASELINE.json metric): one step = one DiLoCo
+outer synchronisation round — pseudo-gradient -> int8 ring all-reduce ->
+Nesterov update — over synthetic fp32 params of the named config.
+
+  python bench.py                       # N=1: config 2 (1B params, 4 workers virtual on one GPU)
+  torchrun --nproc-per-node N bench.py --gpus N   # one DiLoCo worker per GPU, NCCL ring
+  python bench.py --impl reference      # the reference's CPU path (oracle/_ref) on host cores
+
+Prints ONE JSON line on rank 0. value = worker-params synchronised per
+second summed over the job (k workers x n params per round / round time).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "outer-sync params/sec (int8 ring AR + update)"
+UNIT = "params/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=float, default=1e9, help="params per worker (config 2: 1B)")
+    ap.add_argument("--workers", type=int, default=0, help="DiLoCo workers k (default: 4 at N=1, N otherwise)")
+    ap.add_argument("--S", type=int, default=16, help="ReduceOptions.pipeline_subchunks")
+    ap.add_argument("--window", type=float, default=0, help="pipelining window elems (0=auto)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=float, default=16e6, help="params per worker in the CPU sample")
+    ap.add_argument("--profile-only", action="store_true", help="1 warm round + 1 round, no JSON (for ncu)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi sampled during the timed region (B200_PROFILING.md recipe)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- CPU (reference) arm
+
+
+def cpu_reference_round(n_sample: int, k: int, S: int, seed: int = 1):
+    """One outer-sync round of the UNMODIFIED reference (oracle/_ref: the
+    reference headers compiled by oracle/Makefile): k node threads over TCP
+    loopback run compute_pseudo_gradient -> ring_allreduce(int8) ->
+    nesterov_outer_step (trainer.hpp:355-382). Returns (seconds, kind)."""
+    import numpy as np
+    from oracle.pyoracle import Oracle, Reference, have_reference
+
+    O = Oracle()
+    g = O.uniform(n_sample, seed, 0)
+    ls = [(g - O.uniform(n_sample, seed, 1 + w, 0, 0, 2.0 ** -10)).astype(np.float32) for w in range(k)]
+    b = np.zeros(n_sample, np.float32)
+    # S must keep every frame under the reference's 16 MiB cap (runtime.hpp:31)
+    if have_reference():
+        R = Reference()
+        _, _, secs = R.outer_sync_tcp(g, ls, b, S, "int8", 0.7, 0.9)
+        return secs, "reference"
+    t0 = time.perf_counter()
+    O.outer_sync(g, ls, b, S, "int8", 0.7, 0.9)
+    return time.perf_counter() - t0, "port"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    k = args.workers or (4 if args.gpus == 1 else args.gpus)
+    n = int(args.cpu_sample)
+    times = []
+    kind = "reference"
+    for i in range(args.warmup + args.steps):
+        t, kind = cpu_reference_round(n, k, args.S, seed=1 + i)
+        if i >= args.warmup:
+            times.append(t)
+    t = statistics.mean(times)
+    value = k * n / t
+    cores = min(os.cpu_count() or 1, 2 * k) if kind == "reference" else 1
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+        "config": config_block(args, k, int(args.n)),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{k} workers x {n} params/worker per round (bounded slice of the "
+                                   f"{int(args.n)}-param workload), S={args.S}, TCP loopback ring, one node thread "
+                                   f"+ one sender task per worker"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- helpers
+
+
+def config_block(args, k, n):
+    return {"workload": f"config 2: DiLoCo outer sync of a {n / 1e9:.3g}B-param synthetic model, {k} workers, "
+                        "int8 ring all-reduce + Nesterov (lr=0.7, mu=0.9)",
+            "params_per_worker": n, "workers": k, "pipeline_subchunks": args.S,
+            "ring": ("virtual (all workers on 1 GPU, zero-copy hand-off)" if args.gpus == 1 and k > 1
+                     else "NCCL send/recv over NVLink, one worker per GPU"),
+            "l2": "inputs larger than L2 (>= 12 B/param x n per worker)",
+            "write_local": False}
+
+
+def alg_bytes_per_param(k):
+    # A(1) = 20, A(k>=2) = 24 + (2k-1)/k + 1 (theta_l write excluded)
+    return 20.0 if k == 1 else 24.0 + (2 * k - 1) / k + 1.0
+
+
+# ----------------------------------------------------------------- our arm
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_01152_b200 as E
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = int(args.n)
+    k = args.workers or (4 if world == 1 else world)
+    virtual = world == 1 and k > 1
+    if not virtual and k != world:
+        raise SystemExit("with N>1 GPUs each GPU is one worker: --workers must equal --gpus")
+
+    nccl_id = None
+    if not virtual and k > 1:
+        obj = [E.RingEngine.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    eng = E.RingEngine(n, k, rank=rank if not virtual else 0, opts=E.ReduceOptions(pipeline_subchunks=args.S),
+                       virtual=virtual, nccl_id=nccl_id, window_elems=int(args.window))
+    W = eng.workers
+    # synthetic replicas: theta_g ~ U[-1,1), theta_l = theta_g - 2^-10 U, b = 0
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1)
+    base = (torch.rand(n, generator=gen, device=dev) * 2 - 1)
+    tg, tl, tb = [], [], []
+    for w in range(W):
+        gen.manual_seed(100 + rank * W + w)
+        tg.append(base.clone())
+        tl.append(base - (torch.rand(n, generator=gen, device=dev) * 2 - 1) * (2.0 ** -10))
+        tb.append(torch.zeros(n, device=dev))
+    del base
+    hp = E.HyperParams()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        eng.outer_sync(tg, tl, tb, hp, write_local=False)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    if args.profile_only:
+        step()
+        torch.cuda.synchronize()
+        step()
+        eng.check()
+        torch.cuda.synchronize()
+        return
+
+    for _ in range(args.warmup):
+        step()
+    eng.check()
+    barrier()
+    launches0 = eng.launches()
+    eng.profile(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    ms_local = ev0.elapsed_time(ev1)
+    launches = eng.launches() - launches0
+    prof = eng.profile_read()
+    eng.profile(False)
+    eng.check()
+    t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    value = k * n / (ms / 1e3)  # all workers' params per second
+
+    # ---- roofline of the dominant kernel family (by device time)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    fams = {kname: v for kname, v in prof.items() if kname not in ("k_stats", "k_bin")}
+    dom = max(fams.items(), key=lambda kv: kv[1]["ms"]) if fams else (None, None)
+    roofline = None
+    if dom[0]:
+        d = dom[1]
+        achieved = d["alg_bytes"] / (d["ms"] / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": dom[0], "achieved": round(achieved, 1), "peak": hbm_peak,
+                    "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                    "share_of_step": round(d["ms"] / (ms_local), 4)}
+    kernels = {kname: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,
+                       "GB/s_alg": round(v["alg_bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] else None}
+               for kname, v in prof.items()}
+    step_alg_gbs = W * n * alg_bytes_per_param(k) / (ms / 1e3) / 1e9
+
+    # ---- e2e through the host-buffer C-ABI entry point (pinned host memory)
+    e2e = None
+    if not args.no_e2e:
+        hg = [x.cpu().pin_memory() for x in tg]
+        hl = [x.cpu().pin_memory() for x in tl]
+        hb = [x.cpu().pin_memory() for x in tb]
+        eng.outer_sync_host(hg, hl, hb, hp, write_local=False)  # warm (allocates device mirrors)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            eng.outer_sync_host(hg, hl, hb, hp, write_local=False)
+        barrier()
+        el = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e2e = {"value": k * n / float(el.item()), "unit": UNIT, "h2d_bytes_per_step": 12 * n * W,
+               "d2h_bytes_per_step": 8 * n * W, "steps": args.e2e_steps,
+               "api": "emesh_engine_outer_sync_host (pinned host theta_g/theta_l/momentum)"}
+        del hg, hl, hb
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            ns = int(args.cpu_sample)
+            secs, kind = cpu_reference_round(ns, k, args.S)
+            cpu = {"value": k * ns / secs, "unit": UNIT, "cores": min(os.cpu_count() or 1, 2 * k) if kind == "reference" else 1,
+                   "kind": kind, "sample": f"one round, {k} workers x {ns} params/worker (slice of the workload), "
+                                           f"S={args.S}, TCP loopback ring"}
+        except Exception as ex:  # the baseline is reported, never required
+            cpu = {"value": None, "error": str(ex)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (theta_g~U[-1,1), theta_l=theta_g-2^-10 U, b=0)",
+            "config": config_block(args, k, n),
+            "hbm_alg_GBps_per_gpu": round(step_alg_gbs, 1),
+            "hbm_frac_step": round(step_alg_gbs / hbm_peak, 4),
+            "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,174 @@
+/*
+ * emesh_b200 — B200-native (sm_100a) outer-synchronisation hot path of the
+ * INTELLECT-1 / PRIME DiLoCo stack, behind a plain C ABI.
+ *
+ * Drop-in boundary for the reference's C++ API in proj/include/emesh
+ * (header-only C++20 library). Each entry point names the reference
+ * interface it replaces. No torch types; plain pointers, sizes, CUDA
+ * streams. Device pointers unless a name says _host. All fp32 arenas and
+ * code arenas must be 16-byte aligned (cudaMalloc gives 256).
+ *
+ * Error convention (maps 1:1 onto the reference's exception hierarchy,
+ * proj/include/emesh/errors.hpp:10-73): functions return EMESH_OK or an
+ * EMESH_E* code; emesh_last_error() gives the message (thread-local).
+ */
+#ifndef EMESH_B200_H
+#define EMESH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* emesh_stream_t; /* == cudaStream_t */
+
+enum {
+    EMESH_OK = 0,
+    EMESH_ESHAPE = 1,   /* emesh::ShapeError   (size mismatch / empty chunk) */
+    EMESH_ENUMERIC = 2, /* emesh::NumericError (non-finite input, quant.hpp:29-31) */
+    EMESH_EDECODE = 3,  /* emesh::DecodeError  (malformed wire buffer, quant.hpp:117-131) */
+    EMESH_ECUDA = 4,    /* CUDA runtime failure */
+    EMESH_ENCCL = 5,    /* NCCL failure (the transport; emesh::LinkError analogue) */
+    EMESH_ERING = 6,    /* emesh::RingFailureError (collective aborted) */
+    EMESH_ECONFIG = 7   /* emesh::ConfigError (invalid plan/options) */
+};
+
+#define EMESH_BUCKETS 256
+
+const char* emesh_last_error(void);
+int emesh_abi_version(void);
+
+/* ---------------- codec: proj/include/emesh/quant.hpp ------------------ */
+
+/* quant.hpp:28 `QuantChunk quantize(std::span<const float>)`: one segment
+ * of n values -> n u8 codes + 256 f32 codebook. Synchronous on `stream`
+ * (the reference throws synchronously): returns EMESH_ESHAPE for n == 0 and
+ * EMESH_ENUMERIC for non-finite input. stats (optional, device, 4 doubles):
+ * {mu, sigma, lo, width}. */
+int emesh_quantize(const float* x, uint64_t n, uint8_t* codes, float* codebook, double* stats,
+                   emesh_stream_t stream);
+
+/* Batched form over a segment table (allreduce.hpp:326-336 sub-slices):
+ * segment i is x[seg_lo[i] .. seg_lo[i]+seg_len[i]) with its codebook at
+ * codebooks[i*256]. seg_lo/seg_len are HOST arrays. codes are written at the
+ * same element offsets as x. Asynchronous; non-finite input is reported by
+ * emesh_codec_check(). */
+int emesh_quantize_segments(const float* x, const uint64_t* seg_lo, const uint64_t* seg_len,
+                            uint32_t nseg, uint8_t* codes, float* codebooks, double* stats,
+                            emesh_stream_t stream);
+/* Synchronizes `stream`; EMESH_ENUMERIC if any quantize since the last check
+ * saw a non-finite value. */
+int emesh_codec_check(emesh_stream_t stream);
+
+/* quant.hpp:89 `dequantize_into`: out[i] = codebook[codes[i]]. */
+int emesh_dequantize(const uint8_t* codes, const float* codebook, uint64_t n, float* out,
+                     emesh_stream_t stream);
+int emesh_dequantize_segments(const uint8_t* codes, const float* codebooks, const uint64_t* seg_lo,
+                              const uint64_t* seg_len, uint32_t nseg, float* out,
+                              emesh_stream_t stream);
+
+/* quant.hpp:102-131 wire layout (u32 LE count, 256 f32 LE, count u8), host
+ * buffers: encode writes 1028+n bytes; decode validates like the reference
+ * (EMESH_EDECODE on truncation, non-finite codebook, count mismatch). */
+uint64_t emesh_encode_quant_chunk(const uint8_t* codes_host, const float* codebook_host, uint32_t n,
+                                  uint8_t* out_host);
+int emesh_decode_quant_chunk(const uint8_t* buf_host, uint64_t len, uint8_t* codes_host,
+                             float* codebook_host, uint32_t* count);
+
+/* ---------------- optimizer: proj/include/emesh/optim.hpp --------------- */
+
+/* optim.hpp:99 `compute_pseudo_gradient`: delta = theta_prev - theta_local
+ * over the flat canonical arena (tensor.hpp:87-93). */
+int emesh_pseudo_gradient(const float* theta_prev, const float* theta_local, float* delta, uint64_t n,
+                          emesh_stream_t stream);
+
+/* optim.hpp:116 `nesterov_outer_step`: b = mu*b + d; theta -= lr*(d + mu*b). */
+int emesh_nesterov_outer_step(float* theta, const float* avg_delta, float* momentum_buf, uint64_t n,
+                              float outer_lr, float outer_momentum, emesh_stream_t stream);
+
+/* ---------------- ring engine: proj/include/emesh/allreduce.hpp --------- */
+
+typedef struct emesh_engine emesh_engine;
+
+typedef struct {
+    uint64_t n;                 /* params per worker (flat arena length) */
+    uint32_t k;                 /* ring size = DiLoCo workers (RingPlan.order.size()) */
+    uint32_t rank;              /* RingPlan.self_index (NCCL mode) */
+    uint32_t pipeline_subchunks;/* ReduceOptions.pipeline_subchunks (S), default 4 */
+    uint32_t virtual_workers;   /* 0/1: one worker per process over NCCL;
+                                   == k: all k workers on this GPU (zero-copy ring) */
+    uint64_t window_elems;      /* pipelining window (0 = auto) */
+    const uint8_t* nccl_id;     /* 128-byte ncclUniqueId (NCCL mode, k > 1) */
+    int device;                 /* CUDA device ordinal, -1 = current */
+} emesh_engine_config;
+
+/* NCCL unique id for emesh_engine_config.nccl_id (rank 0 creates, broadcast). */
+int emesh_nccl_unique_id(uint8_t out[128]);
+
+/* RingPlan + ReduceOptions (allreduce.hpp:25-62): builds the segment table,
+ * the pipelining windows, all device scratch (no allocation afterwards) and
+ * the NCCL communicator. */
+int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out);
+int emesh_engine_destroy(emesh_engine* e);
+
+/* Segment table (allreduce.hpp:107-118,326-336), chunk-major; returns the
+ * count, fills lo/len when non-NULL (host arrays). */
+uint64_t emesh_engine_segments(const emesh_engine* e, uint64_t* seg_lo, uint64_t* seg_len);
+
+/* allreduce.hpp:314 `ring_allreduce` (ReduceMode::int8): output = the
+ * elementwise mean of the workers' inputs as every rank decodes it. Inputs
+ * are preserved (ReduceJob contract, allreduce.hpp:47-48). Arrays have one
+ * entry per local worker (1 in NCCL mode, k in virtual mode). */
+int emesh_engine_ring_allreduce(emesh_engine* e, const float* const* input, float* const* output,
+                                emesh_stream_t stream);
+
+/* One DiLoCo outer sync (trainer.hpp:355-382): delta = theta_g - theta_l
+ * (never materialized) -> int8 ring all-reduce -> Nesterov fused with the
+ * final dequantize; theta_g and momentum_buf updated in place; with
+ * write_local, theta_l <- theta_g (trainer.hpp:382). */
+int emesh_engine_outer_sync(emesh_engine* e, float* const* theta_g, float* const* theta_l,
+                            float* const* momentum_buf, float outer_lr, float outer_momentum,
+                            int write_local, emesh_stream_t stream);
+
+/* Same round with HOST buffers (what the reference's Trainer holds):
+ * H2D of theta_g/theta_l/momentum_buf, the round, D2H of the updated
+ * theta_g/momentum_buf (+theta_l with write_local). Synchronous. Pinned
+ * host memory gives full PCIe bandwidth. */
+int emesh_engine_outer_sync_host(emesh_engine* e, float* const* theta_g, float* const* theta_l,
+                                 float* const* momentum_buf, float outer_lr, float outer_momentum,
+                                 int write_local);
+
+/* Synchronizes the engine; EMESH_ENUMERIC if a quantize saw non-finite data
+ * since the last check (the reference's NumericError, quant.hpp:31). */
+int emesh_engine_check(emesh_engine* e);
+
+/* Device views of a local worker's final payload arenas after a round:
+ * codes (n bytes, arena-indexed) and codebooks (nseg x 256). In NCCL mode
+ * every chunk's final payload is present (the all-gather delivered it); in
+ * virtual mode chunk c's lives in worker (c-1)%k's arena. */
+int emesh_engine_payload(emesh_engine* e, uint32_t worker, const uint8_t** codes, const float** codebooks,
+                         const double** seg_stats, uint64_t* stats_stride_bytes);
+
+/* Host copies of the same: codes (n bytes), codebooks (nseg*256 f32),
+ * stats (nseg*4 f64: mu, sigma, lo, width). Synchronizes the engine. */
+int emesh_engine_payload_host(emesh_engine* e, uint32_t worker, uint8_t* codes_host, float* codebooks_host,
+                              double* stats_host);
+
+/* Number of kernels this engine launched since creation (for the bench's
+ * gpu_launches claim). */
+uint64_t emesh_engine_launches(const emesh_engine* e);
+
+/* Per-kernel profiling with CUDA events on the launching stream. enable
+ * resets the record. kind: 0 k_stats, 1 k_bin, 2 hop-0 quantize pair,
+ * 3 RS hop pair, 4 owner-final pair, 5 plain quantize pair, 6 dequant +
+ * Nesterov, 7 dequantize, 8 k==1 fused PG+Nesterov. Reads launches, total
+ * device ms and total ALGORITHMIC bytes of that kind. */
+int emesh_engine_profile(emesh_engine* e, int enable);
+int emesh_engine_profile_read(emesh_engine* e, uint32_t kind, uint64_t* launches, double* ms, double* alg_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMESH_B200_H */

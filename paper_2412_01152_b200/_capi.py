@@ -1,0 +1,97 @@
+"""ctypes binding of the C ABI in include/emesh_b200.h (libemesh_b200.so).
+
+The product path has no fallback: if the shared library is missing or the
+CUDA driver is absent, every entry point raises. Build it with
+``python -c "import __graft_entry__ as g; g.build()"`` (or ``make -C
+paper_2412_01152_b200/csrc``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libemesh_b200.so")
+
+# every symbol include/emesh_b200.h declares (checked by tests/test_capi_symbols.py)
+EXPORTS = (
+    "emesh_last_error", "emesh_abi_version",
+    "emesh_quantize", "emesh_quantize_segments", "emesh_codec_check",
+    "emesh_dequantize", "emesh_dequantize_segments",
+    "emesh_encode_quant_chunk", "emesh_decode_quant_chunk",
+    "emesh_pseudo_gradient", "emesh_nesterov_outer_step",
+    "emesh_nccl_unique_id", "emesh_engine_create", "emesh_engine_destroy",
+    "emesh_engine_segments", "emesh_engine_ring_allreduce", "emesh_engine_outer_sync",
+    "emesh_engine_outer_sync_host", "emesh_engine_check", "emesh_engine_payload", "emesh_engine_payload_host",
+    "emesh_engine_launches", "emesh_engine_profile", "emesh_engine_profile_read",
+)
+
+OK, ESHAPE, ENUMERIC, EDECODE, ECUDA, ENCCL, ERING, ECONFIG = range(8)
+
+
+class EngineConfig(C.Structure):
+    _fields_ = [
+        ("n", C.c_uint64),
+        ("k", C.c_uint32),
+        ("rank", C.c_uint32),
+        ("pipeline_subchunks", C.c_uint32),
+        ("virtual_workers", C.c_uint32),
+        ("window_elems", C.c_uint64),
+        ("nccl_id", C.c_void_p),
+        ("device", C.c_int),
+    ]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libemesh_b200.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: the CUDA extension is not built (no CPU fallback exists)")
+    L = C.CDLL(LIB_PATH)
+    vp, u64, u32, i32, f32 = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.c_float
+    P = C.POINTER
+    sig = {
+        "emesh_last_error": (C.c_char_p, []),
+        "emesh_abi_version": (i32, []),
+        "emesh_quantize": (i32, [vp, u64, vp, vp, vp, vp]),
+        "emesh_quantize_segments": (i32, [vp, P(u64), P(u64), u32, vp, vp, vp, vp]),
+        "emesh_codec_check": (i32, [vp]),
+        "emesh_dequantize": (i32, [vp, vp, u64, vp, vp]),
+        "emesh_dequantize_segments": (i32, [vp, vp, P(u64), P(u64), u32, vp, vp]),
+        "emesh_encode_quant_chunk": (u64, [vp, vp, u32, vp]),
+        "emesh_decode_quant_chunk": (i32, [vp, u64, vp, vp, P(u32)]),
+        "emesh_pseudo_gradient": (i32, [vp, vp, vp, u64, vp]),
+        "emesh_nesterov_outer_step": (i32, [vp, vp, vp, u64, f32, f32, vp]),
+        "emesh_nccl_unique_id": (i32, [vp]),
+        "emesh_engine_create": (i32, [P(EngineConfig), P(vp)]),
+        "emesh_engine_destroy": (i32, [vp]),
+        "emesh_engine_segments": (u64, [vp, vp, vp]),
+        "emesh_engine_ring_allreduce": (i32, [vp, P(vp), P(vp), vp]),
+        "emesh_engine_outer_sync": (i32, [vp, P(vp), P(vp), P(vp), f32, f32, i32, vp]),
+        "emesh_engine_outer_sync_host": (i32, [vp, P(vp), P(vp), P(vp), f32, f32, i32]),
+        "emesh_engine_check": (i32, [vp]),
+        "emesh_engine_payload": (i32, [vp, u32, P(vp), P(vp), P(vp), P(u64)]),
+        "emesh_engine_payload_host": (i32, [vp, u32, vp, vp, vp]),
+        "emesh_engine_launches": (u64, [vp]),
+        "emesh_engine_profile": (i32, [vp, i32]),
+        "emesh_engine_profile_read": (i32, [vp, u32, P(u64), P(C.c_double), P(C.c_double)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return lib().emesh_last_error().decode(errors="replace")
+
+
+def ptr_array(ptrs):
+    return (C.c_void_p * len(ptrs))(*ptrs)

@@ -1,0 +1,995 @@
+// C-ABI, segment planning and the ring engine (NCCL over NVLink, or k
+// virtual workers on one GPU) for the outer-synchronisation hot path.
+// See include/emesh_b200.h for the reference interface each entry replaces.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "emesh_b200.h"
+#include "kernels.cuh"
+
+using namespace emesh_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CU(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(EMESH_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+#define NC(call)                                                                          \
+    do {                                                                                  \
+        ncclResult_t r_ = (call);                                                         \
+        if (r_ != ncclSuccess)                                                            \
+            return fail(EMESH_ENCCL, "%s: %s (%s:%d)", #call, ncclGetErrorString(r_), __FILE__, __LINE__); \
+    } while (0)
+#define TRY(expr)                   \
+    do {                            \
+        int rc_ = (expr);           \
+        if (rc_ != EMESH_OK) return rc_; \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// Segment plan: allreduce.hpp:107-118 (split) and :326-336 (subs_of).
+
+void split_piece(uint64_t total, uint64_t parts, uint64_t i, uint64_t* lo, uint64_t* len) {
+    const uint64_t base = parts ? total / parts : 0, rem = parts ? total % parts : 0;
+    *len = base + (i < rem ? 1 : 0);
+    *lo = i * base + (i < rem ? i : rem);
+}
+
+struct Seg {
+    uint64_t lo, len;
+};
+
+// One pipelining window: consecutive segments of one rank chunk.
+struct Batch {
+    uint32_t chunk = 0, window = 0;
+    uint32_t slot0 = 0, nseg = 0;
+    uint64_t el_lo = 0, el_hi = 0;  // element range [el_lo, el_hi)
+    uint64_t q_lo = 0, q_hi = 0;    // float4 slot range [q_lo, q_hi)
+    uint32_t ncta = 0, nnodes = 0;
+    size_t off_segs = 0, off_cta = 0;  // byte offsets into the table arena
+    const SegInfo* d_segs = nullptr;
+    const uint32_t* d_cta_seg = nullptr;
+
+    void bind(void* base) {
+        d_segs = reinterpret_cast<const SegInfo*>((char*)base + off_segs);
+        d_cta_seg = reinterpret_cast<const uint32_t*>((char*)base + off_cta);
+    }
+};
+
+struct Plan {
+    uint64_t n = 0;
+    uint32_t k = 1, S = 4;
+    std::vector<Seg> segs;                      // global slot order (chunk-major)
+    std::vector<std::vector<Batch>> batches;    // [chunk][window]
+    std::vector<uint8_t> host_tables;
+    void* d_tables = nullptr;
+    size_t max_cta = 0, max_nodes = 0, max_segs = 0, max_slots = 0;
+
+    // Appends the device tables for one batch over segments [s0, s1).
+    void add_batch(uint32_t chunk, uint32_t window, uint32_t s0, uint32_t s1) {
+        Batch b;
+        b.chunk = chunk;
+        b.window = window;
+        b.slot0 = s0;
+        b.nseg = s1 - s0;
+        std::vector<SegInfo> infos;
+        std::vector<uint32_t> cseg;
+        bool first = true;
+        uint32_t nodes = 0;
+        for (uint32_t s = s0; s < s1; ++s) {
+            const Seg& g = segs[s];
+            SegInfo si{};
+            si.lo = g.lo;
+            si.len = g.len;
+            si.q0 = g.lo >> 2;
+            si.cta0 = (uint32_t)cseg.size();
+            si.slot = s;
+            si.in_slot = s;
+            si.node_base = nodes;
+            if (g.len > 0) {
+                const uint64_t q_last = (g.lo + g.len - 1) >> 2;
+                const uint64_t nq = q_last - si.q0 + 1;
+                si.nunits = (uint32_t)((nq + kUnitSlots - 1) / kUnitSlots);
+                si.ncta = (si.nunits + kWarps - 1) / kWarps;
+                if (first) { b.el_lo = g.lo; b.q_lo = si.q0; first = false; }
+                b.el_hi = g.lo + g.len;
+                b.q_hi = q_last + 1;
+            }
+            for (uint32_t n = si.ncta; n > 1;) {  // internal nodes of the combine tree
+                n = (n + kFan - 1) / kFan;
+                nodes += n;
+            }
+            for (uint32_t t = 0; t < si.ncta; ++t) cseg.push_back((uint32_t)infos.size());
+            infos.push_back(si);
+        }
+        b.ncta = (uint32_t)cseg.size();
+        b.nnodes = nodes;
+        auto append = [&](const void* p, size_t bytes) {
+            size_t off = (host_tables.size() + 15) & ~size_t(15);
+            host_tables.resize(off + bytes);
+            if (bytes) std::memcpy(host_tables.data() + off, p, bytes);
+            return off;
+        };
+        b.off_segs = append(infos.data(), infos.size() * sizeof(SegInfo));
+        b.off_cta = append(cseg.data(), cseg.size() * sizeof(uint32_t));
+        max_cta = std::max<size_t>(max_cta, b.ncta);
+        max_nodes = std::max<size_t>(max_nodes, b.nnodes);
+        max_segs = std::max<size_t>(max_segs, b.nseg);
+        max_slots = std::max<size_t>(max_slots, b.q_hi > b.q_lo ? b.q_hi - b.q_lo : 0);
+        batches[chunk].push_back(b);
+    }
+
+    int upload() {
+        if (d_tables) cudaFree(d_tables);
+        CU(cudaMalloc(&d_tables, std::max<size_t>(host_tables.size(), 16)));
+        CU(cudaMemcpy(d_tables, host_tables.data(), host_tables.size(), cudaMemcpyHostToDevice));
+        for (auto& row : batches)
+            for (auto& b : row) b.bind(d_tables);
+        return EMESH_OK;
+    }
+    void release() {
+        if (d_tables) cudaFree(d_tables);
+        d_tables = nullptr;
+    }
+};
+
+// Ring plan: k chunks, min(S, len) subs each, windows of G segments.
+Plan make_ring_plan(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems) {
+    Plan p;
+    p.n = n;
+    p.k = k;
+    p.S = S;
+    p.batches.resize(k);
+    std::vector<uint32_t> first(k + 1);
+    uint64_t max_seg = 1;
+    for (uint32_t c = 0; c < k; ++c) {
+        uint64_t clo, clen;
+        split_piece(n, k, c, &clo, &clen);
+        const uint64_t ns = clen == 0 ? 1 : std::min<uint64_t>(S, clen);
+        first[c] = (uint32_t)p.segs.size();
+        for (uint64_t j = 0; j < ns; ++j) {
+            uint64_t slo, slen;
+            split_piece(clen, ns, j, &slo, &slen);
+            p.segs.push_back({clo + slo, slen});
+            max_seg = std::max(max_seg, slen);
+        }
+    }
+    first[k] = (uint32_t)p.segs.size();
+    uint64_t G = std::max<uint64_t>(1, window_elems / max_seg);
+    // chunks shorter than S have fewer sub-slices; keep one window per chunk
+    // then so every rank agrees on the window count (NCCL send/recv pairing).
+    if (n < (uint64_t)k * S) G = S;
+    for (uint32_t c = 0; c < k; ++c) {
+        uint32_t w = 0;
+        for (uint32_t s = first[c]; s < first[c + 1]; s += (uint32_t)G, ++w)
+            p.add_batch(c, w, s, (uint32_t)std::min<uint64_t>(first[c + 1], s + G));
+    }
+    return p;
+}
+
+// Plan over an explicit segment list (the standalone codec API): one batch.
+Plan make_list_plan(const uint64_t* lo, const uint64_t* len, uint32_t nseg) {
+    Plan p;
+    p.k = 1;
+    p.batches.resize(1);
+    for (uint32_t i = 0; i < nseg; ++i) p.segs.push_back({lo[i], len[i]});
+    p.add_batch(0, 0, 0, nseg);
+    return p;
+}
+
+// Device scratch shared by every batch launched on one stream.
+struct Workspace {
+    float* scratch = nullptr;
+    StatP* leaf_stat = nullptr;
+    StatP* node_stat = nullptr;
+    double* leaf_sum = nullptr;
+    uint32_t* leaf_cnt = nullptr;
+    double* node_sum = nullptr;
+    uint32_t* node_cnt = nullptr;
+    uint32_t* tree_cnt = nullptr;
+    uint32_t* seg_flags = nullptr;
+    uint32_t* err = nullptr;
+    size_t cap_slots = 0, cap_cta = 0, cap_nodes = 0, cap_segs = 0;
+
+    template <typename T>
+    static int grow(T*& p, size_t& cap, size_t want, size_t elems_per, bool zero) {
+        if (want <= cap && p) return EMESH_OK;
+        if (p) CU(cudaFree(p));
+        const size_t bytes = std::max<size_t>(want, 1) * elems_per * sizeof(T);
+        CU(cudaMalloc(&p, bytes));
+        if (zero) CU(cudaMemset(p, 0, bytes));
+        return EMESH_OK;
+    }
+
+    int reserve(size_t slots, size_t ctas, size_t nodes, size_t segs) {
+        if (!err) {
+            CU(cudaMalloc(&err, sizeof(uint32_t)));
+            CU(cudaMemset(err, 0, sizeof(uint32_t)));
+        }
+        if (slots > cap_slots || !scratch) {
+            size_t c = 0;
+            TRY(grow(scratch, c, slots, 4, false));
+            cap_slots = std::max<size_t>(slots, 1);
+        }
+        if (ctas > cap_cta || !leaf_stat) {
+            size_t c = 0;
+            TRY(grow(leaf_stat, c, ctas, 1, false));
+            c = 0;
+            TRY(grow(leaf_sum, c, ctas, kBuckets, false));
+            c = 0;
+            TRY(grow(leaf_cnt, c, ctas, kBuckets, false));
+            cap_cta = std::max<size_t>(ctas, 1);
+        }
+        if (nodes > cap_nodes || !node_stat) {
+            size_t c = 0;
+            TRY(grow(node_stat, c, nodes, 1, false));
+            c = 0;
+            TRY(grow(node_sum, c, nodes, kBuckets, false));
+            c = 0;
+            TRY(grow(node_cnt, c, nodes, kBuckets, false));
+            c = 0;
+            TRY(grow(tree_cnt, c, nodes, 2, true));
+            cap_nodes = std::max<size_t>(nodes, 1);
+        }
+        if (segs > cap_segs || !seg_flags) {
+            size_t c = 0;
+            TRY(grow(seg_flags, c, segs, 1, true));
+            cap_segs = std::max<size_t>(segs, 1);
+        }
+        return EMESH_OK;
+    }
+    void release() {
+        cudaFree(scratch); cudaFree(leaf_stat); cudaFree(node_stat); cudaFree(leaf_sum); cudaFree(leaf_cnt);
+        cudaFree(node_sum); cudaFree(node_cnt); cudaFree(tree_cnt); cudaFree(seg_flags); cudaFree(err);
+        *this = Workspace();
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Launchers
+
+struct QuantIO {
+    int src;                  // kSrc* | kHasIn | kDivK
+    const float* a;
+    const float* b;
+    const uint8_t* in_codes;
+    const float* in_cb;
+    float divisor;
+    uint8_t* out_codes;
+    float* out_cb;
+    SegStat* stats;
+};
+
+enum ProfKind : int {
+    kProfStats = 0,      // k_stats (all producers)
+    kProfBin = 1,        // k_bin
+    kProfQuantPG = 2,    // k_stats+k_bin, hop-0 payload Q(theta_g - theta_l)
+    kProfQuantHop = 3,   // k_stats+k_bin, reduce-scatter hop (dequant-add-requant)
+    kProfQuantFinal = 4, // k_stats+k_bin, owner mean (/k) + quantize
+    kProfQuantPlain = 5, // k_stats+k_bin, plain buffer
+    kProfNesterov = 6,   // k_apply<1>: dequant + Nesterov (+ theta_l write)
+    kProfDequant = 7,    // k_apply<0>
+    kProfFusedK1 = 8,    // k_nesterov_f32 (k == 1: PG + Nesterov)
+};
+
+// Launch accounting + optional per-kernel CUDA-event profiling on the
+// launching stream (bench.py's roofline numbers come from here).
+struct Tracker {
+    uint64_t launches = 0;
+    bool prof = false;
+    struct Rec {
+        int kind;
+        cudaEvent_t a, b;
+        double bytes;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    cudaEvent_t ev(cudaStream_t st) {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        cudaEvent_t e = pool[used++];
+        cudaEventRecord(e, st);
+        return e;
+    }
+    void reset() {
+        recs.clear();
+        used = 0;
+    }
+    void release() {
+        for (auto e : pool) cudaEventDestroy(e);
+        pool.clear();
+        recs.clear();
+        used = 0;
+    }
+};
+Tracker g_codec_tracker;
+
+int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t st, Tracker* tr) {
+    if (bt.ncta == 0) return EMESH_OK;
+    QuantArgs a{};
+    a.segs = bt.d_segs;
+    a.cta_seg = bt.d_cta_seg;
+    a.ncta = bt.ncta;
+    a.nseg = bt.nseg;
+    a.scratch_q0 = bt.q_lo;
+    a.a = io.a;
+    a.b = io.b;
+    a.in_codes = io.in_codes;
+    a.in_cb = io.in_cb;
+    a.divisor = io.divisor;
+    a.scratch = ws.scratch;
+    a.out_codes = io.out_codes;
+    a.out_cb = io.out_cb;
+    a.stats = io.stats;
+    a.leaf_stat = ws.leaf_stat;
+    a.node_stat = ws.node_stat;
+    a.leaf_sum = ws.leaf_sum;
+    a.leaf_cnt = ws.leaf_cnt;
+    a.node_sum = ws.node_sum;
+    a.node_cnt = ws.node_cnt;
+    a.tree_cnt = ws.tree_cnt;
+    a.nnodes = (uint32_t)ws.cap_nodes;
+    a.seg_flags = ws.seg_flags;
+    a.err = ws.err;
+    const dim3 g1(bt.ncta), g2(bt.ncta), blk(kThreads);
+    const bool prof = tr && tr->prof;
+    cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
+    switch (io.src) {
+        case kSrcA: k_stats<kSrcA><<<g1, blk, 0, st>>>(a); break;
+        case kSrcAminusB: k_stats<kSrcAminusB><<<g1, blk, 0, st>>>(a); break;
+        case kSrcA | kHasIn: k_stats<kSrcA | kHasIn><<<g1, blk, 0, st>>>(a); break;
+        case kSrcAminusB | kHasIn: k_stats<kSrcAminusB | kHasIn><<<g1, blk, 0, st>>>(a); break;
+        case kSrcA | kHasIn | kDivK: k_stats<kSrcA | kHasIn | kDivK><<<g1, blk, 0, st>>>(a); break;
+        case kSrcAminusB | kHasIn | kDivK: k_stats<kSrcAminusB | kHasIn | kDivK><<<g1, blk, 0, st>>>(a); break;
+        default: return fail(EMESH_ECONFIG, "unsupported producer %d", io.src);
+    }
+    cudaEvent_t e1 = prof ? tr->ev(st) : nullptr;
+    if (io.src == kSrcA) k_bin<false><<<g2, blk, 0, st>>>(a);
+    else k_bin<true><<<g2, blk, 0, st>>>(a);
+    if (tr) tr->launches += 2;
+    if (prof) {
+        cudaEvent_t e2 = tr->ev(st);
+        const double elems = (double)(bt.el_hi - bt.el_lo);
+        const double rd = elems * (((io.src & kSrcAminusB) ? 8.0 : 4.0) + ((io.src & kHasIn) ? 1.0 : 0.0)) +
+                          ((io.src & kHasIn) ? 1028.0 * bt.nseg : 0.0);
+        const double wr = elems + 1028.0 * bt.nseg;
+        const int fam = (io.src & kDivK) ? 2 : (io.src & kHasIn) ? 1 : (io.src & kSrcAminusB) ? 0 : 3;
+        tr->recs.push_back({kProfStats, e0, e1, rd});
+        tr->recs.push_back({kProfBin, e1, e2, wr});
+        tr->recs.push_back({kProfQuantPG + fam, e0, e2, rd + wr});
+    }
+    CU(cudaGetLastError());
+    return EMESH_OK;
+}
+
+int launch_apply(const Batch& bt, int mode, const uint8_t* codes, const float* cb, float* theta, float* buf,
+                 float* theta_local, float* out, float lr, float mom, cudaStream_t st, Tracker* tr) {
+    if (bt.ncta == 0) return EMESH_OK;
+    ApplyArgs a{};
+    a.segs = bt.d_segs;
+    a.cta_seg = bt.d_cta_seg;
+    a.ncta = bt.ncta;
+    a.codes = codes;
+    a.cb = cb;
+    a.theta = theta;
+    a.buf = buf;
+    a.theta_local = theta_local;
+    a.out = out;
+    a.lr = lr;
+    a.mom = mom;
+    const dim3 g(bt.ncta), blk(kThreads);
+    const bool prof = tr && tr->prof;
+    cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
+    if (mode == 0) k_apply<0><<<g, blk, 0, st>>>(a);
+    else k_apply<1><<<g, blk, 0, st>>>(a);
+    if (tr) tr->launches += 1;
+    if (prof) {
+        const double elems = (double)(bt.el_hi - bt.el_lo);
+        const double by = mode == 0 ? elems * 5.0 : elems * (theta_local ? 21.0 : 17.0);
+        tr->recs.push_back({mode == 0 ? kProfDequant : kProfNesterov, e0, tr->ev(st), by + 1024.0 * bt.nseg});
+    }
+    CU(cudaGetLastError());
+    return EMESH_OK;
+}
+
+int flat_grid(uint64_t n) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t want = (n / 4 + kThreads - 1) / kThreads;
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)sms * 8));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Process-global workspace for the standalone codec entry points.
+std::mutex g_codec_mu;
+Workspace g_codec_ws;
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+
+extern "C" {
+
+const char* emesh_last_error(void) { return g_err.c_str(); }
+int emesh_abi_version(void) { return 1; }
+
+// ---------------- codec ----------------------------------------------------
+
+int emesh_quantize_segments(const float* x, const uint64_t* seg_lo, const uint64_t* seg_len, uint32_t nseg,
+                            uint8_t* codes, float* codebooks, double* stats, emesh_stream_t stream) {
+    if (nseg == 0) return EMESH_OK;
+    if (!aligned16(x) || (reinterpret_cast<uintptr_t>(codes) & 3u))
+        return fail(EMESH_ESHAPE, "quantize: x must be 16-byte and codes 4-byte aligned");
+    for (uint32_t i = 0; i < nseg; ++i)
+        if (seg_len[i] == 0) return fail(EMESH_ESHAPE, "quantize: empty chunk");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> g(g_codec_mu);
+    Plan p = make_list_plan(seg_lo, seg_len, nseg);
+    TRY(g_codec_ws.reserve(p.max_slots, p.max_cta, p.max_nodes, p.max_segs));
+    // stream-ordered tables + stats (freed in stream order)
+    void* d_tables = nullptr;
+    SegStat* d_stats = nullptr;
+    CU(cudaMallocAsync(&d_tables, std::max<size_t>(p.host_tables.size(), 16), st));
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&d_stats), sizeof(SegStat) * nseg, st));
+    CU(cudaMemcpyAsync(d_tables, p.host_tables.data(), p.host_tables.size(), cudaMemcpyHostToDevice, st));
+    Batch& b = p.batches[0][0];
+    b.bind(d_tables);
+    QuantIO io{kSrcA, x, nullptr, nullptr, nullptr, 1.f, codes, codebooks, d_stats};
+    TRY(launch_quant(b, g_codec_ws, io, st, &g_codec_tracker));
+    if (stats)
+        CU(cudaMemcpy2DAsync(stats, 4 * sizeof(double), d_stats, sizeof(SegStat), 4 * sizeof(double), nseg,
+                             cudaMemcpyDeviceToDevice, st));
+    // pageable host_tables: the H2D copy above completed synchronously
+    CU(cudaFreeAsync(d_tables, st));
+    CU(cudaFreeAsync(d_stats, st));
+    return EMESH_OK;
+}
+
+int emesh_codec_check(emesh_stream_t stream) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    CU(cudaStreamSynchronize(st));
+    std::lock_guard<std::mutex> g(g_codec_mu);
+    if (!g_codec_ws.err) return EMESH_OK;
+    uint32_t e = 0;
+    CU(cudaMemcpy(&e, g_codec_ws.err, sizeof e, cudaMemcpyDeviceToHost));
+    if (e) {
+        CU(cudaMemset(g_codec_ws.err, 0, sizeof(uint32_t)));
+        return fail(EMESH_ENUMERIC, "quantize: non-finite input");
+    }
+    return EMESH_OK;
+}
+
+int emesh_quantize(const float* x, uint64_t n, uint8_t* codes, float* codebook, double* stats,
+                   emesh_stream_t stream) {
+    if (n == 0) return fail(EMESH_ESHAPE, "quantize: empty chunk");
+    const uint64_t lo = 0;
+    TRY(emesh_quantize_segments(x, &lo, &n, 1, codes, codebook, stats, stream));
+    return emesh_codec_check(stream);
+}
+
+int emesh_dequantize_segments(const uint8_t* codes, const float* codebooks, const uint64_t* seg_lo,
+                              const uint64_t* seg_len, uint32_t nseg, float* out, emesh_stream_t stream) {
+    if (nseg == 0) return EMESH_OK;
+    if (!aligned16(out) || (reinterpret_cast<uintptr_t>(codes) & 3u))
+        return fail(EMESH_ESHAPE, "dequantize: out must be 16-byte and codes 4-byte aligned");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Plan p = make_list_plan(seg_lo, seg_len, nseg);
+    void* d_tables = nullptr;
+    CU(cudaMallocAsync(&d_tables, std::max<size_t>(p.host_tables.size(), 16), st));
+    CU(cudaMemcpyAsync(d_tables, p.host_tables.data(), p.host_tables.size(), cudaMemcpyHostToDevice, st));
+    Batch& b = p.batches[0][0];
+    b.bind(d_tables);
+    TRY(launch_apply(b, 0, codes, codebooks, nullptr, nullptr, nullptr, out, 0.f, 0.f, st, &g_codec_tracker));
+    CU(cudaFreeAsync(d_tables, st));
+    return EMESH_OK;
+}
+
+int emesh_dequantize(const uint8_t* codes, const float* codebook, uint64_t n, float* out, emesh_stream_t stream) {
+    if (n == 0) return EMESH_OK;
+    const uint64_t lo = 0;
+    return emesh_dequantize_segments(codes, codebook, &lo, &n, 1, out, stream);
+}
+
+uint64_t emesh_encode_quant_chunk(const uint8_t* codes, const float* cb, uint32_t n, uint8_t* out) {
+    uint8_t* p = out;
+    for (int i = 0; i < 4; ++i) *p++ = (uint8_t)(n >> (8 * i));
+    for (int b = 0; b < kBuckets; ++b) {
+        uint32_t u;
+        std::memcpy(&u, &cb[b], 4);
+        for (int i = 0; i < 4; ++i) *p++ = (uint8_t)(u >> (8 * i));
+    }
+    if (n) std::memcpy(p, codes, n);
+    return 4 + 4 * kBuckets + (uint64_t)n;
+}
+
+int emesh_decode_quant_chunk(const uint8_t* buf, uint64_t len, uint8_t* codes, float* cb, uint32_t* count) {
+    if (len < 4) return fail(EMESH_EDECODE, "truncated buffer");
+    const uint32_t c = (uint32_t)buf[0] | ((uint32_t)buf[1] << 8) | ((uint32_t)buf[2] << 16) | ((uint32_t)buf[3] << 24);
+    if (len - 4 < 4u * kBuckets) return fail(EMESH_EDECODE, "truncated buffer");
+    for (int b = 0; b < kBuckets; ++b) {
+        const uint8_t* q = buf + 4 + 4 * b;
+        const uint32_t u = (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16) | ((uint32_t)q[3] << 24);
+        float v;
+        std::memcpy(&v, &u, 4);
+        if (!std::isfinite(v)) return fail(EMESH_EDECODE, "non-finite codebook entry");
+        cb[b] = v;
+    }
+    if (len - 4 - 4u * kBuckets != c) return fail(EMESH_EDECODE, "quant chunk count does not match payload");
+    if (c && codes) std::memcpy(codes, buf + 4 + 4 * kBuckets, c);
+    *count = c;
+    return EMESH_OK;
+}
+
+// ---------------- optimizer ----------------------------------------------
+
+int emesh_pseudo_gradient(const float* prev, const float* local, float* delta, uint64_t n, emesh_stream_t stream) {
+    if (n == 0) return EMESH_OK;
+    if (!aligned16(prev) || !aligned16(local) || !aligned16(delta))
+        return fail(EMESH_ESHAPE, "pseudo_gradient: arenas must be 16-byte aligned");
+    k_pseudo_gradient<<<flat_grid(n), kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(prev, local, delta, n);
+    ++g_codec_tracker.launches;
+    CU(cudaGetLastError());
+    return EMESH_OK;
+}
+
+int emesh_nesterov_outer_step(float* theta, const float* avg, float* buf, uint64_t n, float lr, float mom,
+                              emesh_stream_t stream) {
+    if (n == 0) return EMESH_OK;
+    if (!aligned16(theta) || !aligned16(avg) || !aligned16(buf))
+        return fail(EMESH_ESHAPE, "nesterov: arenas must be 16-byte aligned");
+    k_nesterov_f32<<<flat_grid(n), kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(theta, avg, nullptr, buf,
+                                                                                       nullptr, n, lr, mom);
+    ++g_codec_tracker.launches;
+    CU(cudaGetLastError());
+    return EMESH_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Ring engine
+// ===========================================================================
+
+struct emesh_engine {
+    emesh_engine_config cfg{};
+    int device = 0;
+    uint32_t k = 1, rank = 0, workers = 1;
+    bool virt = false;
+    Plan plan;
+    Workspace ws;
+    ncclComm_t comm = nullptr;
+    cudaStream_t s_comp = nullptr, s_comm = nullptr;
+    cudaEvent_t ev_entry = nullptr, ev_done = nullptr, ev_comm_done = nullptr;
+    std::vector<cudaEvent_t> ev_send, ev_recv;  // per window
+    struct Arena {
+        uint8_t* codes = nullptr;
+        float* cbs = nullptr;
+        SegStat* stats = nullptr;
+    };
+    std::vector<Arena> arenas;  // per local worker
+    // device mirrors for the host-buffer entry point
+    std::vector<float*> h_theta, h_local, h_buf;
+    Tracker tr;
+    uint32_t windows = 1;
+};
+
+namespace {
+
+int engine_alloc(emesh_engine* e) {
+    const uint64_t n = e->plan.n;
+    const size_t nslots = e->plan.segs.size();
+    e->arenas.resize(e->workers);
+    for (auto& a : e->arenas) {
+        CU(cudaMalloc(&a.codes, ((n + 15) & ~uint64_t(15)) + 16));
+        CU(cudaMalloc(&a.cbs, nslots * kBuckets * sizeof(float)));
+        CU(cudaMalloc(&a.stats, nslots * sizeof(SegStat)));
+        CU(cudaMemset(a.stats, 0, nslots * sizeof(SegStat)));
+    }
+    TRY(e->ws.reserve(e->plan.max_slots, e->plan.max_cta, e->plan.max_nodes, e->plan.max_segs));
+    return EMESH_OK;
+}
+
+// Producer flags for reduce-scatter hop s of a k-ring (s == k-2 finalizes).
+int hop_src(bool from_theta, uint32_t s, uint32_t k) {
+    int src = (from_theta ? kSrcAminusB : kSrcA) | kHasIn;
+    if (s + 2 == k) src |= kDivK;
+    return src;
+}
+
+// ---- virtual ring: all k workers on this GPU, one stream, zero-copy hand-off
+// (worker w reads its predecessor's payload arena in place of a recv).
+int run_virtual(emesh_engine* e, const float* const* A, const float* const* B, float* const* theta, float* const* buf,
+                float* const* local_out, float* const* out, float lr, float mom) {
+    const uint32_t k = e->k;
+    cudaStream_t st = e->s_comp;
+    const bool pg = B != nullptr;
+    // hop 0 payload: Q(own chunk) (allreduce.hpp:411-414 with s = 0)
+    for (uint32_t w = 0; w < k; ++w)
+        for (const Batch& bt : e->plan.batches[w]) {
+            QuantIO io{pg ? kSrcAminusB : kSrcA, A[w], pg ? B[w] : nullptr, nullptr, nullptr, 1.f,
+                       e->arenas[w].codes, e->arenas[w].cbs, e->arenas[w].stats};
+            TRY(launch_quant(bt, e->ws, io, st, &e->tr));
+        }
+    for (uint32_t s = 0; s + 1 < k; ++s)
+        for (uint32_t w = 0; w < k; ++w) {
+            const uint32_t pred = (w + k - 1) % k;
+            const uint32_t recv_c = (w + k - s - 1) % k;
+            for (const Batch& bt : e->plan.batches[recv_c]) {
+                QuantIO io{hop_src(pg, s, k), A[w], pg ? B[w] : nullptr, e->arenas[pred].codes,
+                           e->arenas[pred].cbs, (float)k, e->arenas[w].codes, e->arenas[w].cbs, e->arenas[w].stats};
+                TRY(launch_quant(bt, e->ws, io, st, &e->tr));
+            }
+        }
+    // every worker decodes the owners' bytes (all-gather is zero-copy here)
+    for (uint32_t w = 0; w < k; ++w)
+        for (uint32_t c = 0; c < k; ++c) {
+            const uint32_t owner = (c + k - 1) % k;
+            for (const Batch& bt : e->plan.batches[c]) {
+                if (out) {
+                    TRY(launch_apply(bt, 0, e->arenas[owner].codes, e->arenas[owner].cbs, nullptr, nullptr, nullptr,
+                                     out[w], 0.f, 0.f, st, &e->tr));
+                } else {
+                    TRY(launch_apply(bt, 1, e->arenas[owner].codes, e->arenas[owner].cbs, theta[w], buf[w],
+                                     local_out ? local_out[w] : nullptr, nullptr, lr, mom, st, &e->tr));
+                }
+            }
+        }
+    return EMESH_OK;
+}
+
+// ---- NCCL ring: this process is ring position `rank`; payload windows move
+// with ncclSend/ncclRecv on s_comm while s_comp runs the fused hop kernels on
+// the previous window.
+int xfer_window(emesh_engine* e, const Batch& snd, const Batch& rcv) {
+    const uint32_t k = e->k, r = e->rank;
+    const int succ = (int)((r + 1) % k), pred = (int)((r + k - 1) % k);
+    auto& ar = e->arenas[0];
+    NC(ncclGroupStart());
+    if (snd.el_hi > snd.el_lo)
+        NC(ncclSend(ar.codes + snd.el_lo, snd.el_hi - snd.el_lo, ncclUint8, succ, e->comm, e->s_comm));
+    NC(ncclSend(ar.cbs + (size_t)snd.slot0 * kBuckets, (size_t)snd.nseg * kBuckets, ncclFloat32, succ, e->comm,
+                e->s_comm));
+    if (rcv.el_hi > rcv.el_lo)
+        NC(ncclRecv(ar.codes + rcv.el_lo, rcv.el_hi - rcv.el_lo, ncclUint8, pred, e->comm, e->s_comm));
+    NC(ncclRecv(ar.cbs + (size_t)rcv.slot0 * kBuckets, (size_t)rcv.nseg * kBuckets, ncclFloat32, pred, e->comm,
+                e->s_comm));
+    NC(ncclGroupEnd());
+    return EMESH_OK;
+}
+
+int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, float* buf, float* local_out, float* out,
+             float lr, float mom) {
+    const uint32_t k = e->k, r = e->rank;
+    const bool pg = B != nullptr;
+    auto& ar = e->arenas[0];
+    cudaStream_t sc = e->s_comp, sm = e->s_comm;
+    const auto& P = e->plan.batches;
+    const uint32_t W = (uint32_t)P[0].size();
+    for (uint32_t c = 1; c < k; ++c)
+        if (P[c].size() != W) return fail(EMESH_ECONFIG, "ring chunks have unequal window counts");
+    // hop-0 payload
+    for (uint32_t j = 0; j < W; ++j) {
+        QuantIO io{pg ? kSrcAminusB : kSrcA, A, B, nullptr, nullptr, 1.f, ar.codes, ar.cbs, ar.stats};
+        TRY(launch_quant(P[r][j], e->ws, io, sc, &e->tr));
+        CU(cudaEventRecord(e->ev_send[j], sc));
+    }
+    // reduce-scatter (allreduce.hpp:411-426), window-pipelined
+    for (uint32_t s = 0; s + 1 < k; ++s) {
+        const uint32_t send_c = (r + k - s) % k, recv_c = (r + k - s - 1) % k;
+        for (uint32_t j = 0; j < W; ++j) {
+            CU(cudaStreamWaitEvent(sm, e->ev_send[j], 0));
+            TRY(xfer_window(e, P[send_c][j], P[recv_c][j]));
+            CU(cudaEventRecord(e->ev_recv[j], sm));
+            CU(cudaStreamWaitEvent(sc, e->ev_recv[j], 0));
+            QuantIO io{hop_src(pg, s, k), A, B, ar.codes, ar.cbs, (float)k, ar.codes, ar.cbs, ar.stats};
+            TRY(launch_quant(P[recv_c][j], e->ws, io, sc, &e->tr));
+            CU(cudaEventRecord(e->ev_send[j], sc));
+        }
+    }
+    // own chunk is final (allreduce.hpp:428-445): apply it while the
+    // all-gather (allreduce.hpp:446-464) forwards bytes verbatim
+    const uint32_t own = (r + 1) % k;
+    for (uint32_t j = 0; j < W; ++j) {
+        if (out) TRY(launch_apply(P[own][j], 0, ar.codes, ar.cbs, nullptr, nullptr, nullptr, out, 0.f, 0.f, sc, &e->tr));
+        else TRY(launch_apply(P[own][j], 1, ar.codes, ar.cbs, theta, buf, local_out, nullptr, lr, mom, sc, &e->tr));
+    }
+    for (uint32_t s = 0; s + 1 < k; ++s) {
+        const uint32_t send_c = (r + 1 + k - s) % k, recv_c = (r + k - s) % k;
+        for (uint32_t j = 0; j < W; ++j) {
+            if (s == 0) CU(cudaStreamWaitEvent(sm, e->ev_send[j], 0));
+            TRY(xfer_window(e, P[send_c][j], P[recv_c][j]));
+            CU(cudaEventRecord(e->ev_recv[j], sm));
+            CU(cudaStreamWaitEvent(sc, e->ev_recv[j], 0));
+            if (out) TRY(launch_apply(P[recv_c][j], 0, ar.codes, ar.cbs, nullptr, nullptr, nullptr, out, 0.f, 0.f, sc, &e->tr));
+            else TRY(launch_apply(P[recv_c][j], 1, ar.codes, ar.cbs, theta, buf, local_out, nullptr, lr, mom, sc, &e->tr));
+        }
+    }
+    return EMESH_OK;
+}
+
+int engine_enter(emesh_engine* e, cudaStream_t user) {
+    CU(cudaSetDevice(e->device));
+    CU(cudaEventRecord(e->ev_entry, user));
+    CU(cudaStreamWaitEvent(e->s_comp, e->ev_entry, 0));
+    CU(cudaStreamWaitEvent(e->s_comm, e->ev_entry, 0));
+    return EMESH_OK;
+}
+
+int engine_exit(emesh_engine* e, cudaStream_t user) {
+    CU(cudaEventRecord(e->ev_comm_done, e->s_comm));
+    CU(cudaStreamWaitEvent(e->s_comp, e->ev_comm_done, 0));
+    CU(cudaEventRecord(e->ev_done, e->s_comp));
+    CU(cudaStreamWaitEvent(user, e->ev_done, 0));
+    return EMESH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int emesh_nccl_unique_id(uint8_t out[128]) {
+    ncclUniqueId id;
+    NC(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+    return EMESH_OK;
+}
+
+int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
+    if (!cfg || !out) return fail(EMESH_ECONFIG, "null argument");
+    if (cfg->k == 0) return fail(EMESH_ESHAPE, "empty ring");
+    const uint32_t S = cfg->pipeline_subchunks ? cfg->pipeline_subchunks : 4;
+    const bool virt = cfg->virtual_workers > 1 || cfg->k == 1;
+    if (cfg->virtual_workers > 1 && cfg->virtual_workers != cfg->k)
+        return fail(EMESH_ECONFIG, "virtual_workers must be 0/1 or equal k");
+    if (!virt && cfg->rank >= cfg->k) return fail(EMESH_ECONFIG, "rank out of range");
+    if (!virt && !cfg->nccl_id) return fail(EMESH_ECONFIG, "NCCL mode needs nccl_id");
+    auto* e = new emesh_engine();
+    e->cfg = *cfg;
+    e->k = cfg->k;
+    e->rank = virt ? 0 : cfg->rank;
+    e->virt = virt;
+    e->workers = virt ? cfg->k : 1;
+    if (cfg->device >= 0) e->device = cfg->device;
+    else cudaGetDevice(&e->device);
+    auto bail = [&](int rc) { emesh_engine_destroy(e); return rc; };
+    if (cudaSetDevice(e->device) != cudaSuccess) return bail(fail(EMESH_ECUDA, "cudaSetDevice"));
+    uint64_t window = cfg->window_elems ? cfg->window_elems : (uint64_t)16 << 20;
+    e->plan = make_ring_plan(cfg->n, cfg->k, S, window);
+    e->windows = (uint32_t)e->plan.batches[0].size();
+    int rc = e->plan.upload();
+    if (rc) return bail(rc);
+    if (e->k > 1 && (rc = engine_alloc(e))) return bail(rc);
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    if (cudaStreamCreateWithPriority(&e->s_comp, cudaStreamNonBlocking, lo_prio) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&e->s_comm, cudaStreamNonBlocking, hi_prio) != cudaSuccess)
+        return bail(fail(EMESH_ECUDA, "stream create"));
+    cudaEventCreateWithFlags(&e->ev_entry, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&e->ev_done, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&e->ev_comm_done, cudaEventDisableTiming);
+    e->ev_send.resize(e->windows);
+    e->ev_recv.resize(e->windows);
+    for (uint32_t j = 0; j < e->windows; ++j) {
+        cudaEventCreateWithFlags(&e->ev_send[j], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&e->ev_recv[j], cudaEventDisableTiming);
+    }
+    if (!virt && e->k > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, cfg->nccl_id, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&e->comm, (int)e->k, id, (int)e->rank);
+        if (r != ncclSuccess) return bail(fail(EMESH_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+    }
+    *out = e;
+    return EMESH_OK;
+}
+
+int emesh_engine_destroy(emesh_engine* e) {
+    if (!e) return EMESH_OK;
+    cudaSetDevice(e->device);
+    if (e->s_comp) cudaStreamSynchronize(e->s_comp);
+    if (e->s_comm) cudaStreamSynchronize(e->s_comm);
+    if (e->comm) ncclCommDestroy(e->comm);
+    for (auto& a : e->arenas) { cudaFree(a.codes); cudaFree(a.cbs); cudaFree(a.stats); }
+    for (auto* p : e->h_theta) cudaFree(p);
+    for (auto* p : e->h_local) cudaFree(p);
+    for (auto* p : e->h_buf) cudaFree(p);
+    e->ws.release();
+    e->plan.release();
+    e->tr.release();
+    for (auto ev : e->ev_send) cudaEventDestroy(ev);
+    for (auto ev : e->ev_recv) cudaEventDestroy(ev);
+    if (e->ev_entry) cudaEventDestroy(e->ev_entry);
+    if (e->ev_done) cudaEventDestroy(e->ev_done);
+    if (e->ev_comm_done) cudaEventDestroy(e->ev_comm_done);
+    if (e->s_comp) cudaStreamDestroy(e->s_comp);
+    if (e->s_comm) cudaStreamDestroy(e->s_comm);
+    delete e;
+    return EMESH_OK;
+}
+
+uint64_t emesh_engine_segments(const emesh_engine* e, uint64_t* lo, uint64_t* len) {
+    const auto& s = e->plan.segs;
+    for (size_t i = 0; i < s.size(); ++i) {
+        if (lo) lo[i] = s[i].lo;
+        if (len) len[i] = s[i].len;
+    }
+    return s.size();
+}
+
+uint64_t emesh_engine_launches(const emesh_engine* e) { return e->tr.launches; }
+
+int emesh_engine_profile(emesh_engine* e, int enable) {
+    CU(cudaSetDevice(e->device));
+    CU(cudaStreamSynchronize(e->s_comp));
+    e->tr.reset();
+    e->tr.prof = enable != 0;
+    return EMESH_OK;
+}
+
+int emesh_engine_profile_read(emesh_engine* e, uint32_t kind, uint64_t* count, double* ms, double* bytes) {
+    CU(cudaSetDevice(e->device));
+    CU(cudaStreamSynchronize(e->s_comp));
+    CU(cudaStreamSynchronize(e->s_comm));
+    uint64_t c = 0;
+    double t = 0, b = 0;
+    for (const auto& r : e->tr.recs) {
+        if ((uint32_t)r.kind != kind) continue;
+        float x = 0.f;
+        CU(cudaEventElapsedTime(&x, r.a, r.b));
+        ++c;
+        t += x;
+        b += r.bytes;
+    }
+    if (count) *count = c;
+    if (ms) *ms = t;
+    if (bytes) *bytes = b;
+    return EMESH_OK;
+}
+
+int emesh_engine_ring_allreduce(emesh_engine* e, const float* const* input, float* const* output,
+                                emesh_stream_t stream) {
+    cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
+    for (uint32_t w = 0; w < e->workers; ++w)
+        if (!aligned16(input[w]) || !aligned16(output[w])) return fail(EMESH_ESHAPE, "arenas must be 16-byte aligned");
+    TRY(engine_enter(e, user));
+    if (e->k == 1) {
+        // allreduce.hpp:319: identity, zero communication
+        CU(cudaMemcpyAsync(output[0], input[0], e->plan.n * sizeof(float), cudaMemcpyDeviceToDevice, e->s_comp));
+    } else if (e->virt) {
+        TRY(run_virtual(e, input, nullptr, nullptr, nullptr, nullptr, output, 0.f, 0.f));
+    } else {
+        TRY(run_nccl(e, input[0], nullptr, nullptr, nullptr, nullptr, output[0], 0.f, 0.f));
+    }
+    return engine_exit(e, user);
+}
+
+int emesh_engine_outer_sync(emesh_engine* e, float* const* theta_g, float* const* theta_l, float* const* buf,
+                            float lr, float mom, int write_local, emesh_stream_t stream) {
+    cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
+    for (uint32_t w = 0; w < e->workers; ++w)
+        if (!aligned16(theta_g[w]) || !aligned16(theta_l[w]) || !aligned16(buf[w]))
+            return fail(EMESH_ESHAPE, "arenas must be 16-byte aligned");
+    TRY(engine_enter(e, user));
+    if (e->k == 1) {
+        // k == 1: avg = delta exactly (allreduce.hpp:319); PG + Nesterov fused, 20 B/param
+        const uint64_t n = e->plan.n;
+        cudaEvent_t e0 = e->tr.prof ? e->tr.ev(e->s_comp) : nullptr;
+        k_nesterov_f32<<<flat_grid(n), kThreads, 0, e->s_comp>>>(theta_g[0], nullptr, theta_l[0], buf[0],
+                                                                 write_local ? theta_l[0] : nullptr, n, lr, mom);
+        if (e->tr.prof)
+            e->tr.recs.push_back({kProfFusedK1, e0, e->tr.ev(e->s_comp), (double)n * (write_local ? 24.0 : 20.0)});
+        e->tr.launches += 1;
+        CU(cudaGetLastError());
+    } else if (e->virt) {
+        TRY(run_virtual(e, (const float* const*)theta_g, (const float* const*)theta_l, theta_g, buf,
+                        write_local ? theta_l : nullptr, nullptr, lr, mom));
+    } else {
+        TRY(run_nccl(e, theta_g[0], theta_l[0], theta_g[0], buf[0], write_local ? theta_l[0] : nullptr, nullptr, lr,
+                     mom));
+    }
+    return engine_exit(e, user);
+}
+
+int emesh_engine_outer_sync_host(emesh_engine* e, float* const* theta_g, float* const* theta_l, float* const* buf,
+                                 float lr, float mom, int write_local) {
+    CU(cudaSetDevice(e->device));
+    const uint64_t n = e->plan.n;
+    const size_t bytes = n * sizeof(float);
+    if (e->h_theta.empty()) {
+        e->h_theta.assign(e->workers, nullptr);
+        e->h_local.assign(e->workers, nullptr);
+        e->h_buf.assign(e->workers, nullptr);
+        for (uint32_t w = 0; w < e->workers; ++w) {
+            CU(cudaMalloc(&e->h_theta[w], bytes + 16));
+            CU(cudaMalloc(&e->h_local[w], bytes + 16));
+            CU(cudaMalloc(&e->h_buf[w], bytes + 16));
+        }
+    }
+    cudaStream_t st = e->s_comp;
+    for (uint32_t w = 0; w < e->workers; ++w) {
+        CU(cudaMemcpyAsync(e->h_theta[w], theta_g[w], bytes, cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(e->h_local[w], theta_l[w], bytes, cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(e->h_buf[w], buf[w], bytes, cudaMemcpyHostToDevice, st));
+    }
+    TRY(emesh_engine_outer_sync(e, e->h_theta.data(), e->h_local.data(), e->h_buf.data(), lr, mom, write_local,
+                                reinterpret_cast<emesh_stream_t>(st)));
+    for (uint32_t w = 0; w < e->workers; ++w) {
+        CU(cudaMemcpyAsync(theta_g[w], e->h_theta[w], bytes, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(buf[w], e->h_buf[w], bytes, cudaMemcpyDeviceToHost, st));
+        if (write_local) CU(cudaMemcpyAsync(theta_l[w], e->h_local[w], bytes, cudaMemcpyDeviceToHost, st));
+    }
+    CU(cudaStreamSynchronize(st));
+    return emesh_engine_check(e);
+}
+
+int emesh_engine_check(emesh_engine* e) {
+    CU(cudaSetDevice(e->device));
+    CU(cudaStreamSynchronize(e->s_comp));
+    CU(cudaStreamSynchronize(e->s_comm));
+    if (!e->ws.err) return EMESH_OK;
+    uint32_t v = 0;
+    CU(cudaMemcpy(&v, e->ws.err, sizeof v, cudaMemcpyDeviceToHost));
+    if (v) {
+        CU(cudaMemset(e->ws.err, 0, sizeof(uint32_t)));
+        return fail(EMESH_ENUMERIC, "quantize: non-finite input");
+    }
+    return EMESH_OK;
+}
+
+int emesh_engine_payload(emesh_engine* e, uint32_t worker, const uint8_t** codes, const float** cbs,
+                         const double** stats, uint64_t* stride) {
+    if (worker >= e->arenas.size()) return fail(EMESH_ECONFIG, "no such local worker");
+    if (codes) *codes = e->arenas[worker].codes;
+    if (cbs) *cbs = e->arenas[worker].cbs;
+    if (stats) *stats = reinterpret_cast<const double*>(e->arenas[worker].stats);
+    if (stride) *stride = sizeof(SegStat);
+    return EMESH_OK;
+}
+
+int emesh_engine_payload_host(emesh_engine* e, uint32_t worker, uint8_t* codes, float* cbs, double* stats) {
+    if (worker >= e->arenas.size()) return fail(EMESH_ECONFIG, "no such local worker");
+    TRY(emesh_engine_check(e));
+    const auto& a = e->arenas[worker];
+    const size_t nseg = e->plan.segs.size();
+    if (codes && e->plan.n) CU(cudaMemcpy(codes, a.codes, e->plan.n, cudaMemcpyDeviceToHost));
+    if (cbs) CU(cudaMemcpy(cbs, a.cbs, nseg * kBuckets * sizeof(float), cudaMemcpyDeviceToHost));
+    if (stats)
+        CU(cudaMemcpy2D(stats, 4 * sizeof(double), a.stats, sizeof(SegStat), 4 * sizeof(double), nseg,
+                        cudaMemcpyDeviceToHost));
+    return EMESH_OK;
+}
+
+}  // extern "C"

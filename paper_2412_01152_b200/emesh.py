@@ -1,0 +1,518 @@
+"""Python mirror of the reference's `emesh` API for the outer-sync hot path.
+
+Same names, argument meaning and error behaviour as the C++ reference
+(proj/include/emesh/{quant,optim,allreduce,tensor,errors}.hpp), backed by
+the sm_100a kernels in libemesh_b200.so through the C ABI
+(include/emesh_b200.h). Tensors are CUDA ``torch.Tensor`` s — torch is the
+device-memory / stream plumbing, never the compute path. There is no CPU
+fallback: without the built library or a GPU every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _capi
+
+# ---------------------------------------------------------------- errors.hpp:10-73
+
+
+class Error(RuntimeError):
+    """emesh::Error"""
+
+
+class ShapeError(Error):
+    """emesh::ShapeError"""
+
+
+class NumericError(Error):
+    """emesh::NumericError"""
+
+
+class DecodeError(Error):
+    """emesh::DecodeError"""
+
+
+class ConfigError(Error):
+    """emesh::ConfigError"""
+
+
+class RingFailureError(Error):
+    """emesh::RingFailureError"""
+
+
+class FatalError(Error):
+    """emesh::FatalError"""
+
+
+class CudaError(FatalError):
+    pass
+
+
+class NcclError(RingFailureError):
+    pass
+
+
+_ERRS = {
+    _capi.ESHAPE: ShapeError, _capi.ENUMERIC: NumericError, _capi.EDECODE: DecodeError,
+    _capi.ECUDA: CudaError, _capi.ENCCL: NcclError, _capi.ERING: RingFailureError,
+    _capi.ECONFIG: ConfigError,
+}
+
+
+def _check(rc: int) -> None:
+    if rc != _capi.OK:
+        raise _ERRS.get(rc, Error)(_capi.last_error())
+
+
+def _stream(stream=None) -> C.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dev_f32(t: torch.Tensor, what: str) -> torch.Tensor:
+    if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+        raise ShapeError(f"{what}: expected a contiguous CUDA float32 tensor")
+    return t
+
+
+def _aligned_empty(n: int, dtype, device) -> torch.Tensor:
+    """Fresh allocations are 256-B aligned by the caching allocator; pad by 16
+    so float4 reads of the last slot stay inside the allocation."""
+    itemsize = torch.empty((), dtype=dtype).element_size()
+    pad = max(1, 16 // itemsize)
+    return torch.empty(n + pad, dtype=dtype, device=device)[:n]
+
+
+# ---------------------------------------------------------------- quant.hpp:19-131
+
+BUCKETS = 256
+
+
+@dataclass
+class QuantChunk:
+    """quant.hpp:19-26 — ``codebook`` (256 f32, nondecreasing) + ``indices`` (u8)."""
+
+    codebook: torch.Tensor
+    indices: torch.Tensor
+    stats: Optional[torch.Tensor] = None  # {mu, sigma, lo, width} (fp64), diagnostic
+
+    def count(self) -> int:
+        return int(self.indices.numel())
+
+
+def quantize(values: torch.Tensor, stream=None) -> QuantChunk:
+    """quant.hpp:28 ``quantize(std::span<const float>)``. Raises ShapeError on
+    an empty chunk, NumericError on non-finite input (synchronous, like the
+    reference)."""
+    _dev_f32(values, "quantize")
+    n = values.numel()
+    if n == 0:
+        raise ShapeError("quantize: empty chunk")
+    if values.data_ptr() % 16:
+        values = values.clone()
+    dev = values.device
+    codes = _aligned_empty(n, torch.uint8, dev)
+    cb = torch.empty(BUCKETS, dtype=torch.float32, device=dev)
+    st = torch.empty(4, dtype=torch.float64, device=dev)
+    _check(_capi.lib().emesh_quantize(values.data_ptr(), n, codes.data_ptr(), cb.data_ptr(), st.data_ptr(),
+                                      _stream(stream)))
+    return QuantChunk(cb, codes, st)
+
+
+def quantize_segments(values: torch.Tensor, seg_lo: Sequence[int], seg_len: Sequence[int], stream=None):
+    """Batched quantize over a segment table (allreduce.hpp:326-336): returns
+    (codes [n], codebooks [nseg,256], stats [nseg,4]). Asynchronous; call
+    ``codec_check()`` for the NumericError of a non-finite segment."""
+    _dev_f32(values, "quantize_segments")
+    lo = np.ascontiguousarray(seg_lo, np.uint64)
+    ln = np.ascontiguousarray(seg_len, np.uint64)
+    if np.any(ln == 0):
+        raise ShapeError("quantize: empty chunk")
+    dev = values.device
+    codes = _aligned_empty(values.numel(), torch.uint8, dev)
+    cbs = torch.empty((len(lo), BUCKETS), dtype=torch.float32, device=dev)
+    st = torch.empty((len(lo), 4), dtype=torch.float64, device=dev)
+    P = C.POINTER(C.c_uint64)
+    _check(_capi.lib().emesh_quantize_segments(values.data_ptr(), lo.ctypes.data_as(P), ln.ctypes.data_as(P), len(lo),
+                                               codes.data_ptr(), cbs.data_ptr(), st.data_ptr(), _stream(stream)))
+    return codes, cbs, st
+
+
+def codec_check(stream=None) -> None:
+    _check(_capi.lib().emesh_codec_check(_stream(stream)))
+
+
+def dequantize_into(chunk: QuantChunk, out: torch.Tensor, stream=None) -> None:
+    """quant.hpp:89 ``dequantize_into``."""
+    _dev_f32(out, "dequantize")
+    if out.numel() != chunk.count():
+        raise ShapeError("dequantize: output size mismatch")
+    if chunk.codebook.numel() != BUCKETS:
+        raise ShapeError("dequantize: malformed codebook")
+    if chunk.count() == 0:
+        return
+    codes = chunk.indices
+    if codes.data_ptr() % 4 or out.data_ptr() % 16:
+        tmp = _aligned_empty(out.numel(), torch.float32, out.device)
+        c2 = _aligned_empty(codes.numel(), torch.uint8, out.device)
+        c2.copy_(codes)
+        _check(_capi.lib().emesh_dequantize(c2.data_ptr(), chunk.codebook.data_ptr(), chunk.count(), tmp.data_ptr(),
+                                            _stream(stream)))
+        out.copy_(tmp)
+        return
+    _check(_capi.lib().emesh_dequantize(codes.data_ptr(), chunk.codebook.contiguous().data_ptr(), chunk.count(),
+                                        out.data_ptr(), _stream(stream)))
+
+
+def dequantize(chunk: QuantChunk, stream=None) -> torch.Tensor:
+    """quant.hpp:96 ``dequantize``."""
+    out = _aligned_empty(chunk.count(), torch.float32, chunk.indices.device)
+    dequantize_into(chunk, out, stream)
+    return out
+
+
+def encode_quant_chunk(chunk: QuantChunk) -> bytes:
+    """quant.hpp:102-115 wire layout: u32 LE count, 256 f32 LE, count u8."""
+    if chunk.codebook.numel() != BUCKETS:
+        raise ShapeError("encode_quant_chunk: malformed codebook")
+    codes = np.ascontiguousarray(chunk.indices.cpu().numpy(), np.uint8)
+    cb = np.ascontiguousarray(chunk.codebook.cpu().numpy(), np.float32)
+    out = np.empty(4 + 4 * BUCKETS + len(codes), np.uint8)
+    n = _capi.lib().emesh_encode_quant_chunk(codes.ctypes.data, cb.ctypes.data, len(codes), out.ctypes.data)
+    return out[:n].tobytes()
+
+
+def decode_quant_chunk(buf: bytes, device="cuda") -> QuantChunk:
+    """quant.hpp:117-131; raises DecodeError like the reference."""
+    b = np.frombuffer(bytes(buf), np.uint8)
+    codes = np.empty(max(len(b), 1), np.uint8)
+    cb = np.empty(BUCKETS, np.float32)
+    cnt = C.c_uint32(0)
+    _check(_capi.lib().emesh_decode_quant_chunk(b.ctypes.data if len(b) else None, len(b), codes.ctypes.data,
+                                                cb.ctypes.data, C.byref(cnt)))
+    return QuantChunk(torch.from_numpy(cb).to(device), torch.from_numpy(codes[: cnt.value].copy()).to(device))
+
+
+# ---------------------------------------------------------------- tensor.hpp:54-109
+
+
+class ModelParams:
+    """tensor.hpp:54-109, B200 layout: ONE flat fp32 arena in HBM in canonical
+    order with per-tensor views, so ``flatten()`` is free (trainer.hpp:356)."""
+
+    def __init__(self, shapes: Dict[str, Sequence[int]] | List, device="cuda", arena: Optional[torch.Tensor] = None):
+        items = list(shapes.items()) if isinstance(shapes, dict) else list(shapes)
+        self.names = [nm for nm, _ in items]
+        if len(set(self.names)) != len(self.names):
+            raise ShapeError("duplicate parameter name")
+        self.shapes = [tuple(int(e) for e in sh) for _, sh in items]
+        for sh in self.shapes:
+            if any(e == 0 for e in sh):
+                raise ShapeError("zero extent in tensor shape")
+        self.sizes = [int(np.prod(sh)) if sh else 1 for sh in self.shapes]
+        n = sum(self.sizes)
+        self.arena = arena if arena is not None else _aligned_empty(n, torch.float32, device).zero_()
+        if self.arena.numel() != n:
+            raise ShapeError("flat buffer size mismatch")
+
+    def element_count(self) -> int:
+        return self.arena.numel()
+
+    def same_shapes(self, other: "ModelParams") -> bool:
+        return self.names == other.names and self.shapes == other.shapes
+
+    def entries(self):
+        off = 0
+        for nm, sh, sz in zip(self.names, self.shapes, self.sizes):
+            yield nm, self.arena[off: off + sz].view(sh)
+            off += sz
+
+    def at(self, name: str) -> torch.Tensor:
+        for nm, t in self.entries():
+            if nm == name:
+                return t
+        raise ShapeError(f"no parameter named {name}")
+
+    def flatten(self) -> torch.Tensor:
+        return self.arena
+
+    def unflatten(self, flat: torch.Tensor) -> None:
+        if flat.numel() != self.element_count():
+            raise ShapeError("flat buffer size mismatch")
+        if flat.data_ptr() != self.arena.data_ptr():
+            self.arena.copy_(flat)
+
+    def zeros_like(self) -> "ModelParams":
+        return ModelParams(list(zip(self.names, self.shapes)), device=self.arena.device)
+
+    def clone(self) -> "ModelParams":
+        p = self.zeros_like()
+        p.arena.copy_(self.arena)
+        return p
+
+
+# ---------------------------------------------------------------- optim.hpp:12-132
+
+
+@dataclass
+class HyperParams:
+    """optim.hpp:12-33 (outer fields are the ones this path uses)."""
+
+    inner_lr: float = 7.5e-5
+    beta1: float = 0.9
+    beta2: float = 0.95
+    eps: float = 1e-8
+    weight_decay: float = 0.1
+    outer_lr: float = 0.7
+    outer_momentum: float = 0.9
+    warmup_steps: int = 1000
+    total_steps: int = 10000
+    cooldown_fraction: float = 0.2
+
+    def validate(self) -> None:
+        if not (0.0 <= self.beta1 < 1.0):
+            raise ConfigError("beta1 must be in [0,1)")
+        if not (0.0 <= self.beta2 < 1.0):
+            raise ConfigError("beta2 must be in [0,1)")
+        if not self.inner_lr > 0.0:
+            raise ConfigError("inner_lr must be > 0")
+        if not self.outer_lr > 0.0:
+            raise ConfigError("outer_lr must be > 0")
+        if not (0.0 <= self.cooldown_fraction < 1.0):
+            raise ConfigError("cooldown_fraction must be in [0,1)")
+        if self.total_steps < 1:
+            raise ConfigError("total_steps must be >= 1")
+
+
+@dataclass
+class NesterovState:
+    """optim.hpp:48-56"""
+
+    buffer: ModelParams
+
+    @staticmethod
+    def zeros_like(params: ModelParams) -> "NesterovState":
+        return NesterovState(params.zeros_like())
+
+
+def compute_pseudo_gradient(theta_prev: ModelParams, theta_local: ModelParams, stream=None) -> ModelParams:
+    """optim.hpp:99 — delta = theta_prev - theta_local (fp32, canonical order)."""
+    if not theta_prev.same_shapes(theta_local):
+        raise ShapeError("compute_pseudo_gradient: shape mismatch")
+    delta = theta_prev.zeros_like()
+    _check(_capi.lib().emesh_pseudo_gradient(theta_prev.arena.data_ptr(), theta_local.arena.data_ptr(),
+                                             delta.arena.data_ptr(), delta.element_count(), _stream(stream)))
+    return delta
+
+
+def nesterov_outer_step(params: ModelParams, avg_delta: ModelParams, state: NesterovState, hp: HyperParams,
+                        stream=None) -> None:
+    """optim.hpp:116 — b = mu*b + d; theta -= lr*(d + mu*b), in place."""
+    if not params.same_shapes(avg_delta):
+        raise ShapeError("nesterov_outer_step: shape mismatch")
+    if not params.same_shapes(state.buffer):
+        raise ShapeError("nesterov_outer_step: momentum buffer shape mismatch")
+    _check(_capi.lib().emesh_nesterov_outer_step(params.arena.data_ptr(), avg_delta.arena.data_ptr(),
+                                                 state.buffer.arena.data_ptr(), params.element_count(),
+                                                 hp.outer_lr, hp.outer_momentum, _stream(stream)))
+
+
+# ---------------------------------------------------------------- allreduce.hpp:21-62
+
+
+class ReduceMode(enum.IntEnum):
+    fp32 = 0
+    int8 = 1
+
+
+@dataclass
+class RingPlan:
+    """allreduce.hpp:25-45 (NVSwitch is uniform: ring order = rank order)."""
+
+    job_id: int = 0
+    epoch: int = 0
+    order: List[str] = field(default_factory=list)
+    self_index: int = 0
+
+
+@dataclass
+class ReduceJob:
+    """allreduce.hpp:49-53 — the input is preserved for retries."""
+
+    id: int
+    input: torch.Tensor
+    mode: ReduceMode = ReduceMode.int8
+
+
+@dataclass
+class ReduceOptions:
+    """allreduce.hpp:55-62; pipeline_subchunks defines the segmentation."""
+
+    pipeline_subchunks: int = 4
+    pipelined: bool = True
+    codec_sec_per_element: float = 0.0
+    step_timeout: float = 30.0
+    max_retries: int = 5
+    evict_wait: float = 20.0
+
+
+def segment_table(n: int, k: int, S: int):
+    """allreduce.hpp:107-118 + :326-336, chunk-major: list of (lo, len)."""
+    out = []
+    base, rem = divmod(n, k)
+    off = 0
+    for c in range(k):
+        ln = base + (1 if c < rem else 0)
+        ns = 1 if ln == 0 else min(S, ln)
+        b2, r2 = divmod(ln, ns)
+        o2 = off
+        for j in range(ns):
+            l2 = b2 + (1 if j < r2 else 0)
+            out.append((o2, l2))
+            o2 += l2
+        off += ln
+    return out
+
+
+class RingEngine:
+    """One ring position (NCCL mode: ``rank`` of ``k`` processes, one GPU each)
+    or all ``k`` DiLoCo workers on this GPU (``virtual=True``). Owns every
+    device buffer the round needs; nothing is allocated per round."""
+
+    def __init__(self, n: int, k: int, rank: int = 0, opts: Optional[ReduceOptions] = None, virtual: bool = False,
+                 nccl_id: Optional[bytes] = None, window_elems: int = 0, device: Optional[int] = None):
+        opts = opts or ReduceOptions()
+        if opts.pipeline_subchunks < 1:
+            raise ConfigError("pipeline_subchunks must be >= 1")
+        self.n, self.k, self.rank = int(n), int(k), int(rank)
+        self.S = int(opts.pipeline_subchunks)
+        self.virtual = bool(virtual) or k == 1
+        self.workers = k if (virtual and k > 1) else 1
+        self._idbuf = None
+        cfg = _capi.EngineConfig()
+        cfg.n, cfg.k, cfg.rank = self.n, self.k, self.rank
+        cfg.pipeline_subchunks = self.S
+        cfg.virtual_workers = k if (virtual and k > 1) else 0
+        cfg.window_elems = int(window_elems)
+        if nccl_id is not None:
+            self._idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+            cfg.nccl_id = C.cast(self._idbuf, C.c_void_p)
+        cfg.device = torch.cuda.current_device() if device is None else int(device)
+        h = C.c_void_p()
+        _check(_capi.lib().emesh_engine_create(C.byref(cfg), C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(_capi.lib().emesh_nccl_unique_id(buf))
+        return buf.raw
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _capi.lib().emesh_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def segments(self):
+        cnt = _capi.lib().emesh_engine_segments(self._h, None, None)
+        lo = np.empty(cnt, np.uint64)
+        ln = np.empty(cnt, np.uint64)
+        _capi.lib().emesh_engine_segments(self._h, lo.ctypes.data, ln.ctypes.data)
+        return lo, ln
+
+    def launches(self) -> int:
+        return int(_capi.lib().emesh_engine_launches(self._h))
+
+    PROFILE_KINDS = ("k_stats", "k_bin", "quant_pg", "quant_hop", "quant_final", "quant_plain",
+                     "dequant_nesterov", "dequantize", "fused_pg_nesterov_k1")
+
+    def profile(self, enable: bool = True) -> None:
+        """Per-kernel CUDA-event timing on the engine's launching stream."""
+        _check(_capi.lib().emesh_engine_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        out = {}
+        for i, name in enumerate(self.PROFILE_KINDS):
+            c, ms, by = C.c_uint64(), C.c_double(), C.c_double()
+            _check(_capi.lib().emesh_engine_profile_read(self._h, i, C.byref(c), C.byref(ms), C.byref(by)))
+            if c.value:
+                out[name] = {"launches": c.value, "ms": ms.value, "alg_bytes": by.value}
+        return out
+
+    def _ptrs(self, ts: Sequence[torch.Tensor], what: str):
+        if len(ts) != self.workers:
+            raise ShapeError(f"{what}: expected {self.workers} worker tensors")
+        for t in ts:
+            _dev_f32(t, what)
+            if t.numel() != self.n:
+                raise ShapeError(f"{what}: flat buffer size mismatch")
+        return _capi.ptr_array([t.data_ptr() for t in ts])
+
+    def ring_allreduce(self, inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor], stream=None) -> None:
+        """allreduce.hpp:314 (ReduceMode::int8), stream-ordered."""
+        _check(_capi.lib().emesh_engine_ring_allreduce(self._h, self._ptrs(inputs, "input"),
+                                                       self._ptrs(outputs, "output"), _stream(stream)))
+
+    def outer_sync(self, theta_g: Sequence[torch.Tensor], theta_l: Sequence[torch.Tensor],
+                   momentum: Sequence[torch.Tensor], hp: Optional[HyperParams] = None, write_local: bool = True,
+                   stream=None) -> None:
+        """trainer.hpp:355-382: PG -> int8 ring all-reduce -> Nesterov, in place."""
+        hp = hp or HyperParams()
+        _check(_capi.lib().emesh_engine_outer_sync(self._h, self._ptrs(theta_g, "theta_g"),
+                                                   self._ptrs(theta_l, "theta_l"), self._ptrs(momentum, "momentum"),
+                                                   hp.outer_lr, hp.outer_momentum, 1 if write_local else 0,
+                                                   _stream(stream)))
+
+    def outer_sync_host(self, theta_g, theta_l, momentum, hp: Optional[HyperParams] = None,
+                        write_local: bool = True) -> None:
+        """Same round on HOST (ideally pinned) buffers: H2D, round, D2H."""
+        hp = hp or HyperParams()
+
+        def ptrs(ts):
+            if len(ts) != self.workers:
+                raise ShapeError("expected one host tensor per local worker")
+            for t in ts:
+                if t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous() or t.numel() != self.n:
+                    raise ShapeError("host buffers must be contiguous CPU float32 of length n")
+            return _capi.ptr_array([t.data_ptr() for t in ts])
+
+        _check(_capi.lib().emesh_engine_outer_sync_host(self._h, ptrs(theta_g), ptrs(theta_l), ptrs(momentum),
+                                                        hp.outer_lr, hp.outer_momentum, 1 if write_local else 0))
+
+    def check(self) -> None:
+        """Synchronize; raise NumericError if any quantize saw non-finite data."""
+        _check(_capi.lib().emesh_engine_check(self._h))
+
+    def payload(self, worker: int = 0):
+        """Host copies (codes u8[n], codebooks f32[nseg,256], stats f64[nseg,4]
+        = {mu, sigma, lo, width}) of a local worker's final payload arena."""
+        nseg = len(self.segments()[0])
+        codes = np.empty(max(self.n, 1), np.uint8)
+        cbs = np.empty((nseg, BUCKETS), np.float32)
+        stats = np.empty((nseg, 4), np.float64)
+        _check(_capi.lib().emesh_engine_payload_host(self._h, worker, codes.ctypes.data, cbs.ctypes.data,
+                                                     stats.ctypes.data))
+        return codes[: self.n], cbs, stats
+
+
+def ring_allreduce(engine: RingEngine, job: ReduceJob, opts: Optional[ReduceOptions] = None,
+                   stream=None) -> torch.Tensor:
+    """allreduce.hpp:314 ``ring_allreduce`` for this process's ring position:
+    returns the mean every rank decodes; ``job.input`` is untouched."""
+    if job.mode != ReduceMode.int8:
+        raise ConfigError("this engine implements ReduceMode::int8 (fp32 mode is the next row, SURVEY §8(f))")
+    out = _aligned_empty(engine.n, torch.float32, job.input.device)
+    engine.ring_allreduce([job.input], [out], stream)
+    return out

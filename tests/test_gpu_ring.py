@@ -1,0 +1,172 @@
+"""GPU parity of the int8 ring engine and the fused outer-sync round against
+the oracle restatement (transport-free ring_allreduce, allreduce.hpp:314-473)
+and the reference's own golden outputs (SimWorld ring, TCP outer sync)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda:0")
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+@pytest.fixture(scope="module")
+def E():
+    import paper_2412_01152_b200 as E
+    return E
+
+
+def run_virtual_allreduce(E, ins, S, window=0):
+    k, n = len(ins), len(ins[0])
+    eng = E.RingEngine(n, k, opts=E.ReduceOptions(pipeline_subchunks=S), virtual=True, window_elems=window)
+    tin = [T(a) for a in ins]
+    outs = [torch.empty(n + 4, dtype=torch.float32, device="cuda:0")[:n] for _ in range(k)]
+    eng.ring_allreduce(tin, outs)
+    eng.check()
+    res = [o.cpu().numpy() for o in outs]
+    for a, t in zip(ins, tin):  # ReduceJob.input is preserved (allreduce.hpp:47-48)
+        assert np.array_equal(bits(t.cpu().numpy()), bits(a))
+    return eng, res
+
+
+def test_ring_golden_reference_outputs(E, golden):
+    g = golden["ring_cases"]
+    keys = sorted({k.rsplit("/", 1)[0] for k in g.files if k.endswith("_int8/out")})
+    assert keys
+    for key in keys:
+        ins = list(g[f"{key}/inputs"])
+        S = int(key.split("_S")[1].split("_")[0])
+        eng, res = run_virtual_allreduce(E, ins, S)
+        for r in res:
+            assert np.array_equal(bits(r), bits(g[f"{key}/out"])), key
+        eng.close()
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 8])
+@pytest.mark.parametrize("n", [1, 5, 17, 4096, 100_003])
+def test_ring_vs_oracle(E, oracle, k, n):
+    ins = [oracle.uniform(n, 100 + n, i) for i in range(k)]
+    S = 4
+    want, codes, cbs, stats = oracle.ring_allreduce(ins, S, "int8", with_payloads=True)
+    eng, res = run_virtual_allreduce(E, ins, S)
+    for r in res:  # every worker decodes the owners' bytes -> bit-identical
+        assert np.array_equal(bits(r), bits(want))
+    # owners' final payloads: codes + codebooks bit-exact
+    lo, ln = eng.segments()
+    for c in range(k):
+        owner = (c + k - 1) % k
+        pc, pcb, pst = eng.payload(owner)
+        base, rem = divmod(n, k)
+        for i, (a, b) in enumerate(zip(lo, ln)):
+            a, b = int(a), int(b)
+            cstart = c * base + min(c, rem)
+            clen = base + (1 if c < rem else 0)
+            if b == 0 or not (cstart <= a < cstart + clen):
+                continue
+            assert np.array_equal(pc[a:a + b], codes[a:a + b]), (c, i)
+            assert np.array_equal(bits(pcb[i]), bits(cbs[i])), (c, i)
+    eng.close()
+
+
+@pytest.mark.parametrize("S", [1, 3, 16])
+def test_ring_subchunks_and_windows(E, oracle, S):
+    k, n = 4, 262_147
+    ins = [oracle.uniform(n, 5, i, 0, 0, 2.0 ** -8) for i in range(k)]
+    want = oracle.ring_allreduce(ins, S, "int8")
+    for window in (0, 1, 40_000):  # one segment per window / auto
+        eng, res = run_virtual_allreduce(E, ins, S, window)
+        assert np.array_equal(bits(res[0]), bits(want)), window
+        eng.close()
+
+
+def test_ring_constant_inputs_exact(E):
+    # test_allreduce.cpp:218-223
+    ins = [np.full(64, 2.5, np.float32) for _ in range(4)]
+    _, res = run_virtual_allreduce(E, ins, 4)
+    assert all((r == 2.5).all() for r in res)
+
+
+def test_ring_nonfinite_raises(E, oracle):
+    ins = [oracle.uniform(1000, 1, i) for i in range(2)]
+    ins[1][17] = np.nan
+    eng = E.RingEngine(1000, 2, virtual=True)
+    outs = [torch.empty(1000, dtype=torch.float32, device="cuda:0") for _ in range(2)]
+    eng.ring_allreduce([T(a) for a in ins], outs)
+    with pytest.raises(E.NumericError):
+        eng.check()
+    eng.check()  # consumed
+    eng.close()
+
+
+def test_outer_sync_golden_reference_round(E, golden):
+    g = golden["outer_sync_case"]
+    k, S = int(g["k"]), int(g["S"])
+    n = g["theta_g"].shape[0]
+    eng = E.RingEngine(n, k, opts=E.ReduceOptions(pipeline_subchunks=S), virtual=True)
+    tg = [T(g["theta_g"]) for _ in range(k)]
+    tl = [T(x) for x in g["theta_l"]]
+    tb = [T(g["buf"]) for _ in range(k)]
+    eng.outer_sync(tg, tl, tb, E.HyperParams(), write_local=True)
+    eng.check()
+    for w in range(k):
+        assert np.array_equal(bits(tg[w].cpu().numpy()), bits(g["theta_g_out"]))
+        assert np.array_equal(bits(tb[w].cpu().numpy()), bits(g["buf_out"]))
+        assert np.array_equal(bits(tl[w].cpu().numpy()), bits(g["theta_g_out"]))  # local = retained
+    eng.close()
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+def test_outer_sync_vs_oracle_two_rounds(E, oracle, k):
+    n, S = 300_007, 4
+    g0 = oracle.uniform(n, 3, 0)
+    b0 = np.zeros(n, np.float32)
+    eng = E.RingEngine(n, k, opts=E.ReduceOptions(pipeline_subchunks=S), virtual=(k > 1))
+    tg = [T(g0) for _ in range(k)]
+    tb = [T(b0) for _ in range(k)]
+    eg, eb = g0, b0
+    for rnd in range(2):  # round 2 exercises a non-zero momentum buffer
+        ls = [(eg - oracle.uniform(n, 3 + rnd, 1 + w, 0, 0, 2.0 ** -10)).astype(np.float32) for w in range(k)]
+        tl = [T(a) for a in ls]
+        eng.outer_sync(tg, tl, tb, E.HyperParams(), write_local=False)
+        eng.check()
+        eg, eb = oracle.outer_sync(eg, ls, eb, S, "int8", 0.7, 0.9)
+        for w in range(k):
+            assert np.array_equal(bits(tg[w].cpu().numpy()), bits(eg)), (rnd, w)
+            assert np.array_equal(bits(tb[w].cpu().numpy()), bits(eb)), (rnd, w)
+    eng.close()
+
+
+def test_outer_sync_host_api(E, oracle):
+    n, k, S = 100_000, 2, 4
+    g = oracle.uniform(n, 8, 0)
+    ls = [(g - oracle.uniform(n, 8, 1 + w, 0, 0, 2.0 ** -10)).astype(np.float32) for w in range(k)]
+    b = oracle.uniform(n, 8, 7, 0, 0, 1e-3)
+    eg, eb = oracle.outer_sync(g, ls, b, S, "int8", 0.7, 0.9)
+    eng = E.RingEngine(n, k, opts=E.ReduceOptions(pipeline_subchunks=S), virtual=True)
+    hg = [torch.from_numpy(g.copy()).pin_memory() for _ in range(k)]
+    hl = [torch.from_numpy(a.copy()).pin_memory() for a in ls]
+    hb = [torch.from_numpy(b.copy()).pin_memory() for _ in range(k)]
+    eng.outer_sync_host(hg, hl, hb, E.HyperParams(), write_local=True)
+    for w in range(k):
+        assert np.array_equal(bits(hg[w].numpy()), bits(eg))
+        assert np.array_equal(bits(hb[w].numpy()), bits(eb))
+        assert np.array_equal(bits(hl[w].numpy()), bits(eg))
+    eng.close()
+
+
+def test_full_size_properties_config1(E, oracle):
+    """Config 1 at full size (N=16,777,216, k=2, S=4): bit-exact vs the
+    oracle's hop-by-hop restatement, all workers identical."""
+    n, k, S = 16_777_216, 2, 4
+    ins = [oracle.uniform(n, 1, 1 + w, 0, 0, 2.0 ** -10) for w in range(k)]
+    want = oracle.ring_allreduce(ins, S, "int8")
+    _, res = run_virtual_allreduce(E, ins, S)
+    for r in res:
+        assert np.array_equal(bits(r), bits(want))
