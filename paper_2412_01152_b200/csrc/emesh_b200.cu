@@ -206,10 +206,8 @@ struct Workspace {
     float* scratch = nullptr;
     StatP* leaf_stat = nullptr;
     StatP* node_stat = nullptr;
-    double* leaf_sum = nullptr;
-    uint32_t* leaf_cnt = nullptr;
-    double* node_sum = nullptr;
-    uint32_t* node_cnt = nullptr;
+    HistP* leaf_hist = nullptr;
+    HistP* node_hist = nullptr;
     uint32_t* tree_cnt = nullptr;
     uint32_t* seg_flags = nullptr;
     uint32_t* err = nullptr;
@@ -239,18 +237,14 @@ struct Workspace {
             size_t c = 0;
             TRY(grow(leaf_stat, c, ctas, 1, false));
             c = 0;
-            TRY(grow(leaf_sum, c, ctas, kBuckets, false));
-            c = 0;
-            TRY(grow(leaf_cnt, c, ctas, kBuckets, false));
+            TRY(grow(leaf_hist, c, ctas, 1, false));
             cap_cta = std::max<size_t>(ctas, 1);
         }
         if (nodes > cap_nodes || !node_stat) {
             size_t c = 0;
             TRY(grow(node_stat, c, nodes, 1, false));
             c = 0;
-            TRY(grow(node_sum, c, nodes, kBuckets, false));
-            c = 0;
-            TRY(grow(node_cnt, c, nodes, kBuckets, false));
+            TRY(grow(node_hist, c, nodes, 1, false));
             c = 0;
             TRY(grow(tree_cnt, c, nodes, 2, true));
             cap_nodes = std::max<size_t>(nodes, 1);
@@ -263,8 +257,8 @@ struct Workspace {
         return EMESH_OK;
     }
     void release() {
-        cudaFree(scratch); cudaFree(leaf_stat); cudaFree(node_stat); cudaFree(leaf_sum); cudaFree(leaf_cnt);
-        cudaFree(node_sum); cudaFree(node_cnt); cudaFree(tree_cnt); cudaFree(seg_flags); cudaFree(err);
+        cudaFree(scratch); cudaFree(leaf_stat); cudaFree(node_stat); cudaFree(leaf_hist); cudaFree(node_hist);
+        cudaFree(tree_cnt); cudaFree(seg_flags); cudaFree(err);
         *this = Workspace();
     }
 };
@@ -345,16 +339,19 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     a.in_codes = io.in_codes;
     a.in_cb = io.in_cb;
     a.divisor = io.divisor;
+    {
+        int ex = 0;
+        const float m = std::frexp(io.divisor, &ex);
+        a.inv_divisor = (m == 0.5f) ? std::ldexp(1.0f, 1 - ex) : 0.f;  // exact reciprocal of a power of two
+    }
     a.scratch = ws.scratch;
     a.out_codes = io.out_codes;
     a.out_cb = io.out_cb;
     a.stats = io.stats;
     a.leaf_stat = ws.leaf_stat;
     a.node_stat = ws.node_stat;
-    a.leaf_sum = ws.leaf_sum;
-    a.leaf_cnt = ws.leaf_cnt;
-    a.node_sum = ws.node_sum;
-    a.node_cnt = ws.node_cnt;
+    a.leaf_hist = ws.leaf_hist;
+    a.node_hist = ws.node_hist;
     a.tree_cnt = ws.tree_cnt;
     a.nnodes = (uint32_t)ws.cap_nodes;
     a.seg_flags = ws.seg_flags;

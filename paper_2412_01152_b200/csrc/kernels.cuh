@@ -38,13 +38,31 @@ constexpr int kThreads = kWarps * 32;  // 256
 constexpr int kSlotsPerLane = 8;       // float4 slots per lane per unit
 constexpr int kUnitSlots = 32 * kSlotsPerLane;  // 256 float4 = 1024 elements
 
-// Per-segment statistics, written once by the finalizing warp of k_stats.
+// Exact fixed-point encoding of one bucket's members for the codebook sums:
+// r(x) = rint((x - base) * scale), a non-negative integer < 2^42 for every
+// fp32 x the bucket can hold. "Narrow" buckets (not touching zero) use
+// base = lower threshold and scale = 1/ulp, so r is exact; "wide" buckets
+// (at or near zero) use a quantum Q = 2^-41 of the bucket's magnitude and
+// base = -2^41 Q, i.e. r = x/Q + 2^41. In both cases base*scale is an exact
+// integer, so sum x = (sum r + cnt*base*scale) / scale. Integer sums are
+// associative: per-bucket sums are identical for any accumulation order, and
+// equal to the reference's sequential fp64 sum whenever that sum is exact
+// (quant.hpp:74) — always, for narrow buckets of fewer than 2^28 members.
+struct BucketParam {
+    double base;
+    double scale;  // 2^-e (power of two)
+};
+constexpr int kWideBiasBits = 41;
+
+// Per-segment statistics, written once by the root CTA of k_stats.
 struct SegStat {
     double mu, sigma, lo, width, hi;  // first four exported as {mu, sigma, lo, width}
     float lo_f, inv_w_f;
-    uint32_t flags;  // kFlagNonFinite | kFlagDegenerate
-    uint32_t pad;
+    float lo_up, hi_dn;  // x < lo <=> x < lo_up ; x > hi <=> x > hi_dn (fp32 x)
+    uint32_t flags;      // kFlagNonFinite | kFlagDegenerate
+    float margin;        // fp32 bucket estimate is exact when its fraction is in (margin, 1-margin)
     float thr[kBuckets];  // thr[j] = smallest fp32 x with code(x) >= j (j=1..255)
+    BucketParam bp[kBuckets];
 };
 constexpr uint32_t kFlagNonFinite = 1u;
 constexpr uint32_t kFlagDegenerate = 2u;  // sigma == 0 (quant.hpp:49-55)
@@ -96,6 +114,17 @@ enum : int {
 
 constexpr int kFan = 16;  // combine-tree fan-in
 
+// Bucket histogram partial of a tile / tree node: exact 128-bit sums of the
+// fixed-point codes r(x) of unclipped members, their counts, and the
+// clipped-low / clipped-high counts (xc = lo / hi, quant.hpp:66-67).
+struct HistP {
+    unsigned long long rlo[kBuckets];
+    unsigned long long rhi[kBuckets];
+    uint32_t cnt[kBuckets];
+    uint32_t clip[2];
+    uint32_t pad[2];
+};
+
 struct QuantArgs {
     const SegInfo* segs;
     const uint32_t* cta_seg;   // CTA -> batch-local segment
@@ -107,16 +136,15 @@ struct QuantArgs {
     const uint8_t* in_codes;
     const float* in_cb;
     float divisor;
+    float inv_divisor;         // 1/k when k is a power of two (exact), else 0
     float* scratch;            // x, float4-slot indexed from scratch_q0
     uint8_t* out_codes;
     float* out_cb;
     SegStat* stats;            // indexed by slot
     StatP* leaf_stat;          // [cta]
     StatP* node_stat;          // [node]
-    double* leaf_sum;          // [cta][256]
-    uint32_t* leaf_cnt;        // [cta][256]
-    double* node_sum;          // [node][256]
-    uint32_t* node_cnt;        // [node][256]
+    struct HistP* leaf_hist;   // [cta]
+    struct HistP* node_hist;   // [node]
     uint32_t* tree_cnt;        // [2][node]: k_stats, k_bin arrival counters
     uint32_t nnodes;
     uint32_t* seg_flags;       // [seg] non-finite bits (reset by the stats root)
@@ -208,9 +236,12 @@ __device__ __forceinline__ bool tree_arrive(TreeCursor& c, uint32_t* counters, u
     const uint32_t first = parent * kFan;
     const uint32_t nch = min((uint32_t)kFan, c.n - first);
     const uint32_t poff = c.level == 0 ? 0u : c.off + c.n;
-    __threadfence();
+    // partials written by any thread of the CTA happen-before the barrier;
+    // thread 0's gpu-scope fence (cumulative) then releases them all with
+    // its arrival, so only one thread pays for the fence.
     __syncthreads();
     if (threadIdx.x == 0) {
+        __threadfence();
         uint32_t* ctr = counters + node_base + poff + parent;
         const bool last = atomicAdd(ctr, 1u) == nch - 1;
         if (last) *ctr = 0;  // re-arm for the next launch (no other arrivals remain)
@@ -224,9 +255,64 @@ __device__ __forceinline__ bool tree_arrive(TreeCursor& c, uint32_t* counters, u
 }
 
 // ---------------------------------------------------------------------------
-// K_stats: fused producer (PG / hop dequant-add / divide) + moments. Writes x
-// to scratch (for k_bin) unless the source is a plain buffer. The combine
-// tree's root publishes SegStat (mu, sigma, lo, hi, width, threshold table).
+// K_stats: fused producer (PG / hop dequant-add / divide) + moments, one
+// pass: each lane accumulates s = sum x, d = sum (x-p), m2 = sum (x-p)^2 around
+// a pivot p (its first value), merged exactly up the warp / CTA / tree. Writes
+// x to scratch (for k_bin) unless the source is a plain buffer. The tree root
+// publishes SegStat: mu, sigma, lo, hi, width (quant.hpp:33-59), the exact
+// threshold table and the bucket fixed-point parameters.
+
+__device__ __forceinline__ StatP shfl_statp(const StatP& p, int src) {
+    StatP o;
+    o.s = __shfl_sync(0xffffffffu, p.s, src);
+    o.m2 = __shfl_sync(0xffffffffu, p.m2, src);
+    o.d = __shfl_sync(0xffffffffu, p.d, src);
+    o.piv = __shfl_sync(0xffffffffu, p.piv, src);
+    o.n = __shfl_sync(0xffffffffu, p.n, src);
+    return o;
+}
+
+// Fixed-order warp merge (lane i absorbs lane i+o): deterministic.
+__device__ __forceinline__ StatP warp_merge(StatP p) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const StatP q = shfl_statp(p, lane + o < 32 ? lane + o : lane);
+        if ((lane & (2 * o - 1)) == 0) p = statp_merge(p, q);
+    }
+    return shfl_statp(p, 0);
+}
+
+__device__ __forceinline__ int exponent_of(float f) {  // floor(log2|f|) for normal f; -127.. for subnormal
+    const uint32_t u = __float_as_uint(f) & 0x7fffffffu;
+    const int e = (int)(u >> 23);
+    if (e) return e - 127;
+    return u ? (31 - __clz(u)) - 149 : -150;
+}
+
+// Fixed-point parameters of bucket b whose fp32 members lie in [t0, t1).
+__device__ BucketParam bucket_param(float t0, float t1) {
+    BucketParam p;
+    p.base = (double)t0;
+    p.scale = 0.0;
+    if (!(t1 > t0)) return p;  // holds no fp32 value
+    const float last = key2f(f2key(t1) - 1);
+    if (t0 > 0.f || last < 0.f) {
+        // narrow: every member is a multiple of the ulp of the smallest magnitude
+        const float mn = t0 > 0.f ? t0 : last;
+        const int e = max(exponent_of(mn) - 23, -149);
+        const double span = ldexp(__dsub_rn((double)last, (double)t0), -e);
+        if (span < 2199023255552.0) {  // 2^41
+            p.scale = ldexp(1.0, -e);
+            return p;
+        }
+    }
+    const float mx = fmaxf(fabsf(t0), fabsf(last));
+    const int e = exponent_of(mx) + 1 - kWideBiasBits;  // |x| < 2^(e+41)
+    p.scale = ldexp(1.0, -e);
+    p.base = -ldexp(1.0, e + kWideBiasBits);
+    return p;
+}
 
 template <int SRC>
 __global__ void __launch_bounds__(kThreads, 3) k_stats(QuantArgs a) {
@@ -234,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stats(QuantArgs a) {
     __shared__ StatP wp[kWarps];
     __shared__ uint32_t s_flag;
     __shared__ double s_red[2];
+    __shared__ float s_thr[kBuckets + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t s = a.cta_seg[blockIdx.x];
     const SegInfo si = a.segs[s];
@@ -247,82 +334,108 @@ __global__ void __launch_bounds__(kThreads, 3) k_stats(QuantArgs a) {
         __syncthreads();
     }
 
-    float v[kSlotsPerLane][4];
-    double sum = 0.0;
-    uint32_t cnt = 0;
-    bool bad = false;
+    StatP p{0.0, 0.0, 0.0, 0.0, 0};
     if (u < si.nunits) {
+        const bool interior = qbase * 4 >= si.lo && (qbase + kUnitSlots) * 4 <= hiel;  // warp-uniform
+        double sum0 = 0.0, sum1 = 0.0, d0 = 0.0, d1 = 0.0, q0 = 0.0, q1 = 0.0;
+        double piv = 0.0;
+        uint32_t cnt = 0;
+        bool have_piv = false;
+        constexpr int kHalf = kSlotsPerLane / 2;
 #pragma unroll
-        for (int j = 0; j < kSlotsPerLane; ++j) {
-            const uint64_t q = qbase + (uint64_t)j * 32 + lane;
-            const uint64_t e0 = q * 4;
+        for (int h = 0; h < 2; ++h) {
+            float4 xa[kHalf], xb[kHalf];
+            uint32_t c4[kHalf];
+            // issue the half's loads first (memory-level parallelism)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) v[j][e] = 0.f;
-            if (e0 >= hiel) continue;
-            float4 xa = ld4_stream(a.a, q);
-            float x[4] = {xa.x, xa.y, xa.z, xa.w};
-            if (SRC & kSrcAminusB) {
-                float4 xb = ld4_stream(a.b, q);
-                x[0] = __fsub_rn(x[0], xb.x); x[1] = __fsub_rn(x[1], xb.y);
-                x[2] = __fsub_rn(x[2], xb.z); x[3] = __fsub_rn(x[3], xb.w);
+            for (int jj = 0; jj < kHalf; ++jj) {
+                const uint64_t q = qbase + (uint64_t)(h * kHalf + jj) * 32 + lane;
+                const bool in = interior || q * 4 < hiel;
+                xa[jj] = in ? ld4_stream(a.a, q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                if (SRC & kSrcAminusB) xb[jj] = in ? ld4_stream(a.b, q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                if (SRC & kHasIn) c4[jj] = in ? __ldcs(reinterpret_cast<const uint32_t*>(a.in_codes) + q) : 0u;
             }
-            if (SRC & kHasIn) {
-                uint32_t c4 = __ldcs(reinterpret_cast<const uint32_t*>(a.in_codes) + q);
 #pragma unroll
-                for (int e = 0; e < 4; ++e) x[e] = __fadd_rn(x[e], lut[(c4 >> (8 * e)) & 0xff]);
-            }
-            if (SRC & kDivK) {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) x[e] = __fdiv_rn(x[e], a.divisor);
-            }
-            const bool full = e0 >= si.lo && e0 + 4 <= hiel;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const bool valid = full || (e0 + e >= si.lo && e0 + e < hiel);
-                if (valid) {
-                    v[j][e] = x[e];
-                    sum = __dadd_rn(sum, (double)x[e]);
-                    cnt += 1;
-                    bad |= !isfinite(x[e]);
+            for (int jj = 0; jj < kHalf; ++jj) {
+                const uint64_t q = qbase + (uint64_t)(h * kHalf + jj) * 32 + lane;
+                const uint64_t e0 = q * 4;
+                float x[4] = {xa[jj].x, xa[jj].y, xa[jj].z, xa[jj].w};
+                if (SRC & kSrcAminusB) {
+                    x[0] = __fsub_rn(x[0], xb[jj].x); x[1] = __fsub_rn(x[1], xb[jj].y);
+                    x[2] = __fsub_rn(x[2], xb[jj].z); x[3] = __fsub_rn(x[3], xb[jj].w);
                 }
-            }
-            if (SRC != kSrcA) {
-                float4* dst = reinterpret_cast<float4*>(a.scratch) + (q - a.scratch_q0);
-                if (full) {
-                    *dst = make_float4(x[0], x[1], x[2], x[3]);
-                } else {
-                    float* d1 = reinterpret_cast<float*>(dst);
+                if (SRC & kHasIn) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        if (e0 + e >= si.lo && e0 + e < hiel) d1[e] = x[e];
+                    for (int e = 0; e < 4; ++e) x[e] = __fadd_rn(x[e], lut[(c4[jj] >> (8 * e)) & 0xff]);
+                }
+                if (SRC & kDivK) {
+                    // x / k (allreduce.hpp:439): a power-of-two k is an exact
+                    // multiply, otherwise IEEE division
+                    if (a.inv_divisor != 0.f) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) x[e] = __fmul_rn(x[e], a.inv_divisor);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) x[e] = __fdiv_rn(x[e], a.divisor);
+                    }
+                }
+                uint32_t vm = 0xfu;  // valid-element mask of this float4
+                if (!interior) {
+                    if (e0 >= hiel || e0 + 4 <= si.lo) vm = 0u;
+                    else if (!(e0 >= si.lo && e0 + 4 <= hiel)) {
+                        vm = 0u;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) vm |= (e0 + e >= si.lo && e0 + e < hiel) ? (1u << e) : 0u;
+                    }
+                }
+                if (!have_piv && vm) {  // pivot: the lane's first value
+                    piv = (double)x[__ffs(vm) - 1];
+                    have_piv = true;
+                }
+                if (vm == 0xfu) {
+                    const double x0 = (double)x[0], x1 = (double)x[1], x2 = (double)x[2], x3 = (double)x[3];
+                    const double v0 = __dsub_rn(x0, piv), v1 = __dsub_rn(x1, piv);
+                    const double v2 = __dsub_rn(x2, piv), v3 = __dsub_rn(x3, piv);
+                    sum0 = __dadd_rn(__dadd_rn(sum0, x0), x2);
+                    sum1 = __dadd_rn(__dadd_rn(sum1, x1), x3);
+                    d0 = __dadd_rn(__dadd_rn(d0, v0), v2);
+                    d1 = __dadd_rn(__dadd_rn(d1, v1), v3);
+                    q0 = __dadd_rn(__dadd_rn(q0, __dmul_rn(v0, v0)), __dmul_rn(v2, v2));
+                    q1 = __dadd_rn(__dadd_rn(q1, __dmul_rn(v1, v1)), __dmul_rn(v3, v3));
+                    cnt += 4;
+                } else if (vm) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        if (vm & (1u << e)) {
+                            const double xd = (double)x[e];
+                            const double dv = __dsub_rn(xd, piv);
+                            sum0 = __dadd_rn(sum0, xd);
+                            d0 = __dadd_rn(d0, dv);
+                            q0 = __dadd_rn(q0, __dmul_rn(dv, dv));
+                            cnt += 1;
+                        }
+                    }
+                }
+                if (SRC != kSrcA && vm) {
+                    float4* dst = reinterpret_cast<float4*>(a.scratch) + (q - a.scratch_q0);
+                    if (vm == 0xfu) {
+                        *dst = make_float4(x[0], x[1], x[2], x[3]);
+                    } else {
+                        float* d1p = reinterpret_cast<float*>(dst);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (vm & (1u << e)) d1p[e] = x[e];
+                    }
                 }
             }
         }
+        p = StatP{__dadd_rn(sum0, sum1), __dadd_rn(q0, q1), __dadd_rn(d0, d1), piv, (uint64_t)cnt};
     }
-    const double S = warp_sum_d(sum);
-    const uint32_t n = warp_sum_u(cnt);
-    const double m = n ? __ddiv_rn(S, (double)n) : 0.0;
-    double m2 = 0.0, dd = 0.0;
-    if (u < si.nunits) {
-#pragma unroll
-        for (int j = 0; j < kSlotsPerLane; ++j) {
-            const uint64_t e0 = (qbase + (uint64_t)j * 32 + lane) * 4;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                if (e0 + e >= si.lo && e0 + e < hiel) {
-                    const double dv = __dsub_rn((double)v[j][e], m);
-                    m2 = __dadd_rn(m2, __dmul_rn(dv, dv));
-                    dd = __dadd_rn(dd, dv);
-                }
-            }
-        }
-    }
-    m2 = warp_sum_d(m2);
-    dd = warp_sum_d(dd);
-    const bool anybad = __any_sync(0xffffffffu, bad);
+    p = warp_merge(p);
     if (lane == 0) {
-        wp[warp] = StatP{S, m2, dd, m, (uint64_t)n};
-        if (anybad) {
+        wp[warp] = p;
+        // finite fp32 inputs cannot overflow an fp64 sum: one check per unit
+        if (!isfinite(p.s) || !isfinite(p.m2)) {
             atomicOr(&a.seg_flags[s], kFlagNonFinite);
             atomicOr(a.err, 1u);
         }
@@ -390,165 +503,247 @@ __global__ void __launch_bounds__(kThreads, 3) k_stats(QuantArgs a) {
         const double lo = __dsub_rn(mu, six);
         const double hi = __dadd_rn(mu, six);
         const double w = __ddiv_rn(__dsub_rn(hi, lo), 256.0);
-        if (threadIdx.x == 0) {
+        // smallest fp32 >= lo, largest fp32 <= hi (clipping in fp32 terms)
+        float lo_up = (float)lo;
+        if ((double)lo_up < lo) lo_up = key2f(f2key(lo_up) + 1);
+        float hi_dn = (float)hi;
+        if ((double)hi_dn > hi) hi_dn = key2f(f2key(hi_dn) - 1);
+        const int b = threadIdx.x;
+        s_thr[b] = b == 0 ? lo_up : threshold(b, lo, hi, w);
+        if (b == 0) s_thr[kBuckets] = key2f(f2key(hi_dn) + 1);
+        __syncthreads();
+        st->thr[b] = b == 0 ? -INFINITY : s_thr[b];
+        st->bp[b] = bucket_param(s_thr[b], s_thr[b + 1]);
+        if (b == 0) {
             st->lo = lo; st->hi = hi; st->width = w;
-            st->lo_f = (float)lo;
-            st->inv_w_f = (float)__ddiv_rn(1.0, w);
-            st->thr[0] = -INFINITY;
-        } else {
-            st->thr[threadIdx.x] = threshold(threadIdx.x, lo, hi, w);
+            const float lo_f = (float)lo, inv_w = (float)__ddiv_rn(1.0, w);
+            st->lo_f = lo_f;
+            st->inv_w_f = inv_w;
+            st->lo_up = lo_up;
+            st->hi_dn = hi_dn;
+            // Error of g = (x - lo_f) * inv_w (fp32) vs (x - lo) / w, in buckets,
+            // for lo <= x <= hi: |lo - lo_f| / w + 3 roundings of a value
+            // <= (|lo| + |hi|) / w, each <= 2^-24 relative; x2 for safety.
+            const double mag = __ddiv_rn(fmax(fabs(lo), fabs(hi)) + fabs(lo), w);
+            const double err = __dadd_rn(__ddiv_rn(fabs(__dsub_rn(lo, (double)lo_f)), w),
+                                         __dmul_rn(mag, 3.0 / 16777216.0));
+            const double mg = __dmul_rn(2.0, err) + 1e-6;
+            st->margin = mg < 0.25 ? (float)mg : 2.0f;  // 2.0: always use the table
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// Deterministic per-warp histogram update: lanes holding the same bucket are
-// combined in lane order by the group's lowest lane, which alone touches the
-// warp-private smem row (no fp64 smem atomics — they are CAS loops on sm_100
-// and their order is nondeterministic).
-__device__ __forceinline__ void warp_hist_add(double* wsum, uint32_t* wcnt, int key, double xc, bool valid) {
-    const int lane = threadIdx.x & 31;
-    const int k = valid ? key : (kBuckets + lane);  // invalid lanes: unique dummy keys
-    const uint32_t peers = __match_any_sync(0xffffffffu, k);
-    const int leader = __ffs(peers) - 1;
-    double acc = xc;
-    uint32_t rem = (lane == leader) ? (peers & (peers - 1)) : 0u;  // others, ascending
-    while (__any_sync(0xffffffffu, rem != 0u)) {
-        const int src = rem ? (__ffs(rem) - 1) : lane;
-        const double o = __shfl_sync(0xffffffffu, xc, src);
-        if (rem) { acc = __dadd_rn(acc, o); rem &= rem - 1; }
-    }
-    if (valid && lane == leader) {
-        wsum[key] = __dadd_rn(wsum[key], acc);
-        wcnt[key] += __popc(peers);
-    }
-    __syncwarp();
-}
-
-// K_bin: codes + per-tile 256-bucket (sum of clipped x, count) histogram;
-// the combine tree's root turns the segment histogram into the codebook
-// (quant.hpp:78-85).
+// K_bin: codes + exact fixed-point bucket histogram. Per warp a private
+// smem histogram of three u32 words per bucket, updated with native 32-bit
+// smem atomics (integer: order-free, hence deterministic):
+//   A += r & 0xffff ; B += (r >> 16) & 0xffff ; C += (r >> 32) + (1 << 21)
+// (one warp unit is <= 1024 elements, so no word overflows). The tile
+// histogram combines the warps into 128-bit sums, then the segment's combine
+// tree; its root turns the sums into the codebook (quant.hpp:78-85).
 template <bool FROM_SCRATCH>
 __global__ void __launch_bounds__(kThreads) k_bin(QuantArgs a) {
-    __shared__ double wsum[kWarps][kBuckets];
-    __shared__ uint32_t wcnt[kWarps][kBuckets];
+    __shared__ uint32_t hA[kWarps][kBuckets], hB[kWarps][kBuckets], hC[kWarps][kBuckets];
     __shared__ float thr[kBuckets + 1];
+    __shared__ __align__(16) BucketParam bp[kBuckets];
+    __shared__ uint32_t s_clip[2];
     __shared__ uint32_t s_flag;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t s = a.cta_seg[blockIdx.x];
     const SegInfo si = a.segs[s];
     const uint32_t tile = blockIdx.x - si.cta0;
     const SegStat* st = &a.stats[si.slot];
-    const double lo = st->lo, hi = st->hi;
-    const float lo_f = st->lo_f, inv_w = st->inv_w_f;
+    const float lo_f = st->lo_f, inv_w = st->inv_w_f, lo_up = st->lo_up, hi_dn = st->hi_dn;
+    const float margin = st->margin;
     const bool degenerate = (st->flags & kFlagDegenerate) != 0;
-    thr[threadIdx.x] = st->thr[threadIdx.x];
+    {
+        const int b = threadIdx.x;
+        thr[b] = st->thr[b];
+        bp[b] = st->bp[b];
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) { wsum[w][threadIdx.x] = 0.0; wcnt[w][threadIdx.x] = 0u; }
-    if (threadIdx.x == 0) { thr[0] = -INFINITY; thr[kBuckets] = INFINITY; }
+        for (int w = 0; w < kWarps; ++w) { hA[w][b] = 0u; hB[w][b] = 0u; hC[w][b] = 0u; }
+        if (b == 0) { thr[0] = -INFINITY; thr[kBuckets] = INFINITY; s_clip[0] = 0u; s_clip[1] = 0u; }
+    }
     __syncthreads();
 
     const uint64_t hiel = si.lo + si.len;
     const uint32_t u = tile * kWarps + warp;
     if (u < si.nunits) {
         const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
-#pragma unroll 2
+        const bool interior = qbase * 4 >= si.lo && (qbase + kUnitSlots) * 4 <= hiel;  // warp-uniform
+        uint32_t* wA = hA[warp];
+        uint32_t* wB = hB[warp];
+        uint32_t* wC = hC[warp];
+        float4 xv[kSlotsPerLane];
+#pragma unroll
+        for (int j = 0; j < kSlotsPerLane; ++j) {
+            const uint64_t q = qbase + (uint64_t)j * 32 + lane;
+            const bool in = interior || q * 4 < hiel;
+            xv[j] = !in ? make_float4(0.f, 0.f, 0.f, 0.f)
+                        : FROM_SCRATCH ? *(reinterpret_cast<const float4*>(a.scratch) + (q - a.scratch_q0))
+                                       : ld4(a.a, q);
+        }
+        uint32_t nclip_lo = 0, nclip_hi = 0;
+#pragma unroll
         for (int j = 0; j < kSlotsPerLane; ++j) {
             const uint64_t q = qbase + (uint64_t)j * 32 + lane;
             const uint64_t e0 = q * 4;
-            const bool any = e0 < hiel;
-            float4 xv = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (any) xv = FROM_SCRATCH ? *(reinterpret_cast<const float4*>(a.scratch) + (q - a.scratch_q0))
-                                       : ld4(a.a, q);
-            const bool full = any && e0 >= si.lo && e0 + 4 <= hiel;
-            uint32_t packed = 0;
+            uint32_t vm = 0xfu;
+            if (!interior) {
+                if (e0 >= hiel || e0 + 4 <= si.lo) vm = 0u;
+                else if (!(e0 >= si.lo && e0 + 4 <= hiel)) {
+                    vm = 0u;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const bool valid = any && (full || (e0 + e >= si.lo && e0 + e < hiel));
-                const float x = f4get(xv, e);
-                int c = 0;
-                double xc = 0.0;
-                if (!degenerate) {
-                    float g = __fmul_rn(__fsub_rn(x, lo_f), inv_w);
-                    c = g < 0.f ? 0 : (g > 255.f ? 255 : (int)g);
-                    if (!(c >= 0 && c <= 255)) c = 0;  // NaN guard
-                    while (c < 255 && x >= thr[c + 1]) ++c;
-                    while (c > 0 && x < thr[c]) --c;
-                    xc = (double)x;
-                    if (xc < lo) xc = lo;
-                    if (xc > hi) xc = hi;
+                    for (int e = 0; e < 4; ++e) vm |= (e0 + e >= si.lo && e0 + e < hiel) ? (1u << e) : 0u;
                 }
-                packed |= (uint32_t)c << (8 * e);
-                if (!degenerate) warp_hist_add(wsum[warp], wcnt[warp], c, xc, valid);
             }
-            if (full) {
+            uint32_t packed = 0;
+            if (!degenerate) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float x = f4get(xv[j], e);
+                    const bool valid = (vm >> e) & 1u;
+                    const bool clo = x < lo_up, chi = x > hi_dn;
+                    // bucket: the fp32 estimate is exact unless it lands within
+                    // `margin` of a bucket edge (or the segment is flagged
+                    // unsafe); then the exact threshold table decides
+                    const float g = fminf(fmaxf(__fmul_rn(__fsub_rn(x, lo_f), inv_w), 0.f), 255.f);
+                    int c = (int)g;
+                    const float fr = __fsub_rn(g, (float)c);
+                    if (!(fr > margin && fr < 1.f - margin)) {
+                        while (c < 255 && x >= thr[c + 1]) ++c;
+                        while (c > 0 && x < thr[c]) --c;
+                    }
+                    c = clo ? 0 : (chi ? 255 : c);
+                    const double2 pb = reinterpret_cast<const double2*>(bp)[c];  // {base, scale}
+                    const double t = (clo || chi) ? pb.x : (double)x;
+                    // r = rint((t - base) * scale) via the 2^52 magic add (exact:
+                    // (t - base) * scale is an exact product, r < 2^42)
+                    const double m = __fma_rn(__dsub_rn(t, pb.x), pb.y, 4503599627370496.0);
+                    const uint32_t rlo = (uint32_t)__double2loint(m);
+                    const uint32_t rhi = (uint32_t)__double2hiint(m) & 0x3ffu;
+                    if (valid) {
+                        atomicAdd(&wA[c], rlo & 0xffffu);
+                        atomicAdd(&wB[c], rlo >> 16);
+                        atomicAdd(&wC[c], rhi + (1u << 21));
+                        nclip_lo += clo ? 1u : 0u;
+                        nclip_hi += chi ? 1u : 0u;
+                    }
+                    packed |= (uint32_t)c << (8 * e);
+                }
+            }
+            if (vm == 0xfu) {
                 reinterpret_cast<uint32_t*>(a.out_codes)[q] = packed;
-            } else if (any) {
+            } else if (vm) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                    if (e0 + e >= si.lo && e0 + e < hiel) a.out_codes[e0 + e] = (uint8_t)(packed >> (8 * e));
+                    if (vm & (1u << e)) a.out_codes[e0 + e] = (uint8_t)(packed >> (8 * e));
             }
+        }
+        nclip_lo = warp_sum_u(nclip_lo);
+        nclip_hi = warp_sum_u(nclip_hi);
+        if (lane == 0 && (nclip_lo | nclip_hi)) {
+            atomicAdd(&s_clip[0], nclip_lo);
+            atomicAdd(&s_clip[1], nclip_hi);
         }
     }
     __syncthreads();
-    {   // tile histogram, fixed warp order
+    {   // tile histogram (exact; warp order irrelevant but fixed anyway)
         const int b = threadIdx.x;
-        double sm = 0.0;
+        unsigned long long r = 0;
         uint32_t cn = 0;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) { sm = __dadd_rn(sm, wsum[w][b]); cn += wcnt[w][b]; }
-        a.leaf_sum[(uint64_t)blockIdx.x * kBuckets + b] = sm;
-        a.leaf_cnt[(uint64_t)blockIdx.x * kBuckets + b] = cn;
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t C = hC[w][b];
+            r += (unsigned long long)hA[w][b] + ((unsigned long long)hB[w][b] << 16) +
+                 ((unsigned long long)(C & 0x1fffffu) << 32);
+            cn += C >> 21;
+        }
+        HistP* L = &a.leaf_hist[blockIdx.x];
+        L->rlo[b] = r;
+        L->rhi[b] = 0ull;
+        L->cnt[b] = cn;
+        if (b < 2) L->clip[b] = s_clip[b];
     }
     // ---- combine tree (16 independent loads per thread per level)
     uint32_t* ctr = a.tree_cnt + a.nnodes;
     TreeCursor c{0, tile, si.ncta, 0};
-    double rs = 0.0;
-    uint64_t rc = 0;
-    bool have = false;
+    const HistP* root = &a.leaf_hist[blockIdx.x];
     while (c.n > 1) {
         const uint32_t lvl = c.level, n_old = c.n, off_old = c.off;
         if (!tree_arrive(c, ctr, si.node_base, &s_flag)) return;
         const uint32_t first = c.idx * kFan, nch = min((uint32_t)kFan, n_old - first);
         const uint32_t poff = lvl == 0 ? 0u : off_old + n_old;
         const int b = threadIdx.x;
-        double ps[kFan];
-        uint32_t pc[kFan];
+        const HistP* src = lvl == 0 ? &a.leaf_hist[si.cta0 + first] : &a.node_hist[si.node_base + off_old + first];
+        unsigned long long lo[kFan], hi[kFan];
+        uint32_t cn[kFan];
 #pragma unroll
         for (int i = 0; i < kFan; ++i) {
             if ((uint32_t)i < nch) {
-                const uint64_t ix = (lvl == 0 ? (uint64_t)(si.cta0 + first + i) : (uint64_t)(si.node_base + off_old + first + i)) * kBuckets + b;
-                ps[i] = __ldcg((lvl == 0 ? a.leaf_sum : a.node_sum) + ix);
-                pc[i] = __ldcg((lvl == 0 ? a.leaf_cnt : a.node_cnt) + ix);
-            } else { ps[i] = 0.0; pc[i] = 0u; }
+                lo[i] = __ldcg(&src[i].rlo[b]);
+                hi[i] = __ldcg(&src[i].rhi[b]);
+                cn[i] = __ldcg(&src[i].cnt[b]);
+            } else { lo[i] = 0ull; hi[i] = 0ull; cn[i] = 0u; }
         }
-        rs = 0.0;
-        rc = 0;
+        unsigned long long rl = 0ull, rh = 0ull;
+        uint32_t rc = 0;
 #pragma unroll
-        for (int i = 0; i < kFan; ++i) { rs = __dadd_rn(rs, ps[i]); rc += pc[i]; }
-        have = true;
-        if ((n_old + kFan - 1) / kFan > 1) {  // not the root yet: publish the node
-            a.node_sum[(uint64_t)(si.node_base + poff + c.idx) * kBuckets + b] = rs;
-            a.node_cnt[(uint64_t)(si.node_base + poff + c.idx) * kBuckets + b] = (uint32_t)rc;
+        for (int i = 0; i < kFan; ++i) {
+            const unsigned long long t = rl + lo[i];
+            rh += hi[i] + (t < rl ? 1ull : 0ull);
+            rl = t;
+            rc += cn[i];
         }
+        HistP* dst = &a.node_hist[si.node_base + poff + c.idx];
+        dst->rlo[b] = rl;
+        dst->rhi[b] = rh;
+        dst->cnt[b] = rc;
+        if (b < 2) {
+            uint32_t cl = 0;
+            for (uint32_t i = 0; i < nch; ++i) cl += __ldcg(&src[i].clip[b]);
+            dst->clip[b] = cl;
+        }
+        root = dst;
         c.level = lvl + 1;
         c.n = (n_old + kFan - 1) / kFan;
         c.off = poff;
     }
-    if (!have) {  // single-tile segment: this CTA's own histogram is the root
-        __syncthreads();
-        double sm = 0.0;
-        uint32_t cn = 0;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) { sm = __dadd_rn(sm, wsum[w][threadIdx.x]); cn += wcnt[w][threadIdx.x]; }
-        rs = sm;
-        rc = cn;
-    }
+    __syncthreads();
+    __threadfence();
+    // ---- root: codebook (quant.hpp:78-85)
     const int b = threadIdx.x;
     float* cb = a.out_cb + (uint64_t)si.slot * kBuckets;
-    if (degenerate) cb[b] = (float)st->mu;
-    else if (rc) cb[b] = (float)__ddiv_rn(rs, (double)rc);
-    else cb[b] = (float)__dadd_rn(lo, __dmul_rn(__dadd_rn((double)b, 0.5), st->width));
+    if (degenerate) { cb[b] = (float)st->mu; return; }
+    const unsigned long long rl = __ldcg(&root->rlo[b]), rh = __ldcg(&root->rhi[b]);
+    const uint32_t total = __ldcg(&root->cnt[b]);  // clipped members included, with r = 0
+    const uint32_t clip = b == 0 ? __ldcg(&root->clip[0]) : (b == 255 ? __ldcg(&root->clip[1]) : 0u);
+    const uint32_t cnt = total - clip;
+    if (total == 0) {
+        cb[b] = (float)__dadd_rn(st->lo, __dmul_rn(__dadd_rn((double)b, 0.5), st->width));
+        return;
+    }
+    double sum = 0.0;
+    if (cnt) {
+        const BucketParam pb = st->bp[b];
+        // sum x / Q = sum r + cnt * base * scale (exact integers, 128-bit)
+        __int128 S = (__int128)(((unsigned __int128)rh << 64) | rl);
+        S += (__int128)(long long)__double2ll_rn(__dmul_rn(pb.base, pb.scale)) * (__int128)cnt;
+        const long long hi64 = (long long)(S >> 64);
+        double v;
+        if (hi64 == 0 || hi64 == -1) {
+            const long long s64 = (long long)(unsigned long long)S;
+            const bool fits = (hi64 == 0 && s64 >= 0) || (hi64 == -1 && s64 < 0);
+            v = fits ? (double)s64
+                     : __dadd_rn(ldexp((double)hi64, 64), (double)(unsigned long long)S);
+        } else {
+            v = __dadd_rn(ldexp((double)hi64, 64), (double)(unsigned long long)S);
+        }
+        sum = __ddiv_rn(v, pb.scale);  // exact: scale is a power of two
+    }
+    if (b == 0 && clip) sum = __dadd_rn(sum, __dmul_rn((double)clip, st->lo));
+    if (b == 255 && clip) sum = __dadd_rn(sum, __dmul_rn((double)clip, st->hi));
+    cb[b] = (float)__ddiv_rn(sum, (double)total);
 }
 
 // ---------------------------------------------------------------------------
