@@ -104,6 +104,26 @@ typedef struct {
     int device;                 /* CUDA device ordinal, -1 = current */
 } emesh_engine_config;
 
+/* Host-only plan queries (no GPU needed). Segment table of an (n, k, S)
+ * ring, chunk-major (allreduce.hpp:107-118, :326-336); returns the count. */
+uint64_t emesh_plan_segments(uint64_t n, uint32_t k, uint32_t S, uint64_t* seg_lo, uint64_t* seg_len);
+
+/* The NCCL ring engine's program for one ring position, in issue order.
+ * kinds: OWN = quantize own chunk's hop-0 payload window; XFER = send
+ * window of send_chunk to rank+1 and receive the window of recv_chunk from
+ * rank-1; QUANT = fused dequant+add+requant of the received window
+ * (final_hop: owner mean /k, allreduce.hpp:435-443); APPLY = decode a final
+ * window (dequant + Nesterov). Windows are ranges of segment slots. */
+enum { EMESH_OP_OWN = 0, EMESH_OP_XFER = 1, EMESH_OP_QUANT = 2, EMESH_OP_APPLY = 3 };
+typedef struct {
+    int32_t kind, phase, hop, window;  /* phase 0 reduce-scatter, 1 all-gather */
+    int32_t send_chunk, recv_chunk;     /* -1 when unused */
+    uint32_t send_seg0, send_nseg, recv_seg0, recv_nseg;
+    int32_t final_hop, pad;
+} emesh_ring_op;
+uint64_t emesh_ring_schedule(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems, uint32_t rank,
+                             emesh_ring_op* ops, uint64_t max_ops);
+
 /* NCCL unique id for emesh_engine_config.nccl_id (rank 0 creates, broadcast). */
 int emesh_nccl_unique_id(uint8_t out[128]);
 

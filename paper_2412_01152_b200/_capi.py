@@ -20,6 +20,7 @@ EXPORTS = (
     "emesh_dequantize", "emesh_dequantize_segments",
     "emesh_encode_quant_chunk", "emesh_decode_quant_chunk",
     "emesh_pseudo_gradient", "emesh_nesterov_outer_step",
+    "emesh_plan_segments", "emesh_ring_schedule",
     "emesh_nccl_unique_id", "emesh_engine_create", "emesh_engine_destroy",
     "emesh_engine_segments", "emesh_engine_ring_allreduce", "emesh_engine_outer_sync",
     "emesh_engine_outer_sync_host", "emesh_engine_check", "emesh_engine_payload", "emesh_engine_payload_host",
@@ -41,6 +42,17 @@ class EngineConfig(C.Structure):
         ("device", C.c_int),
     ]
 
+
+class RingOp(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32), ("phase", C.c_int32), ("hop", C.c_int32), ("window", C.c_int32),
+        ("send_chunk", C.c_int32), ("recv_chunk", C.c_int32),
+        ("send_seg0", C.c_uint32), ("send_nseg", C.c_uint32), ("recv_seg0", C.c_uint32), ("recv_nseg", C.c_uint32),
+        ("final_hop", C.c_int32), ("pad", C.c_int32),
+    ]
+
+
+OP_OWN, OP_XFER, OP_QUANT, OP_APPLY = range(4)
 
 _lib = None
 
@@ -67,6 +79,8 @@ def lib() -> C.CDLL:
         "emesh_decode_quant_chunk": (i32, [vp, u64, vp, vp, P(u32)]),
         "emesh_pseudo_gradient": (i32, [vp, vp, vp, u64, vp]),
         "emesh_nesterov_outer_step": (i32, [vp, vp, vp, u64, f32, f32, vp]),
+        "emesh_plan_segments": (u64, [u64, u32, u32, vp, vp]),
+        "emesh_ring_schedule": (u64, [u64, u32, u32, u64, u32, vp, u64]),
         "emesh_nccl_unique_id": (i32, [vp]),
         "emesh_engine_create": (i32, [P(EngineConfig), P(vp)]),
         "emesh_engine_destroy": (i32, [vp]),

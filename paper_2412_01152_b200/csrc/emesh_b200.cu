@@ -157,6 +157,8 @@ struct Plan {
     }
 };
 
+constexpr uint64_t kDefaultWindow = (uint64_t)16 << 20;  // elements per pipelining window
+
 // Ring plan: k chunks, min(S, len) subs each, windows of G segments.
 Plan make_ring_plan(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems) {
     Plan p;
@@ -183,10 +185,11 @@ Plan make_ring_plan(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems) {
     // chunks shorter than S have fewer sub-slices; keep one window per chunk
     // then so every rank agrees on the window count (NCCL send/recv pairing).
     if (n < (uint64_t)k * S) G = S;
+    G = std::min<uint64_t>(G, S);  // a chunk never has more than S segments
     for (uint32_t c = 0; c < k; ++c) {
         uint32_t w = 0;
-        for (uint32_t s = first[c]; s < first[c + 1]; s += (uint32_t)G, ++w)
-            p.add_batch(c, w, s, (uint32_t)std::min<uint64_t>(first[c + 1], s + G));
+        for (uint64_t s = first[c]; s < first[c + 1]; s += G, ++w)
+            p.add_batch(c, w, (uint32_t)s, (uint32_t)std::min<uint64_t>(first[c + 1], s + G));
     }
     return p;
 }
@@ -590,6 +593,7 @@ struct emesh_engine {
     cudaStream_t s_comp = nullptr, s_comm = nullptr;
     cudaEvent_t ev_entry = nullptr, ev_done = nullptr, ev_comm_done = nullptr;
     std::vector<cudaEvent_t> ev_send, ev_recv;  // per window
+    std::vector<emesh_ring_op> schedule;        // NCCL mode program (build_schedule)
     struct Arena {
         uint8_t* codes = nullptr;
         float* cbs = nullptr;
@@ -686,6 +690,52 @@ int xfer_window(emesh_engine* e, const Batch& snd, const Batch& rcv) {
     return EMESH_OK;
 }
 
+// The NCCL ring's program for ring position r, in issue order (pure host
+// logic, exported as emesh_ring_schedule so CPU tests can execute it):
+//   OWN   : quantize the hop-0 payload Q(delta[chunk r]) window by window
+//   XFER  : send window j of send_chunk to r+1, receive window j of recv_chunk from r-1
+//   QUANT : fused hop on the received window (dequant + add + requant; /k on the last hop)
+//   APPLY : decode a final window (dequant + Nesterov, or plain dequantize)
+// Reduce-scatter: allreduce.hpp:411-426; owner finalize :428-445; all-gather :446-464.
+std::vector<emesh_ring_op> build_schedule(const Plan& P, uint32_t r) {
+    const uint32_t k = P.k;
+    std::vector<emesh_ring_op> ops;
+    auto win = [&](uint32_t c, uint32_t j) -> const Batch& { return P.batches[c][j]; };
+    const uint32_t W = (uint32_t)P.batches[0].size();
+    auto op = [&](int32_t kind, int32_t phase, int32_t hop, uint32_t j, int32_t sc, int32_t rc) {
+        emesh_ring_op o{};
+        o.kind = kind;
+        o.phase = phase;
+        o.hop = hop;
+        o.window = (int32_t)j;
+        o.send_chunk = sc;
+        o.recv_chunk = rc;
+        if (sc >= 0) { o.send_seg0 = win(sc, j).slot0; o.send_nseg = win(sc, j).nseg; }
+        if (rc >= 0) { o.recv_seg0 = win(rc, j).slot0; o.recv_nseg = win(rc, j).nseg; }
+        o.final_hop = (kind == EMESH_OP_QUANT && hop + 2 == (int32_t)k) ? 1 : 0;
+        ops.push_back(o);
+    };
+    if (k < 2) return ops;
+    for (uint32_t j = 0; j < W; ++j) op(EMESH_OP_OWN, 0, 0, j, -1, (int32_t)r);
+    for (uint32_t s = 0; s + 1 < k; ++s) {
+        const int32_t send_c = (int32_t)((r + k - s) % k), recv_c = (int32_t)((r + k - s - 1) % k);
+        for (uint32_t j = 0; j < W; ++j) {
+            op(EMESH_OP_XFER, 0, (int32_t)s, j, send_c, recv_c);
+            op(EMESH_OP_QUANT, 0, (int32_t)s, j, -1, recv_c);
+        }
+    }
+    const int32_t own = (int32_t)((r + 1) % k);
+    for (uint32_t j = 0; j < W; ++j) op(EMESH_OP_APPLY, 1, -1, j, -1, own);
+    for (uint32_t s = 0; s + 1 < k; ++s) {
+        const int32_t send_c = (int32_t)((r + 1 + k - s) % k), recv_c = (int32_t)((r + k - s) % k);
+        for (uint32_t j = 0; j < W; ++j) {
+            op(EMESH_OP_XFER, 1, (int32_t)s, j, send_c, recv_c);
+            op(EMESH_OP_APPLY, 1, (int32_t)s, j, -1, recv_c);
+        }
+    }
+    return ops;
+}
+
 int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, float* buf, float* local_out, float* out,
              float lr, float mom) {
     const uint32_t k = e->k, r = e->rank;
@@ -696,41 +746,41 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
     const uint32_t W = (uint32_t)P[0].size();
     for (uint32_t c = 1; c < k; ++c)
         if (P[c].size() != W) return fail(EMESH_ECONFIG, "ring chunks have unequal window counts");
-    // hop-0 payload
-    for (uint32_t j = 0; j < W; ++j) {
-        QuantIO io{pg ? kSrcAminusB : kSrcA, A, B, nullptr, nullptr, 1.f, ar.codes, ar.cbs, ar.stats};
-        TRY(launch_quant(P[r][j], e->ws, io, sc, &e->tr));
-        CU(cudaEventRecord(e->ev_send[j], sc));
-    }
-    // reduce-scatter (allreduce.hpp:411-426), window-pipelined
-    for (uint32_t s = 0; s + 1 < k; ++s) {
-        const uint32_t send_c = (r + k - s) % k, recv_c = (r + k - s - 1) % k;
-        for (uint32_t j = 0; j < W; ++j) {
-            CU(cudaStreamWaitEvent(sm, e->ev_send[j], 0));
-            TRY(xfer_window(e, P[send_c][j], P[recv_c][j]));
-            CU(cudaEventRecord(e->ev_recv[j], sm));
-            CU(cudaStreamWaitEvent(sc, e->ev_recv[j], 0));
-            QuantIO io{hop_src(pg, s, k), A, B, ar.codes, ar.cbs, (float)k, ar.codes, ar.cbs, ar.stats};
-            TRY(launch_quant(P[recv_c][j], e->ws, io, sc, &e->tr));
-            CU(cudaEventRecord(e->ev_send[j], sc));
-        }
-    }
-    // own chunk is final (allreduce.hpp:428-445): apply it while the
-    // all-gather (allreduce.hpp:446-464) forwards bytes verbatim
-    const uint32_t own = (r + 1) % k;
-    for (uint32_t j = 0; j < W; ++j) {
-        if (out) TRY(launch_apply(P[own][j], 0, ar.codes, ar.cbs, nullptr, nullptr, nullptr, out, 0.f, 0.f, sc, &e->tr));
-        else TRY(launch_apply(P[own][j], 1, ar.codes, ar.cbs, theta, buf, local_out, nullptr, lr, mom, sc, &e->tr));
-    }
-    for (uint32_t s = 0; s + 1 < k; ++s) {
-        const uint32_t send_c = (r + 1 + k - s) % k, recv_c = (r + k - s) % k;
-        for (uint32_t j = 0; j < W; ++j) {
-            if (s == 0) CU(cudaStreamWaitEvent(sm, e->ev_send[j], 0));
-            TRY(xfer_window(e, P[send_c][j], P[recv_c][j]));
-            CU(cudaEventRecord(e->ev_recv[j], sm));
-            CU(cudaStreamWaitEvent(sc, e->ev_recv[j], 0));
-            if (out) TRY(launch_apply(P[recv_c][j], 0, ar.codes, ar.cbs, nullptr, nullptr, nullptr, out, 0.f, 0.f, sc, &e->tr));
-            else TRY(launch_apply(P[recv_c][j], 1, ar.codes, ar.cbs, theta, buf, local_out, nullptr, lr, mom, sc, &e->tr));
+    for (const emesh_ring_op& o : e->schedule) {
+        const uint32_t j = (uint32_t)o.window;
+        switch (o.kind) {
+            case EMESH_OP_OWN: {
+                QuantIO io{pg ? kSrcAminusB : kSrcA, A, B, nullptr, nullptr, 1.f, ar.codes, ar.cbs, ar.stats};
+                TRY(launch_quant(P[o.recv_chunk][j], e->ws, io, sc, &e->tr));
+                CU(cudaEventRecord(e->ev_send[j], sc));
+                break;
+            }
+            case EMESH_OP_XFER:
+                // RS: the payload was produced by compute (ev_send); AG hop 0
+                // forwards the owner's final bytes, later AG hops bytes this
+                // stream itself received
+                if (o.phase == 0 || o.hop == 0) CU(cudaStreamWaitEvent(sm, e->ev_send[j], 0));
+                TRY(xfer_window(e, P[o.send_chunk][j], P[o.recv_chunk][j]));
+                CU(cudaEventRecord(e->ev_recv[j], sm));
+                break;
+            case EMESH_OP_QUANT: {
+                CU(cudaStreamWaitEvent(sc, e->ev_recv[j], 0));
+                QuantIO io{hop_src(pg, (uint32_t)o.hop, k), A, B, ar.codes, ar.cbs, (float)k, ar.codes, ar.cbs, ar.stats};
+                TRY(launch_quant(P[o.recv_chunk][j], e->ws, io, sc, &e->tr));
+                CU(cudaEventRecord(e->ev_send[j], sc));
+                break;
+            }
+            case EMESH_OP_APPLY:
+                if (o.hop >= 0) CU(cudaStreamWaitEvent(sc, e->ev_recv[j], 0));
+                if (out)
+                    TRY(launch_apply(P[o.recv_chunk][j], 0, ar.codes, ar.cbs, nullptr, nullptr, nullptr, out, 0.f, 0.f,
+                                     sc, &e->tr));
+                else
+                    TRY(launch_apply(P[o.recv_chunk][j], 1, ar.codes, ar.cbs, theta, buf, local_out, nullptr, lr, mom,
+                                     sc, &e->tr));
+                break;
+            default:
+                return fail(EMESH_ECONFIG, "bad schedule op");
         }
     }
     return EMESH_OK;
@@ -755,6 +805,26 @@ int engine_exit(emesh_engine* e, cudaStream_t user) {
 }  // namespace
 
 extern "C" {
+
+uint64_t emesh_plan_segments(uint64_t n, uint32_t k, uint32_t S, uint64_t* seg_lo, uint64_t* seg_len) {
+    if (k == 0) return 0;
+    Plan p = make_ring_plan(n, k, S ? S : 4, (uint64_t)1 << 62);
+    for (size_t i = 0; i < p.segs.size(); ++i) {
+        if (seg_lo) seg_lo[i] = p.segs[i].lo;
+        if (seg_len) seg_len[i] = p.segs[i].len;
+    }
+    return p.segs.size();
+}
+
+uint64_t emesh_ring_schedule(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems, uint32_t rank,
+                             emesh_ring_op* ops, uint64_t max_ops) {
+    if (k == 0 || rank >= k) return 0;
+    Plan p = make_ring_plan(n, k, S ? S : 4, window_elems ? window_elems : kDefaultWindow);
+    std::vector<emesh_ring_op> v = build_schedule(p, rank);
+    if (ops)
+        for (size_t i = 0; i < v.size() && i < max_ops; ++i) ops[i] = v[i];
+    return v.size();
+}
 
 int emesh_nccl_unique_id(uint8_t out[128]) {
     ncclUniqueId id;
@@ -783,7 +853,7 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
     else cudaGetDevice(&e->device);
     auto bail = [&](int rc) { emesh_engine_destroy(e); return rc; };
     if (cudaSetDevice(e->device) != cudaSuccess) return bail(fail(EMESH_ECUDA, "cudaSetDevice"));
-    uint64_t window = cfg->window_elems ? cfg->window_elems : (uint64_t)16 << 20;
+    uint64_t window = cfg->window_elems ? cfg->window_elems : kDefaultWindow;
     e->plan = make_ring_plan(cfg->n, cfg->k, S, window);
     e->windows = (uint32_t)e->plan.batches[0].size();
     int rc = e->plan.upload();
@@ -804,6 +874,7 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
         cudaEventCreateWithFlags(&e->ev_recv[j], cudaEventDisableTiming);
     }
     if (!virt && e->k > 1) {
+        e->schedule = build_schedule(e->plan, e->rank);
         ncclUniqueId id;
         std::memcpy(&id, cfg->nccl_id, sizeof id);
         ncclResult_t r = ncclCommInitRank(&e->comm, (int)e->k, id, (int)e->rank);

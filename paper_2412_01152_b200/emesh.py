@@ -380,6 +380,23 @@ def segment_table(n: int, k: int, S: int):
     return out
 
 
+def plan_segments(n: int, k: int, S: int):
+    """Segment table from the C++ planner (host-only, no GPU)."""
+    cnt = _capi.lib().emesh_plan_segments(n, k, S, None, None)
+    lo = np.empty(cnt, np.uint64)
+    ln = np.empty(cnt, np.uint64)
+    _capi.lib().emesh_plan_segments(n, k, S, lo.ctypes.data, ln.ctypes.data)
+    return lo, ln
+
+
+def ring_schedule(n: int, k: int, S: int, rank: int, window_elems: int = 0):
+    """The NCCL engine's program for one ring position (host-only, no GPU)."""
+    cnt = _capi.lib().emesh_ring_schedule(n, k, S, window_elems, rank, None, 0)
+    ops = (_capi.RingOp * max(cnt, 1))()
+    _capi.lib().emesh_ring_schedule(n, k, S, window_elems, rank, ops, cnt)
+    return [ops[i] for i in range(cnt)]
+
+
 class RingEngine:
     """One ring position (NCCL mode: ``rank`` of ``k`` processes, one GPU each)
     or all ``k`` DiLoCo workers on this GPU (``virtual=True``). Owns every

@@ -1,0 +1,66 @@
+"""Run under torchrun (one rank per GPU): the NCCL ring engine vs the oracle.
+Used by tests/test_gpu_nccl.py. Exit code 0 iff every check passes."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from oracle.pyoracle import Oracle  # noqa: E402  (checker)
+import paper_2412_01152_b200 as E  # noqa: E402
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    lr = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(lr)
+    dev = torch.device("cuda", lr)
+    dist.init_process_group("nccl", device_id=dev)
+    O = Oracle()
+    ok = True
+    for n, S, window in [(100_003, 4, 0), (4099, 3, 1), (5, 4, 0), (2_000_000, 8, 300_000)]:
+        obj = [E.RingEngine.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        eng = E.RingEngine(n, world, rank=rank, opts=E.ReduceOptions(pipeline_subchunks=S), nccl_id=obj[0],
+                           window_elems=window)
+        ins = [O.uniform(n, 7 + n, w, 0, 0, 2.0 ** -6) for w in range(world)]
+        want = O.ring_allreduce(ins, S, "int8")
+        out = torch.empty(n + 4, dtype=torch.float32, device=dev)[:n]
+        eng.ring_allreduce([torch.from_numpy(ins[rank]).to(dev)], [out])
+        eng.check()
+        got = out.cpu().numpy()
+        if not np.array_equal(bits(got), bits(want)):
+            print(f"rank {rank}: ring n={n} S={S} MISMATCH ({int((bits(got) != bits(want)).sum())} elems)", flush=True)
+            ok = False
+        # two outer-sync rounds (trainer.hpp:355-382)
+        g = O.uniform(n, 3, 0)
+        b = np.zeros(n, np.float32)
+        tg = torch.from_numpy(g).to(dev)
+        tb = torch.from_numpy(b).to(dev)
+        eg, eb = g, b
+        for rnd in range(2):
+            ls = [(eg - O.uniform(n, 30 + rnd, 1 + w, 0, 0, 2.0 ** -10)).astype(np.float32) for w in range(world)]
+            eng.outer_sync([tg], [torch.from_numpy(ls[rank]).to(dev)], [tb], E.HyperParams(), write_local=False)
+            eng.check()
+            eg, eb = O.outer_sync(eg, ls, eb, S, "int8", 0.7, 0.9)
+            if not (np.array_equal(bits(tg.cpu().numpy()), bits(eg)) and np.array_equal(bits(tb.cpu().numpy()), bits(eb))):
+                print(f"rank {rank}: outer sync n={n} round {rnd} MISMATCH", flush=True)
+                ok = False
+        eng.close()
+    flag = torch.tensor([0 if ok else 1], device=dev)
+    dist.all_reduce(flag)
+    dist.destroy_process_group()
+    if rank == 0:
+        print("NCCL parity", "OK" if flag.item() == 0 else "FAILED", flush=True)
+    sys.exit(0 if flag.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()
