@@ -176,6 +176,12 @@ int emesh_engine_payload(emesh_engine* e, uint32_t worker, const uint8_t** codes
 int emesh_engine_payload_host(emesh_engine* e, uint32_t worker, uint8_t* codes_host, float* codebooks_host,
                               double* stats_host);
 
+/* Development aid: per-task timeline of the persistent quantizer (records of
+ * 4 x u64 globaltimer ns {start, ready, main-loop done, end} + 4 x u32
+ * {kind, segment, tile, smid}). enable(0) turns it off. */
+int emesh_trace_enable(uint64_t records);
+uint64_t emesh_trace_read(void* host, uint64_t max_records);
+
 /* Number of kernels this engine launched since creation (for the bench's
  * gpu_launches claim). */
 uint64_t emesh_engine_launches(const emesh_engine* e);

@@ -25,6 +25,7 @@ EXPORTS = (
     "emesh_engine_segments", "emesh_engine_ring_allreduce", "emesh_engine_outer_sync",
     "emesh_engine_outer_sync_host", "emesh_engine_check", "emesh_engine_payload", "emesh_engine_payload_host",
     "emesh_engine_launches", "emesh_engine_profile", "emesh_engine_profile_read",
+    "emesh_trace_enable", "emesh_trace_read",
 )
 
 OK, ESHAPE, ENUMERIC, EDECODE, ECUDA, ENCCL, ERING, ECONFIG = range(8)
@@ -92,6 +93,8 @@ def lib() -> C.CDLL:
         "emesh_engine_payload": (i32, [vp, u32, P(vp), P(vp), P(vp), P(u64)]),
         "emesh_engine_payload_host": (i32, [vp, u32, vp, vp, vp]),
         "emesh_engine_launches": (u64, [vp]),
+        "emesh_trace_enable": (i32, [u64]),
+        "emesh_trace_read": (u64, [vp, u64]),
         "emesh_engine_profile": (i32, [vp, i32]),
         "emesh_engine_profile_read": (i32, [vp, u32, P(u64), P(C.c_double), P(C.c_double)]),
     }

@@ -63,6 +63,8 @@ struct Seg {
     uint64_t lo, len;
 };
 
+uint32_t quant_lag_tiles();
+
 // One pipelining window: consecutive segments of one rank chunk.
 struct Batch {
     uint32_t chunk = 0, window = 0;
@@ -70,13 +72,15 @@ struct Batch {
     uint64_t el_lo = 0, el_hi = 0;  // element range [el_lo, el_hi)
     uint64_t q_lo = 0, q_hi = 0;    // float4 slot range [q_lo, q_hi)
     uint32_t ncta = 0, nnodes = 0;
-    size_t off_segs = 0, off_cta = 0;  // byte offsets into the table arena
+    size_t off_segs = 0, off_cta = 0, off_order = 0;  // byte offsets into the table arena
     const SegInfo* d_segs = nullptr;
     const uint32_t* d_cta_seg = nullptr;
+    const uint32_t* d_order = nullptr;
 
     void bind(void* base) {
         d_segs = reinterpret_cast<const SegInfo*>((char*)base + off_segs);
         d_cta_seg = reinterpret_cast<const uint32_t*>((char*)base + off_cta);
+        d_order = reinterpret_cast<const uint32_t*>((char*)base + off_order);
     }
 };
 
@@ -114,7 +118,7 @@ struct Plan {
                 const uint64_t q_last = (g.lo + g.len - 1) >> 2;
                 const uint64_t nq = q_last - si.q0 + 1;
                 si.nunits = (uint32_t)((nq + kUnitSlots - 1) / kUnitSlots);
-                si.ncta = (si.nunits + kWarps - 1) / kWarps;
+                si.ncta = (si.nunits + kTileUnits - 1) / kTileUnits;
                 if (first) { b.el_lo = g.lo; b.q_lo = si.q0; first = false; }
                 b.el_hi = g.lo + g.len;
                 b.q_hi = q_last + 1;
@@ -128,6 +132,29 @@ struct Plan {
         }
         b.ncta = (uint32_t)cseg.size();
         b.nnodes = nodes;
+        // persistent-kernel task order: STATS tiles in segment order; the BIN
+        // tiles of segment s after `lag` further STATS tiles (see kernels.cuh)
+        std::vector<uint32_t> order;
+        {
+            const uint32_t lag = quant_lag_tiles();
+            uint32_t stats_issued = 0;
+            std::vector<std::pair<uint32_t, uint32_t>> pending;  // (segment, stats tiles issued through it)
+            size_t head = 0;
+            auto bins = [&](uint32_t seg) {
+                for (uint32_t t = 0; t < infos[seg].ncta; ++t) order.push_back(0x80000000u | (infos[seg].cta0 + t));
+            };
+            for (uint32_t i = 0; i < infos.size(); ++i) {
+                if (infos[i].ncta == 0) continue;
+                for (uint32_t t = 0; t < infos[i].ncta; ++t) {
+                    order.push_back(infos[i].cta0 + t);
+                    ++stats_issued;
+                    while (head < pending.size() && stats_issued - pending[head].second >= lag) bins(pending[head++].first);
+                }
+                pending.push_back({i, stats_issued});
+            }
+            while (head < pending.size()) bins(pending[head++].first);
+        }
+
         auto append = [&](const void* p, size_t bytes) {
             size_t off = (host_tables.size() + 15) & ~size_t(15);
             host_tables.resize(off + bytes);
@@ -136,6 +163,8 @@ struct Plan {
         };
         b.off_segs = append(infos.data(), infos.size() * sizeof(SegInfo));
         b.off_cta = append(cseg.data(), cseg.size() * sizeof(uint32_t));
+        b.off_order = append(order.data(), order.size() * sizeof(uint32_t));
+
         max_cta = std::max<size_t>(max_cta, b.ncta);
         max_nodes = std::max<size_t>(max_nodes, b.nnodes);
         max_segs = std::max<size_t>(max_segs, b.nseg);
@@ -158,6 +187,14 @@ struct Plan {
 };
 
 constexpr uint64_t kDefaultWindow = (uint64_t)16 << 20;  // elements per pipelining window
+
+int persistent_grid(const void* fn, uint32_t ntasks);
+// Lag between a segment's last STATS tile and its first BIN tile in the task
+// order: 1.5 persistent grids.
+uint32_t quant_lag_tiles() {
+    const int g = persistent_grid((const void*)k_quant<kSrcAminusB | kHasIn>, 1u << 30);
+    return g > 0 ? (uint32_t)(g + g / 2) : 512u;
+}
 
 // Ring plan: k chunks, min(S, len) subs each, windows of G segments.
 Plan make_ring_plan(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems) {
@@ -213,6 +250,7 @@ struct Workspace {
     HistP* node_hist = nullptr;
     uint32_t* tree_cnt = nullptr;
     uint32_t* seg_flags = nullptr;
+    uint32_t* sync = nullptr;
     uint32_t* err = nullptr;
     size_t cap_slots = 0, cap_cta = 0, cap_nodes = 0, cap_segs = 0;
 
@@ -255,13 +293,15 @@ struct Workspace {
         if (segs > cap_segs || !seg_flags) {
             size_t c = 0;
             TRY(grow(seg_flags, c, segs, 1, true));
+            c = 0;
+            TRY(grow(sync, c, kSyncReady + segs, 1, true));
             cap_segs = std::max<size_t>(segs, 1);
         }
         return EMESH_OK;
     }
     void release() {
         cudaFree(scratch); cudaFree(leaf_stat); cudaFree(node_stat); cudaFree(leaf_hist); cudaFree(node_hist);
-        cudaFree(tree_cnt); cudaFree(seg_flags); cudaFree(err);
+        cudaFree(tree_cnt); cudaFree(seg_flags); cudaFree(sync); cudaFree(err);
         *this = Workspace();
     }
 };
@@ -329,6 +369,38 @@ struct Tracker {
 };
 Tracker g_codec_tracker;
 
+// Optional task trace (development aid): emesh_trace_enable / emesh_trace_read.
+struct TraceBuf {
+    TraceRec* buf = nullptr;
+    uint32_t* n = nullptr;
+    size_t cap = 0;
+} g_trace;
+
+// Co-resident grid for the persistent quantizer (cooperative launch).
+int persistent_grid(const void* fn, uint32_t ntasks) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        for (auto& kv : cache)
+            if (kv.first == fn) per_sm = kv.second;
+        if (!per_sm) {
+            if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(QSmem)) != cudaSuccess)
+                return -1;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, sizeof(QSmem)) != cudaSuccess)
+                return -1;
+            cache.push_back({fn, per_sm});
+        }
+    }
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long want = (long long)per_sm * sms;
+    return (int)std::max<long long>(1, std::min<long long>(want, ntasks));
+}
+
 int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t st, Tracker* tr) {
     if (bt.ncta == 0) return EMESH_OK;
     QuantArgs a{};
@@ -359,22 +431,29 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     a.nnodes = (uint32_t)ws.cap_nodes;
     a.seg_flags = ws.seg_flags;
     a.err = ws.err;
-    const dim3 g1(bt.ncta), g2(bt.ncta), blk(kThreads);
+    a.order = bt.d_order;
+    a.sync = ws.sync;
+    a.trace = g_trace.buf;
+    a.trace_n = g_trace.n;
+    a.trace_cap = (uint32_t)g_trace.cap;
+    CU(cudaMemsetAsync(ws.sync, 0, (kSyncReady + (size_t)bt.nseg) * sizeof(uint32_t), st));
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
+    void* args[] = {&a};
+    const void* fn = nullptr;
     switch (io.src) {
-        case kSrcA: k_stats<kSrcA><<<g1, blk, 0, st>>>(a); break;
-        case kSrcAminusB: k_stats<kSrcAminusB><<<g1, blk, 0, st>>>(a); break;
-        case kSrcA | kHasIn: k_stats<kSrcA | kHasIn><<<g1, blk, 0, st>>>(a); break;
-        case kSrcAminusB | kHasIn: k_stats<kSrcAminusB | kHasIn><<<g1, blk, 0, st>>>(a); break;
-        case kSrcA | kHasIn | kDivK: k_stats<kSrcA | kHasIn | kDivK><<<g1, blk, 0, st>>>(a); break;
-        case kSrcAminusB | kHasIn | kDivK: k_stats<kSrcAminusB | kHasIn | kDivK><<<g1, blk, 0, st>>>(a); break;
+        case kSrcA: fn = (const void*)k_quant<kSrcA>; break;
+        case kSrcAminusB: fn = (const void*)k_quant<kSrcAminusB>; break;
+        case kSrcA | kHasIn: fn = (const void*)k_quant<kSrcA | kHasIn>; break;
+        case kSrcAminusB | kHasIn: fn = (const void*)k_quant<kSrcAminusB | kHasIn>; break;
+        case kSrcA | kHasIn | kDivK: fn = (const void*)k_quant<kSrcA | kHasIn | kDivK>; break;
+        case kSrcAminusB | kHasIn | kDivK: fn = (const void*)k_quant<kSrcAminusB | kHasIn | kDivK>; break;
         default: return fail(EMESH_ECONFIG, "unsupported producer %d", io.src);
     }
-    cudaEvent_t e1 = prof ? tr->ev(st) : nullptr;
-    if (io.src == kSrcA) k_bin<false><<<g2, blk, 0, st>>>(a);
-    else k_bin<true><<<g2, blk, 0, st>>>(a);
-    if (tr) tr->launches += 2;
+    const int grid = persistent_grid(fn, 2 * bt.ncta);
+    if (grid <= 0) return fail(EMESH_ECUDA, "k_quant: occupancy query failed");
+    CU(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, sizeof(QSmem), st));
+    if (tr) tr->launches += 1;
     if (prof) {
         cudaEvent_t e2 = tr->ev(st);
         const double elems = (double)(bt.el_hi - bt.el_lo);
@@ -382,8 +461,6 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
                           ((io.src & kHasIn) ? 1028.0 * bt.nseg : 0.0);
         const double wr = elems + 1028.0 * bt.nseg;
         const int fam = (io.src & kDivK) ? 2 : (io.src & kHasIn) ? 1 : (io.src & kSrcAminusB) ? 0 : 3;
-        tr->recs.push_back({kProfStats, e0, e1, rd});
-        tr->recs.push_back({kProfBin, e1, e2, wr});
         tr->recs.push_back({kProfQuantPG + fam, e0, e2, rd + wr});
     }
     CU(cudaGetLastError());
@@ -475,6 +552,27 @@ int emesh_quantize_segments(const float* x, const uint64_t* seg_lo, const uint64
     CU(cudaFreeAsync(d_tables, st));
     CU(cudaFreeAsync(d_stats, st));
     return EMESH_OK;
+}
+
+int emesh_trace_enable(uint64_t records) {
+    if (g_trace.buf) { cudaFree(g_trace.buf); cudaFree(g_trace.n); g_trace = TraceBuf(); }
+    if (!records) return EMESH_OK;
+    CU(cudaMalloc(&g_trace.buf, records * sizeof(TraceRec)));
+    CU(cudaMalloc(&g_trace.n, sizeof(uint32_t)));
+    CU(cudaMemset(g_trace.n, 0, sizeof(uint32_t)));
+    g_trace.cap = records;
+    return EMESH_OK;
+}
+
+uint64_t emesh_trace_read(void* host, uint64_t max_records) {
+    if (!g_trace.buf) return 0;
+    cudaDeviceSynchronize();
+    uint32_t n = 0;
+    cudaMemcpy(&n, g_trace.n, sizeof n, cudaMemcpyDeviceToHost);
+    const uint64_t m = std::min<uint64_t>({(uint64_t)n, (uint64_t)g_trace.cap, max_records});
+    if (host && m) cudaMemcpy(host, g_trace.buf, m * sizeof(TraceRec), cudaMemcpyDeviceToHost);
+    cudaMemset(g_trace.n, 0, sizeof(uint32_t));
+    return m;
 }
 
 int emesh_codec_check(emesh_stream_t stream) {
@@ -738,7 +836,7 @@ std::vector<emesh_ring_op> build_schedule(const Plan& P, uint32_t r) {
 
 int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, float* buf, float* local_out, float* out,
              float lr, float mom) {
-    const uint32_t k = e->k, r = e->rank;
+    const uint32_t k = e->k;
     const bool pg = B != nullptr;
     auto& ar = e->arenas[0];
     cudaStream_t sc = e->s_comp, sm = e->s_comm;
@@ -853,7 +951,14 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
     else cudaGetDevice(&e->device);
     auto bail = [&](int rc) { emesh_engine_destroy(e); return rc; };
     if (cudaSetDevice(e->device) != cudaSuccess) return bail(fail(EMESH_ECUDA, "cudaSetDevice"));
-    uint64_t window = cfg->window_elems ? cfg->window_elems : kDefaultWindow;
+    // default window: a whole chunk for the virtual ring (nothing to overlap
+    // with, and the persistent quantizer pipelines stats and bins across the
+    // segments of a batch); a quarter chunk (>= 16M) under NCCL so transfers
+    // of window j+1 overlap the kernels of window j
+    const uint64_t chunk = (cfg->n + cfg->k - 1) / cfg->k;
+    uint64_t window = cfg->window_elems ? cfg->window_elems
+                      : virt ? std::max<uint64_t>(chunk, 1)
+                             : std::max<uint64_t>(chunk / 4, kDefaultWindow);
     e->plan = make_ring_plan(cfg->n, cfg->k, S, window);
     e->windows = (uint32_t)e->plan.batches[0].size();
     int rc = e->plan.upload();

@@ -37,10 +37,13 @@ constexpr int kWarps = 8;              // warps per CTA
 constexpr int kThreads = kWarps * 32;  // 256
 constexpr int kSlotsPerLane = 8;       // float4 slots per lane per unit
 constexpr int kUnitSlots = 32 * kSlotsPerLane;  // 256 float4 = 1024 elements
+constexpr int kUnitsPerWarp = 4;                 // warp units per tile task
+constexpr int kTileUnits = kWarps * kUnitsPerWarp;  // 32 units = 32768 elements per tile
 
 // Exact fixed-point encoding of one bucket's members for the codebook sums:
 // r(x) = rint((x - base) * scale), a non-negative integer < 2^42 for every
-// fp32 x the bucket can hold. "Narrow" buckets (not touching zero) use
+// fp32 x the bucket can hold, produced by ONE fma: fma(x, scale, K) with
+// K = 2^52 - base*scale lands in [2^52, 2^53), whose mantissa bits are r. "Narrow" buckets (not touching zero) use
 // base = lower threshold and scale = 1/ulp, so r is exact; "wide" buckets
 // (at or near zero) use a quantum Q = 2^-41 of the bucket's magnitude and
 // base = -2^41 Q, i.e. r = x/Q + 2^41. In both cases base*scale is an exact
@@ -49,9 +52,18 @@ constexpr int kUnitSlots = 32 * kSlotsPerLane;  // 256 float4 = 1024 elements
 // equal to the reference's sequential fp64 sum whenever that sum is exact
 // (quant.hpp:74) — always, for narrow buckets of fewer than 2^28 members.
 struct BucketParam {
-    double base;
     double scale;  // 2^-e (power of two)
+    double K;      // 2^52 - base * scale (exact: base * scale is an integer < 2^42)
 };
+// fp32 fast path of the same encoding for buckets whose members lie within a
+// factor of two in magnitude: x - base is exact in fp32 (Sterbenz) and
+// r = (x - base) * scale < 2^24, so r = f2i((x - base) * scale) exactly.
+// scale == 0 marks a bucket that needs the fp64 path.
+struct BucketFast {
+    float base;
+    float scale;
+};
+constexpr double kMagic52 = 4503599627370496.0;  // 2^52
 constexpr int kWideBiasBits = 41;
 
 // Per-segment statistics, written once by the root CTA of k_stats.
@@ -63,6 +75,7 @@ struct SegStat {
     float margin;        // fp32 bucket estimate is exact when its fraction is in (margin, 1-margin)
     float thr[kBuckets];  // thr[j] = smallest fp32 x with code(x) >= j (j=1..255)
     BucketParam bp[kBuckets];
+    BucketFast bf[kBuckets];
 };
 constexpr uint32_t kFlagNonFinite = 1u;
 constexpr uint32_t kFlagDegenerate = 2u;  // sigma == 0 (quant.hpp:49-55)
@@ -149,7 +162,24 @@ struct QuantArgs {
     uint32_t nnodes;
     uint32_t* seg_flags;       // [seg] non-finite bits (reset by the stats root)
     uint32_t* err;             // sticky error word (bit 0: non-finite)
+    uint32_t* sync;            // [0] task counter, [kSyncReady + s] segment s published (zeroed per launch)
+    const uint32_t* order;     // task order, 2 * ncta entries
+    struct TraceRec* trace;    // optional task timeline (nullptr: off)
+    uint32_t* trace_n;
+    uint32_t trace_cap;
 };
+
+
+// Optional per-task timeline (globaltimer ns), for tuning the task plan.
+struct TraceRec {
+    unsigned long long t0, t1, t2, t3;  // claimed/start, ready, main loop done, end
+    uint32_t kind, seg, tile, smid;
+};
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // ---------------------------------------------------------------------------
 // small helpers
@@ -172,6 +202,23 @@ __device__ __forceinline__ uint32_t warp_sum_u(uint32_t v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void spin_until_nonzero(const uint32_t* p) {
+    while (ld_acquire(p) == 0u) __nanosleep(32);
 }
 
 // The reference's bucket function, exactly (quant.hpp:65-72).
@@ -241,15 +288,15 @@ __device__ __forceinline__ bool tree_arrive(TreeCursor& c, uint32_t* counters, u
     // its arrival, so only one thread pays for the fence.
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
+        // acq_rel: releases every partial the CTA wrote before the barrier
+        // (cumulativity) and, for the last arriver, acquires the siblings'
         uint32_t* ctr = counters + node_base + poff + parent;
-        const bool last = atomicAdd(ctr, 1u) == nch - 1;
+        const bool last = atom_add_acq_rel(ctr, 1u) == nch - 1;
         if (last) *ctr = 0;  // re-arm for the next launch (no other arrivals remain)
         *s_flag = last ? 1u : 0u;
     }
     __syncthreads();
     if (!*s_flag) return false;
-    __threadfence();
     c.idx = parent;  // caller combines children [first, first+nch) of the old level
     return true;
 }
@@ -291,62 +338,104 @@ __device__ __forceinline__ int exponent_of(float f) {  // floor(log2|f|) for nor
 }
 
 // Fixed-point parameters of bucket b whose fp32 members lie in [t0, t1).
-__device__ BucketParam bucket_param(float t0, float t1) {
+__device__ BucketParam bucket_param(float t0, float t1, BucketFast* fast) {
     BucketParam p;
-    p.base = (double)t0;
     p.scale = 0.0;
+    p.K = kMagic52;
+    fast->base = t0;
+    fast->scale = 0.f;
     if (!(t1 > t0)) return p;  // holds no fp32 value
     const float last = key2f(f2key(t1) - 1);
     if (t0 > 0.f || last < 0.f) {
         // narrow: every member is a multiple of the ulp of the smallest magnitude
         const float mn = t0 > 0.f ? t0 : last;
+        const float mx = t0 > 0.f ? last : t0;
         const int e = max(exponent_of(mn) - 23, -149);
         const double span = ldexp(__dsub_rn((double)last, (double)t0), -e);
         if (span < 2199023255552.0) {  // 2^41
             p.scale = ldexp(1.0, -e);
+            p.K = __dsub_rn(kMagic52, ldexp((double)t0, -e));  // base = t0
+            // Sterbenz: |max| <= 2 |min| makes x - t0 exact in fp32; then r < 2^24
+            if (fabsf(mx) <= 2.f * fabsf(mn) && e >= -126 && e <= 127 && span < 16777216.0)
+                fast->scale = ldexpf(1.f, -e);
             return p;
         }
     }
     const float mx = fmaxf(fabsf(t0), fabsf(last));
     const int e = exponent_of(mx) + 1 - kWideBiasBits;  // |x| < 2^(e+41)
     p.scale = ldexp(1.0, -e);
-    p.base = -ldexp(1.0, e + kWideBiasBits);
+    p.K = __dadd_rn(kMagic52, 2199023255552.0);  // base = -2^41 Q: r = x/Q + 2^41
     return p;
 }
 
+// ---------------------------------------------------------------------------
+// Persistent quantizer: one launch per batch (pipelining window). CTAs claim
+// tile tasks in plan order (atomic counter); a task only ever waits on work
+// claimed before it (stats of its segment, or the bins that free its scratch
+// slot), and the cooperative launch keeps every CTA resident, so the spins
+// always make progress.
+
+struct QSmem {
+    uint32_t hist[kWarps][kBuckets][3];  // per-warp limbs of one unit (bin), see bin_tile
+    unsigned long long wsum[kWarps][kBuckets];  // per-warp exact sum of r over the tile's units
+    uint32_t wcnt[kWarps][kBuckets];
+    float thr[kBuckets + 1];             // exact threshold table (bin)
+    BucketParam bp[kBuckets];            // fixed-point parameters (bin)
+    BucketFast bf[kBuckets];             // fp32 fast path of the same (bin)
+    float lut[kBuckets];                 // incoming codebook (stats, hop)
+    StatP wp[kWarps];
+    double red[2];
+    uint32_t clip[2];
+    uint32_t flag;
+    uint32_t task;
+    int32_t bin_seg, lut_seg;
+    uint32_t run_idx;
+    unsigned long long t_main;  // trace: main loop done
+};
+
+// Task order (host-built, QuantArgs::order): STATS tiles in segment order,
+// with the BIN tiles of segment s inserted once `lag` further STATS tiles
+// were issued after its last one (lag ~ 1.5 grids: the stats root of s
+// normally publishes before its bins are claimed, and the scratch x of a
+// tile is re-read soon enough to still be in L2). Entry: bit 31 = BIN,
+// low bits = batch tile. Claims are one atomicAdd; a BIN task only ever
+// waits on STATS tiles claimed before it, and only at the top of the loop
+// (when its CTA owes no tree arrival), so the persistent grid always
+// progresses.
+constexpr uint32_t kSyncReady = 32;  // ready flags start on their own 128-B line
+
+
+
 template <int SRC>
-__global__ void __launch_bounds__(kThreads, 3) k_stats(QuantArgs a) {
-    __shared__ float lut[kBuckets];
-    __shared__ StatP wp[kWarps];
-    __shared__ uint32_t s_flag;
-    __shared__ double s_red[2];
-    __shared__ float s_thr[kBuckets + 1];
+__device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si,
+                                           uint32_t tile) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t s = a.cta_seg[blockIdx.x];
-    const SegInfo si = a.segs[s];
-    const uint32_t tile = blockIdx.x - si.cta0;
-    const uint32_t u = tile * kWarps + warp;  // segment-relative unit
     const uint64_t hiel = si.lo + si.len;     // exclusive
-    const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
+    float4* xs = reinterpret_cast<float4*>(a.scratch) - a.scratch_q0;
 
     if (SRC & kHasIn) {
-        lut[threadIdx.x] = a.in_cb[(uint64_t)si.in_slot * kBuckets + threadIdx.x];
-        __syncthreads();
+        if (sm.lut_seg != (int32_t)s) {
+            __syncthreads();
+            sm.lut[threadIdx.x] = __ldcg(a.in_cb + (uint64_t)si.in_slot * kBuckets + threadIdx.x);
+            __syncthreads();
+            if (threadIdx.x == 0) sm.lut_seg = (int32_t)s;
+        }
     }
-
     StatP p{0.0, 0.0, 0.0, 0.0, 0};
-    if (u < si.nunits) {
+    double sum0 = 0.0, sum1 = 0.0, d0 = 0.0, d1 = 0.0, q0 = 0.0, q1 = 0.0;
+    double piv = 0.0;
+    uint32_t cnt = 0;
+    bool have_piv = false;
+    for (int ui = 0; ui < kUnitsPerWarp; ++ui) {
+        const uint32_t u = tile * kTileUnits + ui * kWarps + warp;  // segment-relative unit
+        if (u >= si.nunits) break;
+        const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
         const bool interior = qbase * 4 >= si.lo && (qbase + kUnitSlots) * 4 <= hiel;  // warp-uniform
-        double sum0 = 0.0, sum1 = 0.0, d0 = 0.0, d1 = 0.0, q0 = 0.0, q1 = 0.0;
-        double piv = 0.0;
-        uint32_t cnt = 0;
-        bool have_piv = false;
         constexpr int kHalf = kSlotsPerLane / 2;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             float4 xa[kHalf], xb[kHalf];
             uint32_t c4[kHalf];
-            // issue the half's loads first (memory-level parallelism)
 #pragma unroll
             for (int jj = 0; jj < kHalf; ++jj) {
                 const uint64_t q = qbase + (uint64_t)(h * kHalf + jj) * 32 + lane;
@@ -366,11 +455,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_stats(QuantArgs a) {
                 }
                 if (SRC & kHasIn) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) x[e] = __fadd_rn(x[e], lut[(c4[jj] >> (8 * e)) & 0xff]);
+                    for (int e = 0; e < 4; ++e) x[e] = __fadd_rn(x[e], sm.lut[(c4[jj] >> (8 * e)) & 0xff]);
                 }
                 if (SRC & kDivK) {
-                    // x / k (allreduce.hpp:439): a power-of-two k is an exact
-                    // multiply, otherwise IEEE division
+                    // x / k (allreduce.hpp:439): exact multiply for a power-of-two k
                     if (a.inv_divisor != 0.f) {
 #pragma unroll
                         for (int e = 0; e < 4; ++e) x[e] = __fmul_rn(x[e], a.inv_divisor);
@@ -379,20 +467,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_stats(QuantArgs a) {
                         for (int e = 0; e < 4; ++e) x[e] = __fdiv_rn(x[e], a.divisor);
                     }
                 }
-                uint32_t vm = 0xfu;  // valid-element mask of this float4
-                if (!interior) {
-                    if (e0 >= hiel || e0 + 4 <= si.lo) vm = 0u;
-                    else if (!(e0 >= si.lo && e0 + 4 <= hiel)) {
-                        vm = 0u;
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) vm |= (e0 + e >= si.lo && e0 + e < hiel) ? (1u << e) : 0u;
-                    }
-                }
-                if (!have_piv && vm) {  // pivot: the lane's first value
-                    piv = (double)x[__ffs(vm) - 1];
+                if (interior && !have_piv) {  // pivot: the lane's first value
+                    piv = (double)x[0];
                     have_piv = true;
                 }
-                if (vm == 0xfu) {
+                if (interior) {
                     const double x0 = (double)x[0], x1 = (double)x[1], x2 = (double)x[2], x3 = (double)x[3];
                     const double v0 = __dsub_rn(x0, piv), v1 = __dsub_rn(x1, piv);
                     const double v2 = __dsub_rn(x2, piv), v3 = __dsub_rn(x3, piv);
@@ -402,38 +481,34 @@ __global__ void __launch_bounds__(kThreads, 3) k_stats(QuantArgs a) {
                     d1 = __dadd_rn(__dadd_rn(d1, v1), v3);
                     q0 = __dadd_rn(__dadd_rn(q0, __dmul_rn(v0, v0)), __dmul_rn(v2, v2));
                     q1 = __dadd_rn(__dadd_rn(q1, __dmul_rn(v1, v1)), __dmul_rn(v3, v3));
-                    cnt += 4;
-                } else if (vm) {
+                    if (SRC != kSrcA) xs[q] = make_float4(x[0], x[1], x[2], x[3]);
+                } else {
+                    uint32_t vm = 0u;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) vm |= (e0 + e >= si.lo && e0 + e < hiel) ? (1u << e) : 0u;
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         if (vm & (1u << e)) {
                             const double xd = (double)x[e];
+                            if (!have_piv) { piv = xd; have_piv = true; }
                             const double dv = __dsub_rn(xd, piv);
                             sum0 = __dadd_rn(sum0, xd);
                             d0 = __dadd_rn(d0, dv);
                             q0 = __dadd_rn(q0, __dmul_rn(dv, dv));
                             cnt += 1;
+                            if (SRC != kSrcA) reinterpret_cast<float*>(xs + q)[e] = x[e];
                         }
-                    }
-                }
-                if (SRC != kSrcA && vm) {
-                    float4* dst = reinterpret_cast<float4*>(a.scratch) + (q - a.scratch_q0);
-                    if (vm == 0xfu) {
-                        *dst = make_float4(x[0], x[1], x[2], x[3]);
-                    } else {
-                        float* d1p = reinterpret_cast<float*>(dst);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            if (vm & (1u << e)) d1p[e] = x[e];
                     }
                 }
             }
         }
-        p = StatP{__dadd_rn(sum0, sum1), __dadd_rn(q0, q1), __dadd_rn(d0, d1), piv, (uint64_t)cnt};
+        if (interior) cnt += kSlotsPerLane * 4;  // per lane
     }
+    p = StatP{__dadd_rn(sum0, sum1), __dadd_rn(q0, q1), __dadd_rn(d0, d1), piv, (uint64_t)cnt};
     p = warp_merge(p);
+    if (a.trace && threadIdx.x == 0) sm.t_main = gtimer();
     if (lane == 0) {
-        wp[warp] = p;
+        sm.wp[warp] = p;
         // finite fp32 inputs cannot overflow an fp64 sum: one check per unit
         if (!isfinite(p.s) || !isfinite(p.m2)) {
             atomicOr(&a.seg_flags[s], kFlagNonFinite);
@@ -442,27 +517,31 @@ __global__ void __launch_bounds__(kThreads, 3) k_stats(QuantArgs a) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        StatP t = wp[0];
-        for (int w = 1; w < kWarps; ++w) t = statp_merge(t, wp[w]);
-        a.leaf_stat[blockIdx.x] = t;
+        const uint32_t nxt = atomicAdd(&a.sync[0], 1u);  // claim the next task (in flight while we merge)
+        StatP t = sm.wp[0];
+        for (int w = 1; w < kWarps; ++w) t = statp_merge(t, sm.wp[w]);
+        a.leaf_stat[si.cta0 + tile] = t;
+        sm.task = nxt;
     }
     // ---- combine tree over this segment's tiles
     TreeCursor c{0, tile, si.ncta, 0};
     while (c.n > 1) {
         const uint32_t lvl = c.level, n_old = c.n, off_old = c.off;
-        if (!tree_arrive(c, a.tree_cnt, si.node_base, &s_flag)) return;
+        if (!tree_arrive(c, a.tree_cnt, si.node_base, &sm.flag)) return;
         const uint32_t first = c.idx * kFan, nch = min((uint32_t)kFan, n_old - first);
         const uint32_t poff = lvl == 0 ? 0u : off_old + n_old;
-        if (threadIdx.x == 0) {
-            StatP t{0, 0, 0, 0, 0};
-            for (uint32_t i = 0; i < nch; ++i) {
-                const StatP* src = lvl == 0 ? &a.leaf_stat[si.cta0 + first + i] : &a.node_stat[si.node_base + off_old + first + i];
-                StatP ch;
+        if (threadIdx.x < 32) {
+            // warp 0: lane i loads child i (one latency for all 16), then a
+            // fixed-shape shuffle tree merges them (deterministic)
+            const int ln = threadIdx.x;
+            StatP ch{0, 0, 0, 0, 0};
+            if ((uint32_t)ln < nch) {
+                const StatP* src = lvl == 0 ? &a.leaf_stat[si.cta0 + first + ln] : &a.node_stat[si.node_base + off_old + first + ln];
                 ch.s = __ldcg(&src->s); ch.m2 = __ldcg(&src->m2); ch.d = __ldcg(&src->d);
                 ch.piv = __ldcg(&src->piv); ch.n = __ldcg(&src->n);
-                t = statp_merge(t, ch);
             }
-            a.node_stat[si.node_base + poff + c.idx] = t;
+            ch = warp_merge(ch);
+            if (ln == 0) a.node_stat[si.node_base + poff + c.idx] = ch;
         }
         c.level = lvl + 1;
         c.n = (n_old + kFan - 1) / kFan;
@@ -470,9 +549,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_stats(QuantArgs a) {
     }
     // ---- root: finalize segment statistics (quant.hpp:33-59)
     __syncthreads();
-    __threadfence();
     if (threadIdx.x == 0) {
-        const StatP* src = c.level == 0 ? &a.leaf_stat[blockIdx.x] : &a.node_stat[si.node_base + c.off];
+        const StatP* src = c.level == 0 ? &a.leaf_stat[si.cta0 + tile] : &a.node_stat[si.node_base + c.off];
         StatP t;
         t.s = __ldcg(&src->s); t.m2 = __ldcg(&src->m2); t.d = __ldcg(&src->d); t.piv = __ldcg(&src->piv);
         t.n = __ldcg(&src->n);
@@ -482,11 +560,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_stats(QuantArgs a) {
         double ss = __dadd_rn(t.m2, __dmul_rn(__dmul_rn(2.0, dm), t.d));
         ss = __dadd_rn(ss, __dmul_rn((double)t.n, __dmul_rn(dm, dm)));
         const double var = __ddiv_rn(ss < 0.0 ? 0.0 : ss, (double)si.len);
-        s_red[0] = mu;
-        s_red[1] = __dsqrt_rn(var);
+        sm.red[0] = mu;
+        sm.red[1] = __dsqrt_rn(var);
     }
     __syncthreads();
-    const double mu = s_red[0], sigma = s_red[1];
+    const double mu = sm.red[0], sigma = sm.red[1];
     SegStat* st = &a.stats[si.slot];
     if (threadIdx.x == 0) {
         st->mu = mu;
@@ -509,11 +587,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_stats(QuantArgs a) {
         float hi_dn = (float)hi;
         if ((double)hi_dn > hi) hi_dn = key2f(f2key(hi_dn) - 1);
         const int b = threadIdx.x;
-        s_thr[b] = b == 0 ? lo_up : threshold(b, lo, hi, w);
-        if (b == 0) s_thr[kBuckets] = key2f(f2key(hi_dn) + 1);
+        sm.thr[b] = b == 0 ? lo_up : threshold(b, lo, hi, w);
+        if (b == 0) sm.thr[kBuckets] = key2f(f2key(hi_dn) + 1);
         __syncthreads();
-        st->thr[b] = b == 0 ? -INFINITY : s_thr[b];
-        st->bp[b] = bucket_param(s_thr[b], s_thr[b + 1]);
+        st->thr[b] = b == 0 ? -INFINITY : sm.thr[b];
+        BucketFast bfast;
+        st->bp[b] = bucket_param(sm.thr[b], sm.thr[b + 1], &bfast);
+        st->bf[b] = bfast;
         if (b == 0) {
             st->lo = lo; st->hi = hi; st->width = w;
             const float lo_f = (float)lo, inv_w = (float)__ddiv_rn(1.0, w);
@@ -531,147 +611,226 @@ __global__ void __launch_bounds__(kThreads, 3) k_stats(QuantArgs a) {
             st->margin = mg < 0.25 ? (float)mg : 2.0f;  // 2.0: always use the table
         }
     }
+    __syncthreads();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        sm.bin_seg = -1;  // thr/bp in smem now hold this segment's raw table: force a reload
+        st_release(&a.sync[kSyncReady + s], 1u);  // publish (cumulative over the CTA's SegStat writes)
+    }
 }
 
-// ---------------------------------------------------------------------------
-// K_bin: codes + exact fixed-point bucket histogram. Per warp a private
-// smem histogram of three u32 words per bucket, updated with native 32-bit
-// smem atomics (integer: order-free, hence deterministic):
-//   A += r & 0xffff ; B += (r >> 16) & 0xffff ; C += (r >> 32) + (1 << 21)
-// (one warp unit is <= 1024 elements, so no word overflows). The tile
-// histogram combines the warps into 128-bit sums, then the segment's combine
-// tree; its root turns the sums into the codebook (quant.hpp:78-85).
+// Exact bucket by the threshold table (the rare path of the fp32 estimate).
+__device__ __noinline__ int bucket_walk(float x, int c, const float* thr) {
+    while (c < 255 && x >= thr[c + 1]) ++c;
+    while (c > 0 && x < thr[c]) --c;
+    return c;
+}
+
 template <bool FROM_SCRATCH>
-__global__ void __launch_bounds__(kThreads) k_bin(QuantArgs a) {
-    __shared__ uint32_t hA[kWarps][kBuckets], hB[kWarps][kBuckets], hC[kWarps][kBuckets];
-    __shared__ float thr[kBuckets + 1];
-    __shared__ __align__(16) BucketParam bp[kBuckets];
-    __shared__ uint32_t s_clip[2];
-    __shared__ uint32_t s_flag;
+__device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si, uint32_t tile) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t s = a.cta_seg[blockIdx.x];
-    const SegInfo si = a.segs[s];
-    const uint32_t tile = blockIdx.x - si.cta0;
     const SegStat* st = &a.stats[si.slot];
-    const float lo_f = st->lo_f, inv_w = st->inv_w_f, lo_up = st->lo_up, hi_dn = st->hi_dn;
-    const float margin = st->margin;
-    const bool degenerate = (st->flags & kFlagDegenerate) != 0;
-    {
+    if (sm.bin_seg != (int32_t)s) {
+        __syncthreads();
         const int b = threadIdx.x;
-        thr[b] = st->thr[b];
-        bp[b] = st->bp[b];
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) { hA[w][b] = 0u; hB[w][b] = 0u; hC[w][b] = 0u; }
-        if (b == 0) { thr[0] = -INFINITY; thr[kBuckets] = INFINITY; s_clip[0] = 0u; s_clip[1] = 0u; }
+        sm.thr[b] = b == 0 ? -INFINITY : __ldcg(&st->thr[b]);
+        BucketParam pb;
+        pb.scale = __ldcg(&st->bp[b].scale);
+        pb.K = __ldcg(&st->bp[b].K);
+        sm.bp[b] = pb;
+        BucketFast fb;
+        fb.base = __ldcg(&st->bf[b].base);
+        fb.scale = __ldcg(&st->bf[b].scale);
+        sm.bf[b] = fb;
+        if (b == 0) sm.thr[kBuckets] = INFINITY;
+        __syncthreads();
+        if (threadIdx.x == 0) sm.bin_seg = (int32_t)s;
     }
+    const float lo_f = __ldcg(&st->lo_f), inv_w = __ldcg(&st->inv_w_f);
+    const float lo_up = __ldcg(&st->lo_up), hi_dn = __ldcg(&st->hi_dn);  // x < lo <=> x < lo_up (fp32 x)
+    const float margin = __ldcg(&st->margin), one_m = 1.f - margin;
+    const bool degenerate = (__ldcg(&st->flags) & kFlagDegenerate) != 0;
+    uint32_t* hw = &sm.hist[warp][0][0];
+#pragma unroll
+    for (int i = lane; i < kBuckets * 3; i += 32) hw[i] = 0u;
+#pragma unroll
+    for (int i = lane; i < kBuckets; i += 32) { sm.wsum[warp][i] = 0ull; sm.wcnt[warp][i] = 0u; }
+    if (threadIdx.x < 2) sm.clip[threadIdx.x] = 0u;
     __syncthreads();
 
     const uint64_t hiel = si.lo + si.len;
-    const uint32_t u = tile * kWarps + warp;
-    if (u < si.nunits) {
+    const float4* xs = reinterpret_cast<const float4*>(a.scratch) - a.scratch_q0;
+    uint32_t nclip_lo = 0, nclip_hi = 0;
+    for (int ui = 0; ui < kUnitsPerWarp; ++ui) {
+        const uint32_t u = tile * kTileUnits + ui * kWarps + warp;
+        if (u >= si.nunits) break;
         const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
         const bool interior = qbase * 4 >= si.lo && (qbase + kUnitSlots) * 4 <= hiel;  // warp-uniform
-        uint32_t* wA = hA[warp];
-        uint32_t* wB = hB[warp];
-        uint32_t* wC = hC[warp];
-        float4 xv[kSlotsPerLane];
+        constexpr int kHalf = kSlotsPerLane / 2;
 #pragma unroll
-        for (int j = 0; j < kSlotsPerLane; ++j) {
-            const uint64_t q = qbase + (uint64_t)j * 32 + lane;
-            const bool in = interior || q * 4 < hiel;
-            xv[j] = !in ? make_float4(0.f, 0.f, 0.f, 0.f)
-                        : FROM_SCRATCH ? *(reinterpret_cast<const float4*>(a.scratch) + (q - a.scratch_q0))
-                                       : ld4(a.a, q);
-        }
-        uint32_t nclip_lo = 0, nclip_hi = 0;
+        for (int h = 0; h < 2; ++h) {
+            float4 xv[kHalf];
 #pragma unroll
-        for (int j = 0; j < kSlotsPerLane; ++j) {
-            const uint64_t q = qbase + (uint64_t)j * 32 + lane;
-            const uint64_t e0 = q * 4;
-            uint32_t vm = 0xfu;
-            if (!interior) {
-                if (e0 >= hiel || e0 + 4 <= si.lo) vm = 0u;
-                else if (!(e0 >= si.lo && e0 + 4 <= hiel)) {
-                    vm = 0u;
+            for (int jj = 0; jj < kHalf; ++jj) {
+                const uint64_t q = qbase + (uint64_t)(h * kHalf + jj) * 32 + lane;
+                const bool in = interior || q * 4 < hiel;
+                xv[jj] = !in ? make_float4(0.f, 0.f, 0.f, 0.f) : FROM_SCRATCH ? __ldcg(xs + q) : ld4(a.a, q);
+            }
+            // staged over pairs of float4 (8 elements): bucket math for all,
+            // rare fix-ups, parameter lookups + fixed point, then the atomics —
+            // independent work the scheduler can overlap
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) vm |= (e0 + e >= si.lo && e0 + e < hiel) ? (1u << e) : 0u;
+            for (int pr = 0; pr < kHalf / 2; ++pr) {
+                float xe[8];
+                uint32_t vmask = 0;  // valid elements
+#pragma unroll
+                for (int f = 0; f < 2; ++f) {
+                    const int jj = pr * 2 + f;
+                    const uint64_t e0 = (qbase + (uint64_t)(h * kHalf + jj) * 32 + lane) * 4;
+                    uint32_t vm = 0xfu;
+                    if (!interior) {
+                        vm = 0u;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) vm |= (e0 + e >= si.lo && e0 + e < hiel) ? (1u << e) : 0u;
+                    }
+                    vmask |= vm << (4 * f);
+                    xe[4 * f + 0] = xv[jj].x; xe[4 * f + 1] = xv[jj].y;
+                    xe[4 * f + 2] = xv[jj].z; xe[4 * f + 3] = xv[jj].w;
+                }
+                int cc[8];
+                uint32_t clo_m = 0, chi_m = 0;
+                if (!degenerate) {
+                    bool okall = true;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const float x = xe[i];
+                        const float g = __fmul_rn(__fsub_rn(x, lo_f), inv_w);
+                        const int c = __float2int_rz(g);
+                        const float fr = __fsub_rn(g, __int2float_rz(c));
+                        okall &= (fr > margin) & (fr < one_m) & (x >= lo_up) & (x <= hi_dn);
+                        cc[i] = c;
+                    }
+                    if (!okall) {  // rare: near an edge (exact table) or clipped (quant.hpp:66-67)
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const float x = xe[i];
+                            const float g = __fmul_rn(__fsub_rn(x, lo_f), inv_w);
+                            const float fr = __fsub_rn(g, __int2float_rz(cc[i]));
+                            if (x < lo_up) { cc[i] = 0; clo_m |= 1u << i; }
+                            else if (x > hi_dn) { cc[i] = 255; chi_m |= 1u << i; }
+                            else if (!(fr > margin && fr < one_m)) cc[i] = bucket_walk(x, min(max(cc[i], 0), 255), sm.thr);
+                        }
+                    }
+                    clo_m &= vmask;
+                    chi_m &= vmask;
+                    uint32_t ra[8], rb[8], rc[8];
+                    uint32_t slow_m = 0;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        // fp32 fast path (exact for factor-2 buckets), fp64 otherwise
+                        const BucketFast fb = sm.bf[cc[i]];
+                        const uint32_t rf = __float2uint_rz(__fmul_rn(__fsub_rn(xe[i], fb.base), fb.scale));
+                        const bool clip = ((clo_m | chi_m) >> i) & 1u;  // counted; lo / hi added at the root
+                        slow_m |= (!clip && fb.scale == 0.f) ? (1u << i) : 0u;
+                        ra[i] = clip ? (1u << 21) : ((rf & 0x7ffu) | (1u << 21));
+                        rb[i] = clip ? 0u : (rf >> 11);
+                        rc[i] = 0u;
+                    }
+                    if (slow_m) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            if ((slow_m >> i) & 1u) {
+                                const BucketParam pb = sm.bp[cc[i]];
+                                const double m = __fma_rn((double)xe[i], pb.scale, pb.K);  // 2^52 + r
+                                const uint32_t rlo = (uint32_t)__double2loint(m);
+                                ra[i] = (rlo & 0x7ffu) | (1u << 21);
+                                rb[i] = rlo >> 11;
+                                rc[i] = (uint32_t)__double2hiint(m) & 0x3ffu;
+                            }
+                        }
+                    }
+                    // unit limbs: A = r[0:11) + count<<21, B = r[11:32), C = r[32:42)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        if ((vmask >> i) & 1u) {
+                            uint32_t* hc = hw + 3 * cc[i];
+                            atomicAdd(hc, ra[i]);
+                            if (rb[i]) atomicAdd(hc + 1, rb[i]);
+                            if (rc[i]) atomicAdd(hc + 2, rc[i]);
+                        }
+                    }
+                    nclip_lo += __popc(clo_m);
+                    nclip_hi += __popc(chi_m);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) cc[i] = 0;
+                }
+#pragma unroll
+                for (int f = 0; f < 2; ++f) {
+                    const int jj = pr * 2 + f;
+                    const uint64_t q = qbase + (uint64_t)(h * kHalf + jj) * 32 + lane;
+                    const uint32_t packed = (uint32_t)cc[4 * f] | ((uint32_t)cc[4 * f + 1] << 8) |
+                                            ((uint32_t)cc[4 * f + 2] << 16) | ((uint32_t)cc[4 * f + 3] << 24);
+                    const uint32_t vm = (vmask >> (4 * f)) & 0xfu;
+                    if (vm == 0xfu) {
+                        reinterpret_cast<uint32_t*>(a.out_codes)[q] = packed;
+                    } else if (vm) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (vm & (1u << e)) a.out_codes[q * 4 + e] = (uint8_t)(packed >> (8 * e));
+                    }
                 }
             }
-            uint32_t packed = 0;
-            if (!degenerate) {
+        }
+        // flush the unit's 32-bit limbs into the warp's 64-bit sums (exact)
+        __syncwarp();
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float x = f4get(xv[j], e);
-                    const bool valid = (vm >> e) & 1u;
-                    const bool clo = x < lo_up, chi = x > hi_dn;
-                    // bucket: the fp32 estimate is exact unless it lands within
-                    // `margin` of a bucket edge (or the segment is flagged
-                    // unsafe); then the exact threshold table decides
-                    const float g = fminf(fmaxf(__fmul_rn(__fsub_rn(x, lo_f), inv_w), 0.f), 255.f);
-                    int c = (int)g;
-                    const float fr = __fsub_rn(g, (float)c);
-                    if (!(fr > margin && fr < 1.f - margin)) {
-                        while (c < 255 && x >= thr[c + 1]) ++c;
-                        while (c > 0 && x < thr[c]) --c;
-                    }
-                    c = clo ? 0 : (chi ? 255 : c);
-                    const double2 pb = reinterpret_cast<const double2*>(bp)[c];  // {base, scale}
-                    const double t = (clo || chi) ? pb.x : (double)x;
-                    // r = rint((t - base) * scale) via the 2^52 magic add (exact:
-                    // (t - base) * scale is an exact product, r < 2^42)
-                    const double m = __fma_rn(__dsub_rn(t, pb.x), pb.y, 4503599627370496.0);
-                    const uint32_t rlo = (uint32_t)__double2loint(m);
-                    const uint32_t rhi = (uint32_t)__double2hiint(m) & 0x3ffu;
-                    if (valid) {
-                        atomicAdd(&wA[c], rlo & 0xffffu);
-                        atomicAdd(&wB[c], rlo >> 16);
-                        atomicAdd(&wC[c], rhi + (1u << 21));
-                        nclip_lo += clo ? 1u : 0u;
-                        nclip_hi += chi ? 1u : 0u;
-                    }
-                    packed |= (uint32_t)c << (8 * e);
-                }
-            }
-            if (vm == 0xfu) {
-                reinterpret_cast<uint32_t*>(a.out_codes)[q] = packed;
-            } else if (vm) {
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (vm & (1u << e)) a.out_codes[e0 + e] = (uint8_t)(packed >> (8 * e));
+        for (int b = lane; b < kBuckets; b += 32) {
+            const uint32_t A = hw[3 * b], B = hw[3 * b + 1], Cw = hw[3 * b + 2];
+            if (A) {
+                sm.wsum[warp][b] += (unsigned long long)(A & 0x1fffffu) + ((unsigned long long)B << 11) +
+                                    ((unsigned long long)Cw << 32);
+                sm.wcnt[warp][b] += A >> 21;
+                hw[3 * b] = 0u;
+                hw[3 * b + 1] = 0u;
+                hw[3 * b + 2] = 0u;
             }
         }
-        nclip_lo = warp_sum_u(nclip_lo);
-        nclip_hi = warp_sum_u(nclip_hi);
-        if (lane == 0 && (nclip_lo | nclip_hi)) {
-            atomicAdd(&s_clip[0], nclip_lo);
-            atomicAdd(&s_clip[1], nclip_hi);
-        }
+        __syncwarp();
+    }
+    nclip_lo = warp_sum_u(nclip_lo);
+    nclip_hi = warp_sum_u(nclip_hi);
+    if (lane == 0 && (nclip_lo | nclip_hi)) {
+        atomicAdd(&sm.clip[0], nclip_lo);
+        atomicAdd(&sm.clip[1], nclip_hi);
     }
     __syncthreads();
-    {   // tile histogram (exact; warp order irrelevant but fixed anyway)
+    if (threadIdx.x == 0) {
+        sm.task = atomicAdd(&a.sync[0], 1u);  // claim the next task
+        if (a.trace) sm.t_main = gtimer();
+    }
+    {   // tile histogram (exact integer; order irrelevant)
         const int b = threadIdx.x;
         unsigned long long r = 0;
         uint32_t cn = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
-            const uint32_t C = hC[w][b];
-            r += (unsigned long long)hA[w][b] + ((unsigned long long)hB[w][b] << 16) +
-                 ((unsigned long long)(C & 0x1fffffu) << 32);
-            cn += C >> 21;
+            r += sm.wsum[w][b];
+            cn += sm.wcnt[w][b];
         }
-        HistP* L = &a.leaf_hist[blockIdx.x];
+        HistP* L = &a.leaf_hist[si.cta0 + tile];
         L->rlo[b] = r;
         L->rhi[b] = 0ull;
         L->cnt[b] = cn;
-        if (b < 2) L->clip[b] = s_clip[b];
+        if (b < 2) L->clip[b] = sm.clip[b];
     }
     // ---- combine tree (16 independent loads per thread per level)
     uint32_t* ctr = a.tree_cnt + a.nnodes;
     TreeCursor c{0, tile, si.ncta, 0};
-    const HistP* root = &a.leaf_hist[blockIdx.x];
+    const HistP* root = &a.leaf_hist[si.cta0 + tile];
     while (c.n > 1) {
         const uint32_t lvl = c.level, n_old = c.n, off_old = c.off;
-        if (!tree_arrive(c, ctr, si.node_base, &s_flag)) return;
+        if (!tree_arrive(c, ctr, si.node_base, &sm.flag)) return;
         const uint32_t first = c.idx * kFan, nch = min((uint32_t)kFan, n_old - first);
         const uint32_t poff = lvl == 0 ? 0u : off_old + n_old;
         const int b = threadIdx.x;
@@ -710,40 +869,78 @@ __global__ void __launch_bounds__(kThreads) k_bin(QuantArgs a) {
         c.off = poff;
     }
     __syncthreads();
-    __threadfence();
     // ---- root: codebook (quant.hpp:78-85)
     const int b = threadIdx.x;
     float* cb = a.out_cb + (uint64_t)si.slot * kBuckets;
-    if (degenerate) { cb[b] = (float)st->mu; return; }
+    if (degenerate) { cb[b] = (float)__ldcg(&st->mu); return; }
     const unsigned long long rl = __ldcg(&root->rlo[b]), rh = __ldcg(&root->rhi[b]);
     const uint32_t total = __ldcg(&root->cnt[b]);  // clipped members included, with r = 0
     const uint32_t clip = b == 0 ? __ldcg(&root->clip[0]) : (b == 255 ? __ldcg(&root->clip[1]) : 0u);
     const uint32_t cnt = total - clip;
     if (total == 0) {
-        cb[b] = (float)__dadd_rn(st->lo, __dmul_rn(__dadd_rn((double)b, 0.5), st->width));
+        cb[b] = (float)__dadd_rn(__ldcg(&st->lo), __dmul_rn(__dadd_rn((double)b, 0.5), __ldcg(&st->width)));
         return;
     }
     double sum = 0.0;
     if (cnt) {
-        const BucketParam pb = st->bp[b];
-        // sum x / Q = sum r + cnt * base * scale (exact integers, 128-bit)
+        const BucketParam pb = sm.bp[b];
+        // sum x * scale = sum r + cnt * base * scale (exact integers, 128-bit);
+        // base * scale = 2^52 - K
         __int128 S = (__int128)(((unsigned __int128)rh << 64) | rl);
-        S += (__int128)(long long)__double2ll_rn(__dmul_rn(pb.base, pb.scale)) * (__int128)cnt;
+        S += (__int128)(long long)__double2ll_rn(__dsub_rn(kMagic52, pb.K)) * (__int128)cnt;
         const long long hi64 = (long long)(S >> 64);
-        double v;
-        if (hi64 == 0 || hi64 == -1) {
-            const long long s64 = (long long)(unsigned long long)S;
-            const bool fits = (hi64 == 0 && s64 >= 0) || (hi64 == -1 && s64 < 0);
-            v = fits ? (double)s64
-                     : __dadd_rn(ldexp((double)hi64, 64), (double)(unsigned long long)S);
-        } else {
-            v = __dadd_rn(ldexp((double)hi64, 64), (double)(unsigned long long)S);
-        }
+        const long long s64 = (long long)(unsigned long long)S;
+        const bool fits = (hi64 == 0 && s64 >= 0) || (hi64 == -1 && s64 < 0);
+        const double v = fits ? (double)s64 : __dadd_rn(ldexp((double)hi64, 64), (double)(unsigned long long)S);
         sum = __ddiv_rn(v, pb.scale);  // exact: scale is a power of two
     }
-    if (b == 0 && clip) sum = __dadd_rn(sum, __dmul_rn((double)clip, st->lo));
-    if (b == 255 && clip) sum = __dadd_rn(sum, __dmul_rn((double)clip, st->hi));
+    if (b == 0 && clip) sum = __dadd_rn(sum, __dmul_rn((double)clip, __ldcg(&st->lo)));
+    if (b == 255 && clip) sum = __dadd_rn(sum, __dmul_rn((double)clip, __ldcg(&st->hi)));
     cb[b] = (float)__ddiv_rn(sum, (double)total);
+}
+
+template <int SRC>
+__global__ void __launch_bounds__(kThreads, 3) k_quant(QuantArgs a) {
+    extern __shared__ __align__(16) unsigned char qsmem_raw[];
+    QSmem& sm = *reinterpret_cast<QSmem*>(qsmem_raw);  // dynamic: sizeof(QSmem) > 48 KB
+    if (threadIdx.x == 0) {
+        sm.bin_seg = -1;
+        sm.lut_seg = -1;
+        sm.task = atomicAdd(&a.sync[0], 1u);
+    }
+    for (;;) {
+        __syncthreads();
+        const uint32_t t = sm.task;  // claimed by thread 0 in the previous tile's epilogue
+        if (t >= 2 * a.ncta) return;
+        const uint32_t v = a.order[t];
+        const bool is_bin = (v >> 31) != 0;
+        const uint32_t ct = v & 0x7fffffffu;
+        const uint32_t s = a.cta_seg[ct];
+        const SegInfo si = a.segs[s];
+        const uint32_t tile = ct - si.cta0;
+        unsigned long long t0 = 0, t1 = 0;
+        if (a.trace) t0 = gtimer();
+        if (is_bin && threadIdx.x == 0) {
+            // acquire SegStat(s); the CTA owes nothing at this point
+            uint32_t ns = 32;
+            while (ld_acquire(&a.sync[kSyncReady + s]) == 0u) {
+                __nanosleep(ns);
+                ns = ns < 1024 ? 2 * ns : ns;
+            }
+        }
+        if (a.trace) t1 = gtimer();
+        __syncthreads();  // everyone has read sm.task; SegStat(s) visible for BIN
+        if (!is_bin) stats_tile<SRC>(a, sm, s, si, tile);
+        else bin_tile<SRC != kSrcA>(a, sm, s, si, tile);
+        if (a.trace && threadIdx.x == 0) {
+            const uint32_t i = atomicAdd(a.trace_n, 1u);
+            if (i < a.trace_cap) {
+                uint32_t smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                a.trace[i] = TraceRec{t0, t1, sm.t_main, gtimer(), is_bin ? 1u : 0u, s, tile, smid};
+            }
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -777,9 +974,10 @@ __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
     const SegInfo si = a.segs[a.cta_seg[blockIdx.x]];
     lut[threadIdx.x] = a.cb[(uint64_t)si.slot * kBuckets + threadIdx.x];
     __syncthreads();
-    const uint32_t u = (blockIdx.x - si.cta0) * kWarps + warp;
-    if (u >= si.nunits) return;
     const uint64_t hiel = si.lo + si.len;
+    for (int ui = 0; ui < kUnitsPerWarp; ++ui) {
+    const uint32_t u = (blockIdx.x - si.cta0) * kTileUnits + ui * kWarps + warp;
+    if (u >= si.nunits) return;
     const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
 #pragma unroll 4
     for (int j = 0; j < kSlotsPerLane; ++j) {
@@ -818,6 +1016,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
                     }
             }
         }
+    }
     }
 }
 
