@@ -190,10 +190,11 @@ constexpr uint64_t kDefaultWindow = (uint64_t)16 << 20;  // elements per pipelin
 
 int persistent_grid(const void* fn, uint32_t ntasks);
 // Lag between a segment's last STATS tile and its first BIN tile in the task
-// order: 1.5 persistent grids.
+// order: one persistent grid (the stats root publishes within about one
+// tile time; longer lags push scratch x out of L2).
 uint32_t quant_lag_tiles() {
     const int g = persistent_grid((const void*)k_quant<kSrcAminusB | kHasIn>, 1u << 30);
-    return g > 0 ? (uint32_t)(g + g / 2) : 512u;
+    return g > 0 ? (uint32_t)g : 512u;
 }
 
 // Ring plan: k chunks, min(S, len) subs each, windows of G segments.

@@ -37,8 +37,8 @@ constexpr int kWarps = 8;              // warps per CTA
 constexpr int kThreads = kWarps * 32;  // 256
 constexpr int kSlotsPerLane = 8;       // float4 slots per lane per unit
 constexpr int kUnitSlots = 32 * kSlotsPerLane;  // 256 float4 = 1024 elements
-constexpr int kUnitsPerWarp = 4;                 // warp units per tile task
-constexpr int kTileUnits = kWarps * kUnitsPerWarp;  // 32 units = 32768 elements per tile
+constexpr int kUnitsPerWarp = 2;                 // warp units per tile task
+constexpr int kTileUnits = kWarps * kUnitsPerWarp;  // 16 units = 16384 elements per tile
 
 // Exact fixed-point encoding of one bucket's members for the codebook sums:
 // r(x) = rint((x - base) * scale), a non-negative integer < 2^42 for every
@@ -376,9 +376,7 @@ __device__ BucketParam bucket_param(float t0, float t1, BucketFast* fast) {
 // always make progress.
 
 struct QSmem {
-    uint32_t hist[kWarps][kBuckets][3];  // per-warp limbs of one unit (bin), see bin_tile
-    unsigned long long wsum[kWarps][kBuckets];  // per-warp exact sum of r over the tile's units
-    uint32_t wcnt[kWarps][kBuckets];
+    uint32_t hist[kWarps][kBuckets][3];  // per-warp limbs over the tile (bin), see bin_unit
     float thr[kBuckets + 1];             // exact threshold table (bin)
     BucketParam bp[kBuckets];            // fixed-point parameters (bin)
     BucketFast bf[kBuckets];             // fp32 fast path of the same (bin)
@@ -626,6 +624,150 @@ __device__ __noinline__ int bucket_walk(float x, int c, const float* thr) {
     return c;
 }
 
+
+struct BinParams {
+    float lo_f, inv_w, lo_up, hi_dn, margin, one_m;
+};
+
+// One warp unit of the bin pass (1024 elements; this lane's 32), in groups of
+// 8: bucket estimates for all 8, rare fix-ups (exact table near an edge,
+// clipping), fixed-point codes via the fp32 fast path (fp64 for the few
+// buckets that need it), then the limb atomics — unconditional, so the
+// common path has no data-dependent branches (invalid lanes add 0).
+// Per-warp limbs over a tile (<= 2048 members per warp):
+//   A += r[0:9) | 1 << 20   (count in bits 20..31)
+//   B += r[9:30)
+//   C += r[30:42)           (fp64 path only; fast-path r < 2^24)
+template <bool INTERIOR, bool FROM_SCRATCH>
+__device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const SegInfo& si, uint64_t qbase,
+                                         uint64_t hiel, const float4* xs, uint32_t* hw, const BinParams& p,
+                                         uint32_t& nclip_lo, uint32_t& nclip_hi) {
+    const int lane = threadIdx.x & 31;
+    constexpr int kHalf = kSlotsPerLane / 2;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+        float4 xv[kHalf];
+#pragma unroll
+        for (int jj = 0; jj < kHalf; ++jj) {
+            const uint64_t q = qbase + (uint64_t)(h * kHalf + jj) * 32 + lane;
+            const bool in = INTERIOR || q * 4 < hiel;
+            xv[jj] = !in ? make_float4(0.f, 0.f, 0.f, 0.f) : FROM_SCRATCH ? __ldcg(xs + q) : ld4(a.a, q);
+        }
+#pragma unroll
+        for (int pr = 0; pr < kHalf / 2; ++pr) {
+            float xe[8] = {xv[2 * pr].x, xv[2 * pr].y, xv[2 * pr].z, xv[2 * pr].w,
+                           xv[2 * pr + 1].x, xv[2 * pr + 1].y, xv[2 * pr + 1].z, xv[2 * pr + 1].w};
+            const uint64_t q0 = qbase + (uint64_t)(h * kHalf + 2 * pr) * 32 + lane;
+            uint32_t vmask = 0xffu;
+            if (!INTERIOR) {
+                vmask = 0u;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const uint64_t e = (q0 + (uint64_t)(i >> 2) * 32) * 4 + (i & 3);
+                    vmask |= (e >= si.lo && e < hiel) ? (1u << i) : 0u;
+                }
+            }
+            int cc[8];
+            bool okall = true;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                // in range and clear of every bucket edge by the proven margin:
+                // then trunc(g) is the exact bucket. Clipped x fails this test
+                // (g < margin or g > 256 - margin), see SegStat::margin.
+                const float g = __fmul_rn(__fsub_rn(xe[i], p.lo_f), p.inv_w);
+                const int c = __float2int_rz(g);
+                const float fr = __fsub_rn(g, __int2float_rz(c));
+                okall &= (fr > p.margin) & (fr < p.one_m) & ((uint32_t)c < 256u);
+                cc[i] = c;
+            }
+            if (!okall) {  // rare: near an edge (exact table) or clipped (quant.hpp:66-67)
+                uint32_t clo_m = 0, chi_m = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float x = xe[i];
+                    const float g = __fmul_rn(__fsub_rn(x, p.lo_f), p.inv_w);
+                    const int c0 = __float2int_rz(g);
+                    const float fr = __fsub_rn(g, __int2float_rz(c0));
+                    if (x < p.lo_up) {
+                        cc[i] = 0; clo_m |= 1u << i;
+                        xe[i] = sm.bf[0].base;   // r = 0: counted, contributes lo at the root
+                    } else if (x > p.hi_dn) {
+                        cc[i] = 255; chi_m |= 1u << i;
+                        xe[i] = sm.bf[255].base;
+                    } else if (!(fr > p.margin && fr < p.one_m && (uint32_t)c0 < 256u)) {
+                        cc[i] = bucket_walk(x, min(max(c0, 0), 255), sm.thr);
+                    }
+                }
+                nclip_lo += __popc(clo_m & vmask);
+                nclip_hi += __popc(chi_m & vmask);
+            }
+            uint32_t ra[8], rb[8];
+            uint32_t slow_m = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const BucketFast fb = sm.bf[cc[i]];
+                const uint32_t rf = __float2uint_rz(__fmul_rn(__fsub_rn(xe[i], fb.base), fb.scale));
+                slow_m |= fb.scale == 0.f ? (1u << i) : 0u;
+                const bool valid = (vmask >> i) & 1u;
+                ra[i] = valid ? ((rf & 0x1ffu) | (1u << 20)) : 0u;
+                rb[i] = valid ? (rf >> 9) : 0u;
+            }
+            slow_m &= vmask;
+            if (slow_m) {  // fp64 path: wide / large-span buckets
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if ((slow_m >> i) & 1u) {
+                        const BucketParam pb = sm.bp[cc[i]];
+                        const double m = __fma_rn((double)xe[i], pb.scale, pb.K);  // 2^52 + r
+                        const uint32_t rlo = (uint32_t)__double2loint(m);
+                        const uint32_t rhi = (uint32_t)__double2hiint(m) & 0x3ffu;
+                        ra[i] = (rlo & 0x1ffu) | (1u << 20);
+                        rb[i] = (rlo >> 9) & 0x1fffffu;
+                        const uint32_t rc = (rlo >> 30) | (rhi << 2);
+                        if (rc) atomicAdd(hw + 3 * cc[i] + 2, rc);
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                uint32_t* hc = hw + 3 * cc[i];
+                atomicAdd(hc, ra[i]);
+                atomicAdd(hc + 1, rb[i]);
+            }
+            const uint32_t p0 = __byte_perm(__byte_perm(cc[0], cc[1], 0x0040), __byte_perm(cc[2], cc[3], 0x0040), 0x5410);
+            const uint32_t p1 = __byte_perm(__byte_perm(cc[4], cc[5], 0x0040), __byte_perm(cc[6], cc[7], 0x0040), 0x5410);
+            if (INTERIOR) {
+                reinterpret_cast<uint32_t*>(a.out_codes)[q0] = p0;
+                reinterpret_cast<uint32_t*>(a.out_codes)[q0 + 32] = p1;
+            } else {
+#pragma unroll
+                for (int f = 0; f < 2; ++f) {
+                    const uint64_t q = q0 + (uint64_t)f * 32;
+                    const uint32_t packed = f ? p1 : p0;
+                    const uint32_t vm = (vmask >> (4 * f)) & 0xfu;
+                    if (vm == 0xfu) {
+                        reinterpret_cast<uint32_t*>(a.out_codes)[q] = packed;
+                    } else if (vm) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (vm & (1u << e)) a.out_codes[q * 4 + e] = (uint8_t)(packed >> (8 * e));
+                    }
+                }
+            }
+        }
+        if (FROM_SCRATCH && INTERIOR) {
+            // this half's 2 KB of scratch x is consumed (each element is read
+            // exactly once): drop the 128-B L2 lines wholly inside it without
+            // write-back — x was only ever meant as an L2 round trip
+            const uintptr_t lo_b = reinterpret_cast<uintptr_t>(xs + qbase + (uint64_t)h * kHalf * 32);
+            const uintptr_t hi_b = lo_b + (uintptr_t)kHalf * 32 * 16;
+            const uintptr_t line = ((lo_b + 127) & ~(uintptr_t)127) + (uintptr_t)lane * 128;
+            if (lane < 16 && line + 128 <= hi_b)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
+        }
+    }
+}
+
 template <bool FROM_SCRATCH>
 __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si, uint32_t tile) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -650,153 +792,30 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
     const float lo_up = __ldcg(&st->lo_up), hi_dn = __ldcg(&st->hi_dn);  // x < lo <=> x < lo_up (fp32 x)
     const float margin = __ldcg(&st->margin), one_m = 1.f - margin;
     const bool degenerate = (__ldcg(&st->flags) & kFlagDegenerate) != 0;
-    uint32_t* hw = &sm.hist[warp][0][0];
-#pragma unroll
-    for (int i = lane; i < kBuckets * 3; i += 32) hw[i] = 0u;
-#pragma unroll
-    for (int i = lane; i < kBuckets; i += 32) { sm.wsum[warp][i] = 0ull; sm.wcnt[warp][i] = 0u; }
+    uint32_t* hw = &sm.hist[warp][0][0];  // zero on entry (kernel start / previous tile's combine)
     if (threadIdx.x < 2) sm.clip[threadIdx.x] = 0u;
     __syncthreads();
 
     const uint64_t hiel = si.lo + si.len;
     const float4* xs = reinterpret_cast<const float4*>(a.scratch) - a.scratch_q0;
     uint32_t nclip_lo = 0, nclip_hi = 0;
+    const BinParams bpar{lo_f, inv_w, lo_up, hi_dn, margin, one_m};
     for (int ui = 0; ui < kUnitsPerWarp; ++ui) {
         const uint32_t u = tile * kTileUnits + ui * kWarps + warp;
         if (u >= si.nunits) break;
         const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
         const bool interior = qbase * 4 >= si.lo && (qbase + kUnitSlots) * 4 <= hiel;  // warp-uniform
-        constexpr int kHalf = kSlotsPerLane / 2;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            float4 xv[kHalf];
-#pragma unroll
-            for (int jj = 0; jj < kHalf; ++jj) {
-                const uint64_t q = qbase + (uint64_t)(h * kHalf + jj) * 32 + lane;
-                const bool in = interior || q * 4 < hiel;
-                xv[jj] = !in ? make_float4(0.f, 0.f, 0.f, 0.f) : FROM_SCRATCH ? __ldcg(xs + q) : ld4(a.a, q);
+        if (degenerate) {  // sigma == 0: every code is 0 (quant.hpp:49-55)
+            for (int j = 0; j < kSlotsPerLane; ++j) {
+                const uint64_t q = qbase + (uint64_t)j * 32 + lane;
+                for (int e = 0; e < 4; ++e)
+                    if (q * 4 + e >= si.lo && q * 4 + e < hiel) a.out_codes[q * 4 + e] = 0;
             }
-            // staged over pairs of float4 (8 elements): bucket math for all,
-            // rare fix-ups, parameter lookups + fixed point, then the atomics —
-            // independent work the scheduler can overlap
-#pragma unroll
-            for (int pr = 0; pr < kHalf / 2; ++pr) {
-                float xe[8];
-                uint32_t vmask = 0;  // valid elements
-#pragma unroll
-                for (int f = 0; f < 2; ++f) {
-                    const int jj = pr * 2 + f;
-                    const uint64_t e0 = (qbase + (uint64_t)(h * kHalf + jj) * 32 + lane) * 4;
-                    uint32_t vm = 0xfu;
-                    if (!interior) {
-                        vm = 0u;
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) vm |= (e0 + e >= si.lo && e0 + e < hiel) ? (1u << e) : 0u;
-                    }
-                    vmask |= vm << (4 * f);
-                    xe[4 * f + 0] = xv[jj].x; xe[4 * f + 1] = xv[jj].y;
-                    xe[4 * f + 2] = xv[jj].z; xe[4 * f + 3] = xv[jj].w;
-                }
-                int cc[8];
-                uint32_t clo_m = 0, chi_m = 0;
-                if (!degenerate) {
-                    bool okall = true;
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const float x = xe[i];
-                        const float g = __fmul_rn(__fsub_rn(x, lo_f), inv_w);
-                        const int c = __float2int_rz(g);
-                        const float fr = __fsub_rn(g, __int2float_rz(c));
-                        okall &= (fr > margin) & (fr < one_m) & (x >= lo_up) & (x <= hi_dn);
-                        cc[i] = c;
-                    }
-                    if (!okall) {  // rare: near an edge (exact table) or clipped (quant.hpp:66-67)
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const float x = xe[i];
-                            const float g = __fmul_rn(__fsub_rn(x, lo_f), inv_w);
-                            const float fr = __fsub_rn(g, __int2float_rz(cc[i]));
-                            if (x < lo_up) { cc[i] = 0; clo_m |= 1u << i; }
-                            else if (x > hi_dn) { cc[i] = 255; chi_m |= 1u << i; }
-                            else if (!(fr > margin && fr < one_m)) cc[i] = bucket_walk(x, min(max(cc[i], 0), 255), sm.thr);
-                        }
-                    }
-                    clo_m &= vmask;
-                    chi_m &= vmask;
-                    uint32_t ra[8], rb[8], rc[8];
-                    uint32_t slow_m = 0;
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        // fp32 fast path (exact for factor-2 buckets), fp64 otherwise
-                        const BucketFast fb = sm.bf[cc[i]];
-                        const uint32_t rf = __float2uint_rz(__fmul_rn(__fsub_rn(xe[i], fb.base), fb.scale));
-                        const bool clip = ((clo_m | chi_m) >> i) & 1u;  // counted; lo / hi added at the root
-                        slow_m |= (!clip && fb.scale == 0.f) ? (1u << i) : 0u;
-                        ra[i] = clip ? (1u << 21) : ((rf & 0x7ffu) | (1u << 21));
-                        rb[i] = clip ? 0u : (rf >> 11);
-                        rc[i] = 0u;
-                    }
-                    if (slow_m) {
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            if ((slow_m >> i) & 1u) {
-                                const BucketParam pb = sm.bp[cc[i]];
-                                const double m = __fma_rn((double)xe[i], pb.scale, pb.K);  // 2^52 + r
-                                const uint32_t rlo = (uint32_t)__double2loint(m);
-                                ra[i] = (rlo & 0x7ffu) | (1u << 21);
-                                rb[i] = rlo >> 11;
-                                rc[i] = (uint32_t)__double2hiint(m) & 0x3ffu;
-                            }
-                        }
-                    }
-                    // unit limbs: A = r[0:11) + count<<21, B = r[11:32), C = r[32:42)
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        if ((vmask >> i) & 1u) {
-                            uint32_t* hc = hw + 3 * cc[i];
-                            atomicAdd(hc, ra[i]);
-                            if (rb[i]) atomicAdd(hc + 1, rb[i]);
-                            if (rc[i]) atomicAdd(hc + 2, rc[i]);
-                        }
-                    }
-                    nclip_lo += __popc(clo_m);
-                    nclip_hi += __popc(chi_m);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) cc[i] = 0;
-                }
-#pragma unroll
-                for (int f = 0; f < 2; ++f) {
-                    const int jj = pr * 2 + f;
-                    const uint64_t q = qbase + (uint64_t)(h * kHalf + jj) * 32 + lane;
-                    const uint32_t packed = (uint32_t)cc[4 * f] | ((uint32_t)cc[4 * f + 1] << 8) |
-                                            ((uint32_t)cc[4 * f + 2] << 16) | ((uint32_t)cc[4 * f + 3] << 24);
-                    const uint32_t vm = (vmask >> (4 * f)) & 0xfu;
-                    if (vm == 0xfu) {
-                        reinterpret_cast<uint32_t*>(a.out_codes)[q] = packed;
-                    } else if (vm) {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            if (vm & (1u << e)) a.out_codes[q * 4 + e] = (uint8_t)(packed >> (8 * e));
-                    }
-                }
-            }
+        } else if (interior) {
+            bin_unit<true, FROM_SCRATCH>(a, sm, si, qbase, hiel, xs, hw, bpar, nclip_lo, nclip_hi);
+        } else {
+            bin_unit<false, FROM_SCRATCH>(a, sm, si, qbase, hiel, xs, hw, bpar, nclip_lo, nclip_hi);
         }
-        // flush the unit's 32-bit limbs into the warp's 64-bit sums (exact)
-        __syncwarp();
-#pragma unroll
-        for (int b = lane; b < kBuckets; b += 32) {
-            const uint32_t A = hw[3 * b], B = hw[3 * b + 1], Cw = hw[3 * b + 2];
-            if (A) {
-                sm.wsum[warp][b] += (unsigned long long)(A & 0x1fffffu) + ((unsigned long long)B << 11) +
-                                    ((unsigned long long)Cw << 32);
-                sm.wcnt[warp][b] += A >> 21;
-                hw[3 * b] = 0u;
-                hw[3 * b + 1] = 0u;
-                hw[3 * b + 2] = 0u;
-            }
-        }
-        __syncwarp();
     }
     nclip_lo = warp_sum_u(nclip_lo);
     nclip_hi = warp_sum_u(nclip_hi);
@@ -809,14 +828,18 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
         sm.task = atomicAdd(&a.sync[0], 1u);  // claim the next task
         if (a.trace) sm.t_main = gtimer();
     }
-    {   // tile histogram (exact integer; order irrelevant)
+    {   // tile histogram (exact integer; order irrelevant); re-zero the limbs
         const int b = threadIdx.x;
         unsigned long long r = 0;
         uint32_t cn = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
-            r += sm.wsum[w][b];
-            cn += sm.wcnt[w][b];
+            const uint32_t A = sm.hist[w][b][0], B = sm.hist[w][b][1], C = sm.hist[w][b][2];
+            r += (unsigned long long)(A & 0xfffffu) + ((unsigned long long)B << 9) + ((unsigned long long)C << 30);
+            cn += A >> 20;
+            sm.hist[w][b][0] = 0u;
+            sm.hist[w][b][1] = 0u;
+            sm.hist[w][b][2] = 0u;
         }
         HistP* L = &a.leaf_hist[si.cta0 + tile];
         L->rlo[b] = r;
@@ -903,6 +926,7 @@ template <int SRC>
 __global__ void __launch_bounds__(kThreads, 3) k_quant(QuantArgs a) {
     extern __shared__ __align__(16) unsigned char qsmem_raw[];
     QSmem& sm = *reinterpret_cast<QSmem*>(qsmem_raw);  // dynamic: sizeof(QSmem) > 48 KB
+    for (uint32_t i = threadIdx.x; i < kWarps * kBuckets * 3; i += kThreads) (&sm.hist[0][0][0])[i] = 0u;
     if (threadIdx.x == 0) {
         sm.bin_seg = -1;
         sm.lut_seg = -1;
