@@ -31,7 +31,7 @@ UNIT = "params/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=float, default=1e9, help="params per worker (config 2: 1B)")
@@ -52,7 +52,7 @@ def parse():
 class ClockSampler:
     """nvidia-smi sampled during the timed region (B200_PROFILING.md recipe)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
@@ -65,7 +65,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except OSError:
@@ -74,7 +74,16 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            if self.live:
+                self.rows.append([c.strip() for c in line.split(",")])
+
+    live = False
+
+    def start(self):
+        self.live = True
+
+    def stop(self):
+        self.live = False
 
     def __exit__(self, *a):
         if self.proc:
@@ -87,12 +96,17 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in self.rows if r and num(r[0]) is not None]
+        mx = [num(r[1]) for r in self.rows if len(r) > 1 and num(r[1]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for r in self.rows:
-            for nm, v in zip(names, r[3:7]):
+            for nm, v in zip(names, r[4:8]):
                 if v.strip().lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
@@ -236,20 +250,24 @@ def main():
         torch.cuda.synchronize()
         return
 
+    clk = ClockSampler(local_rank).__enter__()  # started early: nvidia-smi needs time to come up
     for _ in range(args.warmup):
         step()
     eng.check()
     barrier()
+    time.sleep(0.3)
     launches0 = eng.launches()
     eng.profile(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
-        barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        barrier()
+    barrier()
+    clk.start()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    barrier()
+    clk.stop()
+    clk.__exit__()
     ms_local = ev0.elapsed_time(ev1)
     launches = eng.launches() - launches0
     prof = eng.profile_read()
@@ -269,15 +287,42 @@ def main():
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    fams = {kname: v for kname, v in prof.items() if kname not in ("k_stats", "k_bin")}
-    dom = max(fams.items(), key=lambda kv: kv[1]["ms"]) if fams else (None, None)
-    roofline = None
-    if dom[0]:
-        d = dom[1]
+    # per KERNEL (the quantizer k_quant serves the pg/hop/final families;
+    # k_apply<1> is dequant+Nesterov; k_nesterov_f32 the k=1 round)
+    by_kernel = {}
+    for kname, v in prof.items():
+        kern = {"quant_pg": "k_quant", "quant_hop": "k_quant", "quant_final": "k_quant", "quant_plain": "k_quant",
+                "dequant_nesterov": "k_apply", "dequantize": "k_apply",
+                "fused_pg_nesterov_k1": "k_nesterov_f32"}.get(kname)
+        if kern is None:
+            continue
+        agg = by_kernel.setdefault(kern, {"ms": 0.0, "alg_bytes": 0.0, "launches": 0})
+        agg["ms"] += v["ms"]
+        agg["alg_bytes"] += v["alg_bytes"]
+        agg["launches"] += v["launches"]
+
+    def roof(kern, d):
         achieved = d["alg_bytes"] / (d["ms"] / 1e3) / 1e9
-        roofline = {"bound": "hbm", "kernel": dom[0], "achieved": round(achieved, 1), "peak": hbm_peak,
-                    "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
-                    "share_of_step": round(d["ms"] / (ms_local), 4)}
+        return {"bound": "hbm", "kernel": kern, "achieved": round(achieved, 1), "peak": hbm_peak,
+                "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                "share_of_step": round(d["ms"] / ms_local, 4),
+                "alg_bytes_per_launch": round(d["alg_bytes"] / max(d["launches"], 1)),
+                "avg_launch_ms": round(d["ms"] / max(d["launches"], 1), 4)}
+
+    ranked = sorted(by_kernel.items(), key=lambda kv: -kv[1]["ms"])
+    roofline = roof(*ranked[0]) if ranked else None
+    roofline_others = [roof(*kv) for kv in ranked[1:]]
+    # DRAM traffic per launch from the committed ncu --set full capture of this
+    # configuration (profiles/), scaled per algorithmic byte; null if absent
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        for r in [roofline] + roofline_others:
+            t = tr.get(r["kernel"]) if r else None
+            if t and t.get("dram_bytes") and t.get("alg_bytes"):
+                r["traffic"] = round(r["alg_bytes_per_launch"] * t["dram_bytes"] / t["alg_bytes"])
+                r["traffic_source"] = t.get("source")
+    except (OSError, ValueError):
+        pass
     kernels = {kname: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,
                        "GB/s_alg": round(v["alg_bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] else None}
                for kname, v in prof.items()}
@@ -322,7 +367,8 @@ def main():
             "config": config_block(args, k, n),
             "hbm_alg_GBps_per_gpu": round(step_alg_gbs, 1),
             "hbm_frac_step": round(step_alg_gbs / hbm_peak, 4),
-            "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "roofline_other_kernels": roofline_others, "kernels": kernels,
+            "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -402,7 +403,8 @@ int persistent_grid(const void* fn, uint32_t ntasks) {
     return (int)std::max<long long>(1, std::min<long long>(want, ntasks));
 }
 
-int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t st, Tracker* tr) {
+int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t st, Tracker* tr,
+                 uint32_t reserve_ctas = 0) {
     if (bt.ncta == 0) return EMESH_OK;
     QuantArgs a{};
     a.segs = bt.d_segs;
@@ -451,9 +453,19 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
         case kSrcAminusB | kHasIn | kDivK: fn = (const void*)k_quant<kSrcAminusB | kHasIn | kDivK>; break;
         default: return fail(EMESH_ECONFIG, "unsupported producer %d", io.src);
     }
-    const int grid = persistent_grid(fn, 2 * bt.ncta);
+    // A plain launch suffices: a task is claimed only by a running CTA and only
+    // ever waits on tasks claimed before it, so progress never depends on
+    // co-residency. `reserve` CTA slots stay free for NCCL's kernels so the
+    // ring's transfers overlap this kernel.
+    int grid = persistent_grid(fn, 2 * bt.ncta);
     if (grid <= 0) return fail(EMESH_ECUDA, "k_quant: occupancy query failed");
-    CU(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, sizeof(QSmem), st));
+    grid = std::max(1, grid - (int)reserve_ctas);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = sizeof(QSmem);
+    lc.stream = st;
+    CU(cudaLaunchKernelExC(&lc, fn, args));
     if (tr) tr->launches += 1;
     if (prof) {
         cudaEvent_t e2 = tr->ev(st);
@@ -693,6 +705,7 @@ struct emesh_engine {
     cudaEvent_t ev_entry = nullptr, ev_done = nullptr, ev_comm_done = nullptr;
     std::vector<cudaEvent_t> ev_send, ev_recv;  // per window
     std::vector<emesh_ring_op> schedule;        // NCCL mode program (build_schedule)
+    uint32_t reserve_ctas = 0;                  // quantizer CTA slots left to NCCL (NCCL mode)
     struct Arena {
         uint8_t* codes = nullptr;
         float* cbs = nullptr;
@@ -850,7 +863,7 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
         switch (o.kind) {
             case EMESH_OP_OWN: {
                 QuantIO io{pg ? kSrcAminusB : kSrcA, A, B, nullptr, nullptr, 1.f, ar.codes, ar.cbs, ar.stats};
-                TRY(launch_quant(P[o.recv_chunk][j], e->ws, io, sc, &e->tr));
+                TRY(launch_quant(P[o.recv_chunk][j], e->ws, io, sc, &e->tr, e->reserve_ctas));
                 CU(cudaEventRecord(e->ev_send[j], sc));
                 break;
             }
@@ -865,7 +878,7 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
             case EMESH_OP_QUANT: {
                 CU(cudaStreamWaitEvent(sc, e->ev_recv[j], 0));
                 QuantIO io{hop_src(pg, (uint32_t)o.hop, k), A, B, ar.codes, ar.cbs, (float)k, ar.codes, ar.cbs, ar.stats};
-                TRY(launch_quant(P[o.recv_chunk][j], e->ws, io, sc, &e->tr));
+                TRY(launch_quant(P[o.recv_chunk][j], e->ws, io, sc, &e->tr, e->reserve_ctas));
                 CU(cudaEventRecord(e->ev_send[j], sc));
                 break;
             }
@@ -981,6 +994,8 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
     }
     if (!virt && e->k > 1) {
         e->schedule = build_schedule(e->plan, e->rank);
+        const char* rs = std::getenv("EMESH_NCCL_RESERVE_CTAS");
+        e->reserve_ctas = rs ? (uint32_t)std::atoi(rs) : 0u;
         ncclUniqueId id;
         std::memcpy(&id, cfg->nccl_id, sizeof id);
         ncclResult_t r = ncclCommInitRank(&e->comm, (int)e->k, id, (int)e->rank);
