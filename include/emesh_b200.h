@@ -124,6 +124,12 @@ typedef struct {
 uint64_t emesh_ring_schedule(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems, uint32_t rank,
                              emesh_ring_op* ops, uint64_t max_ops);
 
+/* Development aid: the persistent quantizer's task plan (runs of {first task,
+ * kind 0 stats / 1 root / 2 bin / 3 codebook, segment, first tile}) for one
+ * batch; info = {ntasks, ncta, nseg, ncta of each segment...}. Host-only. */
+uint64_t emesh_debug_batch_runs(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems, uint32_t chunk,
+                                uint32_t window, uint32_t* runs4, uint64_t max_runs, uint32_t* info);
+
 /* NCCL unique id for emesh_engine_config.nccl_id (rank 0 creates, broadcast). */
 int emesh_nccl_unique_id(uint8_t out[128]);
 

@@ -20,7 +20,7 @@ EXPORTS = (
     "emesh_dequantize", "emesh_dequantize_segments",
     "emesh_encode_quant_chunk", "emesh_decode_quant_chunk",
     "emesh_pseudo_gradient", "emesh_nesterov_outer_step",
-    "emesh_plan_segments", "emesh_ring_schedule",
+    "emesh_plan_segments", "emesh_ring_schedule", "emesh_debug_batch_runs",
     "emesh_nccl_unique_id", "emesh_engine_create", "emesh_engine_destroy",
     "emesh_engine_segments", "emesh_engine_ring_allreduce", "emesh_engine_outer_sync",
     "emesh_engine_outer_sync_host", "emesh_engine_check", "emesh_engine_payload", "emesh_engine_payload_host",
@@ -82,6 +82,7 @@ def lib() -> C.CDLL:
         "emesh_nesterov_outer_step": (i32, [vp, vp, vp, u64, f32, f32, vp]),
         "emesh_plan_segments": (u64, [u64, u32, u32, vp, vp]),
         "emesh_ring_schedule": (u64, [u64, u32, u32, u64, u32, vp, u64]),
+        "emesh_debug_batch_runs": (u64, [u64, u32, u32, u64, u32, u32, vp, u64, vp]),
         "emesh_nccl_unique_id": (i32, [vp]),
         "emesh_engine_create": (i32, [P(EngineConfig), P(vp)]),
         "emesh_engine_destroy": (i32, [vp]),

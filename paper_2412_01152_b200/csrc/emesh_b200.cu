@@ -72,16 +72,16 @@ struct Batch {
     uint32_t slot0 = 0, nseg = 0;
     uint64_t el_lo = 0, el_hi = 0;  // element range [el_lo, el_hi)
     uint64_t q_lo = 0, q_hi = 0;    // float4 slot range [q_lo, q_hi)
-    uint32_t ncta = 0, nnodes = 0;
-    size_t off_segs = 0, off_cta = 0, off_order = 0;  // byte offsets into the table arena
+    uint32_t ncta = 0, nruns = 0, ntasks = 0;
+    size_t off_segs = 0, off_cta = 0, off_runs = 0;  // byte offsets into the table arena
     const SegInfo* d_segs = nullptr;
     const uint32_t* d_cta_seg = nullptr;
-    const uint32_t* d_order = nullptr;
+    const uint4* d_runs = nullptr;
 
     void bind(void* base) {
         d_segs = reinterpret_cast<const SegInfo*>((char*)base + off_segs);
         d_cta_seg = reinterpret_cast<const uint32_t*>((char*)base + off_cta);
-        d_order = reinterpret_cast<const uint32_t*>((char*)base + off_order);
+        d_runs = reinterpret_cast<const uint4*>((char*)base + off_runs);
     }
 };
 
@@ -92,7 +92,7 @@ struct Plan {
     std::vector<std::vector<Batch>> batches;    // [chunk][window]
     std::vector<uint8_t> host_tables;
     void* d_tables = nullptr;
-    size_t max_cta = 0, max_nodes = 0, max_segs = 0, max_slots = 0;
+    size_t max_cta = 0, max_segs = 0, max_slots = 0;
 
     // Appends the device tables for one batch over segments [s0, s1).
     void add_batch(uint32_t chunk, uint32_t window, uint32_t s0, uint32_t s1) {
@@ -104,7 +104,6 @@ struct Plan {
         std::vector<SegInfo> infos;
         std::vector<uint32_t> cseg;
         bool first = true;
-        uint32_t nodes = 0;
         for (uint32_t s = s0; s < s1; ++s) {
             const Seg& g = segs[s];
             SegInfo si{};
@@ -114,7 +113,6 @@ struct Plan {
             si.cta0 = (uint32_t)cseg.size();
             si.slot = s;
             si.in_slot = s;
-            si.node_base = nodes;
             if (g.len > 0) {
                 const uint64_t q_last = (g.lo + g.len - 1) >> 2;
                 const uint64_t nq = q_last - si.q0 + 1;
@@ -124,37 +122,39 @@ struct Plan {
                 b.el_hi = g.lo + g.len;
                 b.q_hi = q_last + 1;
             }
-            for (uint32_t n = si.ncta; n > 1;) {  // internal nodes of the combine tree
-                n = (n + kFan - 1) / kFan;
-                nodes += n;
-            }
             for (uint32_t t = 0; t < si.ncta; ++t) cseg.push_back((uint32_t)infos.size());
             infos.push_back(si);
         }
         b.ncta = (uint32_t)cseg.size();
-        b.nnodes = nodes;
-        // persistent-kernel task order: STATS tiles in segment order; the BIN
-        // tiles of segment s after `lag` further STATS tiles (see kernels.cuh)
-        std::vector<uint32_t> order;
+        // persistent-kernel task order (see kernels.cuh): STATS tiles in
+        // segment order; the BIN tiles of s once `lag` more tasks were issued
+        // after its last STATS tile. Runs {first task, kind, segment, first tile}.
+        std::vector<uint4> runs;
         {
             const uint32_t lag = quant_lag_tiles();
-            uint32_t stats_issued = 0;
-            std::vector<std::pair<uint32_t, uint32_t>> pending;  // (segment, stats tiles issued through it)
-            size_t head = 0;
-            auto bins = [&](uint32_t seg) {
-                for (uint32_t t = 0; t < infos[seg].ncta; ++t) order.push_back(0x80000000u | (infos[seg].cta0 + t));
+            uint32_t issued = 0;
+            std::vector<std::pair<uint32_t, uint32_t>> bins;  // (segment, issue position that releases it)
+            size_t hb = 0;
+            auto release = [&](bool all) {
+                while (hb < bins.size() && (all || issued >= bins[hb].second)) {
+                    const uint32_t seg = bins[hb++].first;
+                    runs.push_back(make_uint4(issued, kTaskBin, seg, 0));
+                    issued += infos[seg].ncta;
+                }
             };
             for (uint32_t i = 0; i < infos.size(); ++i) {
-                if (infos[i].ncta == 0) continue;
                 for (uint32_t t = 0; t < infos[i].ncta; ++t) {
-                    order.push_back(infos[i].cta0 + t);
-                    ++stats_issued;
-                    while (head < pending.size() && stats_issued - pending[head].second >= lag) bins(pending[head++].first);
+                    const bool extend = t > 0 && runs.back().y == kTaskStats && runs.back().z == i;
+                    if (!extend) runs.push_back(make_uint4(issued, kTaskStats, i, t));
+                    ++issued;
+                    release(false);
                 }
-                pending.push_back({i, stats_issued});
+                if (infos[i].ncta) bins.push_back({i, issued + lag});
             }
-            while (head < pending.size()) bins(pending[head++].first);
+            release(true);
+            b.ntasks = issued;
         }
+        b.nruns = (uint32_t)runs.size();
 
         auto append = [&](const void* p, size_t bytes) {
             size_t off = (host_tables.size() + 15) & ~size_t(15);
@@ -164,10 +164,9 @@ struct Plan {
         };
         b.off_segs = append(infos.data(), infos.size() * sizeof(SegInfo));
         b.off_cta = append(cseg.data(), cseg.size() * sizeof(uint32_t));
-        b.off_order = append(order.data(), order.size() * sizeof(uint32_t));
+        b.off_runs = append(runs.data(), runs.size() * sizeof(uint4));
 
         max_cta = std::max<size_t>(max_cta, b.ncta);
-        max_nodes = std::max<size_t>(max_nodes, b.nnodes);
         max_segs = std::max<size_t>(max_segs, b.nseg);
         max_slots = std::max<size_t>(max_slots, b.q_hi > b.q_lo ? b.q_hi - b.q_lo : 0);
         batches[chunk].push_back(b);
@@ -195,7 +194,11 @@ int persistent_grid(const void* fn, uint32_t ntasks);
 // tile time; longer lags push scratch x out of L2).
 uint32_t quant_lag_tiles() {
     const int g = persistent_grid((const void*)k_quant<kSrcAminusB | kHasIn>, 1u << 30);
-    return g > 0 ? (uint32_t)g : 512u;
+    static const double mult = [] {
+        const char* e = std::getenv("EMESH_QUANT_LAG");  // tuning knob, in persistent grids
+        return e ? std::atof(e) : 2.0;
+    }();
+    return (uint32_t)(std::max(1.0, mult * (g > 0 ? g : 512)));
 }
 
 // Ring plan: k chunks, min(S, len) subs each, windows of G segments.
@@ -247,14 +250,11 @@ Plan make_list_plan(const uint64_t* lo, const uint64_t* len, uint32_t nseg) {
 struct Workspace {
     float* scratch = nullptr;
     StatP* leaf_stat = nullptr;
-    StatP* node_stat = nullptr;
-    HistP* leaf_hist = nullptr;
-    HistP* node_hist = nullptr;
-    uint32_t* tree_cnt = nullptr;
+    SegAcc* acc = nullptr;  // zero between launches (self-cleaning, see SegAcc)
     uint32_t* seg_flags = nullptr;
     uint32_t* sync = nullptr;
     uint32_t* err = nullptr;
-    size_t cap_slots = 0, cap_cta = 0, cap_nodes = 0, cap_segs = 0;
+    size_t cap_slots = 0, cap_cta = 0, cap_segs = 0;
 
     template <typename T>
     static int grow(T*& p, size_t& cap, size_t want, size_t elems_per, bool zero) {
@@ -266,7 +266,7 @@ struct Workspace {
         return EMESH_OK;
     }
 
-    int reserve(size_t slots, size_t ctas, size_t nodes, size_t segs) {
+    int reserve(size_t slots, size_t ctas, size_t segs) {
         if (!err) {
             CU(cudaMalloc(&err, sizeof(uint32_t)));
             CU(cudaMemset(err, 0, sizeof(uint32_t)));
@@ -279,31 +279,21 @@ struct Workspace {
         if (ctas > cap_cta || !leaf_stat) {
             size_t c = 0;
             TRY(grow(leaf_stat, c, ctas, 1, false));
-            c = 0;
-            TRY(grow(leaf_hist, c, ctas, 1, false));
             cap_cta = std::max<size_t>(ctas, 1);
-        }
-        if (nodes > cap_nodes || !node_stat) {
-            size_t c = 0;
-            TRY(grow(node_stat, c, nodes, 1, false));
-            c = 0;
-            TRY(grow(node_hist, c, nodes, 1, false));
-            c = 0;
-            TRY(grow(tree_cnt, c, nodes, 2, true));
-            cap_nodes = std::max<size_t>(nodes, 1);
         }
         if (segs > cap_segs || !seg_flags) {
             size_t c = 0;
             TRY(grow(seg_flags, c, segs, 1, true));
             c = 0;
-            TRY(grow(sync, c, kSyncReady + segs, 1, true));
+            TRY(grow(acc, c, segs, 1, true));
+            c = 0;
+            TRY(grow(sync, c, kSyncReady + 3 * segs, 1, true));
             cap_segs = std::max<size_t>(segs, 1);
         }
         return EMESH_OK;
     }
     void release() {
-        cudaFree(scratch); cudaFree(leaf_stat); cudaFree(node_stat); cudaFree(leaf_hist); cudaFree(node_hist);
-        cudaFree(tree_cnt); cudaFree(seg_flags); cudaFree(sync); cudaFree(err);
+        cudaFree(scratch); cudaFree(leaf_stat); cudaFree(acc); cudaFree(seg_flags); cudaFree(sync); cudaFree(err);
         *this = Workspace();
     }
 };
@@ -390,9 +380,9 @@ int persistent_grid(const void* fn, uint32_t ntasks) {
         for (auto& kv : cache)
             if (kv.first == fn) per_sm = kv.second;
         if (!per_sm) {
-            if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(QSmem)) != cudaSuccess)
+            if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQuantSmemBytes) != cudaSuccess)
                 return -1;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, sizeof(QSmem)) != cudaSuccess)
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, kQuantSmemBytes) != cudaSuccess)
                 return -1;
             cache.push_back({fn, per_sm});
         }
@@ -427,19 +417,17 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     a.out_cb = io.out_cb;
     a.stats = io.stats;
     a.leaf_stat = ws.leaf_stat;
-    a.node_stat = ws.node_stat;
-    a.leaf_hist = ws.leaf_hist;
-    a.node_hist = ws.node_hist;
-    a.tree_cnt = ws.tree_cnt;
-    a.nnodes = (uint32_t)ws.cap_nodes;
+    a.acc = ws.acc;
     a.seg_flags = ws.seg_flags;
     a.err = ws.err;
-    a.order = bt.d_order;
+    a.runs = bt.d_runs;
+    a.nruns = bt.nruns;
+    a.ntasks = bt.ntasks;
     a.sync = ws.sync;
     a.trace = g_trace.buf;
     a.trace_n = g_trace.n;
     a.trace_cap = (uint32_t)g_trace.cap;
-    CU(cudaMemsetAsync(ws.sync, 0, (kSyncReady + (size_t)bt.nseg) * sizeof(uint32_t), st));
+    CU(cudaMemsetAsync(ws.sync, 0, (kSyncReady + 3 * (size_t)bt.nseg) * sizeof(uint32_t), st));
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
     void* args[] = {&a};
@@ -457,13 +445,13 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     // ever waits on tasks claimed before it, so progress never depends on
     // co-residency. `reserve` CTA slots stay free for NCCL's kernels so the
     // ring's transfers overlap this kernel.
-    int grid = persistent_grid(fn, 2 * bt.ncta);
+    int grid = persistent_grid(fn, bt.ntasks);
     if (grid <= 0) return fail(EMESH_ECUDA, "k_quant: occupancy query failed");
     grid = std::max(1, grid - (int)reserve_ctas);
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(grid);
     lc.blockDim = dim3(kThreads);
-    lc.dynamicSmemBytes = sizeof(QSmem);
+    lc.dynamicSmemBytes = kQuantSmemBytes;
     lc.stream = st;
     CU(cudaLaunchKernelExC(&lc, fn, args));
     if (tr) tr->launches += 1;
@@ -547,7 +535,7 @@ int emesh_quantize_segments(const float* x, const uint64_t* seg_lo, const uint64
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     std::lock_guard<std::mutex> g(g_codec_mu);
     Plan p = make_list_plan(seg_lo, seg_len, nseg);
-    TRY(g_codec_ws.reserve(p.max_slots, p.max_cta, p.max_nodes, p.max_segs));
+    TRY(g_codec_ws.reserve(p.max_slots, p.max_cta, p.max_segs));
     // stream-ordered tables + stats (freed in stream order)
     void* d_tables = nullptr;
     SegStat* d_stats = nullptr;
@@ -730,7 +718,7 @@ int engine_alloc(emesh_engine* e) {
         CU(cudaMalloc(&a.stats, nslots * sizeof(SegStat)));
         CU(cudaMemset(a.stats, 0, nslots * sizeof(SegStat)));
     }
-    TRY(e->ws.reserve(e->plan.max_slots, e->plan.max_cta, e->plan.max_nodes, e->plan.max_segs));
+    TRY(e->ws.reserve(e->plan.max_slots, e->plan.max_cta, e->plan.max_segs));
     return EMESH_OK;
 }
 
@@ -926,6 +914,26 @@ uint64_t emesh_plan_segments(uint64_t n, uint32_t k, uint32_t S, uint64_t* seg_l
         if (seg_len) seg_len[i] = p.segs[i].len;
     }
     return p.segs.size();
+}
+
+uint64_t emesh_debug_batch_runs(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems, uint32_t chunk,
+                                uint32_t window, uint32_t* out4, uint64_t max_runs, uint32_t* ntasks_ncta) {
+    if (k == 0 || chunk >= k) return 0;
+    Plan p = make_ring_plan(n, k, S ? S : 4, window_elems ? window_elems : kDefaultWindow);
+    if (window >= p.batches[chunk].size()) return 0;
+    const Batch& b = p.batches[chunk][window];
+    const uint4* r = reinterpret_cast<const uint4*>(p.host_tables.data() + b.off_runs);
+    for (uint32_t i = 0; i < b.nruns && i < max_runs; ++i) {
+        out4[4 * i] = r[i].x; out4[4 * i + 1] = r[i].y; out4[4 * i + 2] = r[i].z; out4[4 * i + 3] = r[i].w;
+    }
+    if (ntasks_ncta) {
+        ntasks_ncta[0] = b.ntasks;
+        ntasks_ncta[1] = b.ncta;
+        ntasks_ncta[2] = b.nseg;
+        const SegInfo* si = reinterpret_cast<const SegInfo*>(p.host_tables.data() + b.off_segs);
+        for (uint32_t i = 0; i < b.nseg; ++i) ntasks_ncta[3 + i] = si[i].ncta;
+    }
+    return b.nruns;
 }
 
 uint64_t emesh_ring_schedule(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems, uint32_t rank,

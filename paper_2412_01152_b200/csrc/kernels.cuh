@@ -26,6 +26,7 @@
 // are per element.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -55,14 +56,6 @@ struct BucketParam {
     double scale;  // 2^-e (power of two)
     double K;      // 2^52 - base * scale (exact: base * scale is an integer < 2^42)
 };
-// fp32 fast path of the same encoding for buckets whose members lie within a
-// factor of two in magnitude: x - base is exact in fp32 (Sterbenz) and
-// r = (x - base) * scale < 2^24, so r = f2i((x - base) * scale) exactly.
-// scale == 0 marks a bucket that needs the fp64 path.
-struct BucketFast {
-    float base;
-    float scale;
-};
 constexpr double kMagic52 = 4503599627370496.0;  // 2^52
 constexpr int kWideBiasBits = 41;
 
@@ -75,7 +68,6 @@ struct SegStat {
     float margin;        // fp32 bucket estimate is exact when its fraction is in (margin, 1-margin)
     float thr[kBuckets];  // thr[j] = smallest fp32 x with code(x) >= j (j=1..255)
     BucketParam bp[kBuckets];
-    BucketFast bf[kBuckets];
 };
 constexpr uint32_t kFlagNonFinite = 1u;
 constexpr uint32_t kFlagDegenerate = 2u;  // sigma == 0 (quant.hpp:49-55)
@@ -88,11 +80,11 @@ struct SegInfo {
     uint64_t len;       // elements
     uint64_t q0;        // lo >> 2: first float4 slot
     uint32_t nunits;    // warp units (1024-element float4-grid spans)
-    uint32_t cta0;      // first CTA (batch-relative)
-    uint32_t ncta;      // tiles = leaves of the combine tree
+    uint32_t cta0;      // first tile (batch-relative): leaf_stat index
+    uint32_t ncta;      // tiles
     uint32_t slot;      // global segment slot (stats / codebook index)
     uint32_t in_slot;   // slot of the incoming payload's codebook (== slot)
-    uint32_t node_base; // internal tree nodes + counters of this segment
+    uint32_t pad;
 };
 
 // Moments of a set of values around a pivot p: s = sum x, m2 = sum (x-p)^2,
@@ -125,17 +117,17 @@ enum : int {
     kDivK = 4,          // x = x / k                  (owner mean, allreduce.hpp:439)
 };
 
-constexpr int kFan = 16;  // combine-tree fan-in
-
-// Bucket histogram partial of a tile / tree node: exact 128-bit sums of the
-// fixed-point codes r(x) of unclipped members, their counts, and the
-// clipped-low / clipped-high counts (xc = lo / hi, quant.hpp:66-67).
-struct HistP {
+// Bucket histogram of a segment, accumulated by integer atomics from every
+// BIN tile (order-free, hence deterministic): the fixed-point codes r(x) of the
+// members split as sum (r mod 2^32) and sum (r >> 32) (no u64 overflow for
+// any segment size), member counts (clipped members included, with r = 0),
+// and the clipped-low / clipped-high counts (xc = lo / hi, quant.hpp:66-67).
+// Zero between launches: the segment's last BIN tile re-zeroes it.
+struct SegAcc {
     unsigned long long rlo[kBuckets];
     unsigned long long rhi[kBuckets];
-    uint32_t cnt[kBuckets];
-    uint32_t clip[2];
-    uint32_t pad[2];
+    unsigned long long cnt[kBuckets];
+    unsigned long long clip[2];
 };
 
 struct QuantArgs {
@@ -154,16 +146,13 @@ struct QuantArgs {
     uint8_t* out_codes;
     float* out_cb;
     SegStat* stats;            // indexed by slot
-    StatP* leaf_stat;          // [cta]
-    StatP* node_stat;          // [node]
-    struct HistP* leaf_hist;   // [cta]
-    struct HistP* node_hist;   // [node]
-    uint32_t* tree_cnt;        // [2][node]: k_stats, k_bin arrival counters
-    uint32_t nnodes;
+    StatP* leaf_stat;          // [tile]
+    SegAcc* acc;               // [seg] bucket histograms (batch-local segment)
     uint32_t* seg_flags;       // [seg] non-finite bits (reset by the stats root)
     uint32_t* err;             // sticky error word (bit 0: non-finite)
-    uint32_t* sync;            // [0] task counter, [kSyncReady + s] segment s published (zeroed per launch)
-    const uint32_t* order;     // task order, 2 * ncta entries
+    uint32_t* sync;            // see kSyncReady (zeroed per launch)
+    const uint4* runs;         // task order as runs {first task, kind, segment, first tile}
+    uint32_t nruns, ntasks;
     struct TraceRec* trace;    // optional task timeline (nullptr: off)
     uint32_t* trace_n;
     uint32_t trace_cap;
@@ -211,6 +200,9 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 }
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
     uint32_t old;
@@ -269,39 +261,6 @@ __device__ float threshold(int j, double lo, double hi, double w) {
 
 
 // ---------------------------------------------------------------------------
-// Deterministic last-arriver combine tree over a segment's tiles. Level 0 =
-// leaves (one per CTA), level l+1 node i = children [16i, 16i+16) of level l.
-// The CTA that completes a node's last child combines the children in index
-// order, so the result is independent of scheduling. Returns false when the
-// calling CTA is not the one to continue upward.
-struct TreeCursor {
-    uint32_t level, idx, n, off;  // off: node offset of this level (level >= 1)
-};
-
-__device__ __forceinline__ bool tree_arrive(TreeCursor& c, uint32_t* counters, uint32_t node_base, uint32_t* s_flag) {
-    const uint32_t parent = c.idx / kFan;
-    const uint32_t first = parent * kFan;
-    const uint32_t nch = min((uint32_t)kFan, c.n - first);
-    const uint32_t poff = c.level == 0 ? 0u : c.off + c.n;
-    // partials written by any thread of the CTA happen-before the barrier;
-    // thread 0's gpu-scope fence (cumulative) then releases them all with
-    // its arrival, so only one thread pays for the fence.
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        // acq_rel: releases every partial the CTA wrote before the barrier
-        // (cumulativity) and, for the last arriver, acquires the siblings'
-        uint32_t* ctr = counters + node_base + poff + parent;
-        const bool last = atom_add_acq_rel(ctr, 1u) == nch - 1;
-        if (last) *ctr = 0;  // re-arm for the next launch (no other arrivals remain)
-        *s_flag = last ? 1u : 0u;
-    }
-    __syncthreads();
-    if (!*s_flag) return false;
-    c.idx = parent;  // caller combines children [first, first+nch) of the old level
-    return true;
-}
-
-// ---------------------------------------------------------------------------
 // K_stats: fused producer (PG / hop dequant-add / divide) + moments, one
 // pass: each lane accumulates s = sum x, d = sum (x-p), m2 = sum (x-p)^2 around
 // a pivot p (its first value), merged exactly up the warp / CTA / tree. Writes
@@ -338,26 +297,20 @@ __device__ __forceinline__ int exponent_of(float f) {  // floor(log2|f|) for nor
 }
 
 // Fixed-point parameters of bucket b whose fp32 members lie in [t0, t1).
-__device__ BucketParam bucket_param(float t0, float t1, BucketFast* fast) {
+__device__ BucketParam bucket_param(float t0, float t1) {
     BucketParam p;
     p.scale = 0.0;
     p.K = kMagic52;
-    fast->base = t0;
-    fast->scale = 0.f;
     if (!(t1 > t0)) return p;  // holds no fp32 value
     const float last = key2f(f2key(t1) - 1);
     if (t0 > 0.f || last < 0.f) {
         // narrow: every member is a multiple of the ulp of the smallest magnitude
         const float mn = t0 > 0.f ? t0 : last;
-        const float mx = t0 > 0.f ? last : t0;
         const int e = max(exponent_of(mn) - 23, -149);
         const double span = ldexp(__dsub_rn((double)last, (double)t0), -e);
         if (span < 2199023255552.0) {  // 2^41
             p.scale = ldexp(1.0, -e);
             p.K = __dsub_rn(kMagic52, ldexp((double)t0, -e));  // base = t0
-            // Sterbenz: |max| <= 2 |min| makes x - t0 exact in fp32; then r < 2^24
-            if (fabsf(mx) <= 2.f * fabsf(mn) && e >= -126 && e <= 127 && span < 16777216.0)
-                fast->scale = ldexpf(1.f, -e);
             return p;
         }
     }
@@ -369,40 +322,44 @@ __device__ BucketParam bucket_param(float t0, float t1, BucketFast* fast) {
 }
 
 // ---------------------------------------------------------------------------
-// Persistent quantizer: one launch per batch (pipelining window). CTAs claim
-// tile tasks in plan order (atomic counter); a task only ever waits on work
-// claimed before it (stats of its segment, or the bins that free its scratch
-// slot), and the cooperative launch keeps every CTA resident, so the spins
-// always make progress.
+// Persistent quantizer: one launch per batch (pipelining window), a grid of
+// co-resident CTAs that claim tile tasks in plan order (one atomicAdd each).
 
 struct QSmem {
     uint32_t hist[kWarps][kBuckets][3];  // per-warp limbs over the tile (bin), see bin_unit
-    float thr[kBuckets + 1];             // exact threshold table (bin)
-    BucketParam bp[kBuckets];            // fixed-point parameters (bin)
-    BucketFast bf[kBuckets];             // fp32 fast path of the same (bin)
+    BucketParam bp[kBuckets];            // fixed-point parameters (bin); 16-B aligned for LDS.128
+    float thr[kBuckets + 2];             // exact threshold table (bin); [257] = bucket 0's base (lo_up)
     float lut[kBuckets];                 // incoming codebook (stats, hop)
     StatP wp[kWarps];
     double red[2];
     uint32_t clip[2];
     uint32_t flag;
     uint32_t task;
-    int32_t bin_seg, lut_seg;
+    int32_t bin_seg, lut_seg, ready_seg;
     uint32_t run_idx;
     unsigned long long t_main;  // trace: main loop done
 };
+static_assert(offsetof(QSmem, bp) % 16 == 0, "bp must be 16-byte aligned");
 
-// Task order (host-built, QuantArgs::order): STATS tiles in segment order,
-// with the BIN tiles of segment s inserted once `lag` further STATS tiles
-// were issued after its last one (lag ~ 1.5 grids: the stats root of s
-// normally publishes before its bins are claimed, and the scratch x of a
-// tile is re-read soon enough to still be in L2). Entry: bit 31 = BIN,
-// low bits = batch tile. Claims are one atomicAdd; a BIN task only ever
-// waits on STATS tiles claimed before it, and only at the top of the loop
-// (when its CTA owes no tree arrival), so the persistent grid always
-// progresses.
-constexpr uint32_t kSyncReady = 32;  // ready flags start on their own 128-B line
+// Task order (host-built run table, QuantArgs::runs): the STATS tiles of
+// the batch in segment order; the BIN tiles of segment s once `lag` more
+// tasks were issued after its last STATS tile (lag ~ 2 grids: the segment's
+// statistics are normally published before its bins are claimed, and a
+// tile's scratch x is re-read soon enough to still be in L2). The last STATS
+// tile of s to finish finalizes SegStat(s); the last BIN tile of s to finish
+// writes its codebook. A BIN task only waits (at the top of the loop, owing
+// nothing) on STATS tiles claimed before it, so the grid always progresses
+// whatever the co-residency.
+// sync layout: [0] task counter, [kSyncReady + s] SegStat(s) published,
+// [kSyncReady + nseg + s] STATS tiles done, [kSyncReady + 2 nseg + s] BIN tiles done.
+constexpr uint32_t kSyncReady = 32;
+enum : uint32_t { kTaskStats = 0, kTaskBin = 2 };
+constexpr uint32_t kMaxRunsSmem = 512;  // run table cached in smem when it fits (8 KB)
+constexpr uint32_t kMaxSegsSmem = 128;  // SegInfo cached in smem when it fits (6 KB)
 
 
+
+__device__ void finalize_stats(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si);
 
 template <int SRC>
 __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si,
@@ -515,43 +472,36 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        const uint32_t nxt = atomicAdd(&a.sync[0], 1u);  // claim the next task (in flight while we merge)
         StatP t = sm.wp[0];
         for (int w = 1; w < kWarps; ++w) t = statp_merge(t, sm.wp[w]);
         a.leaf_stat[si.cta0 + tile] = t;
-        sm.task = nxt;
+        // acq_rel: publishes this leaf; the last tile to arrive acquires all
+        sm.flag = atom_add_acq_rel(&a.sync[kSyncReady + a.nseg + s], 1u) == si.ncta - 1 ? 1u : 0u;
     }
-    // ---- combine tree over this segment's tiles
-    TreeCursor c{0, tile, si.ncta, 0};
-    while (c.n > 1) {
-        const uint32_t lvl = c.level, n_old = c.n, off_old = c.off;
-        if (!tree_arrive(c, a.tree_cnt, si.node_base, &sm.flag)) return;
-        const uint32_t first = c.idx * kFan, nch = min((uint32_t)kFan, n_old - first);
-        const uint32_t poff = lvl == 0 ? 0u : off_old + n_old;
-        if (threadIdx.x < 32) {
-            // warp 0: lane i loads child i (one latency for all 16), then a
-            // fixed-shape shuffle tree merges them (deterministic)
-            const int ln = threadIdx.x;
-            StatP ch{0, 0, 0, 0, 0};
-            if ((uint32_t)ln < nch) {
-                const StatP* src = lvl == 0 ? &a.leaf_stat[si.cta0 + first + ln] : &a.node_stat[si.node_base + off_old + first + ln];
-                ch.s = __ldcg(&src->s); ch.m2 = __ldcg(&src->m2); ch.d = __ldcg(&src->d);
-                ch.piv = __ldcg(&src->piv); ch.n = __ldcg(&src->n);
-            }
-            ch = warp_merge(ch);
-            if (ln == 0) a.node_stat[si.node_base + poff + c.idx] = ch;
-        }
-        c.level = lvl + 1;
-        c.n = (n_old + kFan - 1) / kFan;
-        c.off = poff;
+    __syncthreads();
+    if (sm.flag) finalize_stats(a, sm, s, si);
+}
+
+// Run by the last STATS tile of s to finish: combine the segment's leaves in
+// a fixed order (thread t: leaves t, t+256, ...; then warps; then the 8 warp
+// partials), finalize mu / sigma / lo / hi / width (quant.hpp:33-59), the
+// exact threshold table and the bucket parameters, and publish SegStat(s).
+__device__ void finalize_stats(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    StatP p{0.0, 0.0, 0.0, 0.0, 0};
+    for (uint32_t i = threadIdx.x; i < si.ncta; i += kThreads) {
+        const StatP* src = &a.leaf_stat[si.cta0 + i];
+        StatP ch;
+        ch.s = __ldcg(&src->s); ch.m2 = __ldcg(&src->m2); ch.d = __ldcg(&src->d);
+        ch.piv = __ldcg(&src->piv); ch.n = __ldcg(&src->n);
+        p = statp_merge(p, ch);
     }
-    // ---- root: finalize segment statistics (quant.hpp:33-59)
+    p = warp_merge(p);
+    if (lane == 0) sm.wp[warp] = p;
     __syncthreads();
     if (threadIdx.x == 0) {
-        const StatP* src = c.level == 0 ? &a.leaf_stat[si.cta0 + tile] : &a.node_stat[si.node_base + c.off];
-        StatP t;
-        t.s = __ldcg(&src->s); t.m2 = __ldcg(&src->m2); t.d = __ldcg(&src->d); t.piv = __ldcg(&src->piv);
-        t.n = __ldcg(&src->n);
+        StatP t = sm.wp[0];
+        for (int w = 1; w < kWarps; ++w) t = statp_merge(t, sm.wp[w]);
         const double mu = __ddiv_rn(t.s, (double)si.len);
         const double dm = __dsub_rn(t.piv, mu);
         // sum (x - mu)^2 = M2 + 2 (p - mu) D + n (p - mu)^2
@@ -589,9 +539,7 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
         if (b == 0) sm.thr[kBuckets] = key2f(f2key(hi_dn) + 1);
         __syncthreads();
         st->thr[b] = b == 0 ? -INFINITY : sm.thr[b];
-        BucketFast bfast;
-        st->bp[b] = bucket_param(sm.thr[b], sm.thr[b + 1], &bfast);
-        st->bf[b] = bfast;
+        st->bp[b] = bucket_param(sm.thr[b], sm.thr[b + 1]);
         if (b == 0) {
             st->lo = lo; st->hi = hi; st->width = w;
             const float lo_f = (float)lo, inv_w = (float)__ddiv_rn(1.0, w);
@@ -610,9 +558,8 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
         }
     }
     __syncthreads();
-    __syncthreads();
     if (threadIdx.x == 0) {
-        sm.bin_seg = -1;  // thr/bp in smem now hold this segment's raw table: force a reload
+        sm.bin_seg = -1;  // thr in smem now holds this segment's raw table: force a reload
         st_release(&a.sync[kSyncReady + s], 1u);  // publish (cumulative over the CTA's SegStat writes)
     }
 }
@@ -690,10 +637,10 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
                     const float fr = __fsub_rn(g, __int2float_rz(c0));
                     if (x < p.lo_up) {
                         cc[i] = 0; clo_m |= 1u << i;
-                        xe[i] = sm.bf[0].base;   // r = 0: counted, contributes lo at the root
+                        xe[i] = sm.thr[kBuckets + 1];  // bucket 0's base: r = 0, counted, contributes lo at the root
                     } else if (x > p.hi_dn) {
                         cc[i] = 255; chi_m |= 1u << i;
-                        xe[i] = sm.bf[255].base;
+                        xe[i] = sm.thr[255];  // bucket 255's base
                     } else if (!(fr > p.margin && fr < p.one_m && (uint32_t)c0 < 256u)) {
                         cc[i] = bucket_walk(x, min(max(c0, 0), 255), sm.thr);
                     }
@@ -701,38 +648,20 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
                 nclip_lo += __popc(clo_m & vmask);
                 nclip_hi += __popc(chi_m & vmask);
             }
-            uint32_t ra[8], rb[8];
-            uint32_t slow_m = 0;
+            // fixed point r = rint(x * scale + K) - 2^52 (one DFMA, exact; clipped
+            // lanes carry x = bucket base, i.e. r = 0), split into the limbs
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const BucketFast fb = sm.bf[cc[i]];
-                const uint32_t rf = __float2uint_rz(__fmul_rn(__fsub_rn(xe[i], fb.base), fb.scale));
-                slow_m |= fb.scale == 0.f ? (1u << i) : 0u;
+                const double2 pb = reinterpret_cast<const double2*>(sm.bp)[cc[i]];  // {scale, K}
+                const double m = __fma_rn((double)xe[i], pb.x, pb.y);
+                const uint32_t rlo = (uint32_t)__double2loint(m);
+                const uint32_t rhi = (uint32_t)__double2hiint(m);
                 const bool valid = (vmask >> i) & 1u;
-                ra[i] = valid ? ((rf & 0x1ffu) | (1u << 20)) : 0u;
-                rb[i] = valid ? (rf >> 9) : 0u;
-            }
-            slow_m &= vmask;
-            if (slow_m) {  // fp64 path: wide / large-span buckets
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    if ((slow_m >> i) & 1u) {
-                        const BucketParam pb = sm.bp[cc[i]];
-                        const double m = __fma_rn((double)xe[i], pb.scale, pb.K);  // 2^52 + r
-                        const uint32_t rlo = (uint32_t)__double2loint(m);
-                        const uint32_t rhi = (uint32_t)__double2hiint(m) & 0x3ffu;
-                        ra[i] = (rlo & 0x1ffu) | (1u << 20);
-                        rb[i] = (rlo >> 9) & 0x1fffffu;
-                        const uint32_t rc = (rlo >> 30) | (rhi << 2);
-                        if (rc) atomicAdd(hw + 3 * cc[i] + 2, rc);
-                    }
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
                 uint32_t* hc = hw + 3 * cc[i];
-                atomicAdd(hc, ra[i]);
-                atomicAdd(hc + 1, rb[i]);
+                atomicAdd(hc, valid ? ((rlo & 0x1ffu) | (1u << 20)) : 0u);
+                atomicAdd(hc + 1, valid ? ((rlo >> 9) & 0x1fffffu) : 0u);
+                const uint32_t rc = __funnelshift_r(rlo, rhi, 30) & 0xfffu;
+                if (valid && rc) atomicAdd(hc + 2, rc);
             }
             const uint32_t p0 = __byte_perm(__byte_perm(cc[0], cc[1], 0x0040), __byte_perm(cc[2], cc[3], 0x0040), 0x5410);
             const uint32_t p1 = __byte_perm(__byte_perm(cc[4], cc[5], 0x0040), __byte_perm(cc[6], cc[7], 0x0040), 0x5410);
@@ -768,6 +697,8 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
     }
 }
 
+__device__ void finalize_codebook(const QuantArgs& a, uint32_t s, const SegInfo& si);
+
 template <bool FROM_SCRATCH>
 __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si, uint32_t tile) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -780,11 +711,11 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
         pb.scale = __ldcg(&st->bp[b].scale);
         pb.K = __ldcg(&st->bp[b].K);
         sm.bp[b] = pb;
-        BucketFast fb;
-        fb.base = __ldcg(&st->bf[b].base);
-        fb.scale = __ldcg(&st->bf[b].scale);
-        sm.bf[b] = fb;
-        if (b == 0) sm.thr[kBuckets] = INFINITY;
+
+        if (b == 0) {
+            sm.thr[kBuckets] = INFINITY;
+            sm.thr[kBuckets + 1] = __ldcg(&st->lo_up);
+        }
         __syncthreads();
         if (threadIdx.x == 0) sm.bin_seg = (int32_t)s;
     }
@@ -824,11 +755,9 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
         atomicAdd(&sm.clip[1], nclip_hi);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        sm.task = atomicAdd(&a.sync[0], 1u);  // claim the next task
-        if (a.trace) sm.t_main = gtimer();
-    }
-    {   // tile histogram (exact integer; order irrelevant); re-zero the limbs
+    if (threadIdx.x == 0 && a.trace) sm.t_main = gtimer();
+    {   // tile histogram (exact integers, order-free) into the segment's
+        // accumulator; re-zero the limbs
         const int b = threadIdx.x;
         unsigned long long r = 0;
         uint32_t cn = 0;
@@ -841,75 +770,51 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
             sm.hist[w][b][1] = 0u;
             sm.hist[w][b][2] = 0u;
         }
-        HistP* L = &a.leaf_hist[si.cta0 + tile];
-        L->rlo[b] = r;
-        L->rhi[b] = 0ull;
-        L->cnt[b] = cn;
-        if (b < 2) L->clip[b] = sm.clip[b];
-    }
-    // ---- combine tree (16 independent loads per thread per level)
-    uint32_t* ctr = a.tree_cnt + a.nnodes;
-    TreeCursor c{0, tile, si.ncta, 0};
-    const HistP* root = &a.leaf_hist[si.cta0 + tile];
-    while (c.n > 1) {
-        const uint32_t lvl = c.level, n_old = c.n, off_old = c.off;
-        if (!tree_arrive(c, ctr, si.node_base, &sm.flag)) return;
-        const uint32_t first = c.idx * kFan, nch = min((uint32_t)kFan, n_old - first);
-        const uint32_t poff = lvl == 0 ? 0u : off_old + n_old;
-        const int b = threadIdx.x;
-        const HistP* src = lvl == 0 ? &a.leaf_hist[si.cta0 + first] : &a.node_hist[si.node_base + off_old + first];
-        unsigned long long lo[kFan], hi[kFan];
-        uint32_t cn[kFan];
-#pragma unroll
-        for (int i = 0; i < kFan; ++i) {
-            if ((uint32_t)i < nch) {
-                lo[i] = __ldcg(&src[i].rlo[b]);
-                hi[i] = __ldcg(&src[i].rhi[b]);
-                cn[i] = __ldcg(&src[i].cnt[b]);
-            } else { lo[i] = 0ull; hi[i] = 0ull; cn[i] = 0u; }
+        SegAcc* acc = &a.acc[s];
+        if (cn) {
+            atomicAdd(&acc->rlo[b], r & 0xffffffffull);
+            if (r >> 32) atomicAdd(&acc->rhi[b], r >> 32);
+            atomicAdd(&acc->cnt[b], (unsigned long long)cn);
         }
-        unsigned long long rl = 0ull, rh = 0ull;
-        uint32_t rc = 0;
-#pragma unroll
-        for (int i = 0; i < kFan; ++i) {
-            const unsigned long long t = rl + lo[i];
-            rh += hi[i] + (t < rl ? 1ull : 0ull);
-            rl = t;
-            rc += cn[i];
-        }
-        HistP* dst = &a.node_hist[si.node_base + poff + c.idx];
-        dst->rlo[b] = rl;
-        dst->rhi[b] = rh;
-        dst->cnt[b] = rc;
-        if (b < 2) {
-            uint32_t cl = 0;
-            for (uint32_t i = 0; i < nch; ++i) cl += __ldcg(&src[i].clip[b]);
-            dst->clip[b] = cl;
-        }
-        root = dst;
-        c.level = lvl + 1;
-        c.n = (n_old + kFan - 1) / kFan;
-        c.off = poff;
+        if (b < 2 && sm.clip[b]) atomicAdd(&acc->clip[b], (unsigned long long)sm.clip[b]);
     }
     __syncthreads();
-    // ---- root: codebook (quant.hpp:78-85)
+    if (threadIdx.x == 0)  // acq_rel: releases the CTA's atomics; the last tile acquires all
+        sm.flag = atom_add_acq_rel(&a.sync[kSyncReady + 2 * a.nseg + s], 1u) == si.ncta - 1 ? 1u : 0u;
+    __syncthreads();
+    if (sm.flag) finalize_codebook(a, s, si);
+}
+
+// Run by the last BIN tile of s to finish: the codebook from the exact
+// bucket sums (quant.hpp:78-85); re-zeroes the accumulator for the next launch.
+__device__ void finalize_codebook(const QuantArgs& a, uint32_t s, const SegInfo& si) {
+    const SegStat* st = &a.stats[si.slot];
+    const bool degenerate = (__ldcg(&st->flags) & kFlagDegenerate) != 0;
     const int b = threadIdx.x;
+    SegAcc* acc = &a.acc[s];
+    const unsigned long long rl = __ldcg(&acc->rlo[b]), rh = __ldcg(&acc->rhi[b]);
+    const unsigned long long total = __ldcg(&acc->cnt[b]);
+    const unsigned long long clip = b == 0 ? __ldcg(&acc->clip[0]) : b == 255 ? __ldcg(&acc->clip[1]) : 0ull;
+    __syncthreads();  // every read done before the re-zeroing
+    acc->rlo[b] = 0ull;
+    acc->rhi[b] = 0ull;
+    acc->cnt[b] = 0ull;
+    if (b < 2) acc->clip[b] = 0ull;
     float* cb = a.out_cb + (uint64_t)si.slot * kBuckets;
     if (degenerate) { cb[b] = (float)__ldcg(&st->mu); return; }
-    const unsigned long long rl = __ldcg(&root->rlo[b]), rh = __ldcg(&root->rhi[b]);
-    const uint32_t total = __ldcg(&root->cnt[b]);  // clipped members included, with r = 0
-    const uint32_t clip = b == 0 ? __ldcg(&root->clip[0]) : (b == 255 ? __ldcg(&root->clip[1]) : 0u);
-    const uint32_t cnt = total - clip;
     if (total == 0) {
         cb[b] = (float)__dadd_rn(__ldcg(&st->lo), __dmul_rn(__dadd_rn((double)b, 0.5), __ldcg(&st->width)));
         return;
     }
+    const unsigned long long cnt = total - clip;  // clipped members are counted with r = 0
     double sum = 0.0;
     if (cnt) {
-        const BucketParam pb = sm.bp[b];
+        BucketParam pb;
+        pb.scale = __ldcg(&st->bp[b].scale);
+        pb.K = __ldcg(&st->bp[b].K);
         // sum x * scale = sum r + cnt * base * scale (exact integers, 128-bit);
         // base * scale = 2^52 - K
-        __int128 S = (__int128)(((unsigned __int128)rh << 64) | rl);
+        __int128 S = (__int128)rl + ((__int128)rh << 32);
         S += (__int128)(long long)__double2ll_rn(__dsub_rn(kMagic52, pb.K)) * (__int128)cnt;
         const long long hi64 = (long long)(S >> 64);
         const long long s64 = (long long)(unsigned long long)S;
@@ -925,47 +830,82 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
 template <int SRC>
 __global__ void __launch_bounds__(kThreads, 3) k_quant(QuantArgs a) {
     extern __shared__ __align__(16) unsigned char qsmem_raw[];
-    QSmem& sm = *reinterpret_cast<QSmem*>(qsmem_raw);  // dynamic: sizeof(QSmem) > 48 KB
+    QSmem& sm = *reinterpret_cast<QSmem*>(qsmem_raw);  // dynamic: > 48 KB in total
+    uint4* runs_s = reinterpret_cast<uint4*>(qsmem_raw + sizeof(QSmem));
+    SegInfo* segs_s = reinterpret_cast<SegInfo*>(qsmem_raw + sizeof(QSmem) + kMaxRunsSmem * sizeof(uint4));
+    const bool runs_in_smem = a.nruns <= kMaxRunsSmem;
+    const bool segs_in_smem = a.nseg <= kMaxSegsSmem;
     for (uint32_t i = threadIdx.x; i < kWarps * kBuckets * 3; i += kThreads) (&sm.hist[0][0][0])[i] = 0u;
+    if (runs_in_smem)
+        for (uint32_t i = threadIdx.x; i < a.nruns; i += kThreads) runs_s[i] = a.runs[i];
+    if (segs_in_smem)
+        for (uint32_t i = threadIdx.x; i < a.nseg; i += kThreads) segs_s[i] = a.segs[i];
+    uint32_t nxt = 0;  // thread 0: the next task, claimed at the start of the current one
     if (threadIdx.x == 0) {
         sm.bin_seg = -1;
         sm.lut_seg = -1;
-        sm.task = atomicAdd(&a.sync[0], 1u);
+        sm.ready_seg = -1;
+        nxt = atomicAdd(&a.sync[0], 1u);
     }
     for (;;) {
+        if (threadIdx.x == 0) sm.task = nxt;
         __syncthreads();
-        const uint32_t t = sm.task;  // claimed by thread 0 in the previous tile's epilogue
-        if (t >= 2 * a.ncta) return;
-        const uint32_t v = a.order[t];
-        const bool is_bin = (v >> 31) != 0;
-        const uint32_t ct = v & 0x7fffffffu;
-        const uint32_t s = a.cta_seg[ct];
-        const SegInfo si = a.segs[s];
-        const uint32_t tile = ct - si.cta0;
+        const uint32_t t = sm.task;
+        if (t >= a.ntasks) return;
+        // claim the following task now: the atomic's latency hides behind this tile
+        if (threadIdx.x == 0) nxt = atomicAdd(&a.sync[0], 1u);
+        uint32_t kind, s, tile;
+        if (runs_in_smem) {  // binary search of the run table (smem)
+            uint32_t lo = 0, hi = a.nruns;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (runs_s[mid].x <= t) lo = mid; else hi = mid;
+            }
+            const uint4 r = runs_s[lo];
+            kind = r.y;
+            s = r.z;
+            tile = r.w + (t - r.x);
+        } else {
+            uint32_t lo = 0, hi = a.nruns;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (a.runs[mid].x <= t) lo = mid; else hi = mid;
+            }
+            const uint4 r = a.runs[lo];
+            kind = r.y;
+            s = r.z;
+            tile = r.w + (t - r.x);
+        }
+        const SegInfo si = segs_in_smem ? segs_s[s] : a.segs[s];
         unsigned long long t0 = 0, t1 = 0;
         if (a.trace) t0 = gtimer();
-        if (is_bin && threadIdx.x == 0) {
-            // acquire SegStat(s); the CTA owes nothing at this point
+        if (kind == kTaskBin && threadIdx.x == 0 && sm.ready_seg != (int32_t)s) {
+            // acquire SegStat(s) (cached per CTA); the CTA owes nothing here
             uint32_t ns = 32;
             while (ld_acquire(&a.sync[kSyncReady + s]) == 0u) {
                 __nanosleep(ns);
                 ns = ns < 1024 ? 2 * ns : ns;
             }
+            sm.ready_seg = (int32_t)s;
         }
         if (a.trace) t1 = gtimer();
         __syncthreads();  // everyone has read sm.task; SegStat(s) visible for BIN
-        if (!is_bin) stats_tile<SRC>(a, sm, s, si, tile);
-        else bin_tile<SRC != kSrcA>(a, sm, s, si, tile);
+        switch (kind) {
+            case kTaskStats: stats_tile<SRC>(a, sm, s, si, tile); break;
+            default: bin_tile<SRC != kSrcA>(a, sm, s, si, tile); break;
+        }
         if (a.trace && threadIdx.x == 0) {
             const uint32_t i = atomicAdd(a.trace_n, 1u);
             if (i < a.trace_cap) {
                 uint32_t smid;
                 asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-                a.trace[i] = TraceRec{t0, t1, sm.t_main, gtimer(), is_bin ? 1u : 0u, s, tile, smid};
+                a.trace[i] = TraceRec{t0, t1, sm.t_main, gtimer(), kind, s, tile, smid};
             }
         }
     }
 }
+
+constexpr size_t kQuantSmemBytes = sizeof(QSmem) + kMaxRunsSmem * sizeof(uint4) + kMaxSegsSmem * sizeof(SegInfo);
 
 // ---------------------------------------------------------------------------
 // Elementwise kernels over segment batches (codebook LUT in smem).

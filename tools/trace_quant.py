@@ -32,27 +32,34 @@ rec = rec[order]
 t = rec["t"].astype(np.int64)
 t0 = t[:, 0].min()
 st = rec["kind"] == 0
-bn = ~st
+bn = rec["kind"] == 2
 dur = (t[:, 3] - t[:, 0]) / 1e3
 wait = (t[:, 1] - t[:, 0]) / 1e3
 main = (t[:, 2] - t[:, 1]) / 1e3
 epi = (t[:, 3] - t[:, 2]) / 1e3
 print(f"n={n} S={S}: records {m}; span {(t[:, 3].max() - t0) / 1e3:.1f} us")
-for nm, msk in (("stats", st), ("bin", bn)):
+for kd, nm in ((0, "stats"), (1, "root"), (2, "bin"), (3, "cb")):
+    msk = rec["kind"] == kd
     if msk.sum() == 0:
         continue
-    print(f"{nm:5s} n={msk.sum():6d} dur mean {dur[msk].mean():6.2f} us  wait {wait[msk].mean():6.2f}  "
-          f"main {main[msk].mean():6.2f}  epilogue {epi[msk].mean():6.2f}   p90 dur {np.percentile(dur[msk], 90):.2f}  "
-          f"max wait {wait[msk].max():.2f}  p90 epi {np.percentile(epi[msk], 90):.2f}")
+    line = (f"{nm:5s} n={msk.sum():6d} dur mean {dur[msk].mean():6.2f} us p50 {np.percentile(dur[msk], 50):.2f} "
+            f"p90 {np.percentile(dur[msk], 90):.2f} max {dur[msk].max():.2f} | wait mean {wait[msk].mean():6.2f} max {wait[msk].max():.2f}")
+    if kd in (0, 2):
+        line += f" | main {main[msk].mean():6.2f} epilogue {epi[msk].mean():6.2f}"
+    print(line)
 ends = np.maximum.accumulate(t[:, 3])
 gaps = np.nonzero(t[1:, 0] > ends[:-1] + 2000)[0]
 bounds = [0] + list(gaps + 1) + [len(t)]
 spans = [(t[b:e, 3].max() - t[b, 0]) / 1e3 for b, e in zip(bounds[:-1], bounds[1:])]
 print("launch groups", len(spans), "span us: mean %.1f min %.1f max %.1f" % (np.mean(spans), np.min(spans), np.max(spans)))
 print("sum of spans %.1f us; idle between %.1f us" % (np.sum(spans), (t[:, 3].max() - t0) / 1e3 - np.sum(spans)))
-# occupancy over time inside the longest group: concurrent tasks
 b, e = bounds[int(np.argmax(spans))], bounds[int(np.argmax(spans)) + 1]
 g = t[b:e]
 grid = np.linspace(g[:, 0].min(), g[:, 3].max(), 40)
 conc = [int(((g[:, 0] <= x) & (g[:, 3] > x)).sum()) for x in grid]
 print("concurrent tasks over the longest launch:", conc)
+# time-weighted breakdown: SM-time spent per kind and in waits
+tot = dur.sum()
+for kd, nm in ((0, "stats"), (1, "root"), (2, "bin"), (3, "cb")):
+    msk = rec["kind"] == kd
+    print(f"  {nm:5s} share of task time {dur[msk].sum() / tot:.3f} (waiting {wait[msk].sum() / tot:.3f})")
