@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--workers", type=int, default=0, help="DiLoCo workers k (default: 4 at N=1, N otherwise)")
     ap.add_argument("--S", type=int, default=16, help="ReduceOptions.pipeline_subchunks")
     ap.add_argument("--window", type=float, default=0, help="pipelining window elems (0=auto)")
+    ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "p2p"],
+                    help="N>1 ring transport (auto: peer memory over NVLink when mappable, else NCCL)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -169,11 +171,13 @@ def run_reference(args, rank, world):
 # ----------------------------------------------------------------- helpers
 
 
-def config_block(args, k, n):
+def config_block(args, k, n, transport=None):
     return {"workload": f"config 2: DiLoCo outer sync of a {n / 1e9:.3g}B-param synthetic model, {k} workers, "
                         "int8 ring all-reduce + Nesterov (lr=0.7, mu=0.9)",
             "params_per_worker": n, "workers": k, "pipeline_subchunks": args.S,
             "ring": ("virtual (all workers on 1 GPU, zero-copy hand-off)" if args.gpus == 1 and k > 1
+                     else "peer memory over NVLink (quantizer stores into the successor's arena, per-segment flags), "
+                          "one worker per GPU" if transport == "p2p"
                      else "NCCL send/recv over NVLink, one worker per GPU"),
             "l2": "inputs larger than L2 (>= 12 B/param x n per worker)",
             "write_local": False}
@@ -218,7 +222,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     eng = E.RingEngine(n, k, rank=rank if not virtual else 0, opts=E.ReduceOptions(pipeline_subchunks=args.S),
-                       virtual=virtual, nccl_id=nccl_id, window_elems=int(args.window))
+                       virtual=virtual, nccl_id=nccl_id, window_elems=int(args.window), transport=args.transport)
     W = eng.workers
     # synthetic replicas: theta_g ~ U[-1,1), theta_l = theta_g - 2^-10 U, b = 0
     gen = torch.Generator(device=dev)
@@ -364,7 +368,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (theta_g~U[-1,1), theta_l=theta_g-2^-10 U, b=0)",
-            "config": config_block(args, k, n),
+            "config": config_block(args, k, n, eng.transport),
             "hbm_alg_GBps_per_gpu": round(step_alg_gbs, 1),
             "hbm_frac_step": round(step_alg_gbs / hbm_peak, 4),
             "roofline": roofline, "roofline_other_kernels": roofline_others, "kernels": kernels,

@@ -102,7 +102,23 @@ typedef struct {
     uint64_t window_elems;      /* pipelining window (0 = auto) */
     const uint8_t* nccl_id;     /* 128-byte ncclUniqueId (NCCL mode, k > 1) */
     int device;                 /* CUDA device ordinal, -1 = current */
+    uint32_t transport;         /* EMESH_TRANSPORT_*: how hop payloads move between ranks */
 } emesh_engine_config;
+
+/* Transports of the one-process-per-GPU ring (k > 1, not virtual):
+ *   AUTO: P2P when every rank's GPU is reachable through CUDA IPC peer memory
+ *         (one NVLink / NVSwitch node), else NCCL;
+ *   NCCL: ncclSend / ncclRecv of each window's codes + codebooks per hop;
+ *   P2P:  the quantizer writes each hop's codes + codebooks straight into the
+ *         successor's arena (the owner's final payload into every rank's)
+ *         and raises a per-segment arrival flag there; the next hop's
+ *         quantizer and the Nesterov apply wait on those flags segment by
+ *         segment (NCCL only bootstraps the IPC handles). */
+enum { EMESH_TRANSPORT_AUTO = 0, EMESH_TRANSPORT_NCCL = 1, EMESH_TRANSPORT_P2P = 2 };
+
+/* Transport the engine resolved to (EMESH_TRANSPORT_NCCL / _P2P; 0 for the
+ * virtual ring and k == 1). */
+int emesh_engine_transport(const emesh_engine* e);
 
 /* Host-only plan queries (no GPU needed). Segment table of an (n, k, S)
  * ring, chunk-major (allreduce.hpp:107-118, :326-336); returns the count. */
@@ -199,6 +215,12 @@ uint64_t emesh_engine_launches(const emesh_engine* e);
  * device ms and total ALGORITHMIC bytes of that kind. */
 int emesh_engine_profile(emesh_engine* e, int enable);
 int emesh_engine_profile_read(emesh_engine* e, uint32_t kind, uint64_t* launches, double* ms, double* alg_bytes);
+
+/* NCCL-mode op timeline of the calls made since emesh_engine_profile(e, 1):
+ * rows of 6 doubles {op kind, phase, hop, window, start ms, end ms} (times on
+ * the op's stream, relative to the first op's start). Returns the row count
+ * (copies at most max_rows). Synchronizes the engine. */
+uint64_t emesh_engine_timeline(emesh_engine* e, double* rows, uint64_t max_rows);
 
 #ifdef __cplusplus
 }

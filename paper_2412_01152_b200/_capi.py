@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libemesh_b200.so")
+LIB_PATH = os.environ.get("EMESH_LIB") or os.path.join(HERE, "libemesh_b200.so")  # EMESH_LIB: build variants
 
 # every symbol include/emesh_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = (
@@ -24,7 +24,7 @@ EXPORTS = (
     "emesh_nccl_unique_id", "emesh_engine_create", "emesh_engine_destroy",
     "emesh_engine_segments", "emesh_engine_ring_allreduce", "emesh_engine_outer_sync",
     "emesh_engine_outer_sync_host", "emesh_engine_check", "emesh_engine_payload", "emesh_engine_payload_host",
-    "emesh_engine_launches", "emesh_engine_profile", "emesh_engine_profile_read",
+    "emesh_engine_launches", "emesh_engine_profile", "emesh_engine_profile_read", "emesh_engine_timeline", "emesh_engine_transport",
     "emesh_trace_enable", "emesh_trace_read",
 )
 
@@ -41,6 +41,7 @@ class EngineConfig(C.Structure):
         ("window_elems", C.c_uint64),
         ("nccl_id", C.c_void_p),
         ("device", C.c_int),
+        ("transport", C.c_uint32),
     ]
 
 
@@ -54,6 +55,7 @@ class RingOp(C.Structure):
 
 
 OP_OWN, OP_XFER, OP_QUANT, OP_APPLY = range(4)
+TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_P2P = range(3)
 
 _lib = None
 
@@ -98,6 +100,8 @@ def lib() -> C.CDLL:
         "emesh_trace_read": (u64, [vp, u64]),
         "emesh_engine_profile": (i32, [vp, i32]),
         "emesh_engine_profile_read": (i32, [vp, u32, P(u64), P(C.c_double), P(C.c_double)]),
+        "emesh_engine_timeline": (u64, [vp, P(C.c_double), u64]),
+        "emesh_engine_transport": (i32, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

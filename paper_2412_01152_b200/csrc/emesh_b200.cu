@@ -65,6 +65,7 @@ struct Seg {
 };
 
 uint32_t quant_lag_tiles();
+bool bin_reverse();
 
 // One pipelining window: consecutive segments of one rank chunk.
 struct Batch {
@@ -138,7 +139,10 @@ struct Plan {
             auto release = [&](bool all) {
                 while (hb < bins.size() && (all || issued >= bins[hb].second)) {
                     const uint32_t seg = bins[hb++].first;
-                    runs.push_back(make_uint4(issued, kTaskBin, seg, 0));
+                    // bins run in reverse tile order: the most recently written scratch
+                    // (the segment's last stats tiles) is re-read while still in L2
+                    runs.push_back(make_uint4(issued, kTaskBin, seg,
+                                              bin_reverse() ? 0x80000000u | (infos[seg].ncta - 1) : 0u));
                     issued += infos[seg].ncta;
                 }
             };
@@ -192,6 +196,13 @@ int persistent_grid(const void* fn, uint32_t ntasks);
 // Lag between a segment's last STATS tile and its first BIN tile in the task
 // order: one persistent grid (the stats root publishes within about one
 // tile time; longer lags push scratch x out of L2).
+bool bin_reverse() {
+    static const bool r = [] {
+        const char* e = std::getenv("EMESH_BIN_REVERSE");  // tuning knob
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    return r;
+}
 uint32_t quant_lag_tiles() {
     const int g = persistent_grid((const void*)k_quant<kSrcAminusB | kHasIn>, 1u << 30);
     static const double mult = [] {
@@ -311,6 +322,16 @@ struct QuantIO {
     uint8_t* out_codes;
     float* out_cb;
     SegStat* stats;
+    // peer transport: extra output destinations (peer arenas), arrival flags
+    // to raise per finished segment, and the input wait
+    uint32_t nx = 0;
+    bool local_out = true;  // out_codes/out_cb is a destination too
+    uint8_t* x_codes[kMaxDest] = {};
+    float* x_cb[kMaxDest] = {};
+    uint32_t nflags = 0;
+    uint32_t* flags[kMaxDest] = {};
+    const uint32_t* in_flag = nullptr;
+    uint32_t epoch = 0;
 };
 
 enum ProfKind : int {
@@ -336,6 +357,11 @@ struct Tracker {
         double bytes;
     };
     std::vector<Rec> recs;
+    struct OpRec {
+        int kind, phase, hop, window;
+        cudaEvent_t a, b;
+    };
+    std::vector<OpRec> ops;  // NCCL-mode op timeline (emesh_engine_timeline)
     std::vector<cudaEvent_t> pool;
     size_t used = 0;
     cudaEvent_t ev(cudaStream_t st) {
@@ -350,6 +376,7 @@ struct Tracker {
     }
     void reset() {
         recs.clear();
+        ops.clear();
         used = 0;
     }
     void release() {
@@ -413,8 +440,29 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
         a.inv_divisor = (m == 0.5f) ? std::ldexp(1.0f, 1 - ex) : 0.f;  // exact reciprocal of a power of two
     }
     a.scratch = ws.scratch;
-    a.out_codes = io.out_codes;
-    a.out_cb = io.out_cb;
+    a.ndest = 0;
+    if (io.local_out) {
+        a.dcodes[0] = io.out_codes;
+        a.dcb[0] = io.out_cb;
+        a.ndest = 1;
+    }
+    if (io.nflags > (uint32_t)kMaxDest || a.ndest + io.nx > (uint32_t)kMaxDest)
+        return fail(EMESH_ECONFIG, "too many quantizer destinations");
+    for (uint32_t d = 0; d < io.nx; ++d) {
+        a.dcodes[a.ndest] = io.x_codes[d];
+        a.dcb[a.ndest] = io.x_cb[d];
+        ++a.ndest;
+    }
+    for (uint32_t f = 0; f < io.nflags; ++f) a.sflag[f] = io.flags[f];
+    a.nflag = io.nflags;
+    a.remote = io.nx > 0 ? 1u : 0u;
+    static const bool tile_fence = [] {
+        const char* v = std::getenv("EMESH_P2P_TILE_FENCE");  // tuning knob
+        return v ? std::atoi(v) != 0 : false;
+    }();
+    if (a.remote && tile_fence) a.remote |= 2u;
+    a.in_flag = io.in_flag;
+    a.epoch = io.epoch;
     a.stats = io.stats;
     a.leaf_stat = ws.leaf_stat;
     a.acc = ws.acc;
@@ -469,9 +517,15 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
 }
 
 int launch_apply(const Batch& bt, int mode, const uint8_t* codes, const float* cb, float* theta, float* buf,
-                 float* theta_local, float* out, float lr, float mom, cudaStream_t st, Tracker* tr) {
+                 float* theta_local, float* out, float lr, float mom, cudaStream_t st, Tracker* tr,
+                 const uint32_t* in_flag = nullptr, uint32_t epoch = 0, uint8_t* keep_codes = nullptr,
+                 float* keep_cb = nullptr) {
     if (bt.ncta == 0) return EMESH_OK;
     ApplyArgs a{};
+    a.in_flag = in_flag;
+    a.epoch = epoch;
+    a.keep_codes = keep_codes;
+    a.keep_cb = keep_cb;
     a.segs = bt.d_segs;
     a.cta_seg = bt.d_cta_seg;
     a.ncta = bt.ncta;
@@ -700,6 +754,22 @@ struct emesh_engine {
         SegStat* stats = nullptr;
     };
     std::vector<Arena> arenas;  // per local worker
+    // peer transport (EMESH_TRANSPORT_P2P): ring over peer memory mapped with
+    // CUDA IPC; codes / codebooks double-buffered by round parity; arrival
+    // flags hold the round (epoch) number, so they never need resetting
+    int transport = EMESH_TRANSPORT_NCCL;
+    uint32_t epoch = 0;
+    uint8_t* codes_alt = nullptr;  // parity-1 codes arena (parity 0: arenas[0].codes)
+    float* cbs_alt = nullptr;
+    uint32_t* rs_flag = nullptr;  // [slot] reduce-scatter payload arrived (epoch)
+    uint32_t* ag_flag = nullptr;  // [slot] owner's final payload arrived (epoch)
+    struct Peer {
+        uint8_t* codes[2] = {nullptr, nullptr};
+        float* cbs[2] = {nullptr, nullptr};
+        uint32_t* rs_flag = nullptr;
+        uint32_t* ag_flag = nullptr;
+    };
+    std::vector<Peer> peers;  // [rank]; own rank: local pointers
     // device mirrors for the host-buffer entry point
     std::vector<float*> h_theta, h_local, h_buf;
     Tracker tr;
@@ -707,6 +777,10 @@ struct emesh_engine {
 };
 
 namespace {
+
+void teardown_p2p(emesh_engine* e);
+const uint8_t* payload_codes(const emesh_engine* e, uint32_t w);
+const float* payload_cbs(const emesh_engine* e, uint32_t w);
 
 int engine_alloc(emesh_engine* e) {
     const uint64_t n = e->plan.n;
@@ -848,6 +922,14 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
         if (P[c].size() != W) return fail(EMESH_ECONFIG, "ring chunks have unequal window counts");
     for (const emesh_ring_op& o : e->schedule) {
         const uint32_t j = (uint32_t)o.window;
+        // timeline (profiling only): events on the op's stream, after its waits
+        cudaStream_t ost = o.kind == EMESH_OP_XFER ? sm : sc;
+        if (e->tr.prof) {
+            if (o.kind == EMESH_OP_XFER && (o.phase == 0 || o.hop == 0)) CU(cudaStreamWaitEvent(sm, e->ev_send[j], 0));
+            if (o.kind == EMESH_OP_QUANT || (o.kind == EMESH_OP_APPLY && o.hop >= 0))
+                CU(cudaStreamWaitEvent(sc, e->ev_recv[j], 0));
+            e->tr.ops.push_back({o.kind, o.phase, o.hop, o.window, e->tr.ev(ost), nullptr});
+        }
         switch (o.kind) {
             case EMESH_OP_OWN: {
                 QuantIO io{pg ? kSrcAminusB : kSrcA, A, B, nullptr, nullptr, 1.f, ar.codes, ar.cbs, ar.stats};
@@ -882,8 +964,194 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
             default:
                 return fail(EMESH_ECONFIG, "bad schedule op");
         }
+        if (e->tr.prof) e->tr.ops.back().b = e->tr.ev(ost);
     }
     return EMESH_OK;
+}
+
+// Peer transport round (EMESH_TRANSPORT_P2P). Same ring as run_nccl
+// (allreduce.hpp:411-464) with the transfers folded into the kernels: each
+// quantizer launch stores its payload into the successor's arena (parity
+// buffer of this round) and flags every finished segment there; the next
+// hop's quantizer waits segment by segment. The owner's final payload goes
+// to every rank at once, which replaces the all-gather's k-1 forwarding hops
+// (the bytes are identical: AG forwards them verbatim, allreduce.hpp:446-464).
+int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float* buf, float* local_out, float* out,
+            float lr, float mom) {
+    const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
+    const bool pg = B != nullptr;
+    const uint32_t ep = ++e->epoch;
+    const int par = (int)(ep & 1u);
+    auto& ar = e->arenas[0];
+    cudaStream_t sc = e->s_comp;
+    const auto& P = e->plan.batches;
+    for (uint32_t c = 0; c < k; ++c)
+        if (P[c].size() != 1) return fail(EMESH_ECONFIG, "peer transport expects one batch per chunk");
+    auto mark = [&](int kind, int hop, bool begin) {
+        if (!e->tr.prof) return;
+        if (begin) e->tr.ops.push_back({kind, kind == EMESH_OP_APPLY ? 1 : 0, hop, 0, e->tr.ev(sc), nullptr});
+        else e->tr.ops.back().b = e->tr.ev(sc);
+    };
+    auto to_succ = [&](QuantIO& io) {
+        io.local_out = false;
+        io.nx = 1;
+        io.x_codes[0] = e->peers[succ].codes[par];
+        io.x_cb[0] = e->peers[succ].cbs[par];
+        io.nflags = 1;
+        io.flags[0] = e->peers[succ].rs_flag;
+    };
+    {   // hop-0 payload Q(delta[chunk r]) -> successor
+        QuantIO io{pg ? kSrcAminusB : kSrcA, A, B, nullptr, nullptr, 1.f, nullptr, nullptr, ar.stats};
+        to_succ(io);
+        io.epoch = ep;
+        mark(EMESH_OP_OWN, 0, true);
+        TRY(launch_quant(P[r][0], e->ws, io, sc, &e->tr));
+        mark(EMESH_OP_OWN, 0, false);
+    }
+    for (uint32_t s = 0; s + 1 < k; ++s) {
+        const uint32_t rc = (r + k - s - 1) % k;
+        QuantIO io{hop_src(pg, s, k), A, B, e->peers[r].codes[par], e->peers[r].cbs[par], (float)k,
+                   e->peers[r].codes[par], e->peers[r].cbs[par], ar.stats};
+        io.in_flag = e->rs_flag;
+        io.epoch = ep;
+        if (s + 2 < k) {
+            to_succ(io);
+        } else {  // owner: final payload local; the copy engines deliver it to every other rank
+            io.local_out = true;
+        }
+        mark(EMESH_OP_QUANT, (int)s, true);
+        TRY(launch_quant(P[rc][0], e->ws, io, sc, &e->tr));
+        mark(EMESH_OP_QUANT, (int)s, false);
+    }
+    {   // all-gather: the owner's final bytes to every rank by DMA over NVLink
+        // (allreduce.hpp:446-464 forwards the same bytes hop by hop), in
+        // segment groups so receivers start decoding while the rest streams;
+        // a group's arrival flags are raised after its bytes (stream order).
+        // Runs on the comm stream, overlapping this rank's own decode.
+        cudaStream_t cm = e->s_comm;
+        CU(cudaEventRecord(e->ev_send[0], sc));
+        CU(cudaStreamWaitEvent(cm, e->ev_send[0], 0));
+        const Batch& fb = P[succ][0];
+        const uint32_t groups = std::min<uint32_t>(fb.nseg, 4);
+        for (uint32_t g = 0; g < groups; ++g) {
+            const uint32_t s0 = fb.slot0 + (uint32_t)((uint64_t)fb.nseg * g / groups);
+            const uint32_t s1 = fb.slot0 + (uint32_t)((uint64_t)fb.nseg * (g + 1) / groups);
+            const uint64_t lo = e->plan.segs[s0].lo, hi = e->plan.segs[s1 - 1].lo + e->plan.segs[s1 - 1].len;
+            for (uint32_t d = 1; d < k; ++d) {
+                const uint32_t q = (r + d) % k;
+                if (hi > lo)
+                    CU(cudaMemcpyAsync(e->peers[q].codes[par] + lo, e->peers[r].codes[par] + lo, hi - lo,
+                                       cudaMemcpyDeviceToDevice, cm));
+                CU(cudaMemcpyAsync(e->peers[q].cbs[par] + (size_t)s0 * kBuckets,
+                                   e->peers[r].cbs[par] + (size_t)s0 * kBuckets,
+                                   (size_t)(s1 - s0) * kBuckets * sizeof(float), cudaMemcpyDeviceToDevice, cm));
+                k_set_flags<<<1, 128, 0, cm>>>(e->peers[q].ag_flag, s0, s1 - s0, ep);
+                CU(cudaGetLastError());
+            }
+        }
+    }
+    // decode every chunk: own final first, then the others as their owners'
+    // copies land (per-segment ag_flag waits inside k_apply)
+    for (uint32_t d = 0; d < k; ++d) {
+        const uint32_t c = (succ + k - d) % k;  // succ = own chunk; then chunks owned by r-1, r-2, ...
+        const uint32_t* flag = d == 0 ? nullptr : e->ag_flag;
+        mark(EMESH_OP_APPLY, (int)d - 1, true);
+        if (out)
+            TRY(launch_apply(P[c][0], 0, e->peers[r].codes[par], e->peers[r].cbs[par], nullptr, nullptr, nullptr, out,
+                             0.f, 0.f, sc, &e->tr, flag, ep));
+        else
+            TRY(launch_apply(P[c][0], 1, e->peers[r].codes[par], e->peers[r].cbs[par], theta, buf, local_out, nullptr,
+                             lr, mom, sc, &e->tr, flag, ep));
+        mark(EMESH_OP_APPLY, (int)d - 1, false);
+    }
+    return EMESH_OK;
+}
+
+// Map every rank's parity arenas and flags (CUDA IPC handles all-gathered
+// over the NCCL communicator). Returns false (and leaves the engine on NCCL)
+// unless every rank mapped every peer.
+bool setup_p2p(emesh_engine* e) {
+    const uint32_t k = e->k, r = e->rank;
+    if (k > (uint32_t)kMaxDest) return false;
+    const uint64_t n = e->plan.n;
+    const size_t nslots = e->plan.segs.size();
+    bool ok = cudaMalloc(&e->codes_alt, ((n + 15) & ~uint64_t(15)) + 16) == cudaSuccess &&
+              cudaMalloc(&e->cbs_alt, nslots * kBuckets * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&e->rs_flag, nslots * sizeof(uint32_t)) == cudaSuccess &&
+              cudaMalloc(&e->ag_flag, nslots * sizeof(uint32_t)) == cudaSuccess &&
+              cudaMemset(e->rs_flag, 0, nslots * sizeof(uint32_t)) == cudaSuccess &&
+              cudaMemset(e->ag_flag, 0, nslots * sizeof(uint32_t)) == cudaSuccess;
+    constexpr int kH = 6;
+    constexpr size_t kRec = kH * sizeof(cudaIpcMemHandle_t);
+    std::vector<uint8_t> mine(kRec, 0), all(kRec * k, 0);
+    void* bufs[kH] = {e->arenas[0].codes, e->codes_alt, e->arenas[0].cbs, e->cbs_alt, e->rs_flag, e->ag_flag};
+    for (int h = 0; ok && h < kH; ++h)
+        ok = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data()) + h, bufs[h]) == cudaSuccess;
+    // all-gather the handle records (and everyone's ok) over NCCL
+    uint8_t* d = nullptr;
+    int* d_ok = nullptr;
+    bool comm_ok = cudaMalloc(&d, kRec * (k + 1)) == cudaSuccess && cudaMalloc(&d_ok, sizeof(int)) == cudaSuccess;
+    if (comm_ok) {
+        comm_ok = cudaMemcpy(d, mine.data(), kRec, cudaMemcpyHostToDevice) == cudaSuccess &&
+                  ncclAllGather(d, d + kRec, kRec, ncclUint8, e->comm, e->s_comm) == ncclSuccess &&
+                  cudaMemcpyAsync(all.data(), d + kRec, kRec * k, cudaMemcpyDeviceToHost, e->s_comm) == cudaSuccess &&
+                  cudaStreamSynchronize(e->s_comm) == cudaSuccess;
+    }
+    e->peers.assign(k, emesh_engine::Peer{});
+    e->peers[r] = emesh_engine::Peer{{e->arenas[0].codes, e->codes_alt}, {e->arenas[0].cbs, e->cbs_alt},
+                                     e->rs_flag, e->ag_flag};
+    for (uint32_t q = 0; ok && comm_ok && q < k; ++q) {
+        if (q == r) continue;
+        void* ptr[kH] = {};
+        for (int h = 0; h < kH && ok; ++h) {
+            cudaIpcMemHandle_t hd;
+            std::memcpy(&hd, all.data() + q * kRec + h * sizeof(cudaIpcMemHandle_t), sizeof hd);
+            ok = cudaIpcOpenMemHandle(&ptr[h], hd, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+        }
+        auto& pq = e->peers[q];
+        pq.codes[0] = (uint8_t*)ptr[0]; pq.codes[1] = (uint8_t*)ptr[1];
+        pq.cbs[0] = (float*)ptr[2]; pq.cbs[1] = (float*)ptr[3];
+        pq.rs_flag = (uint32_t*)ptr[4]; pq.ag_flag = (uint32_t*)ptr[5];
+    }
+    cudaGetLastError();  // clear a failed open, if any
+    // agree: every rank must have mapped every peer
+    int v = (ok && comm_ok) ? 1 : 0;
+    bool agreed = false;
+    if (d_ok && cudaMemcpy(d_ok, &v, sizeof v, cudaMemcpyHostToDevice) == cudaSuccess &&
+        ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, e->comm, e->s_comm) == ncclSuccess &&
+        cudaMemcpyAsync(&v, d_ok, sizeof v, cudaMemcpyDeviceToHost, e->s_comm) == cudaSuccess &&
+        cudaStreamSynchronize(e->s_comm) == cudaSuccess)
+        agreed = v == 1;
+    cudaFree(d);
+    cudaFree(d_ok);
+    if (!agreed) teardown_p2p(e);
+    return agreed;
+}
+
+void teardown_p2p(emesh_engine* e) {
+    for (uint32_t q = 0; q < e->peers.size(); ++q) {
+        if (q == e->rank) continue;
+        auto& pq = e->peers[q];
+        void* ptrs[] = {pq.codes[0], pq.codes[1], pq.cbs[0], pq.cbs[1], pq.rs_flag, pq.ag_flag};
+        for (void* p : ptrs)
+            if (p) cudaIpcCloseMemHandle(p);
+    }
+    e->peers.clear();
+    cudaFree(e->codes_alt);
+    cudaFree(e->cbs_alt);
+    cudaFree(e->rs_flag);
+    cudaFree(e->ag_flag);
+    e->codes_alt = nullptr;
+    e->cbs_alt = nullptr;
+    e->rs_flag = e->ag_flag = nullptr;
+    cudaGetLastError();
+}
+
+const uint8_t* payload_codes(const emesh_engine* e, uint32_t w) {
+    return (e->transport == EMESH_TRANSPORT_P2P && (e->epoch & 1u)) ? e->codes_alt : e->arenas[w].codes;
+}
+const float* payload_cbs(const emesh_engine* e, uint32_t w) {
+    return (e->transport == EMESH_TRANSPORT_P2P && (e->epoch & 1u)) ? e->cbs_alt : e->arenas[w].cbs;
 }
 
 int engine_enter(emesh_engine* e, cudaStream_t user) {
@@ -977,10 +1245,12 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
     // with, and the persistent quantizer pipelines stats and bins across the
     // segments of a batch); a quarter chunk (>= 16M) under NCCL so transfers
     // of window j+1 overlap the kernels of window j
+    if (cfg->transport > EMESH_TRANSPORT_P2P) return bail(fail(EMESH_ECONFIG, "unknown transport %u", cfg->transport));
     const uint64_t chunk = (cfg->n + cfg->k - 1) / cfg->k;
-    uint64_t window = cfg->window_elems ? cfg->window_elems
-                      : virt ? std::max<uint64_t>(chunk, 1)
-                             : std::max<uint64_t>(chunk / 4, kDefaultWindow);
+    // the peer transport synchronizes per segment: one batch per chunk
+    const bool try_p2p = !virt && cfg->k > 1 && cfg->transport != EMESH_TRANSPORT_NCCL;
+    const uint64_t nccl_window = cfg->window_elems ? cfg->window_elems : std::max<uint64_t>(chunk / 4, kDefaultWindow);
+    uint64_t window = (virt || try_p2p) ? ~uint64_t(0) >> 2 : nccl_window;  // whole chunks
     e->plan = make_ring_plan(cfg->n, cfg->k, S, window);
     e->windows = (uint32_t)e->plan.batches[0].size();
     int rc = e->plan.upload();
@@ -1008,6 +1278,27 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
         std::memcpy(&id, cfg->nccl_id, sizeof id);
         ncclResult_t r = ncclCommInitRank(&e->comm, (int)e->k, id, (int)e->rank);
         if (r != ncclSuccess) return bail(fail(EMESH_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+        e->transport = EMESH_TRANSPORT_NCCL;
+        if (try_p2p && setup_p2p(e)) {
+            e->transport = EMESH_TRANSPORT_P2P;
+        } else if (cfg->transport == EMESH_TRANSPORT_P2P) {
+            return bail(fail(EMESH_ECONFIG, "peer transport unavailable (CUDA IPC mapping failed on some rank)"));
+        } else if (try_p2p) {  // AUTO fell back: NCCL windows
+            e->plan.release();
+            e->plan = make_ring_plan(cfg->n, cfg->k, S, nccl_window);
+            e->windows = (uint32_t)e->plan.batches[0].size();
+            if ((rc = e->plan.upload()) || (rc = e->ws.reserve(e->plan.max_slots, e->plan.max_cta, e->plan.max_segs)))
+                return bail(rc);
+            e->schedule = build_schedule(e->plan, e->rank);
+            for (auto ev : e->ev_send) cudaEventDestroy(ev);
+            for (auto ev : e->ev_recv) cudaEventDestroy(ev);
+            e->ev_send.assign(e->windows, nullptr);
+            e->ev_recv.assign(e->windows, nullptr);
+            for (uint32_t j = 0; j < e->windows; ++j) {
+                cudaEventCreateWithFlags(&e->ev_send[j], cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&e->ev_recv[j], cudaEventDisableTiming);
+            }
+        }
     }
     *out = e;
     return EMESH_OK;
@@ -1018,6 +1309,7 @@ int emesh_engine_destroy(emesh_engine* e) {
     cudaSetDevice(e->device);
     if (e->s_comp) cudaStreamSynchronize(e->s_comp);
     if (e->s_comm) cudaStreamSynchronize(e->s_comm);
+    teardown_p2p(e);
     if (e->comm) ncclCommDestroy(e->comm);
     for (auto& a : e->arenas) { cudaFree(a.codes); cudaFree(a.cbs); cudaFree(a.stats); }
     for (auto* p : e->h_theta) cudaFree(p);
@@ -1048,12 +1340,30 @@ uint64_t emesh_engine_segments(const emesh_engine* e, uint64_t* lo, uint64_t* le
 
 uint64_t emesh_engine_launches(const emesh_engine* e) { return e->tr.launches; }
 
+int emesh_engine_transport(const emesh_engine* e) { return (e && !e->virt && e->k > 1) ? e->transport : 0; }
+
 int emesh_engine_profile(emesh_engine* e, int enable) {
     CU(cudaSetDevice(e->device));
     CU(cudaStreamSynchronize(e->s_comp));
     e->tr.reset();
     e->tr.prof = enable != 0;
     return EMESH_OK;
+}
+
+uint64_t emesh_engine_timeline(emesh_engine* e, double* rows, uint64_t max_rows) {
+    if (!e) return 0;
+    if (cudaSetDevice(e->device) != cudaSuccess || cudaStreamSynchronize(e->s_comp) != cudaSuccess ||
+        cudaStreamSynchronize(e->s_comm) != cudaSuccess)
+        return 0;
+    const auto& v = e->tr.ops;
+    for (size_t i = 0; i < v.size() && i < max_rows; ++i) {
+        float t0 = 0.f, t1 = 0.f;
+        cudaEventElapsedTime(&t0, v[0].a, v[i].a);
+        cudaEventElapsedTime(&t1, v[0].a, v[i].b);
+        double* r = rows + 6 * i;
+        r[0] = v[i].kind; r[1] = v[i].phase; r[2] = v[i].hop; r[3] = v[i].window; r[4] = t0; r[5] = t1;
+    }
+    return v.size();
 }
 
 int emesh_engine_profile_read(emesh_engine* e, uint32_t kind, uint64_t* count, double* ms, double* bytes) {
@@ -1087,6 +1397,8 @@ int emesh_engine_ring_allreduce(emesh_engine* e, const float* const* input, floa
         CU(cudaMemcpyAsync(output[0], input[0], e->plan.n * sizeof(float), cudaMemcpyDeviceToDevice, e->s_comp));
     } else if (e->virt) {
         TRY(run_virtual(e, input, nullptr, nullptr, nullptr, nullptr, output, 0.f, 0.f));
+    } else if (e->transport == EMESH_TRANSPORT_P2P) {
+        TRY(run_p2p(e, input[0], nullptr, nullptr, nullptr, nullptr, output[0], 0.f, 0.f));
     } else {
         TRY(run_nccl(e, input[0], nullptr, nullptr, nullptr, nullptr, output[0], 0.f, 0.f));
     }
@@ -1113,6 +1425,9 @@ int emesh_engine_outer_sync(emesh_engine* e, float* const* theta_g, float* const
     } else if (e->virt) {
         TRY(run_virtual(e, (const float* const*)theta_g, (const float* const*)theta_l, theta_g, buf,
                         write_local ? theta_l : nullptr, nullptr, lr, mom));
+    } else if (e->transport == EMESH_TRANSPORT_P2P) {
+        TRY(run_p2p(e, theta_g[0], theta_l[0], theta_g[0], buf[0], write_local ? theta_l[0] : nullptr, nullptr, lr,
+                    mom));
     } else {
         TRY(run_nccl(e, theta_g[0], theta_l[0], theta_g[0], buf[0], write_local ? theta_l[0] : nullptr, nullptr, lr,
                      mom));
@@ -1169,8 +1484,8 @@ int emesh_engine_check(emesh_engine* e) {
 int emesh_engine_payload(emesh_engine* e, uint32_t worker, const uint8_t** codes, const float** cbs,
                          const double** stats, uint64_t* stride) {
     if (worker >= e->arenas.size()) return fail(EMESH_ECONFIG, "no such local worker");
-    if (codes) *codes = e->arenas[worker].codes;
-    if (cbs) *cbs = e->arenas[worker].cbs;
+    if (codes) *codes = payload_codes(e, worker);
+    if (cbs) *cbs = payload_cbs(e, worker);
     if (stats) *stats = reinterpret_cast<const double*>(e->arenas[worker].stats);
     if (stride) *stride = sizeof(SegStat);
     return EMESH_OK;
@@ -1181,8 +1496,8 @@ int emesh_engine_payload_host(emesh_engine* e, uint32_t worker, uint8_t* codes, 
     TRY(emesh_engine_check(e));
     const auto& a = e->arenas[worker];
     const size_t nseg = e->plan.segs.size();
-    if (codes && e->plan.n) CU(cudaMemcpy(codes, a.codes, e->plan.n, cudaMemcpyDeviceToHost));
-    if (cbs) CU(cudaMemcpy(cbs, a.cbs, nseg * kBuckets * sizeof(float), cudaMemcpyDeviceToHost));
+    if (codes && e->plan.n) CU(cudaMemcpy(codes, payload_codes(e, worker), e->plan.n, cudaMemcpyDeviceToHost));
+    if (cbs) CU(cudaMemcpy(cbs, payload_cbs(e, worker), nseg * kBuckets * sizeof(float), cudaMemcpyDeviceToHost));
     if (stats)
         CU(cudaMemcpy2D(stats, 4 * sizeof(double), a.stats, sizeof(SegStat), 4 * sizeof(double), nseg,
                         cudaMemcpyDeviceToHost));

@@ -38,7 +38,21 @@ constexpr int kWarps = 8;              // warps per CTA
 constexpr int kThreads = kWarps * 32;  // 256
 constexpr int kSlotsPerLane = 8;       // float4 slots per lane per unit
 constexpr int kUnitSlots = 32 * kSlotsPerLane;  // 256 float4 = 1024 elements
-constexpr int kUnitsPerWarp = 2;                 // warp units per tile task
+#ifndef EMESH_QUANT_MINB
+#define EMESH_QUANT_MINB 3
+#endif
+#ifndef EMESH_UNITS_PER_WARP
+#define EMESH_UNITS_PER_WARP 2
+#endif
+constexpr int kUnitsPerWarp = EMESH_UNITS_PER_WARP;  // warp units per tile task (2 or 4)
+static_assert(kUnitsPerWarp == 2 || kUnitsPerWarp == 4, "limb layout sized for <= 4096 members per warp");
+// Bin-pass limbs (32-bit smem atomics per warp over one tile, see bin_unit):
+// A = r[0:kLoBits) | 1 << kCntShift, B = r[kLoBits:kMidEnd), C = r[kMidEnd:42).
+// With m = 1024 kUnitsPerWarp members: m (2^kLoBits - 1) < 2^kCntShift,
+// m < 2^(32 - kCntShift), m 2^(kMidEnd - kLoBits) <= 2^32, m 2^(42 - kMidEnd) < 2^32.
+constexpr int kLoBits = kUnitsPerWarp == 2 ? 9 : 7;
+constexpr int kCntShift = kUnitsPerWarp == 2 ? 20 : 19;
+constexpr int kMidEnd = kUnitsPerWarp == 2 ? 30 : 26;
 constexpr int kTileUnits = kWarps * kUnitsPerWarp;  // 16 units = 16384 elements per tile
 
 // Exact fixed-point encoding of one bucket's members for the codebook sums:
@@ -109,6 +123,8 @@ __device__ __forceinline__ StatP statp_merge(StatP a, const StatP& b) {
     return a;
 }
 
+constexpr int kMaxDest = 8;  // output destinations of one quantizer launch (ranks of a peer ring)
+
 // Producer of the value being quantized, fused into the statistics pass.
 enum : int {
     kSrcA = 0,          // x = a                      (plain buffer)
@@ -143,8 +159,18 @@ struct QuantArgs {
     float divisor;
     float inv_divisor;         // 1/k when k is a power of two (exact), else 0
     float* scratch;            // x, float4-slot indexed from scratch_q0
-    uint8_t* out_codes;
-    float* out_cb;
+    // output destinations (peer transport: the successor's arena); after a
+    // segment's codes + codebook are stored everywhere, store `epoch` to
+    // sflag[f][slot] for every flag f (the successor's arrival flags, or
+    // every rank's for the owner's final payload)
+    uint8_t* dcodes[kMaxDest];
+    float* dcb[kMaxDest];
+    uint32_t ndest;
+    uint32_t* sflag[kMaxDest];
+    uint32_t nflag;
+    uint32_t remote;           // bit 0: peer-memory outputs; bit 1: system fence per tile
+    const uint32_t* in_flag;   // peer transport: in_codes / in_cb of slot s valid once in_flag[s] >= epoch
+    uint32_t epoch;
     SegStat* stats;            // indexed by slot
     StatP* leaf_stat;          // [tile]
     SegAcc* acc;               // [seg] bucket histograms (batch-local segment)
@@ -211,6 +237,22 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
 }
 __device__ __forceinline__ void spin_until_nonzero(const uint32_t* p) {
     while (ld_acquire(p) == 0u) __nanosleep(32);
+}
+// Cross-GPU signalling (peer transport): flags live in the receiver's memory.
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void spin_until_ge_sys(const uint32_t* p, uint32_t epoch) {
+    uint32_t ns = 64;
+    while ((int32_t)(ld_acquire_sys(p) - epoch) < 0) {
+        __nanosleep(ns);
+        ns = ns < 2048 ? 2 * ns : ns;
+    }
 }
 
 // The reference's bucket function, exactly (quant.hpp:65-72).
@@ -371,6 +413,10 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
     if (SRC & kHasIn) {
         if (sm.lut_seg != (int32_t)s) {
             __syncthreads();
+            if (a.in_flag) {  // peer transport: wait until the predecessor's payload of s landed
+                if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.in_slot, a.epoch);
+                __syncthreads();
+            }
             sm.lut[threadIdx.x] = __ldcg(a.in_cb + (uint64_t)si.in_slot * kBuckets + threadIdx.x);
             __syncthreads();
             if (threadIdx.x == 0) sm.lut_seg = (int32_t)s;
@@ -581,10 +627,8 @@ struct BinParams {
 // clipping), fixed-point codes via the fp32 fast path (fp64 for the few
 // buckets that need it), then the limb atomics — unconditional, so the
 // common path has no data-dependent branches (invalid lanes add 0).
-// Per-warp limbs over a tile (<= 2048 members per warp):
-//   A += r[0:9) | 1 << 20   (count in bits 20..31)
-//   B += r[9:30)
-//   C += r[30:42)           (fp64 path only; fast-path r < 2^24)
+// Per-warp limbs over a tile (see kLoBits): A += low bits | one count,
+// B += middle bits, C += high bits (only when nonzero: rare).
 template <bool INTERIOR, bool FROM_SCRATCH>
 __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const SegInfo& si, uint64_t qbase,
                                          uint64_t hiel, const float4* xs, uint32_t* hw, const BinParams& p,
@@ -658,28 +702,31 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
                 const uint32_t rhi = (uint32_t)__double2hiint(m);
                 const bool valid = (vmask >> i) & 1u;
                 uint32_t* hc = hw + 3 * cc[i];
-                atomicAdd(hc, valid ? ((rlo & 0x1ffu) | (1u << 20)) : 0u);
-                atomicAdd(hc + 1, valid ? ((rlo >> 9) & 0x1fffffu) : 0u);
-                const uint32_t rc = __funnelshift_r(rlo, rhi, 30) & 0xfffu;
+                atomicAdd(hc, valid ? ((rlo & ((1u << kLoBits) - 1u)) | (1u << kCntShift)) : 0u);
+                atomicAdd(hc + 1, valid ? ((rlo >> kLoBits) & ((1u << (kMidEnd - kLoBits)) - 1u)) : 0u);
+                const uint32_t rc = __funnelshift_r(rlo, rhi, kMidEnd) & ((1u << (42 - kMidEnd)) - 1u);
                 if (valid && rc) atomicAdd(hc + 2, rc);
             }
             const uint32_t p0 = __byte_perm(__byte_perm(cc[0], cc[1], 0x0040), __byte_perm(cc[2], cc[3], 0x0040), 0x5410);
             const uint32_t p1 = __byte_perm(__byte_perm(cc[4], cc[5], 0x0040), __byte_perm(cc[6], cc[7], 0x0040), 0x5410);
-            if (INTERIOR) {
-                reinterpret_cast<uint32_t*>(a.out_codes)[q0] = p0;
-                reinterpret_cast<uint32_t*>(a.out_codes)[q0 + 32] = p1;
-            } else {
+            for (uint32_t d = 0; d < a.ndest; ++d) {
+                uint8_t* oc = a.dcodes[d];
+                if (INTERIOR) {
+                    reinterpret_cast<uint32_t*>(oc)[q0] = p0;
+                    reinterpret_cast<uint32_t*>(oc)[q0 + 32] = p1;
+                } else {
 #pragma unroll
-                for (int f = 0; f < 2; ++f) {
-                    const uint64_t q = q0 + (uint64_t)f * 32;
-                    const uint32_t packed = f ? p1 : p0;
-                    const uint32_t vm = (vmask >> (4 * f)) & 0xfu;
-                    if (vm == 0xfu) {
-                        reinterpret_cast<uint32_t*>(a.out_codes)[q] = packed;
-                    } else if (vm) {
+                    for (int f = 0; f < 2; ++f) {
+                        const uint64_t q = q0 + (uint64_t)f * 32;
+                        const uint32_t packed = f ? p1 : p0;
+                        const uint32_t vm = (vmask >> (4 * f)) & 0xfu;
+                        if (vm == 0xfu) {
+                            reinterpret_cast<uint32_t*>(oc)[q] = packed;
+                        } else if (vm) {
 #pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            if (vm & (1u << e)) a.out_codes[q * 4 + e] = (uint8_t)(packed >> (8 * e));
+                            for (int e = 0; e < 4; ++e)
+                                if (vm & (1u << e)) oc[q * 4 + e] = (uint8_t)(packed >> (8 * e));
+                        }
                     }
                 }
             }
@@ -698,6 +745,8 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
 }
 
 __device__ void finalize_codebook(const QuantArgs& a, uint32_t s, const SegInfo& si);
+__device__ float codebook_entry(const SegStat* st, int b, unsigned long long rl, unsigned long long rh,
+                                unsigned long long total, unsigned long long clip);
 
 template <bool FROM_SCRATCH>
 __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si, uint32_t tile) {
@@ -740,7 +789,8 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
             for (int j = 0; j < kSlotsPerLane; ++j) {
                 const uint64_t q = qbase + (uint64_t)j * 32 + lane;
                 for (int e = 0; e < 4; ++e)
-                    if (q * 4 + e >= si.lo && q * 4 + e < hiel) a.out_codes[q * 4 + e] = 0;
+                    if (q * 4 + e >= si.lo && q * 4 + e < hiel)
+                        for (uint32_t d = 0; d < a.ndest; ++d) a.dcodes[d][q * 4 + e] = 0;
             }
         } else if (interior) {
             bin_unit<true, FROM_SCRATCH>(a, sm, si, qbase, hiel, xs, hw, bpar, nclip_lo, nclip_hi);
@@ -764,8 +814,9 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
             const uint32_t A = sm.hist[w][b][0], B = sm.hist[w][b][1], C = sm.hist[w][b][2];
-            r += (unsigned long long)(A & 0xfffffu) + ((unsigned long long)B << 9) + ((unsigned long long)C << 30);
-            cn += A >> 20;
+            r += (unsigned long long)(A & ((1u << kCntShift) - 1u)) + ((unsigned long long)B << kLoBits) +
+                 ((unsigned long long)C << kMidEnd);
+            cn += A >> kCntShift;
             sm.hist[w][b][0] = 0u;
             sm.hist[w][b][1] = 0u;
             sm.hist[w][b][2] = 0u;
@@ -779,8 +830,13 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
         if (b < 2 && sm.clip[b]) atomicAdd(&acc->clip[b], (unsigned long long)sm.clip[b]);
     }
     __syncthreads();
-    if (threadIdx.x == 0)  // acq_rel: releases the CTA's atomics; the last tile acquires all
+    if (threadIdx.x == 0) {
+        // codes stored to peer memory are performed system-wide before the
+        // arrival, so the last tile's flag store (system scope) covers them
+        if (a.remote & 2u) __threadfence_system();
+        // acq_rel: releases the CTA's atomics; the last tile acquires all
         sm.flag = atom_add_acq_rel(&a.sync[kSyncReady + 2 * a.nseg + s], 1u) == si.ncta - 1 ? 1u : 0u;
+    }
     __syncthreads();
     if (sm.flag) finalize_codebook(a, s, si);
 }
@@ -800,12 +856,30 @@ __device__ void finalize_codebook(const QuantArgs& a, uint32_t s, const SegInfo&
     acc->rhi[b] = 0ull;
     acc->cnt[b] = 0ull;
     if (b < 2) acc->clip[b] = 0ull;
-    float* cb = a.out_cb + (uint64_t)si.slot * kBuckets;
-    if (degenerate) { cb[b] = (float)__ldcg(&st->mu); return; }
-    if (total == 0) {
-        cb[b] = (float)__dadd_rn(__ldcg(&st->lo), __dmul_rn(__dadd_rn((double)b, 0.5), __ldcg(&st->width)));
-        return;
+    float v;
+    if (degenerate) {
+        v = (float)__ldcg(&st->mu);
+    } else if (total == 0) {
+        v = (float)__dadd_rn(__ldcg(&st->lo), __dmul_rn(__dadd_rn((double)b, 0.5), __ldcg(&st->width)));
+    } else {
+        v = codebook_entry(st, b, rl, rh, total, clip);
     }
+    for (uint32_t d = 0; d < a.ndest; ++d) a.dcb[d][(uint64_t)si.slot * kBuckets + b] = v;
+    if (a.nflag) {
+        // Every tile of s released its stores (gpu scope) to the arrival
+        // counter this CTA acquired; the system-scope fence + release here
+        // extends that causality chain to the peers polling the flags.
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence_system();
+            for (uint32_t f = 0; f < a.nflag; ++f) st_release_sys(a.sflag[f] + si.slot, a.epoch);
+        }
+    }
+}
+
+// Codebook entry b from the exact bucket sums (quant.hpp:78-85).
+__device__ float codebook_entry(const SegStat* st, int b, unsigned long long rl, unsigned long long rh,
+                                unsigned long long total, unsigned long long clip) {
     const unsigned long long cnt = total - clip;  // clipped members are counted with r = 0
     double sum = 0.0;
     if (cnt) {
@@ -824,11 +898,11 @@ __device__ void finalize_codebook(const QuantArgs& a, uint32_t s, const SegInfo&
     }
     if (b == 0 && clip) sum = __dadd_rn(sum, __dmul_rn((double)clip, __ldcg(&st->lo)));
     if (b == 255 && clip) sum = __dadd_rn(sum, __dmul_rn((double)clip, __ldcg(&st->hi)));
-    cb[b] = (float)__ddiv_rn(sum, (double)total);
+    return (float)__ddiv_rn(sum, (double)total);
 }
 
 template <int SRC>
-__global__ void __launch_bounds__(kThreads, 3) k_quant(QuantArgs a) {
+__global__ void __launch_bounds__(kThreads, EMESH_QUANT_MINB) k_quant(QuantArgs a) {
     extern __shared__ __align__(16) unsigned char qsmem_raw[];
     QSmem& sm = *reinterpret_cast<QSmem*>(qsmem_raw);  // dynamic: > 48 KB in total
     uint4* runs_s = reinterpret_cast<uint4*>(qsmem_raw + sizeof(QSmem));
@@ -864,7 +938,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_quant(QuantArgs a) {
             const uint4 r = runs_s[lo];
             kind = r.y;
             s = r.z;
-            tile = r.w + (t - r.x);
+            tile = (r.w & 0x80000000u) ? (r.w & 0x7fffffffu) - (t - r.x) : r.w + (t - r.x);
         } else {
             uint32_t lo = 0, hi = a.nruns;
             while (hi - lo > 1) {
@@ -874,7 +948,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_quant(QuantArgs a) {
             const uint4 r = a.runs[lo];
             kind = r.y;
             s = r.z;
-            tile = r.w + (t - r.x);
+            tile = (r.w & 0x80000000u) ? (r.w & 0x7fffffffu) - (t - r.x) : r.w + (t - r.x);
         }
         const SegInfo si = segs_in_smem ? segs_s[s] : a.segs[s];
         unsigned long long t0 = 0, t1 = 0;
@@ -921,6 +995,10 @@ struct ApplyArgs {
     float* theta_local;    // optional: theta_l <- theta_g (trainer.hpp:382)
     float* out;            // dequantize target (arena-indexed)
     float lr, mom;
+    const uint32_t* in_flag;  // peer transport: codes / codebook of slot s valid once in_flag[s] >= epoch
+    uint32_t epoch;
+    uint8_t* keep_codes;      // peer transport: local copy of the (remote) codes / codebook read
+    float* keep_cb;
 };
 
 __device__ __forceinline__ void nesterov1(float& th, float& b, float d, float lr, float mom) {
@@ -936,7 +1014,12 @@ __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
     __shared__ float lut[kBuckets];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const SegInfo si = a.segs[a.cta_seg[blockIdx.x]];
-    lut[threadIdx.x] = a.cb[(uint64_t)si.slot * kBuckets + threadIdx.x];
+    if (a.in_flag) {
+        if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.slot, a.epoch);
+        __syncthreads();
+    }
+    lut[threadIdx.x] = __ldcg(a.cb + (uint64_t)si.slot * kBuckets + threadIdx.x);
+    if (a.keep_cb && blockIdx.x == si.cta0) a.keep_cb[(uint64_t)si.slot * kBuckets + threadIdx.x] = lut[threadIdx.x];
     __syncthreads();
     const uint64_t hiel = si.lo + si.len;
     for (int ui = 0; ui < kUnitsPerWarp; ++ui) {
@@ -950,6 +1033,14 @@ __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
         if (e0 >= hiel) continue;
         const bool full = e0 >= si.lo && e0 + 4 <= hiel;
         const uint32_t c4 = __ldcs(reinterpret_cast<const uint32_t*>(a.codes) + q);
+        if (a.keep_codes) {
+            if (full) {
+                reinterpret_cast<uint32_t*>(a.keep_codes)[q] = c4;
+            } else {
+                for (int e = 0; e < 4; ++e)
+                    if (e0 + e >= si.lo && e0 + e < hiel) a.keep_codes[e0 + e] = (uint8_t)(c4 >> (8 * e));
+            }
+        }
         float d[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) d[e] = lut[(c4 >> (8 * e)) & 0xff];
@@ -982,6 +1073,12 @@ __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
         }
     }
     }
+}
+
+// Peer transport: raise the arrival flags of slots [slot0, slot0 + n) on a
+// peer after the copy engine delivered their bytes (stream-ordered before).
+__global__ void k_set_flags(uint32_t* flags, uint32_t slot0, uint32_t n, uint32_t epoch) {
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) st_release_sys(flags + slot0 + i, epoch);
 }
 
 // ---------------------------------------------------------------------------

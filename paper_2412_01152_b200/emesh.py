@@ -403,7 +403,8 @@ class RingEngine:
     device buffer the round needs; nothing is allocated per round."""
 
     def __init__(self, n: int, k: int, rank: int = 0, opts: Optional[ReduceOptions] = None, virtual: bool = False,
-                 nccl_id: Optional[bytes] = None, window_elems: int = 0, device: Optional[int] = None):
+                 nccl_id: Optional[bytes] = None, window_elems: int = 0, device: Optional[int] = None,
+                 transport: str = "auto"):
         opts = opts or ReduceOptions()
         if opts.pipeline_subchunks < 1:
             raise ConfigError("pipeline_subchunks must be >= 1")
@@ -417,6 +418,10 @@ class RingEngine:
         cfg.pipeline_subchunks = self.S
         cfg.virtual_workers = k if (virtual and k > 1) else 0
         cfg.window_elems = int(window_elems)
+        tmap = {"auto": _capi.TRANSPORT_AUTO, "nccl": _capi.TRANSPORT_NCCL, "p2p": _capi.TRANSPORT_P2P}
+        if transport not in tmap:
+            raise ConfigError(f"transport must be one of {sorted(tmap)}")
+        cfg.transport = tmap[transport]
         if nccl_id is not None:
             self._idbuf = C.create_string_buffer(bytes(nccl_id), 128)
             cfg.nccl_id = C.cast(self._idbuf, C.c_void_p)
@@ -441,6 +446,11 @@ class RingEngine:
             self.close()
         except Exception:
             pass
+
+    @property
+    def transport(self) -> str:
+        """The resolved transport: "p2p", "nccl", or "local" (virtual ring / k == 1)."""
+        return {1: "nccl", 2: "p2p"}.get(_capi.lib().emesh_engine_transport(self._h), "local")
 
     def segments(self):
         cnt = _capi.lib().emesh_engine_segments(self._h, None, None)
@@ -467,6 +477,14 @@ class RingEngine:
             if c.value:
                 out[name] = {"launches": c.value, "ms": ms.value, "alg_bytes": by.value}
         return out
+
+    def timeline(self, max_rows: int = 1 << 16):
+        """NCCL-mode op timeline since profile(True): list of
+        (kind, phase, hop, window, start_ms, end_ms); kind in OP_* of _capi."""
+        import numpy as np
+        buf = np.zeros((max_rows, 6), dtype=np.float64)
+        m = _capi.lib().emesh_engine_timeline(self._h, buf.ctypes.data_as(C.POINTER(C.c_double)), max_rows)
+        return [tuple(r) for r in buf[:min(m, max_rows)]]
 
     def _ptrs(self, ts: Sequence[torch.Tensor], what: str):
         if len(ts) != self.workers:

@@ -25,11 +25,15 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     O = Oracle()
     ok = True
-    for n, S, window in [(100_003, 4, 0), (4099, 3, 1), (5, 4, 0), (2_000_000, 8, 300_000)]:
+    cases = [(100_003, 4, 0), (4099, 3, 1), (5, 4, 0), (2_000_000, 8, 300_000)]
+    for (n, S, window), transport in [(c, t) for t in ("nccl", "p2p") for c in cases]:
         obj = [E.RingEngine.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         eng = E.RingEngine(n, world, rank=rank, opts=E.ReduceOptions(pipeline_subchunks=S), nccl_id=obj[0],
-                           window_elems=window)
+                           window_elems=window, transport=transport)
+        if eng.transport != transport:
+            print(f"rank {rank}: asked for {transport}, engine runs {eng.transport}", flush=True)
+            ok = False
         ins = [O.uniform(n, 7 + n, w, 0, 0, 2.0 ** -6) for w in range(world)]
         want = O.ring_allreduce(ins, S, "int8")
         out = torch.empty(n + 4, dtype=torch.float32, device=dev)[:n]
@@ -37,7 +41,7 @@ def main():
         eng.check()
         got = out.cpu().numpy()
         if not np.array_equal(bits(got), bits(want)):
-            print(f"rank {rank}: ring n={n} S={S} MISMATCH ({int((bits(got) != bits(want)).sum())} elems)", flush=True)
+            print(f"rank {rank}: [{transport}] ring n={n} S={S} MISMATCH ({int((bits(got) != bits(want)).sum())} elems)", flush=True)
             ok = False
         # two outer-sync rounds (trainer.hpp:355-382)
         g = O.uniform(n, 3, 0)
@@ -51,7 +55,7 @@ def main():
             eng.check()
             eg, eb = O.outer_sync(eg, ls, eb, S, "int8", 0.7, 0.9)
             if not (np.array_equal(bits(tg.cpu().numpy()), bits(eg)) and np.array_equal(bits(tb.cpu().numpy()), bits(eb))):
-                print(f"rank {rank}: outer sync n={n} round {rnd} MISMATCH", flush=True)
+                print(f"rank {rank}: [{transport}] outer sync n={n} round {rnd} MISMATCH", flush=True)
                 ok = False
         eng.close()
     flag = torch.tensor([0 if ok else 1], device=dev)
