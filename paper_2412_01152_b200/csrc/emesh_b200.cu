@@ -518,14 +518,11 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
 
 int launch_apply(const Batch& bt, int mode, const uint8_t* codes, const float* cb, float* theta, float* buf,
                  float* theta_local, float* out, float lr, float mom, cudaStream_t st, Tracker* tr,
-                 const uint32_t* in_flag = nullptr, uint32_t epoch = 0, uint8_t* keep_codes = nullptr,
-                 float* keep_cb = nullptr) {
+                 const uint32_t* in_flag = nullptr, uint32_t epoch = 0) {
     if (bt.ncta == 0) return EMESH_OK;
     ApplyArgs a{};
     a.in_flag = in_flag;
     a.epoch = epoch;
-    a.keep_codes = keep_codes;
-    a.keep_cb = keep_cb;
     a.segs = bt.d_segs;
     a.cta_seg = bt.d_cta_seg;
     a.ncta = bt.ncta;
@@ -537,7 +534,7 @@ int launch_apply(const Batch& bt, int mode, const uint8_t* codes, const float* c
     a.out = out;
     a.lr = lr;
     a.mom = mom;
-    const dim3 g(bt.ncta), blk(kThreads);
+    const dim3 g(bt.ncta * kApplySplit), blk(kThreads);
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
     if (mode == 0) k_apply<0><<<g, blk, 0, st>>>(a);

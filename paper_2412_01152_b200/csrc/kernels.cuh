@@ -42,7 +42,7 @@ constexpr int kUnitSlots = 32 * kSlotsPerLane;  // 256 float4 = 1024 elements
 #define EMESH_QUANT_MINB 3
 #endif
 #ifndef EMESH_UNITS_PER_WARP
-#define EMESH_UNITS_PER_WARP 2
+#define EMESH_UNITS_PER_WARP 4
 #endif
 constexpr int kUnitsPerWarp = EMESH_UNITS_PER_WARP;  // warp units per tile task (2 or 4)
 static_assert(kUnitsPerWarp == 2 || kUnitsPerWarp == 4, "limb layout sized for <= 4096 members per warp");
@@ -56,21 +56,22 @@ constexpr int kMidEnd = kUnitsPerWarp == 2 ? 30 : 26;
 constexpr int kTileUnits = kWarps * kUnitsPerWarp;  // 16 units = 16384 elements per tile
 
 // Exact fixed-point encoding of one bucket's members for the codebook sums:
-// r(x) = rint((x - base) * scale), a non-negative integer < 2^42 for every
-// fp32 x the bucket can hold, produced by ONE fma: fma(x, scale, K) with
-// K = 2^52 - base*scale lands in [2^52, 2^53), whose mantissa bits are r. "Narrow" buckets (not touching zero) use
-// base = lower threshold and scale = 1/ulp, so r is exact; "wide" buckets
-// (at or near zero) use a quantum Q = 2^-41 of the bucket's magnitude and
-// base = -2^41 Q, i.e. r = x/Q + 2^41. In both cases base*scale is an exact
-// integer, so sum x = (sum r + cnt*base*scale) / scale. Integer sums are
-// associative: per-bucket sums are identical for any accumulation order, and
-// equal to the reference's sequential fp64 sum whenever that sum is exact
-// (quant.hpp:74) — always, for narrow buckets of fewer than 2^28 members.
-struct BucketParam {
-    double scale;  // 2^-e (power of two)
-    double K;      // 2^52 - base * scale (exact: base * scale is an integer < 2^42)
-};
+// each member x maps to a non-negative integer r(x) < 2^42 with
+// sum x = f(sum r, count), so per-bucket sums are integer sums — associative,
+// identical for any accumulation order, and equal to the reference's
+// sequential fp64 sum whenever that sum is exact (quant.hpp:74).
+//  * "narrow" buckets (all members of one sign, magnitudes within 2^17 of
+//    each other, normal): r = m24(x) << (E(x) - E0), the 24-bit significand
+//    shifted to the unit 2^(E0 - 150) (E = biased exponent, E0 = that of the
+//    smallest-magnitude member) — pure integer ops on the fp32 bits, exact;
+//    x = +-r 2^(E0 - 150).
+//  * "wide" buckets (at or near zero): r = rint(x / Q) + 2^41 with a quantum
+//    Q = 2^e = 2^-41 of the bucket's magnitude, one fp64 fma.
+// Per-bucket info word: [0:8) E0, bit 8 negative, bit 9 wide, [16:26) e + 512.
+constexpr uint32_t kInfoNeg = 1u << 8;
+constexpr uint32_t kInfoWide = 1u << 9;
 constexpr double kMagic52 = 4503599627370496.0;  // 2^52
+constexpr double kWideK = 4503599627370496.0 + 2199023255552.0;  // 2^52 + 2^41
 constexpr int kWideBiasBits = 41;
 
 // Per-segment statistics, written once by the root CTA of k_stats.
@@ -81,7 +82,7 @@ struct SegStat {
     uint32_t flags;      // kFlagNonFinite | kFlagDegenerate
     float margin;        // fp32 bucket estimate is exact when its fraction is in (margin, 1-margin)
     float thr[kBuckets];  // thr[j] = smallest fp32 x with code(x) >= j (j=1..255)
-    BucketParam bp[kBuckets];
+    uint32_t binfo[kBuckets];  // bucket encodings (see kInfoWide)
 };
 constexpr uint32_t kFlagNonFinite = 1u;
 constexpr uint32_t kFlagDegenerate = 2u;  // sigma == 0 (quant.hpp:49-55)
@@ -338,29 +339,18 @@ __device__ __forceinline__ int exponent_of(float f) {  // floor(log2|f|) for nor
     return u ? (31 - __clz(u)) - 149 : -150;
 }
 
-// Fixed-point parameters of bucket b whose fp32 members lie in [t0, t1).
-__device__ BucketParam bucket_param(float t0, float t1) {
-    BucketParam p;
-    p.scale = 0.0;
-    p.K = kMagic52;
-    if (!(t1 > t0)) return p;  // holds no fp32 value
+// Encoding of bucket b whose fp32 members lie in [t0, t1) (see kInfoWide).
+__device__ uint32_t bucket_info(float t0, float t1) {
+    if (!(t1 > t0)) return kInfoWide | (512u << 16);  // holds no fp32 value
     const float last = key2f(f2key(t1) - 1);
     if (t0 > 0.f || last < 0.f) {
-        // narrow: every member is a multiple of the ulp of the smallest magnitude
-        const float mn = t0 > 0.f ? t0 : last;
-        const int e = max(exponent_of(mn) - 23, -149);
-        const double span = ldexp(__dsub_rn((double)last, (double)t0), -e);
-        if (span < 2199023255552.0) {  // 2^41
-            p.scale = ldexp(1.0, -e);
-            p.K = __dsub_rn(kMagic52, ldexp((double)t0, -e));  // base = t0
-            return p;
-        }
+        const float mn = t0 > 0.f ? t0 : last, mx = t0 > 0.f ? last : t0;
+        const uint32_t e_lo = (__float_as_uint(mn) >> 23) & 0xffu, e_hi = (__float_as_uint(mx) >> 23) & 0xffu;
+        if (e_lo >= 1u && e_hi - e_lo <= 17u) return e_lo | (t0 > 0.f ? 0u : kInfoNeg);  // r < 2^41
     }
     const float mx = fmaxf(fabsf(t0), fabsf(last));
     const int e = exponent_of(mx) + 1 - kWideBiasBits;  // |x| < 2^(e+41)
-    p.scale = ldexp(1.0, -e);
-    p.K = __dadd_rn(kMagic52, 2199023255552.0);  // base = -2^41 Q: r = x/Q + 2^41
-    return p;
+    return kInfoWide | ((uint32_t)(e + 512) << 16);
 }
 
 // ---------------------------------------------------------------------------
@@ -369,7 +359,7 @@ __device__ BucketParam bucket_param(float t0, float t1) {
 
 struct QSmem {
     uint32_t hist[kWarps][kBuckets][3];  // per-warp limbs over the tile (bin), see bin_unit
-    BucketParam bp[kBuckets];            // fixed-point parameters (bin); 16-B aligned for LDS.128
+    uint32_t binfo[kBuckets];            // bucket encodings (bin)
     float thr[kBuckets + 2];             // exact threshold table (bin); [257] = bucket 0's base (lo_up)
     float lut[kBuckets];                 // incoming codebook (stats, hop)
     StatP wp[kWarps];
@@ -381,7 +371,6 @@ struct QSmem {
     uint32_t run_idx;
     unsigned long long t_main;  // trace: main loop done
 };
-static_assert(offsetof(QSmem, bp) % 16 == 0, "bp must be 16-byte aligned");
 
 // Task order (host-built run table, QuantArgs::runs): the STATS tiles of
 // the batch in segment order; the BIN tiles of segment s once `lag` more
@@ -585,7 +574,7 @@ __device__ void finalize_stats(const QuantArgs& a, QSmem& sm, uint32_t s, const 
         if (b == 0) sm.thr[kBuckets] = key2f(f2key(hi_dn) + 1);
         __syncthreads();
         st->thr[b] = b == 0 ? -INFINITY : sm.thr[b];
-        st->bp[b] = bucket_param(sm.thr[b], sm.thr[b + 1]);
+        st->binfo[b] = bucket_info(sm.thr[b], sm.thr[b + 1]);
         if (b == 0) {
             st->lo = lo; st->hi = hi; st->width = w;
             const float lo_f = (float)lo, inv_w = (float)__ddiv_rn(1.0, w);
@@ -671,6 +660,7 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
                 okall &= (fr > p.margin) & (fr < p.one_m) & ((uint32_t)c < 256u);
                 cc[i] = c;
             }
+            uint32_t clip_m = 0;  // clipped lanes: counted with r = 0 (xc = lo / hi added at the codebook)
             if (!okall) {  // rare: near an edge (exact table) or clipped (quant.hpp:66-67)
                 uint32_t clo_m = 0, chi_m = 0;
 #pragma unroll
@@ -681,25 +671,34 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
                     const float fr = __fsub_rn(g, __int2float_rz(c0));
                     if (x < p.lo_up) {
                         cc[i] = 0; clo_m |= 1u << i;
-                        xe[i] = sm.thr[kBuckets + 1];  // bucket 0's base: r = 0, counted, contributes lo at the root
                     } else if (x > p.hi_dn) {
                         cc[i] = 255; chi_m |= 1u << i;
-                        xe[i] = sm.thr[255];  // bucket 255's base
                     } else if (!(fr > p.margin && fr < p.one_m && (uint32_t)c0 < 256u)) {
                         cc[i] = bucket_walk(x, min(max(c0, 0), 255), sm.thr);
                     }
                 }
                 nclip_lo += __popc(clo_m & vmask);
                 nclip_hi += __popc(chi_m & vmask);
+                clip_m = clo_m | chi_m;
             }
-            // fixed point r = rint(x * scale + K) - 2^52 (one DFMA, exact; clipped
-            // lanes carry x = bucket base, i.e. r = 0), split into the limbs
+            // fixed point r(x) (see kInfoWide), split into the limbs
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const double2 pb = reinterpret_cast<const double2*>(sm.bp)[cc[i]];  // {scale, K}
-                const double m = __fma_rn((double)xe[i], pb.x, pb.y);
-                const uint32_t rlo = (uint32_t)__double2loint(m);
-                const uint32_t rhi = (uint32_t)__double2hiint(m);
+                const uint32_t info = sm.binfo[cc[i]];
+                const uint32_t bits = __float_as_uint(xe[i]);
+                uint32_t rlo, rhi;
+                if (info & kInfoWide) {  // at / near zero: r = rint(x / Q) + 2^41
+                    const double scale = __hiloint2double((int)((1023u + 512u - (info >> 16)) << 20), 0);
+                    const double m = __fma_rn((double)xe[i], scale, kWideK);
+                    rlo = (uint32_t)__double2loint(m);
+                    rhi = (uint32_t)__double2hiint(m);
+                } else {  // r = m24 << (E - E0)
+                    const uint32_t sh = ((bits >> 23) & 0xffu) - (info & 0xffu);
+                    const uint32_t m24 = (bits & 0x7fffffu) | 0x800000u;
+                    rlo = m24 << sh;
+                    rhi = __funnelshift_l(m24, 0u, sh);
+                }
+                if ((clip_m >> i) & 1u) rlo = rhi = 0u;
                 const bool valid = (vmask >> i) & 1u;
                 uint32_t* hc = hw + 3 * cc[i];
                 atomicAdd(hc, valid ? ((rlo & ((1u << kLoBits) - 1u)) | (1u << kCntShift)) : 0u);
@@ -756,10 +755,7 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
         __syncthreads();
         const int b = threadIdx.x;
         sm.thr[b] = b == 0 ? -INFINITY : __ldcg(&st->thr[b]);
-        BucketParam pb;
-        pb.scale = __ldcg(&st->bp[b].scale);
-        pb.K = __ldcg(&st->bp[b].K);
-        sm.bp[b] = pb;
+        sm.binfo[b] = __ldcg(&st->binfo[b]);
 
         if (b == 0) {
             sm.thr[kBuckets] = INFINITY;
@@ -883,18 +879,21 @@ __device__ float codebook_entry(const SegStat* st, int b, unsigned long long rl,
     const unsigned long long cnt = total - clip;  // clipped members are counted with r = 0
     double sum = 0.0;
     if (cnt) {
-        BucketParam pb;
-        pb.scale = __ldcg(&st->bp[b].scale);
-        pb.K = __ldcg(&st->bp[b].K);
-        // sum x * scale = sum r + cnt * base * scale (exact integers, 128-bit);
-        // base * scale = 2^52 - K
+        const uint32_t info = __ldcg(&st->binfo[b]);
+        // sum r (exact, 128-bit); wide: sum x = (sum r - cnt 2^41) Q;
+        // narrow: sum x = +-(sum r) 2^(E0 - 150)
         __int128 S = (__int128)rl + ((__int128)rh << 32);
-        S += (__int128)(long long)__double2ll_rn(__dsub_rn(kMagic52, pb.K)) * (__int128)cnt;
+        if (info & kInfoWide) S -= (__int128)cnt << kWideBiasBits;
         const long long hi64 = (long long)(S >> 64);
         const long long s64 = (long long)(unsigned long long)S;
         const bool fits = (hi64 == 0 && s64 >= 0) || (hi64 == -1 && s64 < 0);
         const double v = fits ? (double)s64 : __dadd_rn(ldexp((double)hi64, 64), (double)(unsigned long long)S);
-        sum = __ddiv_rn(v, pb.scale);  // exact: scale is a power of two
+        if (info & kInfoWide) {
+            sum = ldexp(v, (int)(info >> 16) - 512);  // exact: power-of-two scaling
+        } else {
+            sum = ldexp(v, (int)(info & 0xffu) - 150);
+            if (info & kInfoNeg) sum = -sum;
+        }
     }
     if (b == 0 && clip) sum = __dadd_rn(sum, __dmul_rn((double)clip, __ldcg(&st->lo)));
     if (b == 255 && clip) sum = __dadd_rn(sum, __dmul_rn((double)clip, __ldcg(&st->hi)));
@@ -997,9 +996,8 @@ struct ApplyArgs {
     float lr, mom;
     const uint32_t* in_flag;  // peer transport: codes / codebook of slot s valid once in_flag[s] >= epoch
     uint32_t epoch;
-    uint8_t* keep_codes;      // peer transport: local copy of the (remote) codes / codebook read
-    float* keep_cb;
 };
+constexpr int kApplySplit = kUnitsPerWarp / 2;  // k_apply CTAs per quantizer tile (2 units per warp each)
 
 __device__ __forceinline__ void nesterov1(float& th, float& b, float d, float lr, float mom) {
     // optim.hpp:127-130, fp32, this exact association, no FMA
@@ -1013,17 +1011,17 @@ template <int MODE>
 __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
     __shared__ float lut[kBuckets];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const SegInfo si = a.segs[a.cta_seg[blockIdx.x]];
+    const uint32_t tile = blockIdx.x / kApplySplit, part = blockIdx.x % kApplySplit;
+    const SegInfo si = a.segs[a.cta_seg[tile]];
     if (a.in_flag) {
         if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.slot, a.epoch);
         __syncthreads();
     }
     lut[threadIdx.x] = __ldcg(a.cb + (uint64_t)si.slot * kBuckets + threadIdx.x);
-    if (a.keep_cb && blockIdx.x == si.cta0) a.keep_cb[(uint64_t)si.slot * kBuckets + threadIdx.x] = lut[threadIdx.x];
     __syncthreads();
     const uint64_t hiel = si.lo + si.len;
-    for (int ui = 0; ui < kUnitsPerWarp; ++ui) {
-    const uint32_t u = (blockIdx.x - si.cta0) * kTileUnits + ui * kWarps + warp;
+    for (int ui = 0; ui < 2; ++ui) {
+    const uint32_t u = (tile - si.cta0) * kTileUnits + (part * 2 + ui) * kWarps + warp;
     if (u >= si.nunits) return;
     const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
 #pragma unroll 4
@@ -1033,14 +1031,6 @@ __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
         if (e0 >= hiel) continue;
         const bool full = e0 >= si.lo && e0 + 4 <= hiel;
         const uint32_t c4 = __ldcs(reinterpret_cast<const uint32_t*>(a.codes) + q);
-        if (a.keep_codes) {
-            if (full) {
-                reinterpret_cast<uint32_t*>(a.keep_codes)[q] = c4;
-            } else {
-                for (int e = 0; e < 4; ++e)
-                    if (e0 + e >= si.lo && e0 + e < hiel) a.keep_codes[e0 + e] = (uint8_t)(c4 >> (8 * e));
-            }
-        }
         float d[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) d[e] = lut[(c4 >> (8 * e)) & 0xff];
