@@ -103,6 +103,9 @@ typedef struct {
     const uint8_t* nccl_id;     /* 128-byte ncclUniqueId (NCCL mode, k > 1) */
     int device;                 /* CUDA device ordinal, -1 = current */
     uint32_t transport;         /* EMESH_TRANSPORT_*: how hop payloads move between ranks */
+    uint32_t reduce_fp32;       /* ReduceJob.mode (allreduce.hpp:49-53, :120-164): 0 = ReduceMode::int8
+                                   (uint8 codes + codebooks), 1 = ReduceMode::fp32 (raw fp32 partial sums).
+                                   One engine serves one mode; make one per mode in use. */
 } emesh_engine_config;
 
 /* Transports of the one-process-per-GPU ring (k > 1, not virtual):

@@ -42,6 +42,7 @@ class EngineConfig(C.Structure):
         ("nccl_id", C.c_void_p),
         ("device", C.c_int),
         ("transport", C.c_uint32),
+        ("reduce_fp32", C.c_uint32),
     ]
 
 

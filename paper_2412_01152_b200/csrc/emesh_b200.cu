@@ -344,6 +344,8 @@ enum ProfKind : int {
     kProfNesterov = 6,   // k_apply<1>: dequant + Nesterov (+ theta_l write)
     kProfDequant = 7,    // k_apply<0>
     kProfFusedK1 = 8,    // k_nesterov_f32 (k == 1: PG + Nesterov)
+    kProfF32Hop = 9,     // k_f32_hop (ReduceMode::fp32 accumulate / mean)
+    kProfF32Apply = 10,  // k_f32_apply (ReduceMode::fp32 decode + Nesterov)
 };
 
 // Launch accounting + optional per-kernel CUDA-event profiling on the
@@ -755,6 +757,9 @@ struct emesh_engine {
     // CUDA IPC; codes / codebooks double-buffered by round parity; arrival
     // flags hold the round (epoch) number, so they never need resetting
     int transport = EMESH_TRANSPORT_NCCL;
+    bool fp32 = false;               // ReduceMode::fp32 engine (raw fp32 payloads)
+    std::vector<float*> pay;         // fp32 payload arenas, per local worker (parity 0 under P2P)
+    float* pay_alt = nullptr;        // fp32 payload arena, parity 1 (P2P)
     uint32_t epoch = 0;
     uint8_t* codes_alt = nullptr;  // parity-1 codes arena (parity 0: arenas[0].codes)
     float* cbs_alt = nullptr;
@@ -763,6 +768,7 @@ struct emesh_engine {
     struct Peer {
         uint8_t* codes[2] = {nullptr, nullptr};
         float* cbs[2] = {nullptr, nullptr};
+        float* pay[2] = {nullptr, nullptr};
         uint32_t* rs_flag = nullptr;
         uint32_t* ag_flag = nullptr;
     };
@@ -789,7 +795,135 @@ int engine_alloc(emesh_engine* e) {
         CU(cudaMalloc(&a.stats, nslots * sizeof(SegStat)));
         CU(cudaMemset(a.stats, 0, nslots * sizeof(SegStat)));
     }
+    if (e->fp32) {
+        e->pay.assign(e->workers, nullptr);
+        for (auto& p : e->pay) CU(cudaMalloc(&p, n * sizeof(float) + 16));
+    }
     TRY(e->ws.reserve(e->plan.max_slots, e->plan.max_cta, e->plan.max_segs));
+    return EMESH_OK;
+}
+
+// ---- ReduceMode::fp32 launchers (allreduce.hpp:120-164)
+struct F32IO {
+    const float* a;
+    const float* b;       // PG: theta_l, else nullptr
+    const float* in;      // incoming partial sums or nullptr
+    bool div = false;     // owner mean
+    float k = 1.f;
+    uint32_t ndest = 0;
+    float* dst[kMaxDest] = {};
+    uint32_t nflags = 0;
+    uint32_t* flags[kMaxDest] = {};
+    const uint32_t* in_flag = nullptr;
+    uint32_t epoch = 0;
+};
+
+int launch_f32_hop(const Batch& bt, Workspace& ws, const F32IO& io, cudaStream_t st, Tracker* tr) {
+    if (bt.ncta == 0) return EMESH_OK;
+    F32HopArgs a{};
+    a.segs = bt.d_segs;
+    a.cta_seg = bt.d_cta_seg;
+    a.a = io.a;
+    a.b = io.b;
+    a.in = io.in;
+    a.divisor = io.k;
+    int ex = 0;
+    a.inv_divisor = std::frexp(io.k, &ex) == 0.5f ? std::ldexp(1.0f, 1 - ex) : 0.f;
+    a.ndest = io.ndest;
+    for (uint32_t d = 0; d < io.ndest; ++d) a.dst[d] = io.dst[d];
+    a.nflag = io.nflags;
+    for (uint32_t f = 0; f < io.nflags; ++f) a.sflag[f] = io.flags[f];
+    a.seg_done = ws.sync + kSyncReady;
+    a.in_flag = io.in_flag;
+    a.epoch = io.epoch;
+    a.nseg = bt.nseg;
+    if (io.nflags) CU(cudaMemsetAsync(ws.sync + kSyncReady, 0, (size_t)bt.nseg * sizeof(uint32_t), st));
+    const bool prof = tr && tr->prof;
+    cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
+    const dim3 g(bt.ncta * kApplySplit), blk(kThreads);
+    const bool pg = io.b != nullptr, hin = io.in != nullptr;
+    if (!hin) {
+        if (pg) k_f32_hop<true, false, false><<<g, blk, 0, st>>>(a);
+        else k_f32_hop<false, false, false><<<g, blk, 0, st>>>(a);
+    } else if (!io.div) {
+        if (pg) k_f32_hop<true, true, false><<<g, blk, 0, st>>>(a);
+        else k_f32_hop<false, true, false><<<g, blk, 0, st>>>(a);
+    } else {
+        if (pg) k_f32_hop<true, true, true><<<g, blk, 0, st>>>(a);
+        else k_f32_hop<false, true, true><<<g, blk, 0, st>>>(a);
+    }
+    if (tr) tr->launches += 1;
+    if (prof) {
+        const double elems = (double)(bt.el_hi - bt.el_lo);
+        const double by = elems * (4.0 * (1 + (pg ? 1 : 0) + (hin ? 1 : 0)) + 4.0 * io.ndest);
+        tr->recs.push_back({kProfF32Hop, e0, tr->ev(st), by});
+    }
+    CU(cudaGetLastError());
+    return EMESH_OK;
+}
+
+int launch_f32_apply(const Batch& bt, int mode, const float* pay, float* theta, float* buf, float* theta_local,
+                     float* out, float lr, float mom, cudaStream_t st, Tracker* tr, const uint32_t* in_flag = nullptr,
+                     uint32_t epoch = 0) {
+    if (bt.ncta == 0) return EMESH_OK;
+    ApplyArgs a{};
+    a.segs = bt.d_segs;
+    a.cta_seg = bt.d_cta_seg;
+    a.ncta = bt.ncta;
+    a.theta = theta;
+    a.buf = buf;
+    a.theta_local = theta_local;
+    a.out = out;
+    a.lr = lr;
+    a.mom = mom;
+    a.in_flag = in_flag;
+    a.epoch = epoch;
+    const dim3 g(bt.ncta * kApplySplit), blk(kThreads);
+    const bool prof = tr && tr->prof;
+    cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
+    if (mode == 0) k_f32_apply<0><<<g, blk, 0, st>>>(a, pay);
+    else k_f32_apply<1><<<g, blk, 0, st>>>(a, pay);
+    if (tr) tr->launches += 1;
+    if (prof) {
+        const double elems = (double)(bt.el_hi - bt.el_lo);
+        const double by = mode == 0 ? elems * 8.0 : elems * (theta_local ? 24.0 : 20.0);
+        tr->recs.push_back({kProfF32Apply, e0, tr->ev(st), by});
+    }
+    CU(cudaGetLastError());
+    return EMESH_OK;
+}
+
+// virtual ring, fp32 payloads (allreduce.hpp:411-464 with ReduceMode::fp32)
+int run_virtual_f32(emesh_engine* e, const float* const* A, const float* const* B, float* const* theta,
+                    float* const* buf, float* const* local_out, float* const* out, float lr, float mom) {
+    const uint32_t k = e->k;
+    cudaStream_t st = e->s_comp;
+    const bool pg = B != nullptr;
+    for (uint32_t w = 0; w < k; ++w)
+        for (const Batch& bt : e->plan.batches[w]) {
+            F32IO io{A[w], pg ? B[w] : nullptr, nullptr};
+            io.ndest = 1;
+            io.dst[0] = e->pay[w];
+            TRY(launch_f32_hop(bt, e->ws, io, st, &e->tr));
+        }
+    for (uint32_t s = 0; s + 1 < k; ++s)
+        for (uint32_t w = 0; w < k; ++w) {
+            const uint32_t pred = (w + k - 1) % k, recv_c = (w + k - s - 1) % k;
+            for (const Batch& bt : e->plan.batches[recv_c]) {
+                F32IO io{A[w], pg ? B[w] : nullptr, e->pay[pred], s + 2 == k, (float)k};
+                io.ndest = 1;
+                io.dst[0] = e->pay[w];
+                TRY(launch_f32_hop(bt, e->ws, io, st, &e->tr));
+            }
+        }
+    for (uint32_t w = 0; w < k; ++w)
+        for (uint32_t c = 0; c < k; ++c) {
+            const uint32_t owner = (c + k - 1) % k;
+            for (const Batch& bt : e->plan.batches[c])
+                TRY(launch_f32_apply(bt, out ? 0 : 1, e->pay[owner], out ? nullptr : theta[w], out ? nullptr : buf[w],
+                                     (!out && local_out) ? local_out[w] : nullptr, out ? out[w] : nullptr, lr, mom,
+                                     st, &e->tr));
+        }
     return EMESH_OK;
 }
 
@@ -804,6 +938,7 @@ int hop_src(bool from_theta, uint32_t s, uint32_t k) {
 // (worker w reads its predecessor's payload arena in place of a recv).
 int run_virtual(emesh_engine* e, const float* const* A, const float* const* B, float* const* theta, float* const* buf,
                 float* const* local_out, float* const* out, float lr, float mom) {
+    if (e->fp32) return run_virtual_f32(e, A, B, theta, buf, local_out, out, lr, mom);
     const uint32_t k = e->k;
     cudaStream_t st = e->s_comp;
     const bool pg = B != nullptr;
@@ -848,6 +983,15 @@ int xfer_window(emesh_engine* e, const Batch& snd, const Batch& rcv) {
     const uint32_t k = e->k, r = e->rank;
     const int succ = (int)((r + 1) % k), pred = (int)((r + k - 1) % k);
     auto& ar = e->arenas[0];
+    if (e->fp32) {  // raw fp32 partial sums / means (allreduce.hpp:120-151)
+        NC(ncclGroupStart());
+        if (snd.el_hi > snd.el_lo)
+            NC(ncclSend(e->pay[0] + snd.el_lo, snd.el_hi - snd.el_lo, ncclFloat32, succ, e->comm, e->s_comm));
+        if (rcv.el_hi > rcv.el_lo)
+            NC(ncclRecv(e->pay[0] + rcv.el_lo, rcv.el_hi - rcv.el_lo, ncclFloat32, pred, e->comm, e->s_comm));
+        NC(ncclGroupEnd());
+        return EMESH_OK;
+    }
     NC(ncclGroupStart());
     if (snd.el_hi > snd.el_lo)
         NC(ncclSend(ar.codes + snd.el_lo, snd.el_hi - snd.el_lo, ncclUint8, succ, e->comm, e->s_comm));
@@ -929,8 +1073,15 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
         }
         switch (o.kind) {
             case EMESH_OP_OWN: {
-                QuantIO io{pg ? kSrcAminusB : kSrcA, A, B, nullptr, nullptr, 1.f, ar.codes, ar.cbs, ar.stats};
-                TRY(launch_quant(P[o.recv_chunk][j], e->ws, io, sc, &e->tr, e->reserve_ctas));
+                if (e->fp32) {
+                    F32IO io{A, B, nullptr};
+                    io.ndest = 1;
+                    io.dst[0] = e->pay[0];
+                    TRY(launch_f32_hop(P[o.recv_chunk][j], e->ws, io, sc, &e->tr));
+                } else {
+                    QuantIO io{pg ? kSrcAminusB : kSrcA, A, B, nullptr, nullptr, 1.f, ar.codes, ar.cbs, ar.stats};
+                    TRY(launch_quant(P[o.recv_chunk][j], e->ws, io, sc, &e->tr, e->reserve_ctas));
+                }
                 CU(cudaEventRecord(e->ev_send[j], sc));
                 break;
             }
@@ -944,14 +1095,25 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
                 break;
             case EMESH_OP_QUANT: {
                 CU(cudaStreamWaitEvent(sc, e->ev_recv[j], 0));
-                QuantIO io{hop_src(pg, (uint32_t)o.hop, k), A, B, ar.codes, ar.cbs, (float)k, ar.codes, ar.cbs, ar.stats};
-                TRY(launch_quant(P[o.recv_chunk][j], e->ws, io, sc, &e->tr, e->reserve_ctas));
+                if (e->fp32) {
+                    F32IO io{A, B, e->pay[0], o.hop + 2 == (int32_t)k, (float)k};
+                    io.ndest = 1;
+                    io.dst[0] = e->pay[0];
+                    TRY(launch_f32_hop(P[o.recv_chunk][j], e->ws, io, sc, &e->tr));
+                } else {
+                    QuantIO io{hop_src(pg, (uint32_t)o.hop, k), A, B, ar.codes, ar.cbs, (float)k, ar.codes, ar.cbs,
+                               ar.stats};
+                    TRY(launch_quant(P[o.recv_chunk][j], e->ws, io, sc, &e->tr, e->reserve_ctas));
+                }
                 CU(cudaEventRecord(e->ev_send[j], sc));
                 break;
             }
             case EMESH_OP_APPLY:
                 if (o.hop >= 0) CU(cudaStreamWaitEvent(sc, e->ev_recv[j], 0));
-                if (out)
+                if (e->fp32)
+                    TRY(launch_f32_apply(P[o.recv_chunk][j], out ? 0 : 1, e->pay[0], theta, buf, local_out, out, lr, mom,
+                                         sc, &e->tr));
+                else if (out)
                     TRY(launch_apply(P[o.recv_chunk][j], 0, ar.codes, ar.cbs, nullptr, nullptr, nullptr, out, 0.f, 0.f,
                                      sc, &e->tr));
                 else
@@ -973,8 +1135,87 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
 // hop's quantizer waits segment by segment. The owner's final payload goes
 // to every rank at once, which replaces the all-gather's k-1 forwarding hops
 // (the bytes are identical: AG forwards them verbatim, allreduce.hpp:446-464).
+// Owner's final chunk -> every other rank by DMA (see run_p2p), in segment
+// groups, each followed by its arrival flags.
+int p2p_allgather(emesh_engine* e, int par, uint32_t ep) {
+    const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
+    cudaStream_t cm = e->s_comm;
+    CU(cudaEventRecord(e->ev_send[0], e->s_comp));
+    CU(cudaStreamWaitEvent(cm, e->ev_send[0], 0));
+    const Batch& fb = e->plan.batches[succ][0];
+    const uint32_t groups = std::min<uint32_t>(fb.nseg, 4);
+    for (uint32_t g = 0; g < groups; ++g) {
+        const uint32_t s0 = fb.slot0 + (uint32_t)((uint64_t)fb.nseg * g / groups);
+        const uint32_t s1 = fb.slot0 + (uint32_t)((uint64_t)fb.nseg * (g + 1) / groups);
+        if (s1 == s0) continue;
+        const uint64_t lo = e->plan.segs[s0].lo, hi = e->plan.segs[s1 - 1].lo + e->plan.segs[s1 - 1].len;
+        for (uint32_t d = 1; d < k; ++d) {
+            const uint32_t q = (r + d) % k;
+            if (e->fp32) {
+                if (hi > lo)
+                    CU(cudaMemcpyAsync(e->peers[q].pay[par] + lo, e->peers[r].pay[par] + lo, (hi - lo) * sizeof(float),
+                                       cudaMemcpyDeviceToDevice, cm));
+            } else {
+                if (hi > lo)
+                    CU(cudaMemcpyAsync(e->peers[q].codes[par] + lo, e->peers[r].codes[par] + lo, hi - lo,
+                                       cudaMemcpyDeviceToDevice, cm));
+                CU(cudaMemcpyAsync(e->peers[q].cbs[par] + (size_t)s0 * kBuckets,
+                                   e->peers[r].cbs[par] + (size_t)s0 * kBuckets,
+                                   (size_t)(s1 - s0) * kBuckets * sizeof(float), cudaMemcpyDeviceToDevice, cm));
+            }
+            k_set_flags<<<1, 128, 0, cm>>>(e->peers[q].ag_flag, s0, s1 - s0, ep);
+            CU(cudaGetLastError());
+        }
+    }
+    return EMESH_OK;
+}
+
+// ReduceMode::fp32 over the peer transport: the same ring with raw fp32
+// partial sums stored into the successor's payload arena.
+int run_p2p_f32(emesh_engine* e, const float* A, const float* B, float* theta, float* buf, float* local_out,
+                float* out, float lr, float mom) {
+    const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
+    const uint32_t ep = ++e->epoch;
+    const int par = (int)(ep & 1u);
+    cudaStream_t sc = e->s_comp;
+    const auto& P = e->plan.batches;
+    {
+        F32IO io{A, B, nullptr};
+        io.ndest = 1;
+        io.dst[0] = e->peers[succ].pay[par];
+        io.nflags = 1;
+        io.flags[0] = e->peers[succ].rs_flag;
+        io.epoch = ep;
+        TRY(launch_f32_hop(P[r][0], e->ws, io, sc, &e->tr));
+    }
+    for (uint32_t s = 0; s + 1 < k; ++s) {
+        const uint32_t rc = (r + k - s - 1) % k;
+        const bool fin = s + 2 == k;
+        F32IO io{A, B, e->peers[r].pay[par], fin, (float)k};
+        io.in_flag = e->rs_flag;
+        io.epoch = ep;
+        io.ndest = 1;
+        if (fin) {
+            io.dst[0] = e->peers[r].pay[par];
+        } else {
+            io.dst[0] = e->peers[succ].pay[par];
+            io.nflags = 1;
+            io.flags[0] = e->peers[succ].rs_flag;
+        }
+        TRY(launch_f32_hop(P[rc][0], e->ws, io, sc, &e->tr));
+    }
+    TRY(p2p_allgather(e, par, ep));
+    for (uint32_t d = 0; d < k; ++d) {
+        const uint32_t c = (succ + k - d) % k;
+        TRY(launch_f32_apply(P[c][0], out ? 0 : 1, e->peers[r].pay[par], theta, buf, local_out, out, lr, mom, sc,
+                             &e->tr, d == 0 ? nullptr : e->ag_flag, ep));
+    }
+    return EMESH_OK;
+}
+
 int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float* buf, float* local_out, float* out,
             float lr, float mom) {
+    if (e->fp32) return run_p2p_f32(e, A, B, theta, buf, local_out, out, lr, mom);
     const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
     const bool pg = B != nullptr;
     const uint32_t ep = ++e->epoch;
@@ -1020,33 +1261,12 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
         TRY(launch_quant(P[rc][0], e->ws, io, sc, &e->tr));
         mark(EMESH_OP_QUANT, (int)s, false);
     }
-    {   // all-gather: the owner's final bytes to every rank by DMA over NVLink
-        // (allreduce.hpp:446-464 forwards the same bytes hop by hop), in
-        // segment groups so receivers start decoding while the rest streams;
-        // a group's arrival flags are raised after its bytes (stream order).
-        // Runs on the comm stream, overlapping this rank's own decode.
-        cudaStream_t cm = e->s_comm;
-        CU(cudaEventRecord(e->ev_send[0], sc));
-        CU(cudaStreamWaitEvent(cm, e->ev_send[0], 0));
-        const Batch& fb = P[succ][0];
-        const uint32_t groups = std::min<uint32_t>(fb.nseg, 4);
-        for (uint32_t g = 0; g < groups; ++g) {
-            const uint32_t s0 = fb.slot0 + (uint32_t)((uint64_t)fb.nseg * g / groups);
-            const uint32_t s1 = fb.slot0 + (uint32_t)((uint64_t)fb.nseg * (g + 1) / groups);
-            const uint64_t lo = e->plan.segs[s0].lo, hi = e->plan.segs[s1 - 1].lo + e->plan.segs[s1 - 1].len;
-            for (uint32_t d = 1; d < k; ++d) {
-                const uint32_t q = (r + d) % k;
-                if (hi > lo)
-                    CU(cudaMemcpyAsync(e->peers[q].codes[par] + lo, e->peers[r].codes[par] + lo, hi - lo,
-                                       cudaMemcpyDeviceToDevice, cm));
-                CU(cudaMemcpyAsync(e->peers[q].cbs[par] + (size_t)s0 * kBuckets,
-                                   e->peers[r].cbs[par] + (size_t)s0 * kBuckets,
-                                   (size_t)(s1 - s0) * kBuckets * sizeof(float), cudaMemcpyDeviceToDevice, cm));
-                k_set_flags<<<1, 128, 0, cm>>>(e->peers[q].ag_flag, s0, s1 - s0, ep);
-                CU(cudaGetLastError());
-            }
-        }
-    }
+    // all-gather: the owner's final bytes to every rank by DMA over NVLink
+    // (allreduce.hpp:446-464 forwards the same bytes hop by hop), in segment
+    // groups so receivers start decoding while the rest streams; a group's
+    // arrival flags are raised after its bytes (stream order). Runs on the
+    // comm stream, overlapping this rank's own decode.
+    TRY(p2p_allgather(e, par, ep));
     // decode every chunk: own final first, then the others as their owners'
     // copies land (per-segment ag_flag waits inside k_apply)
     for (uint32_t d = 0; d < k; ++d) {
@@ -1072,17 +1292,20 @@ bool setup_p2p(emesh_engine* e) {
     if (k > (uint32_t)kMaxDest) return false;
     const uint64_t n = e->plan.n;
     const size_t nslots = e->plan.segs.size();
-    bool ok = cudaMalloc(&e->codes_alt, ((n + 15) & ~uint64_t(15)) + 16) == cudaSuccess &&
+    bool ok = (!e->fp32 || cudaMalloc(&e->pay_alt, n * sizeof(float) + 16) == cudaSuccess) &&
+              cudaMalloc(&e->codes_alt, ((n + 15) & ~uint64_t(15)) + 16) == cudaSuccess &&
               cudaMalloc(&e->cbs_alt, nslots * kBuckets * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&e->rs_flag, nslots * sizeof(uint32_t)) == cudaSuccess &&
               cudaMalloc(&e->ag_flag, nslots * sizeof(uint32_t)) == cudaSuccess &&
               cudaMemset(e->rs_flag, 0, nslots * sizeof(uint32_t)) == cudaSuccess &&
               cudaMemset(e->ag_flag, 0, nslots * sizeof(uint32_t)) == cudaSuccess;
-    constexpr int kH = 6;
+    constexpr int kH = 8;
     constexpr size_t kRec = kH * sizeof(cudaIpcMemHandle_t);
     std::vector<uint8_t> mine(kRec, 0), all(kRec * k, 0);
-    void* bufs[kH] = {e->arenas[0].codes, e->codes_alt, e->arenas[0].cbs, e->cbs_alt, e->rs_flag, e->ag_flag};
-    for (int h = 0; ok && h < kH; ++h)
+    void* bufs[kH] = {e->arenas[0].codes, e->codes_alt, e->arenas[0].cbs, e->cbs_alt, e->rs_flag, e->ag_flag,
+                      e->fp32 ? e->pay[0] : nullptr, e->pay_alt};
+    const int nh = e->fp32 ? 8 : 6;  // every rank runs the same mode
+    for (int h = 0; ok && h < nh; ++h)
         ok = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data()) + h, bufs[h]) == cudaSuccess;
     // all-gather the handle records (and everyone's ok) over NCCL
     uint8_t* d = nullptr;
@@ -1096,11 +1319,11 @@ bool setup_p2p(emesh_engine* e) {
     }
     e->peers.assign(k, emesh_engine::Peer{});
     e->peers[r] = emesh_engine::Peer{{e->arenas[0].codes, e->codes_alt}, {e->arenas[0].cbs, e->cbs_alt},
-                                     e->rs_flag, e->ag_flag};
+                                     {e->fp32 ? e->pay[0] : nullptr, e->pay_alt}, e->rs_flag, e->ag_flag};
     for (uint32_t q = 0; ok && comm_ok && q < k; ++q) {
         if (q == r) continue;
         void* ptr[kH] = {};
-        for (int h = 0; h < kH && ok; ++h) {
+        for (int h = 0; h < nh && ok; ++h) {
             cudaIpcMemHandle_t hd;
             std::memcpy(&hd, all.data() + q * kRec + h * sizeof(cudaIpcMemHandle_t), sizeof hd);
             ok = cudaIpcOpenMemHandle(&ptr[h], hd, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
@@ -1109,6 +1332,7 @@ bool setup_p2p(emesh_engine* e) {
         pq.codes[0] = (uint8_t*)ptr[0]; pq.codes[1] = (uint8_t*)ptr[1];
         pq.cbs[0] = (float*)ptr[2]; pq.cbs[1] = (float*)ptr[3];
         pq.rs_flag = (uint32_t*)ptr[4]; pq.ag_flag = (uint32_t*)ptr[5];
+        pq.pay[0] = (float*)ptr[6]; pq.pay[1] = (float*)ptr[7];
     }
     cudaGetLastError();  // clear a failed open, if any
     // agree: every rank must have mapped every peer
@@ -1129,13 +1353,15 @@ void teardown_p2p(emesh_engine* e) {
     for (uint32_t q = 0; q < e->peers.size(); ++q) {
         if (q == e->rank) continue;
         auto& pq = e->peers[q];
-        void* ptrs[] = {pq.codes[0], pq.codes[1], pq.cbs[0], pq.cbs[1], pq.rs_flag, pq.ag_flag};
+        void* ptrs[] = {pq.codes[0], pq.codes[1], pq.cbs[0], pq.cbs[1], pq.rs_flag, pq.ag_flag, pq.pay[0], pq.pay[1]};
         for (void* p : ptrs)
             if (p) cudaIpcCloseMemHandle(p);
     }
     e->peers.clear();
     cudaFree(e->codes_alt);
     cudaFree(e->cbs_alt);
+    cudaFree(e->pay_alt);
+    e->pay_alt = nullptr;
     cudaFree(e->rs_flag);
     cudaFree(e->ag_flag);
     e->codes_alt = nullptr;
@@ -1243,6 +1469,8 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
     // segments of a batch); a quarter chunk (>= 16M) under NCCL so transfers
     // of window j+1 overlap the kernels of window j
     if (cfg->transport > EMESH_TRANSPORT_P2P) return bail(fail(EMESH_ECONFIG, "unknown transport %u", cfg->transport));
+    if (cfg->reduce_fp32 > 1) return bail(fail(EMESH_ECONFIG, "reduce_fp32 must be 0 or 1"));
+    e->fp32 = cfg->reduce_fp32 == 1;
     const uint64_t chunk = (cfg->n + cfg->k - 1) / cfg->k;
     // the peer transport synchronizes per segment: one batch per chunk
     const bool try_p2p = !virt && cfg->k > 1 && cfg->transport != EMESH_TRANSPORT_NCCL;
@@ -1309,6 +1537,7 @@ int emesh_engine_destroy(emesh_engine* e) {
     teardown_p2p(e);
     if (e->comm) ncclCommDestroy(e->comm);
     for (auto& a : e->arenas) { cudaFree(a.codes); cudaFree(a.cbs); cudaFree(a.stats); }
+    for (auto* p : e->pay) cudaFree(p);
     for (auto* p : e->h_theta) cudaFree(p);
     for (auto* p : e->h_local) cudaFree(p);
     for (auto* p : e->h_buf) cudaFree(p);

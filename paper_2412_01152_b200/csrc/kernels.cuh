@@ -1065,6 +1065,147 @@ __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// ReduceMode::fp32 ring (allreduce.hpp:120-164: raw fp32 payloads). One CTA
+// per half quantizer tile (like k_apply); segments are still the framing
+// unit (allreduce.hpp:326-336), and with the peer transport the last CTA of
+// a segment raises its arrival flags.
+
+struct F32HopArgs {
+    const SegInfo* segs;
+    const uint32_t* cta_seg;
+    const float* a;            // theta_g (PG) or the ring input
+    const float* b;            // theta_l (PG) or nullptr
+    const float* in;           // incoming partial sums (arena-indexed) or nullptr (hop 0)
+    float divisor, inv_divisor;  // owner mean: x / k (allreduce.hpp:435-440)
+    float* dst[kMaxDest];      // payload destinations (arena-indexed)
+    uint32_t ndest;
+    uint32_t* sflag[kMaxDest];  // peer arrival flags raised per finished segment
+    uint32_t nflag;
+    uint32_t* seg_done;        // [batch segment] CTA arrival counters (zeroed per launch)
+    const uint32_t* in_flag;   // peer transport: wait in_flag[slot] >= epoch before reading `in`
+    uint32_t epoch;
+    uint32_t nseg;
+};
+
+// x = (a - b | a) (+ in) (/ k), the reduce-scatter accumulate
+// accum[lo + i] += vals[i] (allreduce.hpp:422) and the owner mean (:435-440).
+template <bool PG, bool HAS_IN, bool DIV>
+__global__ void __launch_bounds__(kThreads) k_f32_hop(F32HopArgs a) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tile = blockIdx.x / kApplySplit, part = blockIdx.x % kApplySplit;
+    const uint32_t s = a.cta_seg[tile];
+    const SegInfo si = a.segs[s];
+    if (HAS_IN && a.in_flag) {
+        if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.in_slot, a.epoch);
+        __syncthreads();
+    }
+    const uint64_t hiel = si.lo + si.len;
+    for (int ui = 0; ui < 2; ++ui) {
+        const uint32_t u = (tile - si.cta0) * kTileUnits + (part * 2 + ui) * kWarps + warp;
+        if (u >= si.nunits) break;
+        const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
+#pragma unroll 4
+        for (int j = 0; j < kSlotsPerLane; ++j) {
+            const uint64_t q = qbase + (uint64_t)j * 32 + lane;
+            const uint64_t e0 = q * 4;
+            if (e0 >= hiel) continue;
+            const bool full = e0 >= si.lo && e0 + 4 <= hiel;
+            float4 v = __ldcs(reinterpret_cast<const float4*>(a.a) + q);
+            float x[4] = {v.x, v.y, v.z, v.w};
+            if (PG) {
+                const float4 l = __ldcs(reinterpret_cast<const float4*>(a.b) + q);
+                x[0] = __fsub_rn(x[0], l.x); x[1] = __fsub_rn(x[1], l.y);
+                x[2] = __fsub_rn(x[2], l.z); x[3] = __fsub_rn(x[3], l.w);
+            }
+            if (HAS_IN) {
+                const float4 w = __ldcs(reinterpret_cast<const float4*>(a.in) + q);
+                x[0] = __fadd_rn(x[0], w.x); x[1] = __fadd_rn(x[1], w.y);
+                x[2] = __fadd_rn(x[2], w.z); x[3] = __fadd_rn(x[3], w.w);
+            }
+            if (DIV) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    x[e] = a.inv_divisor != 0.f ? __fmul_rn(x[e], a.inv_divisor) : __fdiv_rn(x[e], a.divisor);
+            }
+            for (uint32_t d = 0; d < a.ndest; ++d) {
+                if (full) {
+                    __stcs(reinterpret_cast<float4*>(a.dst[d]) + q, make_float4(x[0], x[1], x[2], x[3]));
+                } else {
+                    for (int e = 0; e < 4; ++e)
+                        if (e0 + e >= si.lo && e0 + e < hiel) a.dst[d][e0 + e] = x[e];
+                }
+            }
+        }
+    }
+    if (a.nflag) {  // last CTA of the segment flags it (see finalize_codebook for the ordering argument)
+        __shared__ uint32_t last;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            last = atom_add_acq_rel(a.seg_done + s, 1u) == si.ncta * kApplySplit - 1 ? 1u : 0u;
+        __syncthreads();
+        if (last && threadIdx.x == 0) {
+            __threadfence_system();
+            for (uint32_t f = 0; f < a.nflag; ++f) st_release_sys(a.sflag[f] + si.slot, a.epoch);
+        }
+    }
+}
+
+// Decode of an fp32 final payload: MODE 0 copy into `out`, MODE 1 Nesterov
+// (optim.hpp:116-132) with avg = payload (+ optional theta_l write).
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_f32_apply(ApplyArgs a, const float* pay) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tile = blockIdx.x / kApplySplit, part = blockIdx.x % kApplySplit;
+    const SegInfo si = a.segs[a.cta_seg[tile]];
+    if (a.in_flag) {
+        if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.slot, a.epoch);
+        __syncthreads();
+    }
+    const uint64_t hiel = si.lo + si.len;
+    for (int ui = 0; ui < 2; ++ui) {
+        const uint32_t u = (tile - si.cta0) * kTileUnits + (part * 2 + ui) * kWarps + warp;
+        if (u >= si.nunits) return;
+        const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
+#pragma unroll 4
+        for (int j = 0; j < kSlotsPerLane; ++j) {
+            const uint64_t q = qbase + (uint64_t)j * 32 + lane;
+            const uint64_t e0 = q * 4;
+            if (e0 >= hiel) continue;
+            const bool full = e0 >= si.lo && e0 + 4 <= hiel;
+            const float4 dv = __ldcs(reinterpret_cast<const float4*>(pay) + q);
+            const float d[4] = {dv.x, dv.y, dv.z, dv.w};
+            if (MODE == 0) {
+                if (full) {
+                    reinterpret_cast<float4*>(a.out)[q] = dv;
+                } else {
+                    for (int e = 0; e < 4; ++e)
+                        if (e0 + e >= si.lo && e0 + e < hiel) a.out[e0 + e] = d[e];
+                }
+            } else {
+                float4 th = __ldcs(reinterpret_cast<const float4*>(a.theta) + q);
+                float4 bb = __ldcs(reinterpret_cast<const float4*>(a.buf) + q);
+                float t4[4] = {th.x, th.y, th.z, th.w}, b4[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) nesterov1(t4[e], b4[e], d[e], a.lr, a.mom);
+                if (full) {
+                    const float4 to = make_float4(t4[0], t4[1], t4[2], t4[3]);
+                    __stcs(reinterpret_cast<float4*>(a.theta) + q, to);
+                    __stcs(reinterpret_cast<float4*>(a.buf) + q, make_float4(b4[0], b4[1], b4[2], b4[3]));
+                    if (a.theta_local) __stcs(reinterpret_cast<float4*>(a.theta_local) + q, to);
+                } else {
+                    for (int e = 0; e < 4; ++e)
+                        if (e0 + e >= si.lo && e0 + e < hiel) {
+                            a.theta[e0 + e] = t4[e];
+                            a.buf[e0 + e] = b4[e];
+                            if (a.theta_local) a.theta_local[e0 + e] = t4[e];
+                        }
+                }
+            }
+        }
+    }
+}
+
 // Peer transport: raise the arrival flags of slots [slot0, slot0 + n) on a
 // peer after the copy engine delivered their bytes (stream-ordered before).
 __global__ void k_set_flags(uint32_t* flags, uint32_t slot0, uint32_t n, uint32_t epoch) {

@@ -404,7 +404,7 @@ class RingEngine:
 
     def __init__(self, n: int, k: int, rank: int = 0, opts: Optional[ReduceOptions] = None, virtual: bool = False,
                  nccl_id: Optional[bytes] = None, window_elems: int = 0, device: Optional[int] = None,
-                 transport: str = "auto"):
+                 transport: str = "auto", mode: "ReduceMode" = None):
         opts = opts or ReduceOptions()
         if opts.pipeline_subchunks < 1:
             raise ConfigError("pipeline_subchunks must be >= 1")
@@ -422,6 +422,8 @@ class RingEngine:
         if transport not in tmap:
             raise ConfigError(f"transport must be one of {sorted(tmap)}")
         cfg.transport = tmap[transport]
+        self.mode = ReduceMode.int8 if mode is None else ReduceMode(mode)
+        cfg.reduce_fp32 = 1 if self.mode == ReduceMode.fp32 else 0
         if nccl_id is not None:
             self._idbuf = C.create_string_buffer(bytes(nccl_id), 128)
             cfg.nccl_id = C.cast(self._idbuf, C.c_void_p)
@@ -496,14 +498,14 @@ class RingEngine:
         return _capi.ptr_array([t.data_ptr() for t in ts])
 
     def ring_allreduce(self, inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor], stream=None) -> None:
-        """allreduce.hpp:314 (ReduceMode::int8), stream-ordered."""
+        """allreduce.hpp:314 in this engine's ReduceMode, stream-ordered."""
         _check(_capi.lib().emesh_engine_ring_allreduce(self._h, self._ptrs(inputs, "input"),
                                                        self._ptrs(outputs, "output"), _stream(stream)))
 
     def outer_sync(self, theta_g: Sequence[torch.Tensor], theta_l: Sequence[torch.Tensor],
                    momentum: Sequence[torch.Tensor], hp: Optional[HyperParams] = None, write_local: bool = True,
                    stream=None) -> None:
-        """trainer.hpp:355-382: PG -> int8 ring all-reduce -> Nesterov, in place."""
+        """trainer.hpp:355-382: PG -> ring all-reduce (this engine's ReduceMode) -> Nesterov, in place."""
         hp = hp or HyperParams()
         _check(_capi.lib().emesh_engine_outer_sync(self._h, self._ptrs(theta_g, "theta_g"),
                                                    self._ptrs(theta_l, "theta_l"), self._ptrs(momentum, "momentum"),
@@ -546,8 +548,8 @@ def ring_allreduce(engine: RingEngine, job: ReduceJob, opts: Optional[ReduceOpti
                    stream=None) -> torch.Tensor:
     """allreduce.hpp:314 ``ring_allreduce`` for this process's ring position:
     returns the mean every rank decodes; ``job.input`` is untouched."""
-    if job.mode != ReduceMode.int8:
-        raise ConfigError("this engine implements ReduceMode::int8 (fp32 mode is the next row, SURVEY §8(f))")
+    if ReduceMode(job.mode) != engine.mode:
+        raise ConfigError(f"job mode {ReduceMode(job.mode).name} != engine mode {engine.mode.name} (one engine per mode)")
     out = _aligned_empty(engine.n, torch.float32, job.input.device)
     engine.ring_allreduce([job.input], [out], stream)
     return out

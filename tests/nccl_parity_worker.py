@@ -26,22 +26,23 @@ def main():
     O = Oracle()
     ok = True
     cases = [(100_003, 4, 0), (4099, 3, 1), (5, 4, 0), (2_000_000, 8, 300_000)]
-    for (n, S, window), transport in [(c, t) for t in ("nccl", "p2p") for c in cases]:
+    runs = [(c, t, m) for m in ("int8", "fp32") for t in ("nccl", "p2p") for c in cases]
+    for (n, S, window), transport, mode in runs:
         obj = [E.RingEngine.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         eng = E.RingEngine(n, world, rank=rank, opts=E.ReduceOptions(pipeline_subchunks=S), nccl_id=obj[0],
-                           window_elems=window, transport=transport)
+                           window_elems=window, transport=transport, mode=E.ReduceMode[mode])
         if eng.transport != transport:
             print(f"rank {rank}: asked for {transport}, engine runs {eng.transport}", flush=True)
             ok = False
         ins = [O.uniform(n, 7 + n, w, 0, 0, 2.0 ** -6) for w in range(world)]
-        want = O.ring_allreduce(ins, S, "int8")
+        want = O.ring_allreduce(ins, S, mode)
         out = torch.empty(n + 4, dtype=torch.float32, device=dev)[:n]
         eng.ring_allreduce([torch.from_numpy(ins[rank]).to(dev)], [out])
         eng.check()
         got = out.cpu().numpy()
         if not np.array_equal(bits(got), bits(want)):
-            print(f"rank {rank}: [{transport}] ring n={n} S={S} MISMATCH ({int((bits(got) != bits(want)).sum())} elems)", flush=True)
+            print(f"rank {rank}: [{transport} {mode}] ring n={n} S={S} MISMATCH ({int((bits(got) != bits(want)).sum())} elems)", flush=True)
             ok = False
         # two outer-sync rounds (trainer.hpp:355-382)
         g = O.uniform(n, 3, 0)
@@ -53,9 +54,9 @@ def main():
             ls = [(eg - O.uniform(n, 30 + rnd, 1 + w, 0, 0, 2.0 ** -10)).astype(np.float32) for w in range(world)]
             eng.outer_sync([tg], [torch.from_numpy(ls[rank]).to(dev)], [tb], E.HyperParams(), write_local=False)
             eng.check()
-            eg, eb = O.outer_sync(eg, ls, eb, S, "int8", 0.7, 0.9)
+            eg, eb = O.outer_sync(eg, ls, eb, S, mode, 0.7, 0.9)
             if not (np.array_equal(bits(tg.cpu().numpy()), bits(eg)) and np.array_equal(bits(tb.cpu().numpy()), bits(eb))):
-                print(f"rank {rank}: [{transport}] outer sync n={n} round {rnd} MISMATCH", flush=True)
+                print(f"rank {rank}: [{transport} {mode}] outer sync n={n} round {rnd} MISMATCH", flush=True)
                 ok = False
         eng.close()
     flag = torch.tensor([0 if ok else 1], device=dev)

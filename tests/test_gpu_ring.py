@@ -170,3 +170,82 @@ def test_full_size_properties_config1(E, oracle):
     _, res = run_virtual_allreduce(E, ins, S)
     for r in res:
         assert np.array_equal(bits(r), bits(want))
+
+
+# ---------------------------------------------------------------- ReduceMode::fp32
+
+
+def run_virtual_allreduce_f32(E, ins, S, window=0):
+    k, n = len(ins), len(ins[0])
+    eng = E.RingEngine(n, k, opts=E.ReduceOptions(pipeline_subchunks=S), virtual=True, window_elems=window,
+                       mode=E.ReduceMode.fp32)
+    tin = [T(a) for a in ins]
+    outs = [torch.empty(n + 4, dtype=torch.float32, device="cuda:0")[:n] for _ in range(k)]
+    eng.ring_allreduce(tin, outs)
+    eng.check()
+    res = [o.cpu().numpy() for o in outs]
+    for a, t in zip(ins, tin):
+        assert np.array_equal(bits(t.cpu().numpy()), bits(a))
+    return eng, res
+
+
+def test_ring_fp32_golden_reference_outputs(E, golden):
+    """The reference's own SimWorld ring in ReduceMode::fp32 (test_allreduce.cpp:195-216 style)."""
+    g = golden["ring_cases"]
+    keys = sorted({k.rsplit("/", 1)[0] for k in g.files if k.endswith("_fp32/out")})
+    assert keys
+    for key in keys:
+        ins = list(g[f"{key}/inputs"])
+        S = int(key.split("_S")[1].split("_")[0])
+        eng, res = run_virtual_allreduce_f32(E, ins, S)
+        for r in res:
+            assert np.array_equal(bits(r), bits(g[f"{key}/out"])), key
+        eng.close()
+
+
+def test_ring_fp32_known_answer(E):
+    """test_allreduce.cpp:195-200: {1,2},{3,4} -> {2,3} on both ranks."""
+    eng, res = run_virtual_allreduce_f32(E, [np.array([1, 2], np.float32), np.array([3, 4], np.float32)], 4)
+    for r in res:
+        assert r.tolist() == [2.0, 3.0]
+    eng.close()
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 8])
+@pytest.mark.parametrize("n", [1, 17, 4096, 100_003])
+def test_ring_fp32_vs_oracle(E, oracle, k, n):
+    ins = [oracle.uniform(n, 100 + n, i) for i in range(k)]
+    want = oracle.ring_allreduce(ins, 4, "fp32")
+    eng, res = run_virtual_allreduce_f32(E, ins, 4)
+    for r in res:
+        assert np.array_equal(bits(r), bits(want))
+    eng.close()
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_outer_sync_fp32_vs_oracle_two_rounds(E, oracle, k):
+    n, S = 200_003, 4
+    g0 = oracle.uniform(n, 3, 0)
+    b0 = np.zeros(n, np.float32)
+    eng = E.RingEngine(n, k, opts=E.ReduceOptions(pipeline_subchunks=S), virtual=True, mode=E.ReduceMode.fp32)
+    tg = [T(g0) for _ in range(k)]
+    tb = [T(b0) for _ in range(k)]
+    eg, eb = g0, b0
+    for rnd in range(2):
+        ls = [(eg - oracle.uniform(n, 3 + rnd, 1 + w, 0, 0, 2.0 ** -10)).astype(np.float32) for w in range(k)]
+        tl = [T(a) for a in ls]
+        eng.outer_sync(tg, tl, tb, E.HyperParams(), write_local=True)
+        eng.check()
+        eg, eb = oracle.outer_sync(eg, ls, eb, S, "fp32", 0.7, 0.9)
+        for w in range(k):
+            assert np.array_equal(bits(tg[w].cpu().numpy()), bits(eg)), (rnd, w)
+            assert np.array_equal(bits(tb[w].cpu().numpy()), bits(eb)), (rnd, w)
+            assert np.array_equal(bits(tl[w].cpu().numpy()), bits(eg)), (rnd, w)
+    eng.close()
+
+
+def test_ring_allreduce_job_mode_checked(E):
+    eng = E.RingEngine(8, 2, virtual=True)
+    with pytest.raises(E.ConfigError):
+        E.ring_allreduce(eng, E.ReduceJob(1, torch.zeros(8, device="cuda:0"), E.ReduceMode.fp32))
+    eng.close()
