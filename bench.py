@@ -158,7 +158,7 @@ def run_reference(args, rank, world):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-        "config": config_block(args, k, int(args.n)),
+        "config": config_block(args, k, int(args.n), "reference"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": f"{k} workers x {n} params/worker per round (bounded slice of the "
                                    f"{int(args.n)}-param workload), S={args.S}, TCP loopback ring, one node thread "
@@ -175,7 +175,8 @@ def config_block(args, k, n, transport=None):
     return {"workload": f"config 2: DiLoCo outer sync of a {n / 1e9:.3g}B-param synthetic model, {k} workers, "
                         "int8 ring all-reduce + Nesterov (lr=0.7, mu=0.9)",
             "params_per_worker": n, "workers": k, "pipeline_subchunks": args.S,
-            "ring": ("virtual (all workers on 1 GPU, zero-copy hand-off)" if args.gpus == 1 and k > 1
+            "ring": ("reference CPU ring_allreduce over TcpEnv loopback (k node threads)" if transport == "reference"
+                     else "virtual (all workers on 1 GPU, zero-copy hand-off)" if args.gpus == 1 and k > 1
                      else "peer memory over NVLink (quantizer stores into the successor's arena, per-segment flags), "
                           "one worker per GPU" if transport == "p2p"
                      else "NCCL send/recv over NVLink, one worker per GPU"),

@@ -106,6 +106,11 @@ typedef struct {
     uint32_t reduce_fp32;       /* ReduceJob.mode (allreduce.hpp:49-53, :120-164): 0 = ReduceMode::int8
                                    (uint8 codes + codebooks), 1 = ReduceMode::fp32 (raw fp32 partial sums).
                                    One engine serves one mode; make one per mode in use. */
+    const uint64_t* tensor_numel; /* optional (ntensors > 0): the flat arena is this list of tensors
+                                   (canonical order, sum = n) and each tensor is its own ReduceJob:
+                                   k chunks x min(S, len) segments per tensor, all tensors' chunk c
+                                   reduced together ("bucketing") */
+    uint32_t ntensors;
 } emesh_engine_config;
 
 /* Transports of the one-process-per-GPU ring (k > 1, not virtual):
@@ -126,6 +131,9 @@ int emesh_engine_transport(const emesh_engine* e);
 /* Host-only plan queries (no GPU needed). Segment table of an (n, k, S)
  * ring, chunk-major (allreduce.hpp:107-118, :326-336); returns the count. */
 uint64_t emesh_plan_segments(uint64_t n, uint32_t k, uint32_t S, uint64_t* seg_lo, uint64_t* seg_len);
+/* Same for a multi-tensor engine (emesh_engine_config.tensor_numel): chunk-major, tensors in order. */
+uint64_t emesh_plan_tensor_segments(const uint64_t* tensor_numel, uint32_t ntensors, uint32_t k, uint32_t S,
+                                    uint64_t* seg_lo, uint64_t* seg_len);
 
 /* The NCCL ring engine's program for one ring position, in issue order.
  * kinds: OWN = quantize own chunk's hop-0 payload window; XFER = send

@@ -71,8 +71,9 @@ bool bin_reverse();
 struct Batch {
     uint32_t chunk = 0, window = 0;
     uint32_t slot0 = 0, nseg = 0;
-    uint64_t el_lo = 0, el_hi = 0;  // element range [el_lo, el_hi)
-    uint64_t q_lo = 0, q_hi = 0;    // float4 slot range [q_lo, q_hi)
+    uint64_t el_lo = 0, el_hi = 0;  // element span [el_lo, el_hi) (contiguous for a flat arena)
+    uint64_t elems = 0;             // elements in the batch
+    std::vector<std::pair<uint64_t, uint64_t>> eruns;  // contiguous element runs {lo, len} (transfers)
     uint32_t ncta = 0, nruns = 0, ntasks = 0;
     size_t off_segs = 0, off_cta = 0, off_runs = 0;  // byte offsets into the table arena
     const SegInfo* d_segs = nullptr;
@@ -105,12 +106,14 @@ struct Plan {
         std::vector<SegInfo> infos;
         std::vector<uint32_t> cseg;
         bool first = true;
+        uint64_t sq = 0;  // scratch float4 slots so far
         for (uint32_t s = s0; s < s1; ++s) {
             const Seg& g = segs[s];
             SegInfo si{};
             si.lo = g.lo;
             si.len = g.len;
             si.q0 = g.lo >> 2;
+            si.sq0 = sq;
             si.cta0 = (uint32_t)cseg.size();
             si.slot = s;
             si.in_slot = s;
@@ -119,9 +122,15 @@ struct Plan {
                 const uint64_t nq = q_last - si.q0 + 1;
                 si.nunits = (uint32_t)((nq + kUnitSlots - 1) / kUnitSlots);
                 si.ncta = (si.nunits + kTileUnits - 1) / kTileUnits;
-                if (first) { b.el_lo = g.lo; b.q_lo = si.q0; first = false; }
-                b.el_hi = g.lo + g.len;
-                b.q_hi = q_last + 1;
+                sq += nq;
+                if (first) { b.el_lo = g.lo; first = false; }
+                b.el_lo = std::min(b.el_lo, g.lo);
+                b.el_hi = std::max(b.el_hi, g.lo + g.len);
+                b.elems += g.len;
+                if (!b.eruns.empty() && b.eruns.back().first + b.eruns.back().second == g.lo)
+                    b.eruns.back().second += g.len;
+                else
+                    b.eruns.push_back({g.lo, g.len});
             }
             for (uint32_t t = 0; t < si.ncta; ++t) cseg.push_back((uint32_t)infos.size());
             infos.push_back(si);
@@ -172,7 +181,7 @@ struct Plan {
 
         max_cta = std::max<size_t>(max_cta, b.ncta);
         max_segs = std::max<size_t>(max_segs, b.nseg);
-        max_slots = std::max<size_t>(max_slots, b.q_hi > b.q_lo ? b.q_hi - b.q_lo : 0);
+        max_slots = std::max<size_t>(max_slots, sq);
         batches[chunk].push_back(b);
     }
 
@@ -243,6 +252,56 @@ Plan make_ring_plan(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems) {
         uint32_t w = 0;
         for (uint64_t s = first[c]; s < first[c + 1]; s += G, ++w)
             p.add_batch(c, w, (uint32_t)s, (uint32_t)std::min<uint64_t>(first[c + 1], s + G));
+    }
+    return p;
+}
+
+// Multi-tensor ring: one ReduceJob per tensor, i.e.
+// every tensor is split into k chunks x min(S, len) segments on its own
+// (allreduce.hpp:107-118, :326-336); ring chunk c is the union of the
+// tensors' chunk c ("bucketing": one launch / one transfer group per hop).
+// Slots are chunk-major, tensors in order within a chunk. Windows: `nwin`
+// per chunk by cumulative elements (equal counts on every chunk, as the
+// NCCL schedule pairs windows); nwin = 0 sizes them from window_elems.
+Plan make_tensor_ring_plan(const uint64_t* sizes, uint32_t nt, uint32_t k, uint32_t S, uint64_t window_elems) {
+    Plan p;
+    p.k = k;
+    p.S = S;
+    p.batches.resize(k);
+    std::vector<uint64_t> off(nt + 1, 0);
+    for (uint32_t t = 0; t < nt; ++t) off[t + 1] = off[t] + sizes[t];
+    p.n = off[nt];
+    std::vector<uint32_t> first(k + 1);
+    uint64_t max_chunk = 1;
+    for (uint32_t c = 0; c < k; ++c) {
+        first[c] = (uint32_t)p.segs.size();
+        uint64_t tot = 0;
+        for (uint32_t t = 0; t < nt; ++t) {
+            uint64_t clo, clen;
+            split_piece(sizes[t], k, c, &clo, &clen);
+            const uint64_t ns = clen == 0 ? 1 : std::min<uint64_t>(S, clen);
+            for (uint64_t j = 0; j < ns; ++j) {
+                uint64_t slo, slen;
+                split_piece(clen, ns, j, &slo, &slen);
+                p.segs.push_back({off[t] + clo + slo, slen});
+            }
+            tot += clen;
+        }
+        max_chunk = std::max(max_chunk, tot);
+    }
+    first[k] = (uint32_t)p.segs.size();
+    const uint64_t W = std::max<uint64_t>(1, std::min<uint64_t>((max_chunk + window_elems - 1) / std::max<uint64_t>(window_elems, 1), 64));
+    for (uint32_t c = 0; c < k; ++c) {
+        uint64_t tot = 0;
+        for (uint32_t s = first[c]; s < first[c + 1]; ++s) tot += p.segs[s].len;
+        uint32_t s = first[c];
+        uint64_t cum = 0;
+        for (uint64_t w = 0; w < W; ++w) {
+            const uint64_t end = tot * (w + 1) / W;  // segments starting before `end` join window w
+            const uint32_t s0 = s;
+            while (s < first[c + 1] && (cum < end || w + 1 == W)) cum += p.segs[s++].len;
+            p.add_batch(c, (uint32_t)w, s0, s);
+        }
     }
     return p;
 }
@@ -430,7 +489,6 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     a.cta_seg = bt.d_cta_seg;
     a.ncta = bt.ncta;
     a.nseg = bt.nseg;
-    a.scratch_q0 = bt.q_lo;
     a.a = io.a;
     a.b = io.b;
     a.in_codes = io.in_codes;
@@ -507,7 +565,7 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     if (tr) tr->launches += 1;
     if (prof) {
         cudaEvent_t e2 = tr->ev(st);
-        const double elems = (double)(bt.el_hi - bt.el_lo);
+        const double elems = (double)bt.elems;
         const double rd = elems * (((io.src & kSrcAminusB) ? 8.0 : 4.0) + ((io.src & kHasIn) ? 1.0 : 0.0)) +
                           ((io.src & kHasIn) ? 1028.0 * bt.nseg : 0.0);
         const double wr = elems + 1028.0 * bt.nseg;
@@ -543,7 +601,7 @@ int launch_apply(const Batch& bt, int mode, const uint8_t* codes, const float* c
     else k_apply<1><<<g, blk, 0, st>>>(a);
     if (tr) tr->launches += 1;
     if (prof) {
-        const double elems = (double)(bt.el_hi - bt.el_lo);
+        const double elems = (double)bt.elems;
         const double by = mode == 0 ? elems * 5.0 : elems * (theta_local ? 21.0 : 17.0);
         tr->recs.push_back({mode == 0 ? kProfDequant : kProfNesterov, e0, tr->ev(st), by + 1024.0 * bt.nseg});
     }
@@ -758,6 +816,7 @@ struct emesh_engine {
     // flags hold the round (epoch) number, so they never need resetting
     int transport = EMESH_TRANSPORT_NCCL;
     bool fp32 = false;               // ReduceMode::fp32 engine (raw fp32 payloads)
+    std::vector<uint64_t> sizes;     // multi-tensor engine: one ReduceJob per tensor (config 5)
     std::vector<float*> pay;         // fp32 payload arenas, per local worker (parity 0 under P2P)
     float* pay_alt = nullptr;        // fp32 payload arena, parity 1 (P2P)
     uint32_t epoch = 0;
@@ -854,7 +913,7 @@ int launch_f32_hop(const Batch& bt, Workspace& ws, const F32IO& io, cudaStream_t
     }
     if (tr) tr->launches += 1;
     if (prof) {
-        const double elems = (double)(bt.el_hi - bt.el_lo);
+        const double elems = (double)bt.elems;
         const double by = elems * (4.0 * (1 + (pg ? 1 : 0) + (hin ? 1 : 0)) + 4.0 * io.ndest);
         tr->recs.push_back({kProfF32Hop, e0, tr->ev(st), by});
     }
@@ -885,7 +944,7 @@ int launch_f32_apply(const Batch& bt, int mode, const float* pay, float* theta, 
     else k_f32_apply<1><<<g, blk, 0, st>>>(a, pay);
     if (tr) tr->launches += 1;
     if (prof) {
-        const double elems = (double)(bt.el_hi - bt.el_lo);
+        const double elems = (double)bt.elems;
         const double by = mode == 0 ? elems * 8.0 : elems * (theta_local ? 24.0 : 20.0);
         tr->recs.push_back({kProfF32Apply, e0, tr->ev(st), by});
     }
@@ -985,20 +1044,18 @@ int xfer_window(emesh_engine* e, const Batch& snd, const Batch& rcv) {
     auto& ar = e->arenas[0];
     if (e->fp32) {  // raw fp32 partial sums / means (allreduce.hpp:120-151)
         NC(ncclGroupStart());
-        if (snd.el_hi > snd.el_lo)
-            NC(ncclSend(e->pay[0] + snd.el_lo, snd.el_hi - snd.el_lo, ncclFloat32, succ, e->comm, e->s_comm));
-        if (rcv.el_hi > rcv.el_lo)
-            NC(ncclRecv(e->pay[0] + rcv.el_lo, rcv.el_hi - rcv.el_lo, ncclFloat32, pred, e->comm, e->s_comm));
+        for (const auto& r : snd.eruns)
+            NC(ncclSend(e->pay[0] + r.first, r.second, ncclFloat32, succ, e->comm, e->s_comm));
+        for (const auto& r : rcv.eruns)
+            NC(ncclRecv(e->pay[0] + r.first, r.second, ncclFloat32, pred, e->comm, e->s_comm));
         NC(ncclGroupEnd());
         return EMESH_OK;
     }
     NC(ncclGroupStart());
-    if (snd.el_hi > snd.el_lo)
-        NC(ncclSend(ar.codes + snd.el_lo, snd.el_hi - snd.el_lo, ncclUint8, succ, e->comm, e->s_comm));
+    for (const auto& r : snd.eruns) NC(ncclSend(ar.codes + r.first, r.second, ncclUint8, succ, e->comm, e->s_comm));
     NC(ncclSend(ar.cbs + (size_t)snd.slot0 * kBuckets, (size_t)snd.nseg * kBuckets, ncclFloat32, succ, e->comm,
                 e->s_comm));
-    if (rcv.el_hi > rcv.el_lo)
-        NC(ncclRecv(ar.codes + rcv.el_lo, rcv.el_hi - rcv.el_lo, ncclUint8, pred, e->comm, e->s_comm));
+    for (const auto& r : rcv.eruns) NC(ncclRecv(ar.codes + r.first, r.second, ncclUint8, pred, e->comm, e->s_comm));
     NC(ncclRecv(ar.cbs + (size_t)rcv.slot0 * kBuckets, (size_t)rcv.nseg * kBuckets, ncclFloat32, pred, e->comm,
                 e->s_comm));
     NC(ncclGroupEnd());
@@ -1135,6 +1192,11 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
 // hop's quantizer waits segment by segment. The owner's final payload goes
 // to every rank at once, which replaces the all-gather's k-1 forwarding hops
 // (the bytes are identical: AG forwards them verbatim, allreduce.hpp:446-464).
+// Above this many contiguous runs in the final chunk (multi-tensor plans),
+// the owner's quantizer stores its final payload to every rank itself
+// instead of one DMA per run and peer.
+constexpr size_t kMaxDmaRuns = 16;
+
 // Owner's final chunk -> every other rank by DMA (see run_p2p), in segment
 // groups, each followed by its arrival flags.
 int p2p_allgather(emesh_engine* e, int par, uint32_t ep) {
@@ -1148,16 +1210,22 @@ int p2p_allgather(emesh_engine* e, int par, uint32_t ep) {
         const uint32_t s0 = fb.slot0 + (uint32_t)((uint64_t)fb.nseg * g / groups);
         const uint32_t s1 = fb.slot0 + (uint32_t)((uint64_t)fb.nseg * (g + 1) / groups);
         if (s1 == s0) continue;
-        const uint64_t lo = e->plan.segs[s0].lo, hi = e->plan.segs[s1 - 1].lo + e->plan.segs[s1 - 1].len;
+        std::vector<std::pair<uint64_t, uint64_t>> runs;  // contiguous element runs of the group
+        for (uint32_t s = s0; s < s1; ++s) {
+            const Seg& g = e->plan.segs[s];
+            if (!g.len) continue;
+            if (!runs.empty() && runs.back().first + runs.back().second == g.lo) runs.back().second += g.len;
+            else runs.push_back({g.lo, g.len});
+        }
         for (uint32_t d = 1; d < k; ++d) {
             const uint32_t q = (r + d) % k;
             if (e->fp32) {
-                if (hi > lo)
-                    CU(cudaMemcpyAsync(e->peers[q].pay[par] + lo, e->peers[r].pay[par] + lo, (hi - lo) * sizeof(float),
-                                       cudaMemcpyDeviceToDevice, cm));
+                for (const auto& ru : runs)
+                    CU(cudaMemcpyAsync(e->peers[q].pay[par] + ru.first, e->peers[r].pay[par] + ru.first,
+                                       ru.second * sizeof(float), cudaMemcpyDeviceToDevice, cm));
             } else {
-                if (hi > lo)
-                    CU(cudaMemcpyAsync(e->peers[q].codes[par] + lo, e->peers[r].codes[par] + lo, hi - lo,
+                for (const auto& ru : runs)
+                    CU(cudaMemcpyAsync(e->peers[q].codes[par] + ru.first, e->peers[r].codes[par] + ru.first, ru.second,
                                        cudaMemcpyDeviceToDevice, cm));
                 CU(cudaMemcpyAsync(e->peers[q].cbs[par] + (size_t)s0 * kBuckets,
                                    e->peers[r].cbs[par] + (size_t)s0 * kBuckets,
@@ -1179,6 +1247,7 @@ int run_p2p_f32(emesh_engine* e, const float* A, const float* B, float* theta, f
     const int par = (int)(ep & 1u);
     cudaStream_t sc = e->s_comp;
     const auto& P = e->plan.batches;
+    const bool push_final = P[succ][0].eruns.size() > kMaxDmaRuns;
     {
         F32IO io{A, B, nullptr};
         io.ndest = 1;
@@ -1197,6 +1266,12 @@ int run_p2p_f32(emesh_engine* e, const float* A, const float* B, float* theta, f
         io.ndest = 1;
         if (fin) {
             io.dst[0] = e->peers[r].pay[par];
+            if (push_final)
+                for (uint32_t q = 0; q < k; ++q)
+                    if (q != r) {
+                        io.dst[io.ndest++] = e->peers[q].pay[par];
+                        io.flags[io.nflags++] = e->peers[q].ag_flag;
+                    }
         } else {
             io.dst[0] = e->peers[succ].pay[par];
             io.nflags = 1;
@@ -1204,7 +1279,7 @@ int run_p2p_f32(emesh_engine* e, const float* A, const float* B, float* theta, f
         }
         TRY(launch_f32_hop(P[rc][0], e->ws, io, sc, &e->tr));
     }
-    TRY(p2p_allgather(e, par, ep));
+    if (!push_final) TRY(p2p_allgather(e, par, ep));
     for (uint32_t d = 0; d < k; ++d) {
         const uint32_t c = (succ + k - d) % k;
         TRY(launch_f32_apply(P[c][0], out ? 0 : 1, e->peers[r].pay[par], theta, buf, local_out, out, lr, mom, sc,
@@ -1217,6 +1292,7 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
             float lr, float mom) {
     if (e->fp32) return run_p2p_f32(e, A, B, theta, buf, local_out, out, lr, mom);
     const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
+    const bool push_final = e->plan.batches[succ][0].eruns.size() > kMaxDmaRuns;
     const bool pg = B != nullptr;
     const uint32_t ep = ++e->epoch;
     const int par = (int)(ep & 1u);
@@ -1256,6 +1332,14 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
             to_succ(io);
         } else {  // owner: final payload local; the copy engines deliver it to every other rank
             io.local_out = true;
+            if (push_final)  // many small runs (multi-tensor): the quantizer stores to every rank itself
+                for (uint32_t q = 0; q < k; ++q)
+                    if (q != r) {
+                        io.x_codes[io.nx] = e->peers[q].codes[par];
+                        io.x_cb[io.nx] = e->peers[q].cbs[par];
+                        ++io.nx;
+                        io.flags[io.nflags++] = e->peers[q].ag_flag;
+                    }
         }
         mark(EMESH_OP_QUANT, (int)s, true);
         TRY(launch_quant(P[rc][0], e->ws, io, sc, &e->tr));
@@ -1266,7 +1350,7 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
     // groups so receivers start decoding while the rest streams; a group's
     // arrival flags are raised after its bytes (stream order). Runs on the
     // comm stream, overlapping this rank's own decode.
-    TRY(p2p_allgather(e, par, ep));
+    if (!push_final) TRY(p2p_allgather(e, par, ep));
     // decode every chunk: own final first, then the others as their owners'
     // copies land (per-segment ag_flag waits inside k_apply)
     for (uint32_t d = 0; d < k; ++d) {
@@ -1407,6 +1491,17 @@ uint64_t emesh_plan_segments(uint64_t n, uint32_t k, uint32_t S, uint64_t* seg_l
     return p.segs.size();
 }
 
+uint64_t emesh_plan_tensor_segments(const uint64_t* sizes, uint32_t nt, uint32_t k, uint32_t S, uint64_t* seg_lo,
+                                    uint64_t* seg_len) {
+    if (k == 0 || (nt && !sizes)) return 0;
+    Plan p = make_tensor_ring_plan(sizes, nt, k, S ? S : 4, (uint64_t)1 << 62);
+    for (size_t i = 0; i < p.segs.size(); ++i) {
+        if (seg_lo) seg_lo[i] = p.segs[i].lo;
+        if (seg_len) seg_len[i] = p.segs[i].len;
+    }
+    return p.segs.size();
+}
+
 uint64_t emesh_debug_batch_runs(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems, uint32_t chunk,
                                 uint32_t window, uint32_t* out4, uint64_t max_runs, uint32_t* ntasks_ncta) {
     if (k == 0 || chunk >= k) return 0;
@@ -1476,7 +1571,19 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
     const bool try_p2p = !virt && cfg->k > 1 && cfg->transport != EMESH_TRANSPORT_NCCL;
     const uint64_t nccl_window = cfg->window_elems ? cfg->window_elems : std::max<uint64_t>(chunk / 4, kDefaultWindow);
     uint64_t window = (virt || try_p2p) ? ~uint64_t(0) >> 2 : nccl_window;  // whole chunks
-    e->plan = make_ring_plan(cfg->n, cfg->k, S, window);
+    if (cfg->ntensors) {
+        if (!cfg->tensor_numel) return bail(fail(EMESH_ECONFIG, "tensor_numel is NULL"));
+        uint64_t tot = 0;
+        for (uint32_t t = 0; t < cfg->ntensors; ++t) tot += cfg->tensor_numel[t];
+        if (tot != cfg->n) return bail(fail(EMESH_ESHAPE, "tensor sizes sum to %llu, n = %llu",
+                                            (unsigned long long)tot, (unsigned long long)cfg->n));
+        e->sizes.assign(cfg->tensor_numel, cfg->tensor_numel + cfg->ntensors);
+    }
+    auto mkplan = [&](uint64_t win) {
+        return e->sizes.empty() ? make_ring_plan(cfg->n, cfg->k, S, win)
+                                : make_tensor_ring_plan(e->sizes.data(), (uint32_t)e->sizes.size(), cfg->k, S, win);
+    };
+    e->plan = mkplan(window);
     e->windows = (uint32_t)e->plan.batches[0].size();
     int rc = e->plan.upload();
     if (rc) return bail(rc);
@@ -1510,7 +1617,7 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
             return bail(fail(EMESH_ECONFIG, "peer transport unavailable (CUDA IPC mapping failed on some rank)"));
         } else if (try_p2p) {  // AUTO fell back: NCCL windows
             e->plan.release();
-            e->plan = make_ring_plan(cfg->n, cfg->k, S, nccl_window);
+            e->plan = mkplan(nccl_window);
             e->windows = (uint32_t)e->plan.batches[0].size();
             if ((rc = e->plan.upload()) || (rc = e->ws.reserve(e->plan.max_slots, e->plan.max_cta, e->plan.max_segs)))
                 return bail(rc);

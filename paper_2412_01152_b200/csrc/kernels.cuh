@@ -94,6 +94,7 @@ struct SegInfo {
     uint64_t lo;        // absolute element offset in the arena
     uint64_t len;       // elements
     uint64_t q0;        // lo >> 2: first float4 slot
+    uint64_t sq0;       // the segment's first float4 slot in the batch's scratch
     uint32_t nunits;    // warp units (1024-element float4-grid spans)
     uint32_t cta0;      // first tile (batch-relative): leaf_stat index
     uint32_t ncta;      // tiles
@@ -152,14 +153,13 @@ struct QuantArgs {
     const uint32_t* cta_seg;   // CTA -> batch-local segment
     uint32_t ncta;
     uint32_t nseg;
-    uint64_t scratch_q0;       // first float4 slot covered by scratch
     const float* a;
     const float* b;
     const uint8_t* in_codes;
     const float* in_cb;
     float divisor;
     float inv_divisor;         // 1/k when k is a power of two (exact), else 0
-    float* scratch;            // x, float4-slot indexed from scratch_q0
+    float* scratch;            // x of the batch; segment s at float4 slots [sq0, sq0 + slots)
     // output destinations (peer transport: the successor's arena); after a
     // segment's codes + codebook are stored everywhere, store `epoch` to
     // sflag[f][slot] for every flag f (the successor's arrival flags, or
@@ -397,7 +397,7 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
                                            uint32_t tile) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t hiel = si.lo + si.len;     // exclusive
-    float4* xs = reinterpret_cast<float4*>(a.scratch) - a.scratch_q0;
+    float4* xs = reinterpret_cast<float4*>(a.scratch) + ((int64_t)si.sq0 - (int64_t)si.q0);
 
     if (SRC & kHasIn) {
         if (sm.lut_seg != (int32_t)s) {
@@ -773,7 +773,7 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
     __syncthreads();
 
     const uint64_t hiel = si.lo + si.len;
-    const float4* xs = reinterpret_cast<const float4*>(a.scratch) - a.scratch_q0;
+    const float4* xs = reinterpret_cast<const float4*>(a.scratch) + ((int64_t)si.sq0 - (int64_t)si.q0);
     uint32_t nclip_lo = 0, nclip_hi = 0;
     const BinParams bpar{lo_f, inv_w, lo_up, hi_dn, margin, one_m};
     for (int ui = 0; ui < kUnitsPerWarp; ++ui) {

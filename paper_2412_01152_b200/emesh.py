@@ -389,6 +389,16 @@ def plan_segments(n: int, k: int, S: int):
     return lo, ln
 
 
+def plan_tensor_segments(sizes, k: int, S: int):
+    """Segment table of a multi-tensor engine (one ReduceJob per tensor; host-only)."""
+    sz = np.ascontiguousarray(np.asarray(sizes, dtype=np.uint64))
+    cnt = _capi.lib().emesh_plan_tensor_segments(sz.ctypes.data, len(sz), k, S, None, None)
+    lo = np.empty(cnt, np.uint64)
+    ln = np.empty(cnt, np.uint64)
+    _capi.lib().emesh_plan_tensor_segments(sz.ctypes.data, len(sz), k, S, lo.ctypes.data, ln.ctypes.data)
+    return lo, ln
+
+
 def ring_schedule(n: int, k: int, S: int, rank: int, window_elems: int = 0):
     """The NCCL engine's program for one ring position (host-only, no GPU)."""
     cnt = _capi.lib().emesh_ring_schedule(n, k, S, window_elems, rank, None, 0)
@@ -404,7 +414,7 @@ class RingEngine:
 
     def __init__(self, n: int, k: int, rank: int = 0, opts: Optional[ReduceOptions] = None, virtual: bool = False,
                  nccl_id: Optional[bytes] = None, window_elems: int = 0, device: Optional[int] = None,
-                 transport: str = "auto", mode: "ReduceMode" = None):
+                 transport: str = "auto", mode: "ReduceMode" = None, tensor_sizes: Optional[Sequence[int]] = None):
         opts = opts or ReduceOptions()
         if opts.pipeline_subchunks < 1:
             raise ConfigError("pipeline_subchunks must be >= 1")
@@ -424,6 +434,11 @@ class RingEngine:
         cfg.transport = tmap[transport]
         self.mode = ReduceMode.int8 if mode is None else ReduceMode(mode)
         cfg.reduce_fp32 = 1 if self.mode == ReduceMode.fp32 else 0
+        self._sizes = None
+        if tensor_sizes is not None:  # one ReduceJob per tensor (config 5)
+            self._sizes = np.ascontiguousarray(np.asarray(tensor_sizes, dtype=np.uint64))
+            cfg.tensor_numel = self._sizes.ctypes.data
+            cfg.ntensors = len(self._sizes)
         if nccl_id is not None:
             self._idbuf = C.create_string_buffer(bytes(nccl_id), 128)
             cfg.nccl_id = C.cast(self._idbuf, C.c_void_p)

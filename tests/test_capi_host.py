@@ -94,3 +94,44 @@ def test_plan_segments_match_oracle(capi, oracle, n, k, S):
     py = E.segment_table(n, k, S)
     assert [int(a) for a in lo] == [a for a, _ in py] and [int(b) for b in ln] == [b for _, b in py]
     assert int(ln.sum()) == n
+
+
+# INTELLECT-1 shape: 42 layers, d=4096, 32/8 heads, FFN 14336, vocab 128256
+def intellect1_tensor_sizes():
+    d, kv, ffn, vocab = 4096, 1024, 14336, 128256
+    sizes = [vocab * d]
+    for _ in range(42):
+        sizes += [d, d * d, d * kv, d * kv, d * d, d, d * ffn, d * ffn, ffn * d]
+    sizes += [d, vocab * d]
+    return sizes
+
+
+def test_intellect1_shape():
+    s = intellect1_tensor_sizes()
+    assert len(s) == 381 and sum(s) == 10_211_381_248
+
+
+@pytest.mark.parametrize("sizes,k,S", [([5, 17, 0, 100], 4, 4), ([1, 2, 3], 8, 4), ([4096] * 3 + [100_003], 2, 16),
+                                       (None, 8, 4)])
+def test_plan_tensor_segments_match_per_tensor_oracle(capi, oracle, sizes, k, S):
+    """Multi-tensor engine (config 5): one ReduceJob per tensor, every tensor's segment table as the
+    reference builds it (allreduce.hpp:107-118, 326-336), chunk-major across tensors."""
+    from paper_2412_01152_b200 import emesh as E
+    if sizes is None:
+        sizes = intellect1_tensor_sizes()
+    lo, ln = E.plan_tensor_segments(sizes, k, S)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.uint64)
+    per = []
+    for t, n_t in enumerate(sizes):
+        tl, tn = oracle.segment_table(int(n_t), k, S) if n_t < 50_000_000 else E.plan_segments(int(n_t), k, S)
+        # per-tensor table is chunk-major: split it back into its k chunks
+        chunks, i = [], 0
+        for c in range(k):
+            clen = n_t // k + (1 if c < n_t % k else 0)
+            ns = 1 if clen == 0 else min(S, clen)
+            chunks.append([(int(off[t] + tl[j]), int(tn[j])) for j in range(i, i + ns)])
+            i += ns
+        per.append(chunks)
+    want = [seg for c in range(k) for t in range(len(sizes)) for seg in per[t][c]]
+    assert [(int(a), int(b)) for a, b in zip(lo, ln)] == want
+    assert int(ln.sum()) == sum(sizes)

@@ -249,3 +249,56 @@ def test_ring_allreduce_job_mode_checked(E):
     with pytest.raises(E.ConfigError):
         E.ring_allreduce(eng, E.ReduceJob(1, torch.zeros(8, device="cuda:0"), E.ReduceMode.fp32))
     eng.close()
+
+
+# ---------------------------------------------------------------- multi-tensor engines (config 5)
+
+MT_SIZES = [4096, 17, 0, 100_003, 1, 65_536, 3, 250_000]
+
+
+@pytest.mark.parametrize("mode", ["int8", "fp32"])
+@pytest.mark.parametrize("k", [2, 4])
+def test_multi_tensor_ring_vs_per_tensor_oracle(E, oracle, k, mode):
+    """One ReduceJob per tensor, all tensors' chunks bucketed per hop: equal to
+    running the reference's ring on every tensor separately."""
+    n = sum(MT_SIZES)
+    off = np.concatenate([[0], np.cumsum(MT_SIZES)])
+    ins = [oracle.uniform(n, 77, i, 0, 0, 2.0 ** -4) for i in range(k)]
+    want = np.concatenate([oracle.ring_allreduce([a[off[t]:off[t + 1]] for a in ins], 4, mode)[:MT_SIZES[t]]
+                           for t in range(len(MT_SIZES))])
+    eng = E.RingEngine(n, k, opts=E.ReduceOptions(pipeline_subchunks=4), virtual=True, mode=E.ReduceMode[mode],
+                       tensor_sizes=MT_SIZES)
+    tin = [T(a) for a in ins]
+    outs = [torch.empty(n + 4, dtype=torch.float32, device="cuda:0")[:n] for _ in range(k)]
+    eng.ring_allreduce(tin, outs)
+    eng.check()
+    for o in outs:
+        assert np.array_equal(bits(o.cpu().numpy()), bits(want))
+    eng.close()
+
+
+def test_multi_tensor_outer_sync_vs_per_tensor_oracle(E, oracle):
+    k, S = 4, 4
+    n = sum(MT_SIZES)
+    off = np.concatenate([[0], np.cumsum(MT_SIZES)])
+    g0 = oracle.uniform(n, 5, 0)
+    ls = [(g0 - oracle.uniform(n, 6, 1 + w, 0, 0, 2.0 ** -10)).astype(np.float32) for w in range(k)]
+    b0 = oracle.uniform(n, 7, 0, 0, 0, 2.0 ** -12)
+    eg, eb = [], []
+    for t in range(len(MT_SIZES)):
+        if MT_SIZES[t] == 0:
+            continue
+        sl = slice(off[t], off[t + 1])
+        g_t, b_t = oracle.outer_sync(g0[sl], [a[sl] for a in ls], b0[sl], S, "int8", 0.7, 0.9)
+        eg.append(g_t[:MT_SIZES[t]])
+        eb.append(b_t[:MT_SIZES[t]])
+    eg, eb = np.concatenate(eg), np.concatenate(eb)
+    eng = E.RingEngine(n, k, opts=E.ReduceOptions(pipeline_subchunks=S), virtual=True, tensor_sizes=MT_SIZES)
+    tg = [T(g0) for _ in range(k)]
+    tb = [T(b0) for _ in range(k)]
+    eng.outer_sync(tg, [T(a) for a in ls], tb, E.HyperParams(), write_local=False)
+    eng.check()
+    for w in range(k):
+        assert np.array_equal(bits(tg[w].cpu().numpy()), bits(eg))
+        assert np.array_equal(bits(tb[w].cpu().numpy()), bits(eb))
+    eng.close()
