@@ -236,6 +236,14 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
     return old;
 }
+__device__ __forceinline__ void red_shared_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+// predicated (no branch): adds only when v != 0
+__device__ __forceinline__ void red_shared_add_nz(uint32_t* p, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q red.shared.add.u32 [%0], %1;\n\t}"
+                 ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
 __device__ __forceinline__ void spin_until_nonzero(const uint32_t* p) {
     while (ld_acquire(p) == 0u) __nanosleep(32);
 }
@@ -358,8 +366,8 @@ __device__ uint32_t bucket_info(float t0, float t1) {
 // co-resident CTAs that claim tile tasks in plan order (one atomicAdd each).
 
 struct QSmem {
-    uint32_t hist[kWarps][kBuckets][3];  // per-warp limbs over the tile (bin), see bin_unit
-    uint32_t binfo[kBuckets];            // bucket encodings (bin)
+    uint32_t hist[kWarps][kBuckets + 1][3];  // per-warp limbs over the tile (bin), see bin_unit; row 256: sink
+    uint32_t binfo[2 * kBuckets];        // bucket encodings (bin), twice: index code | 256 = same bucket
     float thr[kBuckets + 2];             // exact threshold table (bin); [257] = bucket 0's base (lo_up)
     float lut[kBuckets];                 // incoming codebook (stats, hop)
     StatP wp[kWarps];
@@ -660,7 +668,13 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
                 okall &= (fr > p.margin) & (fr < p.one_m) & ((uint32_t)c < 256u);
                 cc[i] = c;
             }
-            uint32_t clip_m = 0;  // clipped lanes: counted with r = 0 (xc = lo / hi added at the codebook)
+            // clipped lanes (and lanes outside the segment) keep their code in the
+            // low byte and set bit 8: their limbs go to the sink row 256; the
+            // codebook adds the clipped ones as count * lo / hi (quant.hpp:66-67)
+            if (!INTERIOR) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) cc[i] |= ((vmask >> i) & 1u) ? 0 : 256;
+            }
             if (!okall) {  // rare: near an edge (exact table) or clipped (quant.hpp:66-67)
                 uint32_t clo_m = 0, chi_m = 0;
 #pragma unroll
@@ -669,17 +683,17 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
                     const float g = __fmul_rn(__fsub_rn(x, p.lo_f), p.inv_w);
                     const int c0 = __float2int_rz(g);
                     const float fr = __fsub_rn(g, __int2float_rz(c0));
+                    const int sink = cc[i] & 256;
                     if (x < p.lo_up) {
-                        cc[i] = 0; clo_m |= 1u << i;
+                        cc[i] = 256; clo_m |= 1u << i;
                     } else if (x > p.hi_dn) {
-                        cc[i] = 255; chi_m |= 1u << i;
+                        cc[i] = 256 | 255; chi_m |= 1u << i;
                     } else if (!(fr > p.margin && fr < p.one_m && (uint32_t)c0 < 256u)) {
-                        cc[i] = bucket_walk(x, min(max(c0, 0), 255), sm.thr);
+                        cc[i] = sink | bucket_walk(x, min(max(c0, 0), 255), sm.thr);
                     }
                 }
                 nclip_lo += __popc(clo_m & vmask);
                 nclip_hi += __popc(chi_m & vmask);
-                clip_m = clo_m | chi_m;
             }
             // fixed point r(x) (see kInfoWide), split into the limbs
 #pragma unroll
@@ -692,19 +706,17 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
                     const double m = __fma_rn((double)xe[i], scale, kWideK);
                     rlo = (uint32_t)__double2loint(m);
                     rhi = (uint32_t)__double2hiint(m);
-                } else {  // r = m24 << (E - E0)
+                } else {  // narrow: r = m24 << (E - E0)
                     const uint32_t sh = ((bits >> 23) & 0xffu) - (info & 0xffu);
                     const uint32_t m24 = (bits & 0x7fffffu) | 0x800000u;
                     rlo = m24 << sh;
                     rhi = __funnelshift_l(m24, 0u, sh);
                 }
-                if ((clip_m >> i) & 1u) rlo = rhi = 0u;
-                const bool valid = (vmask >> i) & 1u;
-                uint32_t* hc = hw + 3 * cc[i];
-                atomicAdd(hc, valid ? ((rlo & ((1u << kLoBits) - 1u)) | (1u << kCntShift)) : 0u);
-                atomicAdd(hc + 1, valid ? ((rlo >> kLoBits) & ((1u << (kMidEnd - kLoBits)) - 1u)) : 0u);
+                uint32_t* hc = hw + 3 * min(cc[i], kBuckets);
+                red_shared_add(hc, (rlo & ((1u << kLoBits) - 1u)) | (1u << kCntShift));
+                red_shared_add(hc + 1, (rlo >> kLoBits) & ((1u << (kMidEnd - kLoBits)) - 1u));
                 const uint32_t rc = __funnelshift_r(rlo, rhi, kMidEnd) & ((1u << (42 - kMidEnd)) - 1u);
-                if (valid && rc) atomicAdd(hc + 2, rc);
+                if (rc) red_shared_add(hc + 2, rc);
             }
             const uint32_t p0 = __byte_perm(__byte_perm(cc[0], cc[1], 0x0040), __byte_perm(cc[2], cc[3], 0x0040), 0x5410);
             const uint32_t p1 = __byte_perm(__byte_perm(cc[4], cc[5], 0x0040), __byte_perm(cc[6], cc[7], 0x0040), 0x5410);
@@ -755,7 +767,7 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
         __syncthreads();
         const int b = threadIdx.x;
         sm.thr[b] = b == 0 ? -INFINITY : __ldcg(&st->thr[b]);
-        sm.binfo[b] = __ldcg(&st->binfo[b]);
+        sm.binfo[b] = sm.binfo[kBuckets + b] = __ldcg(&st->binfo[b]);
 
         if (b == 0) {
             sm.thr[kBuckets] = INFINITY;
@@ -845,8 +857,8 @@ __device__ void finalize_codebook(const QuantArgs& a, uint32_t s, const SegInfo&
     const int b = threadIdx.x;
     SegAcc* acc = &a.acc[s];
     const unsigned long long rl = __ldcg(&acc->rlo[b]), rh = __ldcg(&acc->rhi[b]);
-    const unsigned long long total = __ldcg(&acc->cnt[b]);
     const unsigned long long clip = b == 0 ? __ldcg(&acc->clip[0]) : b == 255 ? __ldcg(&acc->clip[1]) : 0ull;
+    const unsigned long long total = __ldcg(&acc->cnt[b]) + clip;  // clipped members sit in the sink row
     __syncthreads();  // every read done before the re-zeroing
     acc->rlo[b] = 0ull;
     acc->rhi[b] = 0ull;
@@ -908,7 +920,7 @@ __global__ void __launch_bounds__(kThreads, EMESH_QUANT_MINB) k_quant(QuantArgs 
     SegInfo* segs_s = reinterpret_cast<SegInfo*>(qsmem_raw + sizeof(QSmem) + kMaxRunsSmem * sizeof(uint4));
     const bool runs_in_smem = a.nruns <= kMaxRunsSmem;
     const bool segs_in_smem = a.nseg <= kMaxSegsSmem;
-    for (uint32_t i = threadIdx.x; i < kWarps * kBuckets * 3; i += kThreads) (&sm.hist[0][0][0])[i] = 0u;
+    for (uint32_t i = threadIdx.x; i < kWarps * (kBuckets + 1) * 3; i += kThreads) (&sm.hist[0][0][0])[i] = 0u;
     if (runs_in_smem)
         for (uint32_t i = threadIdx.x; i < a.nruns; i += kThreads) runs_s[i] = a.runs[i];
     if (segs_in_smem)
