@@ -45,6 +45,7 @@ class EngineConfig(C.Structure):
         ("reduce_fp32", C.c_uint32),
         ("tensor_numel", C.c_void_p),
         ("ntensors", C.c_uint32),
+        ("step_timeout_s", C.c_double),
     ]
 
 

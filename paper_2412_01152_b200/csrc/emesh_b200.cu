@@ -412,6 +412,9 @@ enum ProfKind : int {
 struct Tracker {
     uint64_t launches = 0;
     bool prof = false;
+    // peer-transport waits of this engine's kernels: error word + budget
+    uint32_t* err = nullptr;
+    unsigned long long timeout_ns = 30ull * 1000000000ull;
     struct Rec {
         int kind;
         cudaEvent_t a, b;
@@ -523,6 +526,7 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     if (a.remote && tile_fence) a.remote |= 2u;
     a.in_flag = io.in_flag;
     a.epoch = io.epoch;
+    a.timeout_ns = tr ? tr->timeout_ns : 30ull * 1000000000ull;
     a.stats = io.stats;
     a.leaf_stat = ws.leaf_stat;
     a.acc = ws.acc;
@@ -583,6 +587,9 @@ int launch_apply(const Batch& bt, int mode, const uint8_t* codes, const float* c
     ApplyArgs a{};
     a.in_flag = in_flag;
     a.epoch = epoch;
+    a.err = tr ? tr->err : nullptr;
+    a.timeout_ns = tr ? tr->timeout_ns : 30ull * 1000000000ull;
+    if (in_flag && !a.err) return fail(EMESH_ECONFIG, "peer wait without an error word");
     a.segs = bt.d_segs;
     a.cta_seg = bt.d_cta_seg;
     a.ncta = bt.ncta;
@@ -815,6 +822,7 @@ struct emesh_engine {
     // CUDA IPC; codes / codebooks double-buffered by round parity; arrival
     // flags hold the round (epoch) number, so they never need resetting
     int transport = EMESH_TRANSPORT_NCCL;
+    bool failed = false;             // a round failed (ring timeout / NCCL): abort, never wait for peers
     bool fp32 = false;               // ReduceMode::fp32 engine (raw fp32 payloads)
     std::vector<uint64_t> sizes;     // multi-tensor engine: one ReduceJob per tensor (config 5)
     std::vector<float*> pay;         // fp32 payload arenas, per local worker (parity 0 under P2P)
@@ -893,8 +901,10 @@ int launch_f32_hop(const Batch& bt, Workspace& ws, const F32IO& io, cudaStream_t
     a.nflag = io.nflags;
     for (uint32_t f = 0; f < io.nflags; ++f) a.sflag[f] = io.flags[f];
     a.seg_done = ws.sync + kSyncReady;
+    a.err = ws.err;
     a.in_flag = io.in_flag;
     a.epoch = io.epoch;
+    a.timeout_ns = tr ? tr->timeout_ns : 30ull * 1000000000ull;
     a.nseg = bt.nseg;
     if (io.nflags) CU(cudaMemsetAsync(ws.sync + kSyncReady, 0, (size_t)bt.nseg * sizeof(uint32_t), st));
     const bool prof = tr && tr->prof;
@@ -937,6 +947,9 @@ int launch_f32_apply(const Batch& bt, int mode, const float* pay, float* theta, 
     a.mom = mom;
     a.in_flag = in_flag;
     a.epoch = epoch;
+    a.err = tr ? tr->err : nullptr;
+    a.timeout_ns = tr ? tr->timeout_ns : 30ull * 1000000000ull;
+    if (in_flag && !a.err) return fail(EMESH_ECONFIG, "peer wait without an error word");
     const dim3 g(bt.ncta * kApplySplit), blk(kThreads);
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
@@ -1588,6 +1601,8 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
     int rc = e->plan.upload();
     if (rc) return bail(rc);
     if (e->k > 1 && (rc = engine_alloc(e))) return bail(rc);
+    e->tr.err = e->ws.err;
+    if (cfg->step_timeout_s > 0) e->tr.timeout_ns = (unsigned long long)(cfg->step_timeout_s * 1e9);
     int lo_prio = 0, hi_prio = 0;
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
     if (cudaStreamCreateWithPriority(&e->s_comp, cudaStreamNonBlocking, lo_prio) != cudaSuccess ||
@@ -1613,6 +1628,10 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
         e->transport = EMESH_TRANSPORT_NCCL;
         if (try_p2p && setup_p2p(e)) {
             e->transport = EMESH_TRANSPORT_P2P;
+            // NCCL only bootstrapped the mappings: release it now, while every
+            // rank is here, so teardown never depends on a peer being alive
+            ncclCommDestroy(e->comm);
+            e->comm = nullptr;
         } else if (cfg->transport == EMESH_TRANSPORT_P2P) {
             return bail(fail(EMESH_ECONFIG, "peer transport unavailable (CUDA IPC mapping failed on some rank)"));
         } else if (try_p2p) {  // AUTO fell back: NCCL windows
@@ -1642,7 +1661,10 @@ int emesh_engine_destroy(emesh_engine* e) {
     if (e->s_comp) cudaStreamSynchronize(e->s_comp);
     if (e->s_comm) cudaStreamSynchronize(e->s_comm);
     teardown_p2p(e);
-    if (e->comm) ncclCommDestroy(e->comm);
+    if (e->comm) {
+        if (e->failed) ncclCommAbort(e->comm);  // peers may be gone: do not wait for them
+        else ncclCommDestroy(e->comm);
+    }
     for (auto& a : e->arenas) { cudaFree(a.codes); cudaFree(a.cbs); cudaFree(a.stats); }
     for (auto* p : e->pay) cudaFree(p);
     for (auto* p : e->h_theta) cudaFree(p);
@@ -1809,6 +1831,11 @@ int emesh_engine_check(emesh_engine* e) {
     CU(cudaMemcpy(&v, e->ws.err, sizeof v, cudaMemcpyDeviceToHost));
     if (v) {
         CU(cudaMemset(e->ws.err, 0, sizeof(uint32_t)));
+        if (v & kErrRingTimeout) {  // allreduce.hpp:466-470: a peer stopped mid-collective
+            e->failed = true;
+            return fail(EMESH_ERING, "ring step timed out waiting for a peer's payload (step_timeout %.1f s)",
+                        (double)e->tr.timeout_ns * 1e-9);
+        }
         return fail(EMESH_ENUMERIC, "quantize: non-finite input");
     }
     return EMESH_OK;

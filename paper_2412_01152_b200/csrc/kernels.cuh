@@ -172,6 +172,7 @@ struct QuantArgs {
     uint32_t remote;           // bit 0: peer-memory outputs; bit 1: system fence per tile
     const uint32_t* in_flag;   // peer transport: in_codes / in_cb of slot s valid once in_flag[s] >= epoch
     uint32_t epoch;
+    unsigned long long timeout_ns;  // peer-wait budget (spin_until_ge_sys)
     SegStat* stats;            // indexed by slot
     StatP* leaf_stat;          // [tile]
     SegAcc* acc;               // [seg] bucket histograms (batch-local segment)
@@ -256,9 +257,21 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void spin_until_ge_sys(const uint32_t* p, uint32_t epoch) {
+// Waits for a peer's arrival flag. A peer that stops (crash, abort) must not
+// hang the GPU: after timeout_ns (ReduceOptions::step_timeout,
+// allreduce.hpp:59) the wait gives up and sets err bit 1 (the host reports
+// RingFailureError); once that bit is set every other wait gives up at once.
+constexpr uint32_t kErrRingTimeout = 2u;
+__device__ __forceinline__ void spin_until_ge_sys(const uint32_t* p, uint32_t epoch, uint32_t* err,
+                                                  unsigned long long timeout_ns) {
     uint32_t ns = 64;
+    const unsigned long long t0 = gtimer();
     while ((int32_t)(ld_acquire_sys(p) - epoch) < 0) {
+        if (ld_acquire(err) & kErrRingTimeout) return;
+        if (gtimer() - t0 > timeout_ns) {
+            atomicOr(err, kErrRingTimeout);
+            return;
+        }
         __nanosleep(ns);
         ns = ns < 2048 ? 2 * ns : ns;
     }
@@ -411,7 +424,7 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
         if (sm.lut_seg != (int32_t)s) {
             __syncthreads();
             if (a.in_flag) {  // peer transport: wait until the predecessor's payload of s landed
-                if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.in_slot, a.epoch);
+                if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.in_slot, a.epoch, a.err, a.timeout_ns);
                 __syncthreads();
             }
             sm.lut[threadIdx.x] = __ldcg(a.in_cb + (uint64_t)si.in_slot * kBuckets + threadIdx.x);
@@ -1008,6 +1021,8 @@ struct ApplyArgs {
     float lr, mom;
     const uint32_t* in_flag;  // peer transport: codes / codebook of slot s valid once in_flag[s] >= epoch
     uint32_t epoch;
+    uint32_t* err;            // sticky error word (kErrRingTimeout)
+    unsigned long long timeout_ns;
 };
 constexpr int kApplySplit = kUnitsPerWarp / 2;  // k_apply CTAs per quantizer tile (2 units per warp each)
 
@@ -1026,7 +1041,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
     const uint32_t tile = blockIdx.x / kApplySplit, part = blockIdx.x % kApplySplit;
     const SegInfo si = a.segs[a.cta_seg[tile]];
     if (a.in_flag) {
-        if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.slot, a.epoch);
+        if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.slot, a.epoch, a.err, a.timeout_ns);
         __syncthreads();
     }
     lut[threadIdx.x] = __ldcg(a.cb + (uint64_t)si.slot * kBuckets + threadIdx.x);
@@ -1098,6 +1113,8 @@ struct F32HopArgs {
     const uint32_t* in_flag;   // peer transport: wait in_flag[slot] >= epoch before reading `in`
     uint32_t epoch;
     uint32_t nseg;
+    uint32_t* err;
+    unsigned long long timeout_ns;
 };
 
 // x = (a - b | a) (+ in) (/ k), the reduce-scatter accumulate
@@ -1109,7 +1126,7 @@ __global__ void __launch_bounds__(kThreads) k_f32_hop(F32HopArgs a) {
     const uint32_t s = a.cta_seg[tile];
     const SegInfo si = a.segs[s];
     if (HAS_IN && a.in_flag) {
-        if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.in_slot, a.epoch);
+        if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.in_slot, a.epoch, a.err, a.timeout_ns);
         __syncthreads();
     }
     const uint64_t hiel = si.lo + si.len;
@@ -1171,7 +1188,7 @@ __global__ void __launch_bounds__(kThreads) k_f32_apply(ApplyArgs a, const float
     const uint32_t tile = blockIdx.x / kApplySplit, part = blockIdx.x % kApplySplit;
     const SegInfo si = a.segs[a.cta_seg[tile]];
     if (a.in_flag) {
-        if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.slot, a.epoch);
+        if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.slot, a.epoch, a.err, a.timeout_ns);
         __syncthreads();
     }
     const uint64_t hiel = si.lo + si.len;

@@ -340,6 +340,32 @@ class RingPlan:
     order: List[str] = field(default_factory=list)
     self_index: int = 0
 
+    @staticmethod
+    def from_mesh(mesh: "MeshState", self_id: str, job_id: int) -> "RingPlan":
+        """allreduce.hpp:31-44."""
+        if self_id not in mesh.ring:
+            raise ShapeError(f"node {self_id} is not in the ring")
+        return RingPlan(job_id, int(mesh.epoch), list(mesh.ring), mesh.ring.index(self_id))
+
+
+@dataclass
+class MeshState:
+    """The part of the reference's MeshState (mesh.hpp) the ring consumes: the
+    membership epoch and the ring order of the current members."""
+
+    epoch: int
+    ring: List[str]
+
+
+@dataclass
+class RetryResult:
+    """allreduce.hpp:477-482."""
+
+    value: torch.Tensor
+    participants: int = 0
+    attempts: int = 0  # failures survived
+    epoch: int = 0
+
 
 @dataclass
 class ReduceJob:
@@ -434,6 +460,7 @@ class RingEngine:
         cfg.transport = tmap[transport]
         self.mode = ReduceMode.int8 if mode is None else ReduceMode(mode)
         cfg.reduce_fp32 = 1 if self.mode == ReduceMode.fp32 else 0
+        cfg.step_timeout_s = float(opts.step_timeout)
         self._sizes = None
         if tensor_sizes is not None:  # one ReduceJob per tensor (config 5)
             self._sizes = np.ascontiguousarray(np.asarray(tensor_sizes, dtype=np.uint64))
@@ -557,6 +584,47 @@ class RingEngine:
         _check(_capi.lib().emesh_engine_payload_host(self._h, worker, codes.ctypes.data, cbs.ctypes.data,
                                                      stats.ctypes.data))
         return codes[: self.n], cbs, stats
+
+
+def allreduce_with_retry(make_engine, mesh, mesh_state: MeshState, self_id: str, job: ReduceJob,
+                         opts: Optional[ReduceOptions] = None) -> RetryResult:
+    """allreduce.hpp:485-518 over GPU engines. ``make_engine(plan)`` builds the
+    engine of one membership epoch (the caller exchanges the NCCL id among
+    ``plan.order``; build it with ``ReduceOptions(step_timeout=...)`` so a peer
+    that stops makes the round fail instead of hang); ``mesh`` is the
+    membership service (the reference's MeshClient): ``report_failure(node)``,
+    ``wait_epoch_change(epoch, timeout) -> MeshState`` (may raise TimeoutError)
+    and ``fetch_mesh() -> MeshState``. A failed round (RingFailureError: a peer
+    timed out, NCCL failed) is retried over the survivors from the preserved
+    ``job.input``; the result is the mean over the final plan's participants."""
+    opts = opts or ReduceOptions()
+    failures = 0
+    while True:
+        if self_id not in mesh_state.ring:
+            raise FatalError("this node is no longer in the mesh")
+        if len(mesh_state.ring) < 1:
+            raise FatalError("no participants left")
+        plan = RingPlan.from_mesh(mesh_state, self_id, job.id)
+        eng = None
+        try:
+            eng = make_engine(plan)
+            value = ring_allreduce(eng, job, opts)
+            eng.check()
+            return RetryResult(value, len(plan.order), failures, int(mesh_state.epoch))
+        except RingFailureError as rf:
+            failures += 1
+            if failures > opts.max_retries:
+                raise FatalError(f"all-reduce retries exhausted: {rf}") from rf
+            failed = getattr(rf, "failed_node", "")
+            if failed and failed != self_id:
+                mesh.report_failure(failed)
+            try:
+                mesh_state = mesh.wait_epoch_change(mesh_state.epoch, opts.evict_wait)
+            except TimeoutError:
+                mesh_state = mesh.fetch_mesh()  # maybe it changed and we missed it
+        finally:
+            if eng is not None and hasattr(eng, "close"):
+                eng.close()
 
 
 def ring_allreduce(engine: RingEngine, job: ReduceJob, opts: Optional[ReduceOptions] = None,

@@ -20,3 +20,15 @@ def test_nccl_ring_parity():
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert out.returncode == 0, (out.stdout[-3000:], out.stderr[-3000:])
     assert "NCCL parity OK" in out.stdout
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_retry_after_peer_stops():
+    """allreduce_with_retry over the peer transport: a peer stops mid-collective, the survivors time out
+    (RingFailureError), re-plan and return the survivor mean (test_allreduce.cpp:431-445 analogue)."""
+    n = min(torch.cuda.device_count(), 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29534", os.path.join(ROOT, "tests", "retry_worker.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, (out.stdout[-3000:], out.stderr[-3000:])
+    assert out.stdout.count("retry OK") == n - 1
