@@ -61,15 +61,15 @@ constexpr int kTileUnits = kWarps * kUnitsPerWarp;  // 16 units = 16384 elements
 // identical for any accumulation order, and equal to the reference's
 // sequential fp64 sum whenever that sum is exact (quant.hpp:74).
 //  * "narrow" buckets (all members of one sign, magnitudes within 2^17 of
-//    each other, normal): r = m24(x) << (E(x) - E0), the 24-bit significand
-//    shifted to the unit 2^(E0 - 150) (E = biased exponent, E0 = that of the
-//    smallest-magnitude member) — pure integer ops on the fp32 bits, exact;
-//    x = +-r 2^(E0 - 150).
+//    each other, normal): r = |x| / Q with Q = 2^e the ulp of the smallest
+//    member — an exact integer < 2^41; x = +-r Q.
 //  * "wide" buckets (at or near zero): r = rint(x / Q) + 2^41 with a quantum
-//    Q = 2^e = 2^-41 of the bucket's magnitude, one fp64 fma.
-// Per-bucket info word: [0:8) E0, bit 8 negative, bit 9 wide, [16:26) e + 512.
-constexpr uint32_t kInfoNeg = 1u << 8;
-constexpr uint32_t kInfoWide = 1u << 9;
+//    Q = 2^e = 2^-41 of the bucket's magnitude.
+// Both are ONE fp64 fma, m = x * s + K with s = +-2^-e and K = 2^52 (narrow) or
+// 2^52 + 2^41 (wide): m lands in [2^52, 2^53) and its mantissa bits are r.
+// Per-bucket info word = the high word of s (sign, exponent; its low mantissa
+// bits are zero) with bit 0 = wide, so a member's m needs no table but this.
+constexpr uint32_t kInfoWide = 1u;
 constexpr double kMagic52 = 4503599627370496.0;  // 2^52
 constexpr double kWideK = 4503599627370496.0 + 2199023255552.0;  // 2^52 + 2^41
 constexpr int kWideBiasBits = 41;
@@ -362,16 +362,17 @@ __device__ __forceinline__ int exponent_of(float f) {  // floor(log2|f|) for nor
 
 // Encoding of bucket b whose fp32 members lie in [t0, t1) (see kInfoWide).
 __device__ uint32_t bucket_info(float t0, float t1) {
-    if (!(t1 > t0)) return kInfoWide | (512u << 16);  // holds no fp32 value
+    if (!(t1 > t0)) return (1023u << 20) | kInfoWide;  // holds no fp32 value
     const float last = key2f(f2key(t1) - 1);
     if (t0 > 0.f || last < 0.f) {
         const float mn = t0 > 0.f ? t0 : last, mx = t0 > 0.f ? last : t0;
         const uint32_t e_lo = (__float_as_uint(mn) >> 23) & 0xffu, e_hi = (__float_as_uint(mx) >> 23) & 0xffu;
-        if (e_lo >= 1u && e_hi - e_lo <= 17u) return e_lo | (t0 > 0.f ? 0u : kInfoNeg);  // r < 2^41
+        // Q = ulp(mn) = 2^(e_lo - 150); s = +-2^(150 - e_lo); r < 2^(24 + 17)
+        if (e_lo >= 1u && e_hi - e_lo <= 17u) return ((1023u + 150u - e_lo) << 20) | (t0 > 0.f ? 0u : 0x80000000u);
     }
     const float mx = fmaxf(fabsf(t0), fabsf(last));
-    const int e = exponent_of(mx) + 1 - kWideBiasBits;  // |x| < 2^(e+41)
-    return kInfoWide | ((uint32_t)(e + 512) << 16);
+    const int e = exponent_of(mx) + 1 - kWideBiasBits;  // |x| < 2^(e+41); s = 2^-e
+    return ((uint32_t)(1023 - e) << 20) | kInfoWide;
 }
 
 // ---------------------------------------------------------------------------
@@ -712,19 +713,12 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const uint32_t info = sm.binfo[cc[i]];
-                const uint32_t bits = __float_as_uint(xe[i]);
-                uint32_t rlo, rhi;
-                if (info & kInfoWide) {  // at / near zero: r = rint(x / Q) + 2^41
-                    const double scale = __hiloint2double((int)((1023u + 512u - (info >> 16)) << 20), 0);
-                    const double m = __fma_rn((double)xe[i], scale, kWideK);
-                    rlo = (uint32_t)__double2loint(m);
-                    rhi = (uint32_t)__double2hiint(m);
-                } else {  // narrow: r = m24 << (E - E0)
-                    const uint32_t sh = ((bits >> 23) & 0xffu) - (info & 0xffu);
-                    const uint32_t m24 = (bits & 0x7fffffu) | 0x800000u;
-                    rlo = m24 << sh;
-                    rhi = __funnelshift_l(m24, 0u, sh);
-                }
+                // m = x * s + K in [2^52, 2^53): mantissa = r (see kInfoWide)
+                const double sc = __hiloint2double((int)(info & ~kInfoWide), 0);
+                const double kk = __hiloint2double((int)(0x43300000u | ((info & kInfoWide) << 9)), 0);
+                const double m = __fma_rn((double)xe[i], sc, kk);
+                const uint32_t rlo = (uint32_t)__double2loint(m);
+                const uint32_t rhi = (uint32_t)__double2hiint(m);
                 uint32_t* hc = hw + 3 * min(cc[i], kBuckets);
                 red_shared_add(hc, (rlo & ((1u << kLoBits) - 1u)) | (1u << kCntShift));
                 red_shared_add(hc + 1, (rlo >> kLoBits) & ((1u << (kMidEnd - kLoBits)) - 1u));
@@ -913,12 +907,10 @@ __device__ float codebook_entry(const SegStat* st, int b, unsigned long long rl,
         const long long s64 = (long long)(unsigned long long)S;
         const bool fits = (hi64 == 0 && s64 >= 0) || (hi64 == -1 && s64 < 0);
         const double v = fits ? (double)s64 : __dadd_rn(ldexp((double)hi64, 64), (double)(unsigned long long)S);
-        if (info & kInfoWide) {
-            sum = ldexp(v, (int)(info >> 16) - 512);  // exact: power-of-two scaling
-        } else {
-            sum = ldexp(v, (int)(info & 0xffu) - 150);
-            if (info & kInfoNeg) sum = -sum;
-        }
+        // sum x = sum(r) / s (wide: after removing the bias): exact power-of-two scaling
+        const int e = 1023 - (int)((info >> 20) & 0x7ffu);  // |s| = 2^-e
+        sum = ldexp(v, e);
+        if (info & 0x80000000u) sum = -sum;
     }
     if (b == 0 && clip) sum = __dadd_rn(sum, __dmul_rn((double)clip, __ldcg(&st->lo)));
     if (b == 255 && clip) sum = __dadd_rn(sum, __dmul_rn((double)clip, __ldcg(&st->hi)));
