@@ -77,7 +77,7 @@ constexpr int kWideBiasBits = 41;
 // Per-segment statistics, written once by the root CTA of k_stats.
 struct SegStat {
     double mu, sigma, lo, width, hi;  // first four exported as {mu, sigma, lo, width}
-    float lo_f, inv_w_f;
+    float c_f, inv_w_f;  // bucket estimate g = fma(x, inv_w_f, -c_f), c_f = (float)(lo / width)
     float lo_up, hi_dn;  // x < lo <=> x < lo_up ; x > hi <=> x > hi_dn (fp32 x)
     uint32_t flags;      // kFlagNonFinite | kFlagDegenerate
     float margin;        // fp32 bucket estimate is exact when its fraction is in (margin, 1-margin)
@@ -578,7 +578,7 @@ __device__ void finalize_stats(const QuantArgs& a, QSmem& sm, uint32_t s, const 
         a.seg_flags[s] = 0;
         if (sigma == 0.0) {
             st->lo = mu; st->hi = mu; st->width = 0.0;
-            st->lo_f = (float)mu; st->inv_w_f = 0.f;
+            st->c_f = 0.f; st->inv_w_f = 0.f;
         }
     }
     if (sigma != 0.0) {
@@ -599,17 +599,17 @@ __device__ void finalize_stats(const QuantArgs& a, QSmem& sm, uint32_t s, const 
         st->binfo[b] = bucket_info(sm.thr[b], sm.thr[b + 1]);
         if (b == 0) {
             st->lo = lo; st->hi = hi; st->width = w;
-            const float lo_f = (float)lo, inv_w = (float)__ddiv_rn(1.0, w);
-            st->lo_f = lo_f;
+            const float c_f = (float)__ddiv_rn(lo, w), inv_w = (float)__ddiv_rn(1.0, w);
+            st->c_f = c_f;
             st->inv_w_f = inv_w;
             st->lo_up = lo_up;
             st->hi_dn = hi_dn;
-            // Error of g = (x - lo_f) * inv_w (fp32) vs (x - lo) / w, in buckets,
-            // for lo <= x <= hi: |lo - lo_f| / w + 3 roundings of a value
-            // <= (|lo| + |hi|) / w, each <= 2^-24 relative; x2 for safety.
+            // Error of g = fma(x, inv_w, -c) (fp32) vs (x - lo) / w, in buckets, for
+            // lo <= x <= hi: inv_w and c carry <= 2^-24 relative error each
+            // (|x| / w and |lo| / w terms), the fma one rounding of |g| <= 256:
+            // err <= ((max(|lo|, |hi|) + |lo|) / w + 256) 2^-24; x2 for safety.
             const double mag = __ddiv_rn(fmax(fabs(lo), fabs(hi)) + fabs(lo), w);
-            const double err = __dadd_rn(__ddiv_rn(fabs(__dsub_rn(lo, (double)lo_f)), w),
-                                         __dmul_rn(mag, 3.0 / 16777216.0));
+            const double err = __dmul_rn(__dadd_rn(mag, 256.0), 1.01 / 16777216.0);
             const double mg = __dmul_rn(2.0, err) + 1e-6;
             st->margin = mg < 0.25 ? (float)mg : 2.0f;  // 2.0: always use the table
         }
@@ -630,7 +630,7 @@ __device__ __noinline__ int bucket_walk(float x, int c, const float* thr) {
 
 
 struct BinParams {
-    float lo_f, inv_w, lo_up, hi_dn, margin, one_m;
+    float c, inv_w, lo_up, hi_dn, margin, one_m;  // bucket estimate g = fma(x, inv_w, -c)
 };
 
 // One warp unit of the bin pass (1024 elements; this lane's 32), in groups of
@@ -676,7 +676,7 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
                 // in range and clear of every bucket edge by the proven margin:
                 // then trunc(g) is the exact bucket. Clipped x fails this test
                 // (g < margin or g > 256 - margin), see SegStat::margin.
-                const float g = __fmul_rn(__fsub_rn(xe[i], p.lo_f), p.inv_w);
+                const float g = __fmaf_rn(xe[i], p.inv_w, -p.c);
                 const int c = __float2int_rz(g);
                 const float fr = __fsub_rn(g, __int2float_rz(c));
                 okall &= (fr > p.margin) & (fr < p.one_m) & ((uint32_t)c < 256u);
@@ -694,7 +694,7 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const float x = xe[i];
-                    const float g = __fmul_rn(__fsub_rn(x, p.lo_f), p.inv_w);
+                    const float g = __fmaf_rn(x, p.inv_w, -p.c);
                     const int c0 = __float2int_rz(g);
                     const float fr = __fsub_rn(g, __int2float_rz(c0));
                     const int sink = cc[i] & 256;
@@ -783,7 +783,7 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
         __syncthreads();
         if (threadIdx.x == 0) sm.bin_seg = (int32_t)s;
     }
-    const float lo_f = __ldcg(&st->lo_f), inv_w = __ldcg(&st->inv_w_f);
+    const float c_f = __ldcg(&st->c_f), inv_w = __ldcg(&st->inv_w_f);
     const float lo_up = __ldcg(&st->lo_up), hi_dn = __ldcg(&st->hi_dn);  // x < lo <=> x < lo_up (fp32 x)
     const float margin = __ldcg(&st->margin), one_m = 1.f - margin;
     const bool degenerate = (__ldcg(&st->flags) & kFlagDegenerate) != 0;
@@ -794,7 +794,7 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
     const uint64_t hiel = si.lo + si.len;
     const float4* xs = reinterpret_cast<const float4*>(a.scratch) + ((int64_t)si.sq0 - (int64_t)si.q0);
     uint32_t nclip_lo = 0, nclip_hi = 0;
-    const BinParams bpar{lo_f, inv_w, lo_up, hi_dn, margin, one_m};
+    const BinParams bpar{c_f, inv_w, lo_up, hi_dn, margin, one_m};
     for (int ui = 0; ui < kUnitsPerWarp; ++ui) {
         const uint32_t u = tile * kTileUnits + ui * kWarps + warp;
         if (u >= si.nunits) break;
