@@ -491,8 +491,10 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
                     sum1 = __dadd_rn(__dadd_rn(sum1, x1), x3);
                     d0 = __dadd_rn(__dadd_rn(d0, v0), v2);
                     d1 = __dadd_rn(__dadd_rn(d1, v1), v3);
-                    q0 = __dadd_rn(__dadd_rn(q0, __dmul_rn(v0, v0)), __dmul_rn(v2, v2));
-                    q1 = __dadd_rn(__dadd_rn(q1, __dmul_rn(v1, v1)), __dmul_rn(v3, v3));
+                    // sigma is not bit-exact vs the sequential reference anyway:
+                    // fused multiply-adds for the squares
+                    q0 = __fma_rn(v2, v2, __fma_rn(v0, v0, q0));
+                    q1 = __fma_rn(v3, v3, __fma_rn(v1, v1, q1));
                     if (SRC != kSrcA) xs[q] = make_float4(x[0], x[1], x[2], x[3]);
                 } else {
                     uint32_t vm = 0u;
@@ -506,7 +508,7 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
                             const double dv = __dsub_rn(xd, piv);
                             sum0 = __dadd_rn(sum0, xd);
                             d0 = __dadd_rn(d0, dv);
-                            q0 = __dadd_rn(q0, __dmul_rn(dv, dv));
+                            q0 = __fma_rn(dv, dv, q0);
                             cnt += 1;
                             if (SRC != kSrcA) reinterpret_cast<float*>(xs + q)[e] = x[e];
                         }
