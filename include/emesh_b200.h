@@ -84,6 +84,15 @@ int emesh_decode_quant_chunk(const uint8_t* buf_host, uint64_t len, uint8_t* cod
 int emesh_pseudo_gradient(const float* theta_prev, const float* theta_local, float* delta, uint64_t n,
                           emesh_stream_t stream);
 
+/* optim.hpp:63-94 `adamw_step` on a flat arena (the inner step that produces
+ * theta_l): `step` = AdamWState.step AFTER the increment (>= 1); bias
+ * corrections use std::pow in double exactly as the reference. A non-finite
+ * gradient sets bit 0 of *err_flag (device word, optional) and leaves that
+ * element untouched; the caller raises NumericError. */
+int emesh_adamw_step(float* params, const float* grads, float* m, float* v, uint64_t n, uint64_t step,
+                     float inner_lr, float lr_scale, float beta1, float beta2, float eps, float weight_decay,
+                     uint32_t* err_flag, emesh_stream_t stream);
+
 /* optim.hpp:116 `nesterov_outer_step`: b = mu*b + d; theta -= lr*(d + mu*b). */
 int emesh_nesterov_outer_step(float* theta, const float* avg_delta, float* momentum_buf, uint64_t n,
                               float outer_lr, float outer_momentum, emesh_stream_t stream);

@@ -195,6 +195,38 @@ void orc_nesterov(float* theta, const float* avg, float* buf, uint64_t n, float 
     }
 }
 
+/* AdamW inner step, optim.hpp:63-94 (bias correction, decoupled decay),
+ * every fp32 operation rounded in the reference's order; `step` is the
+ * state's step AFTER the increment (optim.hpp:71). Returns ORC_ENUMERIC at
+ * the first non-finite gradient, elements before it updated (as the
+ * reference's loop leaves them). */
+int orc_adamw(float* p, const float* g, float* m, float* v, uint64_t n, uint64_t step, float inner_lr,
+              float lr_scale, float beta1, float beta2, float eps, float weight_decay) {
+    const float lr = inner_lr * lr_scale;
+    const float bc1 = (float)(1.0 - pow((double)beta1, (double)step));
+    const float bc2 = (float)(1.0 - pow((double)beta2, (double)step));
+    for (uint64_t i = 0; i < n; ++i) {
+        const float gi = g[i];
+        if (!isfinite(gi)) return ORC_ENUMERIC;
+        const float lrwd = lr * weight_decay;
+        const float dec = lrwd * p[i];
+        p[i] = p[i] - dec;
+        const float m1 = beta1 * m[i];
+        const float m2 = (1.0f - beta1) * gi;
+        m[i] = m1 + m2;
+        const float v1 = beta2 * v[i];
+        const float v2a = (1.0f - beta2) * gi;
+        const float v2 = v2a * gi;
+        v[i] = v1 + v2;
+        const float mhat = m[i] / bc1;
+        const float vhat = v[i] / bc2;
+        const float num = lr * mhat;
+        const float den = sqrtf(vhat) + eps;
+        p[i] = p[i] - num / den;
+    }
+    return ORC_OK;
+}
+
 /* ---- ring all-reduce, transport-free: allreduce.hpp:314-473 ----------
  * inputs: k pointers to n floats (worker r's ReduceJob.input, untouched).
  * out:    n floats — the result every rank ends with (they are identical,

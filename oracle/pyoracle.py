@@ -67,6 +67,8 @@ class Oracle:
         L.orc_boundary_margin.argtypes = [_f32p, C.c_uint64, C.c_double, C.c_double, C.c_double]
         L.orc_pseudo_gradient.argtypes = [_f32p, _f32p, C.c_uint64, _f32p]
         L.orc_nesterov.argtypes = [_f32p, _f32p, _f32p, C.c_uint64, C.c_float, C.c_float]
+        L.orc_adamw.restype = C.c_int
+        L.orc_adamw.argtypes = [_f32p, _f32p, _f32p, _f32p, C.c_uint64, C.c_uint64] + [C.c_float] * 6
         L.orc_ring_allreduce.restype = C.c_int
         L.orc_ring_allreduce.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_int,
                                          _f32p, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -128,6 +130,16 @@ class Oracle:
         buf = buf.copy()
         self.L.orc_nesterov(theta, np.ascontiguousarray(avg, np.float32), buf, len(theta), lr, momentum)
         return theta, buf
+
+    def adamw(self, p, g, m, v, step, inner_lr=7.5e-5, lr_scale=1.0, beta1=0.9, beta2=0.95, eps=1e-8,
+              weight_decay=0.1):
+        """optim.hpp:63-94; `step` = the state's step after the increment. Returns (p, m, v)."""
+        p, m, v = (np.array(a, np.float32, copy=True) for a in (p, m, v))
+        rc = self.L.orc_adamw(p, np.ascontiguousarray(g, np.float32), m, v, len(p), step, inner_lr, lr_scale,
+                              beta1, beta2, eps, weight_decay)
+        if rc:
+            raise OracleError(rc, "orc adamw")
+        return p, m, v
 
     # -- allreduce.hpp:314-473 (transport-free)
     def ring_allreduce(self, inputs, S=4, mode="int8", with_payloads=False):
@@ -198,6 +210,8 @@ class Reference:
         L.ref_pseudo_gradient.argtypes = [_f32p, _f32p, C.c_uint64, _f32p]
         L.ref_nesterov.restype = C.c_int
         L.ref_nesterov.argtypes = [_f32p, _f32p, _f32p, C.c_uint64, C.c_float, C.c_float]
+        L.ref_adamw.restype = C.c_int
+        L.ref_adamw.argtypes = [_f32p, _f32p, _f32p, _f32p, C.c_uint64, C.c_uint64] + [C.c_float] * 6
         L.ref_ring_allreduce_sim.restype = C.c_int
         L.ref_ring_allreduce_sim.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_int, C.c_int,
                                              _f32p, _u64p]
@@ -259,6 +273,16 @@ class Reference:
         if rc:
             raise OracleError(rc, "ref nesterov")
         return theta, buf
+
+    def adamw(self, p, g, m, v, step, inner_lr=7.5e-5, lr_scale=1.0, beta1=0.9, beta2=0.95, eps=1e-8,
+              weight_decay=0.1):
+        """emesh::adamw_step itself (state.step = step - 1 before the call)."""
+        p, m, v = (np.array(a, np.float32, copy=True) for a in (p, m, v))
+        rc = self.L.ref_adamw(p, np.ascontiguousarray(g, np.float32), m, v, len(p), step - 1, inner_lr, lr_scale,
+                              beta1, beta2, eps, weight_decay)
+        if rc:
+            raise OracleError(rc, "ref adamw")
+        return p, m, v
 
     def ring_allreduce_sim(self, inputs, S=4, mode="int8", pipelined=True):
         inputs = [np.ascontiguousarray(a, np.float32) for a in inputs]

@@ -139,6 +139,27 @@ int ref_nesterov(float* theta, const float* avg, float* buf, uint64_t n, float l
     });
 }
 
+int ref_adamw(float* p, const float* g, float* m, float* v, uint64_t n, uint64_t step_before, float inner_lr,
+              float lr_scale, float beta1, float beta2, float eps, float weight_decay) {
+    return guarded([&] {
+        HyperParams hp;
+        hp.inner_lr = inner_lr;
+        hp.beta1 = beta1;
+        hp.beta2 = beta2;
+        hp.eps = eps;
+        hp.weight_decay = weight_decay;
+        ModelParams params = single_tensor(p, n);
+        AdamWState st;
+        st.step = step_before;
+        st.m = single_tensor(m, n);
+        st.v = single_tensor(v, n);
+        adamw_step(params, single_tensor(g, n), st, hp, lr_scale);
+        std::memcpy(p, params.entries[0].second.data.data(), n * sizeof(float));
+        std::memcpy(m, st.m.entries[0].second.data.data(), n * sizeof(float));
+        std::memcpy(v, st.v.entries[0].second.data.data(), n * sizeof(float));
+    });
+}
+
 // ring_allreduce over the deterministic simulator (allreduce.hpp:314 via
 // the same driver shape as the reference test harness). outs: k*n floats.
 int ref_ring_allreduce_sim(const float* const* inputs, uint32_t k, uint64_t n, uint32_t S,

@@ -12,7 +12,7 @@ from .emesh import (  # noqa: F401
     QuantChunk, ReduceJob, ReduceMode, ReduceOptions, RingEngine, RingFailureError, RingPlan, ShapeError,
     compute_pseudo_gradient, decode_quant_chunk, dequantize, dequantize_into, encode_quant_chunk,
     nesterov_outer_step, quantize, quantize_segments, codec_check, ring_allreduce, segment_table,
-    MeshState, RetryResult, allreduce_with_retry, plan_tensor_segments,
+    MeshState, RetryResult, allreduce_with_retry, plan_tensor_segments, AdamWState, adamw_step,
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]

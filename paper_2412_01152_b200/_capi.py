@@ -20,7 +20,7 @@ EXPORTS = (
     "emesh_dequantize", "emesh_dequantize_segments",
     "emesh_encode_quant_chunk", "emesh_decode_quant_chunk",
     "emesh_pseudo_gradient", "emesh_nesterov_outer_step",
-    "emesh_plan_segments", "emesh_plan_tensor_segments", "emesh_ring_schedule", "emesh_debug_batch_runs",
+    "emesh_adamw_step", "emesh_plan_segments", "emesh_plan_tensor_segments", "emesh_ring_schedule", "emesh_debug_batch_runs",
     "emesh_nccl_unique_id", "emesh_engine_create", "emesh_engine_destroy",
     "emesh_engine_segments", "emesh_engine_ring_allreduce", "emesh_engine_outer_sync",
     "emesh_engine_outer_sync_host", "emesh_engine_check", "emesh_engine_payload", "emesh_engine_payload_host",
@@ -87,6 +87,7 @@ def lib() -> C.CDLL:
         "emesh_pseudo_gradient": (i32, [vp, vp, vp, u64, vp]),
         "emesh_nesterov_outer_step": (i32, [vp, vp, vp, u64, f32, f32, vp]),
         "emesh_plan_segments": (u64, [u64, u32, u32, vp, vp]),
+        "emesh_adamw_step": (i32, [vp, vp, vp, vp, u64, u64] + [C.c_float] * 6 + [vp, vp]),
         "emesh_plan_tensor_segments": (u64, [vp, u32, u32, u32, vp, vp]),
         "emesh_ring_schedule": (u64, [u64, u32, u32, u64, u32, vp, u64]),
         "emesh_debug_batch_runs": (u64, [u64, u32, u32, u64, u32, u32, vp, u64, vp]),

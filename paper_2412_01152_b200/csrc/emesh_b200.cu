@@ -781,6 +781,31 @@ int emesh_pseudo_gradient(const float* prev, const float* local, float* delta, u
     return EMESH_OK;
 }
 
+int emesh_adamw_step(float* params, const float* grads, float* m, float* v, uint64_t n, uint64_t step,
+                     float inner_lr, float lr_scale, float beta1, float beta2, float eps, float weight_decay,
+                     uint32_t* err_flag, emesh_stream_t stream) {
+    if (!(lr_scale >= 0.0f && lr_scale <= 1.0f)) return fail(EMESH_ECONFIG, "lr_scale must be in [0,1]");
+    if (step == 0) return fail(EMESH_ECONFIG, "adamw: step counts from 1 (the state's step after the increment)");
+    if (n == 0) return EMESH_OK;
+    if (!aligned16(params) || !aligned16(grads) || !aligned16(m) || !aligned16(v))
+        return fail(EMESH_ESHAPE, "adamw: arenas must be 16-byte aligned");
+    AdamWArgs h;
+    h.lr = inner_lr * lr_scale;  // optim.hpp:72
+    h.lrwd = h.lr * weight_decay;
+    h.b1 = beta1;
+    h.omb1 = 1.0f - beta1;
+    h.b2 = beta2;
+    h.omb2 = 1.0f - beta2;
+    h.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(beta1), static_cast<double>(step)));
+    h.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(beta2), static_cast<double>(step)));
+    h.eps = eps;
+    k_adamw<<<flat_grid(n), kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(params, grads, m, v, n, h,
+                                                                                 err_flag);
+    ++g_codec_tracker.launches;
+    CU(cudaGetLastError());
+    return EMESH_OK;
+}
+
 int emesh_nesterov_outer_step(float* theta, const float* avg, float* buf, uint64_t n, float lr, float mom,
                               emesh_stream_t stream) {
     if (n == 0) return EMESH_OK;

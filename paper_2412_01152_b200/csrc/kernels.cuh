@@ -1229,6 +1229,51 @@ __global__ void __launch_bounds__(kThreads) k_f32_apply(ApplyArgs a, const float
     }
 }
 
+// ---------------------------------------------------------------------------
+// AdamW inner step (optim.hpp:63-94), the producer of theta_l: decoupled
+// weight decay on p, bias-corrected moments, every fp32 operation rounded in
+// the reference's order (no FMA). bc1 / bc2 come from the host (std::pow in
+// double, optim.hpp:73-76). A non-finite gradient leaves its element
+// untouched and sets err bit 0 (the host raises NumericError, optim.hpp:84-85).
+struct AdamWArgs {
+    float lr, lrwd, b1, omb1, b2, omb2, bc1, bc2, eps;
+};
+
+__device__ __forceinline__ void adamw1(float& p, float g, float& m, float& v, const AdamWArgs& h) {
+    p = __fsub_rn(p, __fmul_rn(h.lrwd, p));
+    m = __fadd_rn(__fmul_rn(h.b1, m), __fmul_rn(h.omb1, g));
+    v = __fadd_rn(__fmul_rn(h.b2, v), __fmul_rn(__fmul_rn(h.omb2, g), g));
+    const float mhat = __fdiv_rn(m, h.bc1), vhat = __fdiv_rn(v, h.bc2);
+    p = __fsub_rn(p, __fdiv_rn(__fmul_rn(h.lr, mhat), __fadd_rn(__fsqrt_rn(vhat), h.eps)));
+}
+
+__global__ void __launch_bounds__(kThreads) k_adamw(float* p, const float* g, float* m, float* v, uint64_t n,
+                                                    AdamWArgs h, uint32_t* err) {
+    const uint64_t n4 = n / 4, stride = (uint64_t)gridDim.x * blockDim.x;
+    bool bad = false;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += stride) {
+        const float4 gv = __ldcs(reinterpret_cast<const float4*>(g) + q);
+        float4 pv = __ldcs(reinterpret_cast<const float4*>(p) + q);
+        float4 mv = __ldcs(reinterpret_cast<const float4*>(m) + q);
+        float4 vv = __ldcs(reinterpret_cast<const float4*>(v) + q);
+        float gg[4] = {gv.x, gv.y, gv.z, gv.w}, pp[4] = {pv.x, pv.y, pv.z, pv.w};
+        float mm[4] = {mv.x, mv.y, mv.z, mv.w}, vw[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (isfinite(gg[e])) adamw1(pp[e], gg[e], mm[e], vw[e], h);
+            else bad = true;
+        }
+        __stcs(reinterpret_cast<float4*>(p) + q, make_float4(pp[0], pp[1], pp[2], pp[3]));
+        __stcs(reinterpret_cast<float4*>(m) + q, make_float4(mm[0], mm[1], mm[2], mm[3]));
+        __stcs(reinterpret_cast<float4*>(v) + q, make_float4(vw[0], vw[1], vw[2], vw[3]));
+    }
+    for (uint64_t i = n4 * 4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        if (isfinite(g[i])) adamw1(p[i], g[i], m[i], v[i], h);
+        else bad = true;
+    }
+    if (bad && err) atomicOr(err, 1u);
+}
+
 // Peer transport: raise the arrival flags of slots [slot0, slot0 + n) on a
 // peer after the copy engine delivered their bytes (stream-ordered before).
 __global__ void k_set_flags(uint32_t* flags, uint32_t slot0, uint32_t n, uint32_t epoch) {

@@ -301,6 +301,39 @@ class NesterovState:
         return NesterovState(params.zeros_like())
 
 
+@dataclass
+class AdamWState:
+    """optim.hpp:35-46"""
+
+    step: int
+    m: ModelParams
+    v: ModelParams
+
+    @staticmethod
+    def zeros_like(params: ModelParams) -> "AdamWState":
+        return AdamWState(0, params.zeros_like(), params.zeros_like())
+
+
+def adamw_step(params: ModelParams, grads: ModelParams, state: AdamWState, hp: HyperParams, lr_scale: float,
+               stream=None) -> None:
+    """optim.hpp:63-94 — one AdamW step on the device arenas (bit-exact fp32),
+    the inner step whose result becomes theta_l for the next outer sync."""
+    if not params.same_shapes(grads):
+        raise ShapeError("adamw_step: params/grads shape mismatch")
+    if not params.same_shapes(state.m) or not params.same_shapes(state.v):
+        raise ShapeError("adamw_step: optimizer state shape mismatch")
+    if not (0.0 <= lr_scale <= 1.0):
+        raise ConfigError("lr_scale must be in [0,1]")
+    state.step += 1
+    err = torch.zeros(1, dtype=torch.int32, device=params.arena.device)
+    _check(_capi.lib().emesh_adamw_step(params.arena.data_ptr(), grads.arena.data_ptr(), state.m.arena.data_ptr(),
+                                        state.v.arena.data_ptr(), params.element_count(), state.step, hp.inner_lr,
+                                        lr_scale, hp.beta1, hp.beta2, hp.eps, hp.weight_decay, err.data_ptr(),
+                                        _stream(stream)))
+    if int(err.item()):
+        raise NumericError("non-finite gradient")
+
+
 def compute_pseudo_gradient(theta_prev: ModelParams, theta_local: ModelParams, stream=None) -> ModelParams:
     """optim.hpp:99 — delta = theta_prev - theta_local (fp32, canonical order)."""
     if not theta_prev.same_shapes(theta_local):

@@ -176,3 +176,40 @@ def test_nesterov_known_answers(E):
     assert b == 1.0 and abs(th - 8.67) <= 8.67 * 1e-6
     assert one(3.0, 0.5, 1.0, 0.0)[0] == 2.5  # :115-124
     assert one(2.0, 0.0, 0.7, 0.9)[0] == 2.0  # :139-145
+
+
+# ---------------------------------------------------------------- AdamW (optim.hpp:63-94)
+
+
+@pytest.mark.parametrize("n", [1, 5, 4096, 300_007])
+def test_adamw_vs_oracle_steps(E, oracle, n):
+    """Three AdamW steps with a warm-up lr_scale: params, moments bit-exact vs the oracle (pinned to the
+    reference's adamw_step in tests/test_oracle_pinned.py)."""
+    p0 = oracle.uniform(n, 11, 0)
+    shapes = {"w": (n,)}
+    params = E.ModelParams(shapes)
+    params.arena.copy_(torch.from_numpy(p0))
+    st = E.AdamWState.zeros_like(params)
+    hp = E.HyperParams()
+    ep, em, ev = p0, np.zeros(n, np.float32), np.zeros(n, np.float32)
+    for step in range(1, 4):
+        g = oracle.uniform(n, 20 + step, 0, 0, 0, 1e-2)
+        grads = E.ModelParams(shapes)
+        grads.arena.copy_(torch.from_numpy(g))
+        E.adamw_step(params, grads, st, hp, lr_scale=0.25 * step)
+        ep, em, ev = oracle.adamw(ep, g, em, ev, step, hp.inner_lr, 0.25 * step, hp.beta1, hp.beta2, hp.eps,
+                                  hp.weight_decay)
+        assert st.step == step
+        for got, want in ((params.arena, ep), (st.m.arena, em), (st.v.arena, ev)):
+            assert np.array_equal(got.cpu().numpy().view(np.uint32), want.view(np.uint32)), step
+
+
+def test_adamw_nonfinite_gradient_raises(E):
+    params = E.ModelParams({"w": (8,)})
+    grads = E.ModelParams({"w": (8,)})
+    grads.arena[3] = float("nan")
+    st = E.AdamWState.zeros_like(params)
+    with pytest.raises(E.NumericError):
+        E.adamw_step(params, grads, st, E.HyperParams(), 1.0)
+    with pytest.raises(E.ConfigError):
+        E.adamw_step(params, E.ModelParams({"w": (8,)}), st, E.HyperParams(), 1.5)

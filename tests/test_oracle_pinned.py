@@ -125,3 +125,26 @@ def test_oracle_vs_compiled_reference_live(oracle):
     a, _ = R.ring_allreduce_sim(ins, 4, "int8", True)
     b, _ = R.ring_allreduce_sim(ins, 4, "int8", False)
     assert np.array_equal(bits(a), bits(b))
+
+
+@pytest.mark.skipif(not have_reference(), reason="oracle/_ref not built (needs /root/reference)")
+def test_adamw_oracle_vs_compiled_reference(oracle):
+    """optim.hpp:63-94: the restated AdamW step equals emesh::adamw_step bit for bit."""
+    R = Reference()
+    n = 20_011
+    p = oracle.uniform(n, 1, 0)
+    m = oracle.uniform(n, 2, 0, 0, 0, 1e-3)
+    v = np.abs(oracle.uniform(n, 3, 0, 0, 0, 1e-5)).astype(np.float32)
+    for step, scale in ((1, 1.0), (2, 0.5), (37, 0.01), (5000, 1.0)):
+        g = oracle.uniform(n, 10 + step, 0, 0, 0, 1e-2)
+        a = oracle.adamw(p, g, m, v, step, 7.5e-5, scale)
+        b = R.adamw(p, g, m, v, step, 7.5e-5, scale)
+        for x, y in zip(a, b):
+            assert np.array_equal(bits(x), bits(y)), step
+        p, m, v = a
+    g = np.zeros(n, np.float32)
+    g[7] = np.inf
+    with pytest.raises(OracleError):
+        oracle.adamw(p, g, m, v, 1)
+    with pytest.raises(OracleError):
+        R.adamw(p, g, m, v, 1)
