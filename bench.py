@@ -34,7 +34,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=float, default=1e9, help="params per worker (config 2: 1B)")
+    ap.add_argument("--params", "--n-params", dest="n", type=float, default=1e9, help="params per worker (config 2: 1B)")
     ap.add_argument("--workers", type=int, default=0, help="DiLoCo workers k (default: 4 at N=1, N otherwise)")
     ap.add_argument("--S", type=int, default=16, help="ReduceOptions.pipeline_subchunks")
     ap.add_argument("--window", type=float, default=0, help="pipelining window elems (0=auto)")
@@ -226,16 +226,23 @@ def main():
                        virtual=virtual, nccl_id=nccl_id, window_elems=int(args.window), transport=args.transport)
     W = eng.workers
     # synthetic replicas: theta_g ~ U[-1,1), theta_l = theta_g - 2^-10 U, b = 0
+    # (generated in 64M-element slices: no full-size temporaries, so 10B-param workers fit in HBM)
     gen = torch.Generator(device=dev)
-    gen.manual_seed(1)
-    base = (torch.rand(n, generator=gen, device=dev) * 2 - 1)
     tg, tl, tb = [], [], []
+    slab = 1 << 26
     for w in range(W):
-        gen.manual_seed(100 + rank * W + w)
-        tg.append(base.clone())
-        tl.append(base - (torch.rand(n, generator=gen, device=dev) * 2 - 1) * (2.0 ** -10))
-        tb.append(torch.zeros(n, device=dev))
-    del base
+        g_w = torch.empty(n + 4, device=dev)[:n]
+        l_w = torch.empty(n + 4, device=dev)[:n]
+        for lo in range(0, n, slab):
+            hi = min(n, lo + slab)
+            gen.manual_seed(1 + lo)
+            g_w[lo:hi].uniform_(-1.0, 1.0, generator=gen)
+            gen.manual_seed(100 + rank * W + w + (lo << 8))
+            l_w[lo:hi].uniform_(-1.0, 1.0, generator=gen)
+            l_w[lo:hi].mul_(-(2.0 ** -10)).add_(g_w[lo:hi])
+        tg.append(g_w)
+        tl.append(l_w)
+        tb.append(torch.zeros(n + 4, device=dev)[:n])
     hp = E.HyperParams()
     stream = torch.cuda.current_stream()
 
