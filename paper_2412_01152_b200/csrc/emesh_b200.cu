@@ -216,7 +216,7 @@ uint32_t quant_lag_tiles() {
     const int g = persistent_grid((const void*)k_quant<kSrcAminusB | kHasIn>, 1u << 30);
     static const double mult = [] {
         const char* e = std::getenv("EMESH_QUANT_LAG");  // tuning knob, in persistent grids
-        return e ? std::atof(e) : 2.0;
+        return e ? std::atof(e) : 1.5;
     }();
     return (uint32_t)(std::max(1.0, mult * (g > 0 ? g : 512)));
 }

@@ -396,7 +396,7 @@ struct QSmem {
 
 // Task order (host-built run table, QuantArgs::runs): the STATS tiles of
 // the batch in segment order; the BIN tiles of segment s once `lag` more
-// tasks were issued after its last STATS tile (lag ~ 2 grids: the segment's
+// tasks were issued after its last STATS tile (lag ~ 1.5 grids: the segment's
 // statistics are normally published before its bins are claimed, and a
 // tile's scratch x is re-read soon enough to still be in L2). The last STATS
 // tile of s to finish finalizes SegStat(s); the last BIN tile of s to finish
