@@ -18,6 +18,13 @@ def build_oracle() -> None:
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), *targets], check=True)
 
 
+def build_cpp_checks() -> None:
+    # the C++ drop-in check compiles against the reference headers (this container only)
+    if os.path.isdir("/root/reference/proj/include/emesh"):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+
+
 if __name__ == "__main__":
     build_product()
     build_oracle()
+    build_cpp_checks()
