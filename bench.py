@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=float, default=16e6, help="params per worker in the CPU sample")
     ap.add_argument("--profile-only", action="store_true", help="1 warm round + 1 round, no JSON (for ncu)")
+    ap.add_argument("--tensors", default="flat", choices=["flat", "intellect1"],
+                    help="flat arena (trainer semantics) or config 5: one ReduceJob per tensor of the "
+                         "381-tensor INTELLECT-1 list (10.2B params; --params is then ignored)")
     return ap.parse_args()
 
 
@@ -172,8 +175,11 @@ def run_reference(args, rank, world):
 
 
 def config_block(args, k, n, transport=None):
-    return {"workload": f"config 2: DiLoCo outer sync of a {n / 1e9:.3g}B-param synthetic model, {k} workers, "
-                        "int8 ring all-reduce + Nesterov (lr=0.7, mu=0.9)",
+    five = getattr(args, "tensors", "flat") == "intellect1"
+    return {"workload": (f"config 5: multi-tensor outer sync, one ReduceJob per tensor of the 381-tensor "
+                         f"INTELLECT-1 shape ({n / 1e9:.3g}B params), {k} workers, int8 ring + Nesterov" if five else
+                         f"config 2: DiLoCo outer sync of a {n / 1e9:.3g}B-param synthetic model, {k} workers, "
+                         "int8 ring all-reduce + Nesterov (lr=0.7, mu=0.9)"),
             "params_per_worker": n, "workers": k, "pipeline_subchunks": args.S,
             "ring": ("reference CPU ring_allreduce over TcpEnv loopback (k node threads)" if transport == "reference"
                      else "virtual (all workers on 1 GPU, zero-copy hand-off)" if args.gpus == 1 and k > 1
@@ -182,6 +188,15 @@ def config_block(args, k, n, transport=None):
                      else "NCCL send/recv over NVLink, one worker per GPU"),
             "l2": "inputs larger than L2 (>= 12 B/param x n per worker)",
             "write_local": False}
+
+
+def intellect1_tensor_sizes():
+    """42 layers, d=4096, 32/8 heads (kv 1024), FFN 14336, vocab 128256, untied."""
+    d, kv, ffn, vocab = 4096, 1024, 14336, 128256
+    sizes = [vocab * d]
+    for _ in range(42):
+        sizes += [d, d * d, d * kv, d * kv, d * d, d, d * ffn, d * ffn, ffn * d]
+    return sizes + [d, vocab * d]
 
 
 def alg_bytes_per_param(k):
@@ -211,7 +226,8 @@ def main():
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    n = int(args.n)
+    sizes = intellect1_tensor_sizes() if args.tensors == "intellect1" else None
+    n = sum(sizes) if sizes else int(args.n)
     k = args.workers or (4 if world == 1 else world)
     virtual = world == 1 and k > 1
     if not virtual and k != world:
@@ -223,7 +239,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     eng = E.RingEngine(n, k, rank=rank if not virtual else 0, opts=E.ReduceOptions(pipeline_subchunks=args.S),
-                       virtual=virtual, nccl_id=nccl_id, window_elems=int(args.window), transport=args.transport)
+                       virtual=virtual, nccl_id=nccl_id, window_elems=int(args.window), transport=args.transport,
+                       tensor_sizes=sizes)
     W = eng.workers
     # synthetic replicas: theta_g ~ U[-1,1), theta_l = theta_g - 2^-10 U, b = 0
     # (generated in 64M-element slices: no full-size temporaries, so 10B-param workers fit in HBM)
