@@ -1230,10 +1230,13 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
 // hop's quantizer waits segment by segment. The owner's final payload goes
 // to every rank at once, which replaces the all-gather's k-1 forwarding hops
 // (the bytes are identical: AG forwards them verbatim, allreduce.hpp:446-464).
-// Above this many contiguous runs in the final chunk (multi-tensor plans),
-// the owner's quantizer stores its final payload to every rank itself
-// instead of one DMA per run and peer.
+// The owner's quantizer stores its final payload to every rank itself
+// (instead of the copy engines) when the final chunk has many contiguous runs
+// (multi-tensor plans: one DMA per run and peer) or is small (the DMA
+// commands' fixed cost would dominate).
 constexpr size_t kMaxDmaRuns = 16;
+constexpr uint64_t kMinDmaElems = (uint64_t)32 << 20;
+bool push_final_payload(const Batch& fb) { return fb.eruns.size() > kMaxDmaRuns || fb.elems < kMinDmaElems; }
 
 // Owner's final chunk -> every other rank by DMA (see run_p2p), in segment
 // groups, each followed by its arrival flags.
@@ -1285,7 +1288,7 @@ int run_p2p_f32(emesh_engine* e, const float* A, const float* B, float* theta, f
     const int par = (int)(ep & 1u);
     cudaStream_t sc = e->s_comp;
     const auto& P = e->plan.batches;
-    const bool push_final = P[succ][0].eruns.size() > kMaxDmaRuns;
+    const bool push_final = push_final_payload(P[succ][0]);
     {
         F32IO io{A, B, nullptr};
         io.ndest = 1;
@@ -1330,7 +1333,7 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
             float lr, float mom) {
     if (e->fp32) return run_p2p_f32(e, A, B, theta, buf, local_out, out, lr, mom);
     const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
-    const bool push_final = e->plan.batches[succ][0].eruns.size() > kMaxDmaRuns;
+    const bool push_final = push_final_payload(e->plan.batches[succ][0]);
     const bool pg = B != nullptr;
     const uint32_t ep = ++e->epoch;
     const int par = (int)(ep & 1u);

@@ -1,3 +1,5 @@
-mkdir -p gpurun_out/r01c
-timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29553 bench.py --gpus 4 --tensors intellect1 --S 4 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r01c/bench_n4_cfg5.json.log 2> gpurun_out/r01c/bench_n4_cfg5.err; echo "cfg5 rc=$?"
-tail -c 700 gpurun_out/r01c/bench_n4_cfg5.json.log
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29541 tests/nccl_parity_worker.py 2>&1 | grep -E "MISMATCH|asked|parity|Error" | head -10
+timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29552 tools/sweep_msg.py 1073741824 5 2>/dev/null | grep '^{' | python -c "
+import json,sys
+for l in sys.stdin:
+    d=json.loads(l); print(f\"{d['fp32_MB']:7.0f} MB  int8 {d['ours_int8_ms']:7.3f}  fp32 {d['ours_fp32_ms']:7.3f}  nccl {d['nccl_fp32_ms']:7.3f}\")"
