@@ -66,6 +66,7 @@ struct Seg {
 
 uint32_t quant_lag_tiles();
 bool bin_reverse();
+bool quant_mix();
 
 // One pipelining window: consecutive segments of one rank chunk.
 struct Batch {
@@ -137,35 +138,79 @@ struct Plan {
         }
         b.ncta = (uint32_t)cseg.size();
         // persistent-kernel task order (see kernels.cuh): STATS tiles in
-        // segment order; the BIN tiles of s once `lag` more tasks were issued
-        // after its last STATS tile. Runs {first task, kind, segment, first tile}.
+        // segment order; the BIN tiles of s (in reverse tile order: the most
+        // recently written scratch is re-read first, while still in L2) become
+        // available `lag` tasks after its last STATS tile and are then
+        // interleaved 1:1 with the following STATS tiles, so every SM always
+        // runs a mix of the HBM-bound STATS and the issue-bound BIN work.
+        // Compressed into runs {first task, kind | bin segment << 2, segment,
+        // first tile}: plain runs (one kind) and mixed runs (S, B, S, B, ...).
         std::vector<uint4> runs;
         {
             const uint32_t lag = quant_lag_tiles();
-            uint32_t issued = 0;
-            std::vector<std::pair<uint32_t, uint32_t>> bins;  // (segment, issue position that releases it)
+            struct Task { uint32_t kind, seg, tile; };
+            std::vector<Task> order;
+            order.reserve(2 * (size_t)b.ncta);
+            struct Pending { uint32_t seg, next, left, at; };
+            std::vector<Pending> bq;
             size_t hb = 0;
-            auto release = [&](bool all) {
-                while (hb < bins.size() && (all || issued >= bins[hb].second)) {
-                    const uint32_t seg = bins[hb++].first;
-                    // bins run in reverse tile order: the most recently written scratch
-                    // (the segment's last stats tiles) is re-read while still in L2
-                    runs.push_back(make_uint4(issued, kTaskBin, seg,
-                                              bin_reverse() ? 0x80000000u | (infos[seg].ncta - 1) : 0u));
-                    issued += infos[seg].ncta;
-                }
+            const bool mix = quant_mix();
+            auto bin_ready = [&]() { return hb < bq.size() && order.size() >= bq[hb].at; };
+            auto pop_bin = [&]() {
+                Pending& pb = bq[hb];
+                order.push_back({kTaskBin, pb.seg, pb.next});
+                if (bin_reverse()) --pb.next; else ++pb.next;
+                if (--pb.left == 0) ++hb;
             };
             for (uint32_t i = 0; i < infos.size(); ++i) {
                 for (uint32_t t = 0; t < infos[i].ncta; ++t) {
-                    const bool extend = t > 0 && runs.back().y == kTaskStats && runs.back().z == i;
-                    if (!extend) runs.push_back(make_uint4(issued, kTaskStats, i, t));
-                    ++issued;
-                    release(false);
+                    order.push_back({kTaskStats, i, t});
+                    if (mix) {
+                        if (bin_ready()) pop_bin();
+                    } else {  // whole-segment BIN blocks (no interleaving)
+                        while (bin_ready()) pop_bin();
+                    }
                 }
-                if (infos[i].ncta) bins.push_back({i, issued + lag});
+                if (infos[i].ncta)
+                    bq.push_back({i, bin_reverse() ? infos[i].ncta - 1 : 0u, infos[i].ncta,
+                                  (uint32_t)order.size() + lag});
             }
-            release(true);
-            b.ntasks = issued;
+            while (hb < bq.size()) pop_bin();
+            b.ntasks = (uint32_t)order.size();
+            const int dir = bin_reverse() ? -1 : 1;
+            size_t p0 = 0;
+            while (p0 < order.size()) {
+                const Task& t0 = order[p0];
+                // mixed run: S(a, i), B(b, j), S(a, i+1), B(b, j+dir), ...
+                size_t q = p0;
+                if (t0.kind == kTaskStats && p0 + 1 < order.size() && order[p0 + 1].kind == kTaskBin) {
+                    const Task& t1 = order[p0 + 1];
+                    while (q + 1 < order.size()) {
+                        const uint32_t i = (uint32_t)((q - p0) / 2);
+                        const Task& s0 = order[q];
+                        const Task& s1 = order[q + 1];
+                        if (s0.kind != kTaskStats || s0.seg != t0.seg || s0.tile != t0.tile + i) break;
+                        if (s1.kind != kTaskBin || s1.seg != t1.seg || (int64_t)s1.tile != (int64_t)t1.tile + dir * (int64_t)i) break;
+                        q += 2;
+                    }
+                    if (q - p0 >= 4 && t0.tile < 0x10000u && t1.tile < 0x10000u) {
+                        runs.push_back(make_uint4((uint32_t)p0, (dir < 0 ? kTaskMixRev : kTaskMixFwd) | (t1.seg << 2), t0.seg,
+                                                  t0.tile | (t1.tile << 16)));
+                        p0 = q;
+                        continue;
+                    }
+                    q = p0;
+                }
+                // plain run of one kind and segment, tiles +1 (STATS) / +dir (BIN)
+                const int step = t0.kind == kTaskBin ? dir : 1;
+                q = p0 + 1;
+                while (q < order.size() && order[q].kind == t0.kind && order[q].seg == t0.seg &&
+                       (int64_t)order[q].tile == (int64_t)t0.tile + step * (int64_t)(q - p0))
+                    ++q;
+                runs.push_back(make_uint4((uint32_t)p0, t0.kind, t0.seg,
+                                          step < 0 ? 0x80000000u | t0.tile : t0.tile));
+                p0 = q;
+            }
         }
         b.nruns = (uint32_t)runs.size();
 
@@ -205,6 +250,13 @@ int persistent_grid(const void* fn, uint32_t ntasks);
 // Lag between a segment's last STATS tile and its first BIN tile in the task
 // order: one persistent grid (the stats root publishes within about one
 // tile time; longer lags push scratch x out of L2).
+bool quant_mix() {
+    static const bool r = [] {
+        const char* e = std::getenv("EMESH_QUANT_MIX");  // tuning knob
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    return r;
+}
 bool bin_reverse() {
     static const bool r = [] {
         const char* e = std::getenv("EMESH_BIN_REVERSE");  // tuning knob

@@ -407,6 +407,9 @@ struct QSmem {
 // [kSyncReady + nseg + s] STATS tiles done, [kSyncReady + 2 nseg + s] BIN tiles done.
 constexpr uint32_t kSyncReady = 32;
 enum : uint32_t { kTaskStats = 0, kTaskBin = 2 };
+// mixed run (alternating STATS / BIN tasks): y = kTaskMix{Rev,Fwd} | bin segment << 2,
+// z = STATS segment, w = first STATS tile | first BIN tile << 16
+constexpr uint32_t kTaskMixRev = 1, kTaskMixFwd = 3;
 constexpr uint32_t kMaxRunsSmem = 512;  // run table cached in smem when it fits (8 KB)
 constexpr uint32_t kMaxSegsSmem = 128;  // SegInfo cached in smem when it fits (6 KB)
 
@@ -919,6 +922,27 @@ __device__ float codebook_entry(const SegStat* st, int b, unsigned long long rl,
     return (float)__ddiv_rn(sum, (double)total);
 }
 
+// Task t of run r -> (kind, segment, tile).
+__device__ __forceinline__ void decode_run(const uint4 r, uint32_t t, uint32_t& kind, uint32_t& s, uint32_t& tile) {
+    const uint32_t off = t - r.x, k = r.y & 3u;
+    if (k == kTaskMixRev || k == kTaskMixFwd) {
+        const uint32_t i = off >> 1;
+        if (off & 1u) {
+            kind = kTaskBin;
+            s = r.y >> 2;
+            tile = k == kTaskMixRev ? (r.w >> 16) - i : (r.w >> 16) + i;
+        } else {
+            kind = kTaskStats;
+            s = r.z;
+            tile = (r.w & 0xffffu) + i;
+        }
+    } else {
+        kind = r.y;
+        s = r.z;
+        tile = (r.w & 0x80000000u) ? (r.w & 0x7fffffffu) - off : r.w + off;
+    }
+}
+
 template <int SRC>
 __global__ void __launch_bounds__(kThreads, EMESH_QUANT_MINB) k_quant(QuantArgs a) {
     extern __shared__ __align__(16) unsigned char qsmem_raw[];
@@ -953,20 +977,14 @@ __global__ void __launch_bounds__(kThreads, EMESH_QUANT_MINB) k_quant(QuantArgs 
                 const uint32_t mid = (lo + hi) >> 1;
                 if (runs_s[mid].x <= t) lo = mid; else hi = mid;
             }
-            const uint4 r = runs_s[lo];
-            kind = r.y;
-            s = r.z;
-            tile = (r.w & 0x80000000u) ? (r.w & 0x7fffffffu) - (t - r.x) : r.w + (t - r.x);
+            decode_run(runs_s[lo], t, kind, s, tile);
         } else {
             uint32_t lo = 0, hi = a.nruns;
             while (hi - lo > 1) {
                 const uint32_t mid = (lo + hi) >> 1;
                 if (a.runs[mid].x <= t) lo = mid; else hi = mid;
             }
-            const uint4 r = a.runs[lo];
-            kind = r.y;
-            s = r.z;
-            tile = (r.w & 0x80000000u) ? (r.w & 0x7fffffffu) - (t - r.x) : r.w + (t - r.x);
+            decode_run(a.runs[lo], t, kind, s, tile);
         }
         const SegInfo si = segs_in_smem ? segs_s[s] : a.segs[s];
         unsigned long long t0 = 0, t1 = 0;

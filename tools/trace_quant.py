@@ -63,3 +63,10 @@ tot = dur.sum()
 for kd, nm in ((0, "stats"), (1, "root"), (2, "bin"), (3, "cb")):
     msk = rec["kind"] == kd
     print(f"  {nm:5s} share of task time {dur[msk].sum() / tot:.3f} (waiting {wait[msk].sum() / tot:.3f})")
+# kind mix over time inside the longest launch: share of running tasks that are STATS
+kinds = rec["kind"][b:e]
+mix = []
+for x in grid:
+    run = (g[:, 0] <= x) & (g[:, 3] > x)
+    mix.append(round(float((kinds[run] == 0).mean()), 2) if run.any() else None)
+print("STATS share of running tasks over the longest launch:", mix)
