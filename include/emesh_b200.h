@@ -163,9 +163,12 @@ typedef struct {
 uint64_t emesh_ring_schedule(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems, uint32_t rank,
                              emesh_ring_op* ops, uint64_t max_ops);
 
-/* Development aid: the persistent quantizer's task plan (runs of {first task,
- * kind 0 stats / 1 root / 2 bin / 3 codebook, segment, first tile}) for one
- * batch; info = {ntasks, ncta, nseg, ncta of each segment...}. Host-only. */
+/* Development aid: the persistent quantizer's task plan for one batch, as
+ * runs of {first task, kind, segment, first tile}: kind 0 = STATS tiles,
+ * 2 = BIN tiles (first tile | 1<<31 = descending), 1 / 3 = mixed run of
+ * alternating STATS / BIN tasks (kind | BIN segment << 2; STATS segment;
+ * first STATS tile | first BIN tile << 16; BIN tiles descending / ascending);
+ * info = {ntasks, ncta, nseg, ncta of each segment...}. Host-only. */
 uint64_t emesh_debug_batch_runs(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems, uint32_t chunk,
                                 uint32_t window, uint32_t* runs4, uint64_t max_runs, uint32_t* info);
 

@@ -38,7 +38,7 @@ wait = (t[:, 1] - t[:, 0]) / 1e3
 main = (t[:, 2] - t[:, 1]) / 1e3
 epi = (t[:, 3] - t[:, 2]) / 1e3
 print(f"n={n} S={S}: records {m}; span {(t[:, 3].max() - t0) / 1e3:.1f} us")
-for kd, nm in ((0, "stats"), (1, "root"), (2, "bin"), (3, "cb")):
+for kd, nm in ((0, "stats"), (2, "bin")):
     msk = rec["kind"] == kd
     if msk.sum() == 0:
         continue
@@ -60,7 +60,7 @@ conc = [int(((g[:, 0] <= x) & (g[:, 3] > x)).sum()) for x in grid]
 print("concurrent tasks over the longest launch:", conc)
 # time-weighted breakdown: SM-time spent per kind and in waits
 tot = dur.sum()
-for kd, nm in ((0, "stats"), (1, "root"), (2, "bin"), (3, "cb")):
+for kd, nm in ((0, "stats"), (2, "bin")):
     msk = rec["kind"] == kd
     print(f"  {nm:5s} share of task time {dur[msk].sum() / tot:.3f} (waiting {wait[msk].sum() / tot:.3f})")
 # kind mix over time inside the longest launch: share of running tasks that are STATS
