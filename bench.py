@@ -199,6 +199,19 @@ def intellect1_tensor_sizes():
     return sizes + [d, vocab * d]
 
 
+def nvlink_block(world, k, n, S, ms, transport):
+    """per GPU per direction, the ring moves 2(k-1)/k B/param of codes + 2(k-1) S 1028 B of
+    codebooks per round; averaged over the round (the transfers overlap the kernels, so this is a floor,
+    not the link's busy rate). NVLink 5: 900 GB/s per direction per GPU."""
+    if world < 2:
+        return None
+    by = 2 * (k - 1) / k * n + 2 * (k - 1) * S * 1028
+    gbs = by / (ms / 1e3) / 1e9
+    return {"bytes_per_gpu_per_round": int(by), "avg_GBps_per_direction": round(gbs, 1), "peak_GBps": 900.0,
+            "frac_of_round": round(gbs / 900.0, 4), "transport": transport,
+            "note": "ring traffic averaged over the whole round; it overlaps the quantize/decode kernels"}
+
+
 def alg_bytes_per_param(k):
     # SURVEY §8(d): A(1) = 20, A(k>=2) = 24 + (2k-1)/k + 1 (theta_l write excluded)
     return 20.0 if k == 1 else 24.0 + (2 * k - 1) / k + 1.0
@@ -397,6 +410,7 @@ def main():
             "hbm_alg_GBps_per_gpu": round(step_alg_gbs, 1),
             "hbm_frac_step": round(step_alg_gbs / hbm_peak, 4),
             "roofline": roofline, "roofline_other_kernels": roofline_others, "kernels": kernels,
+            "nvlink": nvlink_block(world, k, n, args.S, ms, eng.transport),
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk.summary(),
         }
