@@ -235,10 +235,11 @@ uint64_t emesh_trace_read(void* host, uint64_t max_records);
 uint64_t emesh_engine_launches(const emesh_engine* e);
 
 /* Per-kernel profiling with CUDA events on the launching stream. enable
- * resets the record. kind: 0 k_stats, 1 k_bin, 2 hop-0 quantize pair,
- * 3 RS hop pair, 4 owner-final pair, 5 plain quantize pair, 6 dequant +
- * Nesterov, 7 dequantize, 8 k==1 fused PG+Nesterov. Reads launches, total
- * device ms and total ALGORITHMIC bytes of that kind. */
+ * resets the record. kind: 0, 1 reserved, 2 hop-0 quantize, 3 RS hop
+ * quantize, 4 owner-final quantize, 5 plain quantize, 6 dequant + Nesterov,
+ * 7 dequantize, 8 k==1 fused PG+Nesterov, 9 fp32-mode hop, 10 fp32-mode
+ * decode (+ Nesterov). Reads launches, total device ms and total
+ * ALGORITHMIC bytes of that kind. */
 int emesh_engine_profile(emesh_engine* e, int enable);
 int emesh_engine_profile_read(emesh_engine* e, uint32_t kind, uint64_t* launches, double* ms, double* alg_bytes);
 

@@ -446,12 +446,11 @@ struct QuantIO {
 };
 
 enum ProfKind : int {
-    kProfStats = 0,      // k_stats (all producers)
-    kProfBin = 1,        // k_bin
-    kProfQuantPG = 2,    // k_stats+k_bin, hop-0 payload Q(theta_g - theta_l)
-    kProfQuantHop = 3,   // k_stats+k_bin, reduce-scatter hop (dequant-add-requant)
-    kProfQuantFinal = 4, // k_stats+k_bin, owner mean (/k) + quantize
-    kProfQuantPlain = 5, // k_stats+k_bin, plain buffer
+    // 0, 1: reserved (the round-1 two-kernel quantizer's separate passes)
+    kProfQuantPG = 2,    // k_quant, hop-0 payload Q(theta_g - theta_l)
+    kProfQuantHop = 3,   // k_quant, reduce-scatter hop (dequant-add-requant)
+    kProfQuantFinal = 4, // k_quant, owner mean (/k) + quantize
+    kProfQuantPlain = 5, // k_quant, plain buffer
     kProfNesterov = 6,   // k_apply<1>: dequant + Nesterov (+ theta_l write)
     kProfDequant = 7,    // k_apply<0>
     kProfFusedK1 = 8,    // k_nesterov_f32 (k == 1: PG + Nesterov)

@@ -207,14 +207,6 @@ __device__ __forceinline__ float4 ld4_stream(const float* p, uint64_t q) {
 __device__ __forceinline__ float4 ld4(const float* p, uint64_t q) {
     return __ldg(reinterpret_cast<const float4*>(p) + q);
 }
-__device__ __forceinline__ float f4get(const float4& v, int e) {
-    return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
-}
-__device__ __forceinline__ double warp_sum_d(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
 __device__ __forceinline__ uint32_t warp_sum_u(uint32_t v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -244,9 +236,6 @@ __device__ __forceinline__ void red_shared_add(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ void red_shared_add_nz(uint32_t* p, uint32_t v) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q red.shared.add.u32 [%0], %1;\n\t}"
                  ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ void spin_until_nonzero(const uint32_t* p) {
-    while (ld_acquire(p) == 0u) __nanosleep(32);
 }
 // Cross-GPU signalling (peer transport): flags live in the receiver's memory.
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {

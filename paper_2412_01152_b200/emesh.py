@@ -539,8 +539,8 @@ class RingEngine:
     def launches(self) -> int:
         return int(_capi.lib().emesh_engine_launches(self._h))
 
-    PROFILE_KINDS = ("k_stats", "k_bin", "quant_pg", "quant_hop", "quant_final", "quant_plain",
-                     "dequant_nesterov", "dequantize", "fused_pg_nesterov_k1")
+    PROFILE_KINDS = ("reserved0", "reserved1", "quant_pg", "quant_hop", "quant_final", "quant_plain",
+                     "dequant_nesterov", "dequantize", "fused_pg_nesterov_k1", "f32_hop", "f32_apply")
 
     def profile(self, enable: bool = True) -> None:
         """Per-kernel CUDA-event timing on the engine's launching stream."""
