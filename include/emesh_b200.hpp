@@ -232,6 +232,7 @@ public:
         cfg.transport = EMESH_TRANSPORT_AUTO;
         cfg.reduce_fp32 = mode == ReduceMode::fp32 ? 1u : 0u;
         cfg.step_timeout_s = opts.step_timeout;
+        S_ = opts.pipeline_subchunks ? opts.pipeline_subchunks : 4;
         check(emesh_engine_create(&cfg, &e_));
     }
     RingEngine(const RingEngine&) = delete;
@@ -299,8 +300,41 @@ public:
         }
     }
 
+    // Wire interop: the reference's wire payload of every
+    // segment of chunk c after the last round, i.e. encode_slice(mean, int8)
+    // (allreduce.hpp:153-157, quant.hpp:102-131) — the bytes the reference's
+    // all-gather forwards, ready for ring_detail::encode_chunk_msg over TCP.
+    std::vector<Bytes> final_payloads(uint32_t chunk, uint32_t worker = 0) const {
+        if (mode_ != ReduceMode::int8) throw ConfigError("final_payloads: int8 engines only");
+        if (chunk >= k_) throw ShapeError("final_payloads: no such chunk");
+        const uint64_t nseg = emesh_engine_segments(e_, nullptr, nullptr);
+        std::vector<uint64_t> lo(nseg), len(nseg);
+        emesh_engine_segments(e_, lo.data(), len.data());
+        std::vector<uint8_t> codes(n_ + 16);
+        std::vector<float> cbs(nseg * QuantChunk::kBuckets);
+        check(emesh_engine_payload_host(e_, worker, codes.data(), cbs.data(), nullptr));
+        // chunk-major segment table: chunk c holds split(n, k)[c] cut into min(S, len) subs
+        uint64_t first = 0;
+        for (uint32_t c = 0; c < chunk; ++c) first += subs_in_chunk(c);
+        std::vector<Bytes> out;
+        for (uint64_t s = first; s < first + subs_in_chunk(chunk); ++s) {
+            if (len[s] == 0) { out.emplace_back(); continue; }  // empty slices travel empty (allreduce.hpp:153)
+            QuantChunk q;
+            q.codebook.assign(cbs.begin() + s * QuantChunk::kBuckets, cbs.begin() + (s + 1) * QuantChunk::kBuckets);
+            q.indices.assign(codes.begin() + lo[s], codes.begin() + lo[s] + len[s]);
+            out.push_back(b200::encode_quant_chunk(q));
+        }
+        return out;
+    }
+
 private:
+    uint64_t subs_in_chunk(uint32_t c) const {
+        const uint64_t clen = n_ / k_ + (c < n_ % k_ ? 1 : 0);
+        return clen == 0 ? 1 : std::min<uint64_t>(S_, clen);
+    }
+
     emesh_engine* e_ = nullptr;
+    uint64_t S_ = 4;
     uint64_t n_;
     uint32_t k_;
     ReduceMode mode_;

@@ -48,8 +48,11 @@ static ModelParams model(uint32_t seed, float scale) {
 static bool same_params(const ModelParams& a, const ModelParams& b) { return same_bits(a.flatten(), b.flatten()); }
 
 // allreduce.hpp:314-464 without a transport: worker r's ring position, hop by hop.
+static std::vector<std::vector<Bytes>> g_final_wire;  // [chunk][sub]: the bytes the all-gather forwards
+
 static std::vector<std::vector<float>> ring_restated(const std::vector<std::vector<float>>& in, uint32_t S,
                                                      ReduceMode mode) {
+    g_final_wire.assign(in.size(), {});
     using namespace ring_detail;
     const size_t k = in.size(), n = in[0].size();
     auto chunks = split(n, k);
@@ -80,7 +83,9 @@ static std::vector<std::vector<float>> ring_restated(const std::vector<std::vect
         for (auto [lo, hi] : subs_of((uint32_t)((r + 1) % k))) {
             std::vector<float> mean(hi - lo);
             for (size_t i = 0; i < mean.size(); ++i) mean[i] = acc[r][lo + i] / static_cast<float>(k);
-            std::vector<float> v = decode_slice(encode_slice(mean, mode), mode);
+            Bytes wire = encode_slice(mean, mode);
+            g_final_wire[(r + 1) % k].push_back(wire);
+            std::vector<float> v = decode_slice(wire, mode);
             std::copy(v.begin(), v.end(), result.begin() + lo);
         }
     }
@@ -164,6 +169,11 @@ int main() {
             auto want = ring_restated(ins, 4, mode);
             for (uint32_t w = 0; w < k; ++w)
                 EXPECT(same_bits(got[w], want[w]), "ring mode=%d k=%u worker %u", (int)mode, k, w);
+            if (mode == ReduceMode::int8)  // wire interop: the reference's all-gather bytes, segment by segment
+                for (uint32_t c = 0; c < k; ++c) {
+                    auto wire = eng.final_payloads(c, (c + k - 1) % k);  // the owner's arena
+                    EXPECT(wire == g_final_wire[c], "final wire payloads k=%u chunk %u", k, c);
+                }
         }
     }
     // trainer.hpp:355-382 outer sync, k = 4 local workers
