@@ -25,7 +25,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     O = Oracle()
     ok = True
-    cases = [(100_003, 4, 0), (4099, 3, 1), (5, 4, 0), (2_000_000, 8, 300_000)]
+    cases = [(100_003, 4, 0), (4099, 3, 1), (5, 4, 0), (3, 4, 0), (2_000_000, 8, 300_000)]
     runs = [(c, t, m) for m in ("int8", "fp32") for t in ("nccl", "p2p") for c in cases]
     for (n, S, window), transport, mode in runs:
         obj = [E.RingEngine.unique_id() if rank == 0 else None]
