@@ -373,9 +373,14 @@ def main():
     # ---- e2e through the host-buffer C-ABI entry point (pinned host memory)
     e2e = None
     if not args.no_e2e:
-        hg = [x.cpu().pin_memory() for x in tg]
-        hl = [x.cpu().pin_memory() for x in tl]
-        hb = [x.cpu().pin_memory() for x in tb]
+        def pinned(x):  # straight into page-locked memory (no pageable staging copy)
+            h = torch.empty(x.numel(), dtype=x.dtype, pin_memory=True)
+            h.copy_(x)
+            return h
+
+        hg = [pinned(x) for x in tg]
+        hl = [pinned(x) for x in tl]
+        hb = [pinned(x) for x in tb]
         eng.outer_sync_host(hg, hl, hb, hp, write_local=False)  # warm (allocates device mirrors)
         barrier()
         t0 = time.perf_counter()
