@@ -510,7 +510,7 @@ struct TraceBuf {
     size_t cap = 0;
 } g_trace;
 
-// Co-resident grid for the persistent quantizer (cooperative launch).
+// Co-resident grid of the persistent quantizer (occupancy x SMs, capped at the task count).
 int persistent_grid(const void* fn, uint32_t ntasks) {
     static std::mutex mu;
     static std::vector<std::pair<const void*, int>> cache;

@@ -74,7 +74,7 @@ constexpr double kMagic52 = 4503599627370496.0;  // 2^52
 constexpr double kWideK = 4503599627370496.0 + 2199023255552.0;  // 2^52 + 2^41
 constexpr int kWideBiasBits = 41;
 
-// Per-segment statistics, written once by the root CTA of k_stats.
+// Per-segment statistics, written once by the segment's last STATS tile (finalize_stats).
 struct SegStat {
     double mu, sigma, lo, width, hi;  // first four exported as {mu, sigma, lo, width}
     float c_f, inv_w_f;  // bucket estimate g = fma(x, inv_w_f, -c_f), c_f = (float)(lo / width)
@@ -105,8 +105,8 @@ struct SegInfo {
 
 // Moments of a set of values around a pivot p: s = sum x, m2 = sum (x-p)^2,
 // d = sum (x-p). Two partials merge exactly (in real arithmetic) by moving
-// one to the other's pivot, so the combine tree can run in any shape; it
-// runs in a fixed order, so results are deterministic.
+// one to the other's pivot, so partials can be combined in any grouping; the
+// kernels combine them in a fixed order, so results are deterministic.
 struct StatP {
     double s, m2, d, piv;
     uint64_t n;
@@ -314,12 +314,13 @@ __device__ float threshold(int j, double lo, double hi, double w) {
 
 
 // ---------------------------------------------------------------------------
-// K_stats: fused producer (PG / hop dequant-add / divide) + moments, one
+// STATS pass: fused producer (PG / hop dequant-add / divide) + moments, one
 // pass: each lane accumulates s = sum x, d = sum (x-p), m2 = sum (x-p)^2 around
-// a pivot p (its first value), merged exactly up the warp / CTA / tree. Writes
-// x to scratch (for k_bin) unless the source is a plain buffer. The tree root
-// publishes SegStat: mu, sigma, lo, hi, width (quant.hpp:33-59), the exact
-// threshold table and the bucket fixed-point parameters.
+// a pivot p (its first value), merged exactly in a fixed order over the warp,
+// the CTA (one leaf per tile) and the segment (finalize_stats). Writes x to
+// scratch for the BIN pass unless the source is a plain buffer. The segment's
+// last tile publishes SegStat: mu, sigma, lo, hi, width (quant.hpp:33-59), the
+// exact threshold table and the bucket encodings.
 
 __device__ __forceinline__ StatP shfl_statp(const StatP& p, int src) {
     StatP o;
