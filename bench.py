@@ -182,6 +182,8 @@ def config_block(args, k, n, transport=None):
                          "int8 ring all-reduce + Nesterov (lr=0.7, mu=0.9)"),
             "params_per_worker": n, "workers": k, "pipeline_subchunks": args.S,
             "ring": ("reference CPU ring_allreduce over TcpEnv loopback (k node threads)" if transport == "reference"
+                     else "none: k = 1, the all-reduce is the identity (allreduce.hpp:319); PG + Nesterov fused"
+                     if k == 1
                      else "virtual (all workers on 1 GPU, zero-copy hand-off)" if args.gpus == 1 and k > 1
                      else "peer memory over NVLink (quantizer stores into the successor's arena, per-segment flags), "
                           "one worker per GPU" if transport == "p2p"
