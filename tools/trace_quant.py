@@ -70,3 +70,11 @@ for x in grid:
     run = (g[:, 0] <= x) & (g[:, 3] > x)
     mix.append(round(float((kinds[run] == 0).mean()), 2) if run.any() else None)
 print("STATS share of running tasks over the longest launch:", mix)
+# grid utilization per launch group: busy CTA-time / (grid slots x span)
+grid_slots = 444
+util = []
+for b0, e0 in zip(bounds[:-1], bounds[1:]):
+    gg = t[b0:e0]
+    span = gg[:, 3].max() - gg[:, 0].min()
+    util.append(float((gg[:, 3] - gg[:, 0]).sum()) / (grid_slots * span))
+print("grid utilization per launch: mean %.3f min %.3f max %.3f" % (np.mean(util), np.min(util), np.max(util)))
