@@ -1026,7 +1026,11 @@ struct ApplyArgs {
     uint32_t* err;            // sticky error word (kErrRingTimeout)
     unsigned long long timeout_ns;
 };
-constexpr int kApplySplit = kUnitsPerWarp / 2;  // k_apply CTAs per quantizer tile (2 units per warp each)
+#ifndef EMESH_APPLY_SPLIT
+#define EMESH_APPLY_SPLIT kUnitsPerWarp  // one unit per warp: measured best (k_apply 11.3 -> 11.0 ms per round)
+#endif
+constexpr int kApplySplit = EMESH_APPLY_SPLIT;               // k_apply CTAs per quantizer tile
+constexpr int kApplyUnits = kUnitsPerWarp / kApplySplit;     // units per warp in one k_apply CTA
 
 __device__ __forceinline__ void nesterov1(float& th, float& b, float d, float lr, float mom) {
     // optim.hpp:127-130, fp32, this exact association, no FMA
@@ -1049,8 +1053,8 @@ __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
     lut[threadIdx.x] = __ldcg(a.cb + (uint64_t)si.slot * kBuckets + threadIdx.x);
     __syncthreads();
     const uint64_t hiel = si.lo + si.len;
-    for (int ui = 0; ui < 2; ++ui) {
-    const uint32_t u = (tile - si.cta0) * kTileUnits + (part * 2 + ui) * kWarps + warp;
+    for (int ui = 0; ui < kApplyUnits; ++ui) {
+    const uint32_t u = (tile - si.cta0) * kTileUnits + (part * kApplyUnits + ui) * kWarps + warp;
     if (u >= si.nunits) return;
     const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
 #pragma unroll 4
@@ -1132,8 +1136,8 @@ __global__ void __launch_bounds__(kThreads) k_f32_hop(F32HopArgs a) {
         __syncthreads();
     }
     const uint64_t hiel = si.lo + si.len;
-    for (int ui = 0; ui < 2; ++ui) {
-        const uint32_t u = (tile - si.cta0) * kTileUnits + (part * 2 + ui) * kWarps + warp;
+    for (int ui = 0; ui < kApplyUnits; ++ui) {
+        const uint32_t u = (tile - si.cta0) * kTileUnits + (part * kApplyUnits + ui) * kWarps + warp;
         if (u >= si.nunits) break;
         const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
 #pragma unroll 4
@@ -1194,8 +1198,8 @@ __global__ void __launch_bounds__(kThreads) k_f32_apply(ApplyArgs a, const float
         __syncthreads();
     }
     const uint64_t hiel = si.lo + si.len;
-    for (int ui = 0; ui < 2; ++ui) {
-        const uint32_t u = (tile - si.cta0) * kTileUnits + (part * 2 + ui) * kWarps + warp;
+    for (int ui = 0; ui < kApplyUnits; ++ui) {
+        const uint32_t u = (tile - si.cta0) * kTileUnits + (part * kApplyUnits + ui) * kWarps + warp;
         if (u >= si.nunits) return;
         const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
 #pragma unroll 4
