@@ -371,7 +371,8 @@ __device__ uint32_t bucket_info(float t0, float t1) {
 
 struct QSmem {
     uint32_t hist[kWarps][kBuckets + 1][3];  // per-warp limbs over the tile (bin), see bin_unit; row 256: sink
-    uint32_t binfo[2 * kBuckets];        // bucket encodings (bin), twice: index code | 256 = same bucket
+    uint2 bsk[2 * kBuckets];             // per bucket {high word of s, high word of K} (bin), twice:
+                                         // index code | 256 = same bucket (see kInfoWide)
     float thr[kBuckets + 2];             // exact threshold table (bin); [257] = bucket 0's base (lo_up)
     float lut[kBuckets];                 // incoming codebook (stats, hop)
     StatP wp[kWarps];
@@ -707,10 +708,10 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
             // fixed point r(x) (see kInfoWide), split into the limbs
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const uint32_t info = sm.binfo[cc[i]];
+                const uint2 sk = sm.bsk[cc[i]];
                 // m = x * s + K in [2^52, 2^53): mantissa = r (see kInfoWide)
-                const double sc = __hiloint2double((int)(info & ~kInfoWide), 0);
-                const double kk = __hiloint2double((int)(0x43300000u | ((info & kInfoWide) << 9)), 0);
+                const double sc = __hiloint2double((int)sk.x, 0);
+                const double kk = __hiloint2double((int)sk.y, 0);
                 const double m = __fma_rn((double)xe[i], sc, kk);
                 const uint32_t rlo = (uint32_t)__double2loint(m);
                 const uint32_t rhi = (uint32_t)__double2hiint(m);
@@ -769,7 +770,9 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
         __syncthreads();
         const int b = threadIdx.x;
         sm.thr[b] = b == 0 ? -INFINITY : __ldcg(&st->thr[b]);
-        sm.binfo[b] = sm.binfo[kBuckets + b] = __ldcg(&st->binfo[b]);
+        const uint32_t info = __ldcg(&st->binfo[b]);
+        const uint2 sk = make_uint2(info & ~kInfoWide, 0x43300000u | ((info & kInfoWide) << 9));  // K = 2^52 (+2^41)
+        sm.bsk[b] = sm.bsk[kBuckets + b] = sk;
 
         if (b == 0) {
             sm.thr[kBuckets] = INFINITY;
