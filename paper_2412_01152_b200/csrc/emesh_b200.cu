@@ -916,6 +916,12 @@ struct emesh_engine {
         uint32_t* ag_flag = nullptr;
     };
     std::vector<Peer> peers;  // [rank]; own rank: local pointers
+    // all-gather arrival flags are written by the copy engine from page-locked
+    // host words holding the round number (per round parity): no kernel is
+    // involved, so a GPU whose SMs are all busy waiting for its peers' flags
+    // can never hold back the flags those peers wait for
+    uint32_t* h_epoch[2] = {nullptr, nullptr};
+    cudaEvent_t ev_flags[2] = {nullptr, nullptr};
     // device mirrors for the host-buffer entry point
     std::vector<float*> h_theta, h_local, h_buf;
     Tracker tr;
@@ -1294,6 +1300,9 @@ bool push_final_payload(const Batch& fb) { return fb.eruns.size() > kMaxDmaRuns 
 int p2p_allgather(emesh_engine* e, int par, uint32_t ep) {
     const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
     cudaStream_t cm = e->s_comm;
+    // the host words of this parity were last read by the copies two rounds ago
+    CU(cudaEventSynchronize(e->ev_flags[par]));
+    std::fill(e->h_epoch[par], e->h_epoch[par] + e->plan.segs.size(), ep);
     CU(cudaEventRecord(e->ev_send[0], e->s_comp));
     CU(cudaStreamWaitEvent(cm, e->ev_send[0], 0));
     const Batch& fb = e->plan.batches[succ][0];
@@ -1323,10 +1332,11 @@ int p2p_allgather(emesh_engine* e, int par, uint32_t ep) {
                                    e->peers[r].cbs[par] + (size_t)s0 * kBuckets,
                                    (size_t)(s1 - s0) * kBuckets * sizeof(float), cudaMemcpyDeviceToDevice, cm));
             }
-            k_set_flags<<<1, 128, 0, cm>>>(e->peers[q].ag_flag, s0, s1 - s0, ep);
-            CU(cudaGetLastError());
+            CU(cudaMemcpyAsync(e->peers[q].ag_flag + s0, e->h_epoch[par] + s0, (size_t)(s1 - s0) * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, cm));  // after this group's bytes (stream order)
         }
     }
+    CU(cudaEventRecord(e->ev_flags[par], cm));
     return EMESH_OK;
 }
 
@@ -1474,7 +1484,11 @@ bool setup_p2p(emesh_engine* e) {
               cudaMalloc(&e->rs_flag, nslots * sizeof(uint32_t)) == cudaSuccess &&
               cudaMalloc(&e->ag_flag, nslots * sizeof(uint32_t)) == cudaSuccess &&
               cudaMemset(e->rs_flag, 0, nslots * sizeof(uint32_t)) == cudaSuccess &&
-              cudaMemset(e->ag_flag, 0, nslots * sizeof(uint32_t)) == cudaSuccess;
+              cudaMemset(e->ag_flag, 0, nslots * sizeof(uint32_t)) == cudaSuccess &&
+              cudaMallocHost(&e->h_epoch[0], nslots * sizeof(uint32_t)) == cudaSuccess &&
+              cudaMallocHost(&e->h_epoch[1], nslots * sizeof(uint32_t)) == cudaSuccess &&
+              cudaEventCreateWithFlags(&e->ev_flags[0], cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&e->ev_flags[1], cudaEventDisableTiming) == cudaSuccess;
     constexpr int kH = 8;
     constexpr size_t kRec = kH * sizeof(cudaIpcMemHandle_t);
     std::vector<uint8_t> mine(kRec, 0), all(kRec * k, 0);
@@ -1534,6 +1548,12 @@ void teardown_p2p(emesh_engine* e) {
             if (p) cudaIpcCloseMemHandle(p);
     }
     e->peers.clear();
+    for (int p = 0; p < 2; ++p) {
+        if (e->h_epoch[p]) cudaFreeHost(e->h_epoch[p]);
+        if (e->ev_flags[p]) cudaEventDestroy(e->ev_flags[p]);
+        e->h_epoch[p] = nullptr;
+        e->ev_flags[p] = nullptr;
+    }
     cudaFree(e->codes_alt);
     cudaFree(e->cbs_alt);
     cudaFree(e->pay_alt);

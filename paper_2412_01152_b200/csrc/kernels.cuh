@@ -1289,12 +1289,6 @@ __global__ void __launch_bounds__(kThreads) k_adamw(float* p, const float* g, fl
     if (bad && err) atomicOr(err, 1u);
 }
 
-// Peer transport: raise the arrival flags of slots [slot0, slot0 + n) on a
-// peer after the copy engine delivered their bytes (stream-ordered before).
-__global__ void k_set_flags(uint32_t* flags, uint32_t slot0, uint32_t n, uint32_t epoch) {
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) st_release_sys(flags + slot0 + i, epoch);
-}
-
 // ---------------------------------------------------------------------------
 // Flat elementwise kernels (no segments).
 
