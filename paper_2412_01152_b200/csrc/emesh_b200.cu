@@ -10,7 +10,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -1133,27 +1135,101 @@ int run_virtual(emesh_engine* e, const float* const* A, const float* const* B, f
 // ---- NCCL ring: this process is ring position `rank`; payload windows move
 // with ncclSend/ncclRecv on s_comm while s_comp runs the fused hop kernels on
 // the previous window.
+//
+// The communicator is non-blocking (ncclConfig_t::blocking = 0) so that no
+// NCCL call can park the host forever on a peer that stopped (connection
+// setup inside ncclGroupEnd does exactly that in blocking mode). Every call
+// that may answer ncclInProgress is settled here against step_timeout; on
+// expiry the communicator is aborted and the round fails with EMESH_ERING
+// (allreduce.hpp:466-470), which allreduce_with_retry turns into a re-plan.
+int nccl_settle(emesh_engine* e, ncclResult_t r, const char* what) {
+    const auto t0 = std::chrono::steady_clock::now();
+    int spins = 0;
+    while (r == ncclInProgress) {
+        if (ncclCommGetAsyncError(e->comm, &r) != ncclSuccess) break;
+        if (r != ncclInProgress) break;
+        const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (waited * 1e9 > (double)e->tr.timeout_ns) {
+            e->failed = true;
+            ncclCommAbort(e->comm);
+            e->comm = nullptr;
+            return fail(EMESH_ERING, "NCCL %s did not complete within step_timeout (%.1f s)", what,
+                        (double)e->tr.timeout_ns * 1e-9);
+        }
+        if (++spins > 1000) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    if (r != ncclSuccess) {
+        e->failed = true;
+        ncclCommAbort(e->comm);
+        e->comm = nullptr;
+        return fail(EMESH_ENCCL, "NCCL %s: %s", what, ncclGetErrorString(r));
+    }
+    return EMESH_OK;
+}
+#define NCS(call) TRY(nccl_settle(e, (call), #call))
+
+// Release the communicator: finalize (settled against step_timeout, so a
+// vanished peer cannot park the host) then destroy; abort after a failure.
+void nccl_close(emesh_engine* e) {
+    if (!e->comm) return;
+    if (!e->failed && nccl_settle(e, ncclCommFinalize(e->comm), "ncclCommFinalize") != EMESH_OK) return;
+    if (e->failed) ncclCommAbort(e->comm);
+    else ncclCommDestroy(e->comm);
+    e->comm = nullptr;
+}
+
+// Wait for `streams` to drain while NCCL kernels may be parked on a peer:
+// polled against step_timeout and the communicator's async error; on expiry
+// or error the communicator is aborted (its kernels exit) -> EMESH_ERING.
+int nccl_drain(emesh_engine* e, std::initializer_list<cudaStream_t> streams, const char* what) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        bool done = true;
+        for (cudaStream_t st : streams) {
+            const cudaError_t q = cudaStreamQuery(st);
+            if (q == cudaErrorNotReady) { done = false; continue; }
+            if (q != cudaSuccess) return fail(EMESH_ECUDA, "%s: stream error: %s", what, cudaGetErrorString(q));
+        }
+        if (done) return EMESH_OK;
+        ncclResult_t ae = ncclSuccess;
+        if (e->comm) ncclCommGetAsyncError(e->comm, &ae);
+        const bool err = ae != ncclSuccess && ae != ncclInProgress;
+        const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (err || waited * 1e9 > (double)e->tr.timeout_ns) {
+            e->failed = true;
+            if (e->comm) ncclCommAbort(e->comm);
+            e->comm = nullptr;
+            for (cudaStream_t st : streams) cudaStreamSynchronize(st);
+            cudaGetLastError();
+            if (err) return fail(EMESH_ERING, "%s: NCCL ring failed: %s", what, ncclGetErrorString(ae));
+            return fail(EMESH_ERING, "%s: NCCL ring step timed out (step_timeout %.1f s)", what,
+                        (double)e->tr.timeout_ns * 1e-9);
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(100));
+    }
+}
+
 int xfer_window(emesh_engine* e, const Batch& snd, const Batch& rcv) {
     const uint32_t k = e->k, r = e->rank;
     const int succ = (int)((r + 1) % k), pred = (int)((r + k - 1) % k);
     auto& ar = e->arenas[0];
     if (e->fp32) {  // raw fp32 partial sums / means (allreduce.hpp:120-151)
-        NC(ncclGroupStart());
+        NCS(ncclGroupStart());
         for (const auto& r : snd.eruns)
-            NC(ncclSend(e->pay[0] + r.first, r.second, ncclFloat32, succ, e->comm, e->s_comm));
+            NCS(ncclSend(e->pay[0] + r.first, r.second, ncclFloat32, succ, e->comm, e->s_comm));
         for (const auto& r : rcv.eruns)
-            NC(ncclRecv(e->pay[0] + r.first, r.second, ncclFloat32, pred, e->comm, e->s_comm));
-        NC(ncclGroupEnd());
+            NCS(ncclRecv(e->pay[0] + r.first, r.second, ncclFloat32, pred, e->comm, e->s_comm));
+        NCS(ncclGroupEnd());
         return EMESH_OK;
     }
-    NC(ncclGroupStart());
-    for (const auto& r : snd.eruns) NC(ncclSend(ar.codes + r.first, r.second, ncclUint8, succ, e->comm, e->s_comm));
-    NC(ncclSend(ar.cbs + (size_t)snd.slot0 * kBuckets, (size_t)snd.nseg * kBuckets, ncclFloat32, succ, e->comm,
+    NCS(ncclGroupStart());
+    for (const auto& r : snd.eruns) NCS(ncclSend(ar.codes + r.first, r.second, ncclUint8, succ, e->comm, e->s_comm));
+    NCS(ncclSend(ar.cbs + (size_t)snd.slot0 * kBuckets, (size_t)snd.nseg * kBuckets, ncclFloat32, succ, e->comm,
                 e->s_comm));
-    for (const auto& r : rcv.eruns) NC(ncclRecv(ar.codes + r.first, r.second, ncclUint8, pred, e->comm, e->s_comm));
-    NC(ncclRecv(ar.cbs + (size_t)rcv.slot0 * kBuckets, (size_t)rcv.nseg * kBuckets, ncclFloat32, pred, e->comm,
+    for (const auto& r : rcv.eruns) NCS(ncclRecv(ar.codes + r.first, r.second, ncclUint8, pred, e->comm, e->s_comm));
+    NCS(ncclRecv(ar.cbs + (size_t)rcv.slot0 * kBuckets, (size_t)rcv.nseg * kBuckets, ncclFloat32, pred, e->comm,
                 e->s_comm));
-    NC(ncclGroupEnd());
+    NCS(ncclGroupEnd());
     return EMESH_OK;
 }
 
@@ -1209,6 +1285,7 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
     const bool pg = B != nullptr;
     auto& ar = e->arenas[0];
     cudaStream_t sc = e->s_comp, sm = e->s_comm;
+    if (!e->comm) return fail(EMESH_ERING, "NCCL communicator was aborted by an earlier ring failure");
     const auto& P = e->plan.batches;
     const uint32_t W = (uint32_t)P[0].size();
     for (uint32_t c = 1; c < k; ++c)
@@ -1503,9 +1580,10 @@ bool setup_p2p(emesh_engine* e) {
     bool comm_ok = cudaMalloc(&d, kRec * (k + 1)) == cudaSuccess && cudaMalloc(&d_ok, sizeof(int)) == cudaSuccess;
     if (comm_ok) {
         comm_ok = cudaMemcpy(d, mine.data(), kRec, cudaMemcpyHostToDevice) == cudaSuccess &&
-                  ncclAllGather(d, d + kRec, kRec, ncclUint8, e->comm, e->s_comm) == ncclSuccess &&
+                  nccl_settle(e, ncclAllGather(d, d + kRec, kRec, ncclUint8, e->comm, e->s_comm), "ncclAllGather") ==
+                      EMESH_OK &&
                   cudaMemcpyAsync(all.data(), d + kRec, kRec * k, cudaMemcpyDeviceToHost, e->s_comm) == cudaSuccess &&
-                  cudaStreamSynchronize(e->s_comm) == cudaSuccess;
+                  nccl_drain(e, {e->s_comm}, "p2p handle exchange") == EMESH_OK;
     }
     e->peers.assign(k, emesh_engine::Peer{});
     e->peers[r] = emesh_engine::Peer{{e->arenas[0].codes, e->codes_alt}, {e->arenas[0].cbs, e->cbs_alt},
@@ -1529,9 +1607,10 @@ bool setup_p2p(emesh_engine* e) {
     int v = (ok && comm_ok) ? 1 : 0;
     bool agreed = false;
     if (d_ok && cudaMemcpy(d_ok, &v, sizeof v, cudaMemcpyHostToDevice) == cudaSuccess &&
-        ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, e->comm, e->s_comm) == ncclSuccess &&
+        nccl_settle(e, ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, e->comm, e->s_comm), "ncclAllReduce") ==
+            EMESH_OK &&
         cudaMemcpyAsync(&v, d_ok, sizeof v, cudaMemcpyDeviceToHost, e->s_comm) == cudaSuccess &&
-        cudaStreamSynchronize(e->s_comm) == cudaSuccess)
+        nccl_drain(e, {e->s_comm}, "p2p mapping agreement") == EMESH_OK)
         agreed = v == 1;
     cudaFree(d);
     cudaFree(d_ok);
@@ -1722,15 +1801,21 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
         e->reserve_ctas = rs ? (uint32_t)std::atoi(rs) : 0u;
         ncclUniqueId id;
         std::memcpy(&id, cfg->nccl_id, sizeof id);
-        ncclResult_t r = ncclCommInitRank(&e->comm, (int)e->k, id, (int)e->rank);
-        if (r != ncclSuccess) return bail(fail(EMESH_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+        ncclConfig_t ncfg = NCCL_CONFIG_INITIALIZER;
+        ncfg.blocking = 0;  // every wait is bounded by step_timeout (nccl_settle)
+        ncclResult_t r = ncclCommInitRankConfig(&e->comm, (int)e->k, id, (int)e->rank, &ncfg);
+        if (r != ncclSuccess && r != ncclInProgress)
+            return bail(fail(EMESH_ENCCL, "ncclCommInitRankConfig: %s", ncclGetErrorString(r)));
+        if ((rc = nccl_settle(e, r, "ncclCommInitRankConfig"))) return bail(rc);
         e->transport = EMESH_TRANSPORT_NCCL;
         if (try_p2p && setup_p2p(e)) {
             e->transport = EMESH_TRANSPORT_P2P;
             // NCCL only bootstrapped the mappings: release it now, while every
             // rank is here, so teardown never depends on a peer being alive
-            ncclCommDestroy(e->comm);
-            e->comm = nullptr;
+            nccl_close(e);
+        } else if (!e->comm) {  // a peer vanished during setup (nccl_settle / nccl_drain aborted)
+            const std::string why = emesh_last_error();
+            return bail(fail(EMESH_ERING, "ring setup failed: %s", why.c_str()));
         } else if (cfg->transport == EMESH_TRANSPORT_P2P) {
             return bail(fail(EMESH_ECONFIG, "peer transport unavailable (CUDA IPC mapping failed on some rank)"));
         } else if (try_p2p) {  // AUTO fell back: NCCL windows
@@ -1757,13 +1842,12 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
 int emesh_engine_destroy(emesh_engine* e) {
     if (!e) return EMESH_OK;
     cudaSetDevice(e->device);
+    if (e->comm && e->s_comp && e->s_comm && nccl_drain(e, {e->s_comp, e->s_comm}, "destroy") != EMESH_OK)
+        cudaGetLastError();  // NCCL kernels parked on a vanished peer: aborted by nccl_drain
     if (e->s_comp) cudaStreamSynchronize(e->s_comp);
     if (e->s_comm) cudaStreamSynchronize(e->s_comm);
     teardown_p2p(e);
-    if (e->comm) {
-        if (e->failed) ncclCommAbort(e->comm);  // peers may be gone: do not wait for them
-        else ncclCommDestroy(e->comm);
-    }
+    nccl_close(e);  // aborts when a round failed: peers may be gone
     for (auto& a : e->arenas) { cudaFree(a.codes); cudaFree(a.cbs); cudaFree(a.stats); }
     for (auto* p : e->pay) cudaFree(p);
     for (auto* p : e->h_theta) cudaFree(p);
@@ -1923,6 +2007,13 @@ int emesh_engine_outer_sync_host(emesh_engine* e, float* const* theta_g, float* 
 
 int emesh_engine_check(emesh_engine* e) {
     CU(cudaSetDevice(e->device));
+    if (e->transport == EMESH_TRANSPORT_NCCL && e->comm && !e->virt) {
+        // NCCL waits have no device-side budget: bound them here. A peer that
+        // stops leaves our send/recv pending; after step_timeout the
+        // communicator is aborted and the round reports RingFailureError
+        // (allreduce.hpp:466-470).
+        TRY(nccl_drain(e, {e->s_comp, e->s_comm}, "ring round"));
+    }
     CU(cudaStreamSynchronize(e->s_comp));
     CU(cudaStreamSynchronize(e->s_comm));
     if (!e->ws.err) return EMESH_OK;

@@ -28,6 +28,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     store = dist.distributed_c10d._get_default_store()
     O = Oracle()
+    transport = sys.argv[1] if len(sys.argv) > 1 else "p2p"
     n, S = 300_007, 4
     ids = [f"r{i}" for i in range(world)]
     crashed = ids[-1]
@@ -45,7 +46,7 @@ def main():
                 store.set(key, uid)
             else:
                 uid = bytes(store.get(key))
-        return E.RingEngine(n, k, rank=plan.self_index, opts=opts, nccl_id=uid, transport="p2p")
+        return E.RingEngine(n, k, rank=plan.self_index, opts=opts, nccl_id=uid, transport=transport)
 
     class Mesh:  # the coordinator's view: the crashed rank is evicted at the next epoch
         def __init__(self):
@@ -70,7 +71,7 @@ def main():
         store.set("crashed_ready", b"1")
         store.get("survivors_done")  # stay alive (our memory stays mapped) until they finish
         print(f"{me}: released", flush=True)
-        eng.close()
+        os._exit(0)  # a crash: no engine teardown, no collective goodbye
     else:
         job = E.ReduceJob(1, torch.from_numpy(ins[me]).to(dev))
         before = job.input.clone()
@@ -85,10 +86,8 @@ def main():
             ok = False
         if rank == 0:
             store.set("survivors_done", b"1")
-        print(f"{me}: retry {'OK' if ok else 'FAILED'}", flush=True)
-    dist.barrier()
-    dist.destroy_process_group()
-    sys.exit(0 if ok else 1)
+        print(f"{me}: retry {'OK' if ok else 'FAILED'} [{transport}]", flush=True)
+        os._exit(0 if ok else 1)  # the crashed peer is gone: no collective teardown
 
 
 if __name__ == "__main__":

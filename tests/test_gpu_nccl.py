@@ -23,12 +23,15 @@ def test_nccl_ring_parity():
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-def test_retry_after_peer_stops():
-    """allreduce_with_retry over the peer transport: a peer stops mid-collective, the survivors time out
-    (RingFailureError), re-plan and return the survivor mean (test_allreduce.cpp:431-445 analogue)."""
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_retry_after_peer_stops(transport):
+    """allreduce_with_retry: a peer stops mid-collective, the survivors time out (RingFailureError; the
+    peer transport's device-side wait budget, or the bounded NCCL wait + communicator abort), re-plan and
+    return the survivor mean (test_allreduce.cpp:431-445 analogue)."""
     n = min(torch.cuda.device_count(), 4)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", "29534", os.path.join(ROOT, "tests", "retry_worker.py")]
+           "--master-addr", "127.0.0.1", "--master-port", "29534" if transport == "p2p" else "29535",
+           os.path.join(ROOT, "tests", "retry_worker.py"), transport]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, (out.stdout[-3000:], out.stderr[-3000:])
     assert out.stdout.count("retry OK") == n - 1
