@@ -32,7 +32,8 @@ enum {
     EMESH_ECUDA = 4,    /* CUDA runtime failure */
     EMESH_ENCCL = 5,    /* NCCL failure (the transport; emesh::LinkError analogue) */
     EMESH_ERING = 6,    /* emesh::RingFailureError (collective aborted) */
-    EMESH_ECONFIG = 7   /* emesh::ConfigError (invalid plan/options) */
+    EMESH_ECONFIG = 7,  /* emesh::ConfigError (invalid plan/options) */
+    EMESH_EIO = 8       /* emesh::Error (checkpoint file I/O, integrity hash mismatch) */
 };
 
 #define EMESH_BUCKETS 256
@@ -248,6 +249,55 @@ int emesh_engine_profile_read(emesh_engine* e, uint32_t kind, uint64_t* launches
  * the op's stream, relative to the first op's start). Returns the row count
  * (copies at most max_rows). Synchronizes the engine. */
 uint64_t emesh_engine_timeline(emesh_engine* e, double* rows, uint64_t max_rows);
+
+/* ---------------- checkpoints: tensor.hpp:111-161, checkpoint.hpp:19-68,190-224 ----
+ * A Checkpoint whose five parameter sets stay in device arenas (flat fp32,
+ * canonical tensor order, `numel` = sum of the tensors' element counts each).
+ * The layout (names, ranks, extents) is the model's; the bytes are exactly
+ * encode_checkpoint's (checkpoint.hpp:32-47). Names are NUL-terminated UTF-8. */
+typedef struct emesh_checkpoint {
+    uint64_t outer_step;
+    uint32_t ntensors;
+    const char* const* names;   /* ntensors */
+    const uint32_t* ranks;      /* ntensors */
+    const uint32_t* extents;    /* sum(ranks), tensor after tensor */
+    float* params;              /* Checkpoint::params (theta after the outer step) */
+    float* retained;            /* Checkpoint::retained (theta_g for the next pseudo-gradient) */
+    float* adam_m;              /* Checkpoint::inner.m */
+    float* adam_v;              /* Checkpoint::inner.v */
+    float* nesterov_buf;        /* Checkpoint::outer.buffer */
+    uint64_t adam_step;         /* Checkpoint::inner.step */
+    uint64_t rng_seed;
+    uint64_t data_counter;
+    uint32_t shard;
+    uint8_t config_hash[32];
+} emesh_checkpoint;
+
+/* Size of encode_checkpoint(ck) in bytes. */
+int emesh_checkpoint_encoded_size(const emesh_checkpoint* ck, uint64_t* bytes);
+/* checkpoint.hpp:32-47 into a host buffer (page-locked: DMA in place; else
+ * staged through pinned blocks). EMESH_ESHAPE if cap is short (*written = need). */
+int emesh_checkpoint_encode(const emesh_checkpoint* ck, uint8_t* out_host, uint64_t cap, uint64_t* written,
+                            emesh_stream_t stream);
+/* checkpoint.hpp:49-66 into the view's arenas: the same DecodeError /
+ * ShapeError cases as the reference (first one in stream order), plus
+ * EMESH_EDECODE when the bytes' layout differs from the view's. Scalars are
+ * written back into *ck. Structural errors leave the arenas untouched; a
+ * non-finite value is detected on the device after the upload. */
+int emesh_checkpoint_decode(const uint8_t* buf_host, uint64_t len, emesh_checkpoint* ck, emesh_stream_t stream);
+/* Layout discovery (the params set): counts, then names (NUL-separated),
+ * ranks and extents. */
+int emesh_checkpoint_probe(const uint8_t* buf_host, uint64_t len, uint32_t* ntensors, uint64_t* numel,
+                           uint64_t* name_bytes, uint32_t* rank_sum);
+int emesh_checkpoint_layout(const uint8_t* buf_host, uint64_t len, char* names, uint64_t names_cap,
+                            uint32_t* ranks, uint32_t* extents, uint32_t extents_cap);
+/* checkpoint.hpp:190-224 file framing: u64 LE length, sha256(payload),
+ * payload. read: EMESH_EIO on open failure / hash mismatch, EMESH_EDECODE on
+ * truncation, then emesh_checkpoint_decode. */
+int emesh_checkpoint_write_file(const char* path, const emesh_checkpoint* ck, emesh_stream_t stream);
+int emesh_checkpoint_read_file(const char* path, emesh_checkpoint* ck, emesh_stream_t stream);
+/* sha256.hpp: one-shot SHA-256 (host). */
+int emesh_sha256(const void* data, uint64_t n, uint8_t out[32]);
 
 #ifdef __cplusplus
 }

@@ -191,6 +191,48 @@ class Oracle:
         return codes[: cnt.value], cb
 
 
+
+# ---- checkpoint byte format: a pure-Python restatement (byte packing) ----
+
+def checkpoint_encode(layout, sets, outer_step, adam_step, rng_seed, data_counter, shard, config_hash):
+    """checkpoint.hpp:32-47 encode_checkpoint over write_params / write_tensor
+    (tensor.hpp:115-120,144-147; ByteWriter LE, bytes.hpp:20-45). layout =
+    [(name, shape)], sets = 5 flat fp32 arrays (params, retained, inner.m,
+    inner.v, outer.buffer)."""
+    import struct
+    out = bytearray()
+
+    def params(flat):
+        out.extend(struct.pack("<I", len(layout)))
+        off = 0
+        for name, shape in layout:
+            nb = name.encode()
+            out.extend(struct.pack("<I", len(nb)) + nb + struct.pack("<I", len(shape)))
+            for e in shape:
+                out.extend(struct.pack("<I", e))
+            n = int(np.prod(shape)) if len(shape) else 1
+            out.extend(np.ascontiguousarray(flat[off: off + n], "<f4").tobytes())
+            off += n
+
+    out.extend(struct.pack("<Q", outer_step))
+    params(sets[0])
+    params(sets[1])
+    out.extend(struct.pack("<Q", adam_step))
+    params(sets[2])
+    params(sets[3])
+    params(sets[4])
+    out.extend(struct.pack("<QQI", rng_seed, data_counter, shard))
+    out.extend(bytes(config_hash))
+    return bytes(out)
+
+
+def checkpoint_file_bytes(payload):
+    """checkpoint.hpp:190-203: u64 LE length, sha256(payload), payload."""
+    import hashlib
+    import struct
+    return struct.pack("<Q", len(payload)) + hashlib.sha256(payload).digest() + payload
+
+
 class Reference:
     """The unmodified reference library (oracle/_ref/libemesh_ref.so)."""
 
@@ -218,6 +260,19 @@ class Reference:
         L.ref_outer_sync_tcp.restype = C.c_int
         L.ref_outer_sync_tcp.argtypes = [_f32p, C.c_void_p, _f32p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_int,
                                          C.c_float, C.c_float, _f64p]
+        vp, u64 = C.c_void_p, C.c_uint64
+        L.ref_encode_checkpoint.restype = C.c_int
+        L.ref_encode_checkpoint.argtypes = [u64, C.c_uint32, vp, vp, vp, vp, u64, u64, u64, C.c_uint32, vp, vp, u64,
+                                            C.POINTER(u64)]
+        L.ref_decode_checkpoint.restype = C.c_int
+        L.ref_decode_checkpoint.argtypes = [vp, u64, vp, u64, vp, vp, vp, u64]
+        L.ref_write_checkpoint_file.restype = C.c_int
+        L.ref_write_checkpoint_file.argtypes = [C.c_char_p, u64, C.c_uint32, vp, vp, vp, vp, u64, u64, u64,
+                                                C.c_uint32, vp]
+        L.ref_read_checkpoint_file.restype = C.c_int
+        L.ref_read_checkpoint_file.argtypes = [C.c_char_p, vp, u64, vp, vp, vp, u64]
+        L.ref_sha256.restype = C.c_int
+        L.ref_sha256.argtypes = [vp, u64, vp]
         self.L = L
 
     def quantize(self, x):
@@ -305,6 +360,69 @@ class Reference:
         if rc:
             raise OracleError(rc, "ref outer sync (tcp)")
         return theta_g, buf, float(secs[0])
+
+
+    @staticmethod
+    def _ck_args(layout, sets):
+        names = (C.c_char_p * max(len(layout), 1))(*[nm.encode() for nm, _ in layout])
+        ranks = np.array([len(sh) for _, sh in layout] or [0], np.uint32)
+        ext = np.array([e for _, sh in layout for e in sh] or [0], np.uint32)
+        arrs = [np.ascontiguousarray(a, np.float32) for a in sets]
+        ptrs = (C.c_void_p * 5)(*[a.ctypes.data for a in arrs])
+        return names, ranks, ext, arrs, ptrs
+
+    def encode_checkpoint(self, layout, sets, outer_step, adam_step, rng_seed, data_counter, shard, config_hash):
+        """emesh::encode_checkpoint itself."""
+        names, ranks, ext, arrs, ptrs = self._ck_args(layout, sets)
+        h = np.frombuffer(bytes(config_hash), np.uint8).copy()
+        n = C.c_uint64(0)
+        self.L.ref_encode_checkpoint(outer_step, len(layout), C.cast(names, C.c_void_p), ranks.ctypes.data,
+                                     ext.ctypes.data, ptrs, adam_step, rng_seed, data_counter, shard, h.ctypes.data,
+                                     None, 0, C.byref(n))
+        out = np.empty(n.value, np.uint8)
+        rc = self.L.ref_encode_checkpoint(outer_step, len(layout), C.cast(names, C.c_void_p), ranks.ctypes.data,
+                                          ext.ctypes.data, ptrs, adam_step, rng_seed, data_counter, shard,
+                                          h.ctypes.data, out.ctypes.data, n.value, C.byref(n))
+        if rc:
+            raise OracleError(rc, "ref encode_checkpoint")
+        return out.tobytes()
+
+    def decode_checkpoint(self, buf, numel_cap):
+        """emesh::decode_checkpoint: (code, message, sets, scalars, hash)."""
+        sets = [np.zeros(max(numel_cap, 1), np.float32) for _ in range(5)]
+        ptrs = (C.c_void_p * 5)(*[a.ctypes.data for a in sets])
+        sc = np.zeros(5, np.uint64)
+        h = np.zeros(32, np.uint8)
+        msg = C.create_string_buffer(512)
+        b = np.frombuffer(bytes(buf), np.uint8) if len(buf) else np.zeros(1, np.uint8)
+        rc = self.L.ref_decode_checkpoint(b.ctypes.data, len(buf), ptrs, numel_cap, sc.ctypes.data, h.ctypes.data,
+                                          msg, 512)
+        return rc, msg.value.decode(errors="replace"), sets, [int(x) for x in sc], h.tobytes()
+
+    def write_checkpoint_file(self, path, layout, sets, outer_step, adam_step, rng_seed, data_counter, shard,
+                              config_hash):
+        names, ranks, ext, arrs, ptrs = self._ck_args(layout, sets)
+        h = np.frombuffer(bytes(config_hash), np.uint8).copy()
+        rc = self.L.ref_write_checkpoint_file(path.encode(), outer_step, len(layout), C.cast(names, C.c_void_p),
+                                              ranks.ctypes.data, ext.ctypes.data, ptrs, adam_step, rng_seed,
+                                              data_counter, shard, h.ctypes.data)
+        if rc:
+            raise OracleError(rc, "ref write_checkpoint_file")
+
+    def read_checkpoint_file(self, path, numel_cap):
+        sets = [np.zeros(max(numel_cap, 1), np.float32) for _ in range(5)]
+        ptrs = (C.c_void_p * 5)(*[a.ctypes.data for a in sets])
+        sc = np.zeros(5, np.uint64)
+        h = np.zeros(32, np.uint8)
+        msg = C.create_string_buffer(512)
+        rc = self.L.ref_read_checkpoint_file(path.encode(), ptrs, numel_cap, sc.ctypes.data, h.ctypes.data, msg, 512)
+        return rc, msg.value.decode(errors="replace"), sets, [int(x) for x in sc], h.tobytes()
+
+    def sha256(self, data):
+        out = np.zeros(32, np.uint8)
+        b = np.frombuffer(bytes(data), np.uint8) if len(data) else np.zeros(1, np.uint8)
+        self.L.ref_sha256(b.ctypes.data, len(data), out.ctypes.data)
+        return out.tobytes()
 
 
 def have_reference() -> bool:

@@ -22,8 +22,10 @@
 #include <vector>
 
 #include "emesh/allreduce.hpp"
+#include "emesh/checkpoint.hpp"
 #include "emesh/optim.hpp"
 #include "emesh/quant.hpp"
+#include "emesh/sha256.hpp"
 #include "emesh/sim.hpp"
 #include "emesh/tcp.hpp"
 #include "emesh/tensor.hpp"
@@ -291,6 +293,121 @@ int ref_outer_sync_tcp(float* theta_g, const float* const* theta_l, float* buf, 
         for (double e : elapsed) mx = e > mx ? e : mx;
         if (seconds) seconds[0] = mx;
     });
+}
+
+}  // extern "C"
+
+// ---- checkpoints (tensor.hpp:111-161, checkpoint.hpp:19-68,190-224) ----
+// A Checkpoint assembled from flat arrays: names[nt], ranks[nt], extents
+// (sum ranks), sets[5] = params, retained, inner.m, inner.v, outer.buffer
+// (each the concatenated tensor data in order).
+static Checkpoint ck_from_flat(uint64_t outer_step, uint32_t nt, const char* const* names, const uint32_t* ranks,
+                               const uint32_t* extents, const float* const* sets, uint64_t adam_step,
+                               uint64_t rng_seed, uint64_t data_counter, uint32_t shard, const uint8_t* hash) {
+    Checkpoint ck;
+    ModelParams* ps[5] = {&ck.params, &ck.retained, &ck.inner.m, &ck.inner.v, &ck.outer.buffer};
+    for (int s = 0; s < 5; ++s) {
+        uint64_t e = 0, off = 0;
+        for (uint32_t i = 0; i < nt; ++i) {
+            std::vector<uint32_t> shape(extents + e, extents + e + ranks[i]);
+            e += ranks[i];
+            size_t n = Tensor::element_count(shape);
+            ps[s]->add(names[i], Tensor(shape, std::vector<float>(sets[s] + off, sets[s] + off + n)));
+            off += n;
+        }
+    }
+    ck.outer_step = outer_step;
+    ck.inner.step = adam_step;
+    ck.rng_seed = rng_seed;
+    ck.data_counter = data_counter;
+    ck.shard = shard;
+    std::memcpy(ck.config_hash.data(), hash, 32);
+    return ck;
+}
+
+// Flat view of a decoded Checkpoint: scalars[5] = outer_step, inner.step,
+// rng_seed, data_counter, shard; sets[s] receive numel floats each (numel_cap).
+static void ck_to_flat(const Checkpoint& ck, float* const* sets, uint64_t numel_cap, uint64_t* scalars,
+                       uint8_t* hash) {
+    const ModelParams* ps[5] = {&ck.params, &ck.retained, &ck.inner.m, &ck.inner.v, &ck.outer.buffer};
+    for (int s = 0; s < 5; ++s) {
+        uint64_t off = 0;
+        for (const auto& [n, t] : ps[s]->entries) {
+            if (off + t.size() > numel_cap) throw Error("numel_cap too small");
+            if (sets && sets[s]) std::memcpy(sets[s] + off, t.data.data(), t.size() * sizeof(float));
+            off += t.size();
+        }
+    }
+    scalars[0] = ck.outer_step;
+    scalars[1] = ck.inner.step;
+    scalars[2] = ck.rng_seed;
+    scalars[3] = ck.data_counter;
+    scalars[4] = ck.shard;
+    std::memcpy(hash, ck.config_hash.data(), 32);
+}
+
+template <typename F>
+static int guarded_msg(char* msg, uint64_t cap, F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const ShapeError& e) {
+        std::snprintf(msg, cap, "%s", e.what());
+        return 1;
+    } catch (const NumericError& e) {
+        std::snprintf(msg, cap, "%s", e.what());
+        return 2;
+    } catch (const DecodeError& e) {
+        std::snprintf(msg, cap, "%s", e.what());
+        return 3;
+    } catch (const std::exception& e) {
+        std::snprintf(msg, cap, "%s", e.what());
+        return 9;
+    }
+}
+
+extern "C" {
+
+int ref_encode_checkpoint(uint64_t outer_step, uint32_t nt, const char* const* names, const uint32_t* ranks,
+                          const uint32_t* extents, const float* const* sets, uint64_t adam_step, uint64_t rng_seed,
+                          uint64_t data_counter, uint32_t shard, const uint8_t* hash, uint8_t* out, uint64_t cap,
+                          uint64_t* len) {
+    return guarded([&] {
+        Bytes b = encode_checkpoint(ck_from_flat(outer_step, nt, names, ranks, extents, sets, adam_step, rng_seed,
+                                                 data_counter, shard, hash));
+        *len = b.size();
+        if (b.size() > cap) throw Error("cap");
+        std::memcpy(out, b.data(), b.size());
+    });
+}
+
+int ref_decode_checkpoint(const uint8_t* buf, uint64_t len, float* const* sets, uint64_t numel_cap,
+                          uint64_t* scalars, uint8_t* hash, char* msg, uint64_t msg_cap) {
+    return guarded_msg(msg, msg_cap, [&] {
+        Bytes b(buf, buf + len);
+        ck_to_flat(decode_checkpoint(b), sets, numel_cap, scalars, hash);
+    });
+}
+
+int ref_write_checkpoint_file(const char* path, uint64_t outer_step, uint32_t nt, const char* const* names,
+                              const uint32_t* ranks, const uint32_t* extents, const float* const* sets,
+                              uint64_t adam_step, uint64_t rng_seed, uint64_t data_counter, uint32_t shard,
+                              const uint8_t* hash) {
+    return guarded([&] {
+        write_checkpoint_file(path, ck_from_flat(outer_step, nt, names, ranks, extents, sets, adam_step, rng_seed,
+                                                 data_counter, shard, hash));
+    });
+}
+
+int ref_read_checkpoint_file(const char* path, float* const* sets, uint64_t numel_cap, uint64_t* scalars,
+                             uint8_t* hash, char* msg, uint64_t msg_cap) {
+    return guarded_msg(msg, msg_cap, [&] { ck_to_flat(read_checkpoint_file(path), sets, numel_cap, scalars, hash); });
+}
+
+int ref_sha256(const uint8_t* p, uint64_t n, uint8_t* out) {
+    auto d = Sha256::hash(p, n);
+    std::memcpy(out, d.data(), 32);
+    return 0;
 }
 
 }  // extern "C"

@@ -13,6 +13,8 @@ from .emesh import (  # noqa: F401
     compute_pseudo_gradient, decode_quant_chunk, dequantize, dequantize_into, encode_quant_chunk,
     nesterov_outer_step, quantize, quantize_segments, codec_check, ring_allreduce, segment_table,
     MeshState, RetryResult, allreduce_with_retry, plan_tensor_segments, AdamWState, adamw_step,
+    Checkpoint, encode_checkpoint, decode_checkpoint, checkpoint_layout, write_checkpoint_file,
+    read_checkpoint_file, sha256,
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -26,9 +26,12 @@ EXPORTS = (
     "emesh_engine_outer_sync_host", "emesh_engine_check", "emesh_engine_payload", "emesh_engine_payload_host",
     "emesh_engine_launches", "emesh_engine_profile", "emesh_engine_profile_read", "emesh_engine_timeline", "emesh_engine_transport",
     "emesh_trace_enable", "emesh_trace_read",
+    "emesh_checkpoint_encoded_size", "emesh_checkpoint_encode", "emesh_checkpoint_decode",
+    "emesh_checkpoint_probe", "emesh_checkpoint_layout", "emesh_checkpoint_write_file",
+    "emesh_checkpoint_read_file", "emesh_sha256",
 )
 
-OK, ESHAPE, ENUMERIC, EDECODE, ECUDA, ENCCL, ERING, ECONFIG = range(8)
+OK, ESHAPE, ENUMERIC, EDECODE, ECUDA, ENCCL, ERING, ECONFIG, EIO = range(9)
 
 
 class EngineConfig(C.Structure):
@@ -55,6 +58,27 @@ class RingOp(C.Structure):
         ("send_chunk", C.c_int32), ("recv_chunk", C.c_int32),
         ("send_seg0", C.c_uint32), ("send_nseg", C.c_uint32), ("recv_seg0", C.c_uint32), ("recv_nseg", C.c_uint32),
         ("final_hop", C.c_int32), ("pad", C.c_int32),
+    ]
+
+
+class CheckpointView(C.Structure):
+    """emesh_checkpoint (include/emesh_b200.h; checkpoint.hpp:19-29)."""
+    _fields_ = [
+        ("outer_step", C.c_uint64),
+        ("ntensors", C.c_uint32),
+        ("names", C.c_void_p),
+        ("ranks", C.c_void_p),
+        ("extents", C.c_void_p),
+        ("params", C.c_void_p),
+        ("retained", C.c_void_p),
+        ("adam_m", C.c_void_p),
+        ("adam_v", C.c_void_p),
+        ("nesterov_buf", C.c_void_p),
+        ("adam_step", C.c_uint64),
+        ("rng_seed", C.c_uint64),
+        ("data_counter", C.c_uint64),
+        ("shard", C.c_uint32),
+        ("config_hash", C.c_uint8 * 32),
     ]
 
 
@@ -108,6 +132,14 @@ def lib() -> C.CDLL:
         "emesh_engine_profile_read": (i32, [vp, u32, P(u64), P(C.c_double), P(C.c_double)]),
         "emesh_engine_timeline": (u64, [vp, P(C.c_double), u64]),
         "emesh_engine_transport": (i32, [vp]),
+        "emesh_checkpoint_encoded_size": (i32, [P(CheckpointView), P(u64)]),
+        "emesh_checkpoint_encode": (i32, [P(CheckpointView), vp, u64, P(u64), vp]),
+        "emesh_checkpoint_decode": (i32, [vp, u64, P(CheckpointView), vp]),
+        "emesh_checkpoint_probe": (i32, [vp, u64, P(u32), P(u64), P(u64), P(u32)]),
+        "emesh_checkpoint_layout": (i32, [vp, u64, vp, u64, vp, vp, u32]),
+        "emesh_checkpoint_write_file": (i32, [C.c_char_p, P(CheckpointView), vp]),
+        "emesh_checkpoint_read_file": (i32, [C.c_char_p, P(CheckpointView), vp]),
+        "emesh_sha256": (i32, [vp, u64, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

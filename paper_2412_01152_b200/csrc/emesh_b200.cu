@@ -35,6 +35,17 @@ int fail(int code, const char* fmt, ...) {
     return code;
 }
 
+}  // namespace
+
+namespace emesh_b200 {
+int set_error(int code, const std::string& msg) {  // for the other translation units (checkpoint.cu)
+    g_err = msg;
+    return code;
+}
+}  // namespace emesh_b200
+
+namespace {
+
 #define CU(call)                                                                          \
     do {                                                                                  \
         cudaError_t e_ = (call);                                                          \

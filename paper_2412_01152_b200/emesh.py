@@ -10,6 +10,7 @@ fallback: without the built library or a GPU every call raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence
@@ -61,7 +62,7 @@ class NcclError(RingFailureError):
 _ERRS = {
     _capi.ESHAPE: ShapeError, _capi.ENUMERIC: NumericError, _capi.EDECODE: DecodeError,
     _capi.ECUDA: CudaError, _capi.ENCCL: NcclError, _capi.ERING: RingFailureError,
-    _capi.ECONFIG: ConfigError,
+    _capi.ECONFIG: ConfigError, _capi.EIO: Error,
 }
 
 
@@ -312,6 +313,129 @@ class AdamWState:
     @staticmethod
     def zeros_like(params: ModelParams) -> "AdamWState":
         return AdamWState(0, params.zeros_like(), params.zeros_like())
+
+
+# ---------------------------------------------------------------- checkpoint.hpp:19-68,190-224
+
+
+@dataclass
+class Checkpoint:
+    """checkpoint.hpp:19-29. The five parameter sets are device ModelParams
+    (flat HBM arenas); (de)serialization moves them straight between HBM and
+    the canonical bytes (include/emesh_b200.h, emesh_checkpoint_*)."""
+
+    outer_step: int
+    params: ModelParams
+    retained: ModelParams
+    inner: AdamWState
+    outer: NesterovState
+    rng_seed: int = 0
+    data_counter: int = 0
+    shard: int = 0
+    config_hash: bytes = bytes(32)
+
+    @staticmethod
+    def zeros_like(params: ModelParams) -> "Checkpoint":
+        return Checkpoint(0, params.zeros_like(), params.zeros_like(), AdamWState.zeros_like(params),
+                          NesterovState.zeros_like(params))
+
+
+def _ck_view(ck: Checkpoint):
+    sets = (ck.params, ck.retained, ck.inner.m, ck.inner.v, ck.outer.buffer)
+    for other in sets[1:]:
+        if not sets[0].same_shapes(other):
+            raise ShapeError("checkpoint tensor shapes inconsistent")
+    p = sets[0]
+    names = [nm.encode() for nm in p.names]
+    c_names = (C.c_char_p * max(len(names), 1))(*names)
+    ranks = (C.c_uint32 * max(len(p.shapes), 1))(*[len(sh) for sh in p.shapes])
+    ext = [e for sh in p.shapes for e in sh]
+    c_ext = (C.c_uint32 * max(len(ext), 1))(*ext)
+    v = _capi.CheckpointView()
+    v.outer_step, v.ntensors = ck.outer_step, len(names)
+    v.names, v.ranks, v.extents = C.cast(c_names, C.c_void_p), C.cast(ranks, C.c_void_p), C.cast(c_ext, C.c_void_p)
+    v.params, v.retained, v.adam_m, v.adam_v, v.nesterov_buf = (s_.arena.data_ptr() for s_ in sets)
+    v.adam_step, v.rng_seed, v.data_counter, v.shard = ck.inner.step, ck.rng_seed, ck.data_counter, ck.shard
+    if len(ck.config_hash) != 32:
+        raise ShapeError("config_hash must be 32 bytes")
+    v.config_hash[:] = list(ck.config_hash)
+    return v, (c_names, ranks, c_ext)  # keep the arrays alive with the view
+
+
+def _ck_scalars_back(ck: Checkpoint, v) -> None:
+    ck.outer_step, ck.inner.step, ck.rng_seed = int(v.outer_step), int(v.adam_step), int(v.rng_seed)
+    ck.data_counter, ck.shard, ck.config_hash = int(v.data_counter), int(v.shard), bytes(v.config_hash)
+
+
+def encode_checkpoint(ck: Checkpoint, stream=None) -> bytes:
+    """checkpoint.hpp:32-47, straight from the device arenas."""
+    v, keep = _ck_view(ck)
+    n = C.c_uint64()
+    _check(_capi.lib().emesh_checkpoint_encoded_size(C.byref(v), C.byref(n)))
+    out = C.create_string_buffer(n.value)
+    _check(_capi.lib().emesh_checkpoint_encode(C.byref(v), C.addressof(out), n.value, C.byref(n), _stream(stream)))
+    return out.raw
+
+
+def checkpoint_layout(buf: bytes) -> List:
+    """The (name, shape) list a checkpoint's bytes hold (its params set)."""
+    L = _capi.lib()
+    nt, numel, nb, rs = C.c_uint32(), C.c_uint64(), C.c_uint64(), C.c_uint32()
+    _check(L.emesh_checkpoint_probe(buf, len(buf), C.byref(nt), C.byref(numel), C.byref(nb), C.byref(rs)))
+    names = C.create_string_buffer(max(nb.value, 1))
+    ranks = (C.c_uint32 * max(nt.value, 1))()
+    ext = (C.c_uint32 * max(rs.value, 1))()
+    _check(L.emesh_checkpoint_layout(buf, len(buf), names, nb.value, ranks, ext, rs.value))
+    out, at, e = [], 0, 0
+    raw = names.raw
+    for i in range(nt.value):
+        end = raw.index(b"\0", at)
+        out.append((raw[at:end].decode(), tuple(ext[e: e + ranks[i]])))
+        at, e = end + 1, e + ranks[i]
+    return out
+
+
+def decode_checkpoint(buf: bytes, like: Optional[ModelParams] = None, device="cuda", stream=None) -> Checkpoint:
+    """checkpoint.hpp:49-66 into device arenas shaped like ``like`` (else
+    the layout the bytes hold); raises DecodeError / ShapeError like the
+    reference."""
+    if like is None:
+        like = ModelParams(checkpoint_layout(buf), device=device)
+    ck = Checkpoint.zeros_like(like)
+    v, keep = _ck_view(ck)
+    _check(_capi.lib().emesh_checkpoint_decode(buf, len(buf), C.byref(v), _stream(stream)))
+    _ck_scalars_back(ck, v)
+    return ck
+
+
+def write_checkpoint_file(path: str, ck: Checkpoint, stream=None) -> None:
+    """checkpoint.hpp:190-203 (length + sha256 head, payload streamed from HBM)."""
+    v, keep = _ck_view(ck)
+    _check(_capi.lib().emesh_checkpoint_write_file(os.fsencode(path), C.byref(v), _stream(stream)))
+
+
+def read_checkpoint_file(path: str, like: Optional[ModelParams] = None, device="cuda", stream=None) -> Checkpoint:
+    """checkpoint.hpp:205-224: Error on a missing file / hash mismatch,
+    DecodeError on truncation, then decode_checkpoint."""
+    if like is None:
+        try:
+            with open(path, "rb") as f:
+                body = f.read()[40:]
+        except OSError as e:
+            raise Error(f"cannot read checkpoint file {path}") from e
+        like = ModelParams(checkpoint_layout(body), device=device)
+    ck = Checkpoint.zeros_like(like)
+    v, keep = _ck_view(ck)
+    _check(_capi.lib().emesh_checkpoint_read_file(os.fsencode(path), C.byref(v), _stream(stream)))
+    _ck_scalars_back(ck, v)
+    return ck
+
+
+def sha256(data: bytes) -> bytes:
+    """sha256.hpp Sha256::hash (host)."""
+    out = (C.c_uint8 * 32)()
+    _check(_capi.lib().emesh_sha256(data, len(data), out))
+    return bytes(out)
 
 
 def adamw_step(params: ModelParams, grads: ModelParams, state: AdamWState, hp: HyperParams, lr_scale: float,
