@@ -408,6 +408,23 @@ constexpr uint32_t kMaxSegsSmem = 128;  // SegInfo cached in smem when it fits (
 
 __device__ void finalize_stats(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si);
 
+#ifndef EMESH_SCRATCH_EVICT_LAST
+#define EMESH_SCRATCH_EVICT_LAST 0
+#endif
+// Scratch x (written by STATS, read once by BIN, then discarded): an
+// L2::evict_last hint keeps it ahead of the streaming (evict-first) inputs.
+__device__ __forceinline__ void st_scratch(float4* p, float4 v) {
+#if EMESH_SCRATCH_EVICT_LAST
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w), "l"(pol)
+                 : "memory");
+#else
+    *p = v;
+#endif
+}
+
 template <int SRC>
 __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si,
                                            uint32_t tile) {
@@ -489,7 +506,7 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
                     // fused multiply-adds for the squares
                     q0 = __fma_rn(v2, v2, __fma_rn(v0, v0, q0));
                     q1 = __fma_rn(v3, v3, __fma_rn(v1, v1, q1));
-                    if (SRC != kSrcA) xs[q] = make_float4(x[0], x[1], x[2], x[3]);
+                    if (SRC != kSrcA) st_scratch(xs + q, make_float4(x[0], x[1], x[2], x[3]));
                 } else {
                     uint32_t vm = 0u;
 #pragma unroll
