@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <chrono>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <string>
@@ -897,6 +898,7 @@ struct emesh_engine {
     Workspace ws;
     ncclComm_t comm = nullptr;
     cudaStream_t s_comp = nullptr, s_comm = nullptr;
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // outer_sync_host's copy engines (created on first use)
     cudaEvent_t ev_entry = nullptr, ev_done = nullptr, ev_comm_done = nullptr;
     std::vector<cudaEvent_t> ev_send, ev_recv;  // per window
     std::vector<emesh_ring_op> schedule;        // NCCL mode program (build_schedule)
@@ -1103,43 +1105,55 @@ int hop_src(bool from_theta, uint32_t s, uint32_t k) {
 
 // ---- virtual ring: all k workers on this GPU, one stream, zero-copy hand-off
 // (worker w reads its predecessor's payload arena in place of a recv).
-int run_virtual(emesh_engine* e, const float* const* A, const float* const* B, float* const* theta, float* const* buf,
-                float* const* local_out, float* const* out, float lr, float mom) {
-    if (e->fp32) return run_virtual_f32(e, A, B, theta, buf, local_out, out, lr, mom);
+// One chunk of the virtual ring: its RS chain (hop 0 on the worker that
+// owns the chunk's first payload, then one requantizing hop per successor,
+// allreduce.hpp:411-446); run_virtual_apply then has every worker decode the
+// owner's final bytes (the all-gather is zero-copy here). Each chunk's chain only
+// reads its own previous hop, so running the ring chunk-major is the same
+// arithmetic as hop-major; it lets host copies of chunk c+1 overlap chunk c.
+int run_virtual_chain(emesh_engine* e, uint32_t c, const float* const* A, const float* const* B) {
     const uint32_t k = e->k;
     cudaStream_t st = e->s_comp;
     const bool pg = B != nullptr;
-    // hop 0 payload: Q(own chunk) (allreduce.hpp:411-414 with s = 0)
-    for (uint32_t w = 0; w < k; ++w)
-        for (const Batch& bt : e->plan.batches[w]) {
-            QuantIO io{pg ? kSrcAminusB : kSrcA, A[w], pg ? B[w] : nullptr, nullptr, nullptr, 1.f,
-                       e->arenas[w].codes, e->arenas[w].cbs, e->arenas[w].stats};
+    for (const Batch& bt : e->plan.batches[c]) {  // hop 0: Q(own chunk) on worker c (s = 0)
+        QuantIO io{pg ? kSrcAminusB : kSrcA, A[c], pg ? B[c] : nullptr, nullptr, nullptr, 1.f,
+                   e->arenas[c].codes, e->arenas[c].cbs, e->arenas[c].stats};
+        TRY(launch_quant(bt, e->ws, io, st, &e->tr));
+    }
+    for (uint32_t s = 0; s + 1 < k; ++s) {  // hop s + 1: worker w receives chunk c from pred
+        const uint32_t w = (c + s + 1) % k, pred = (w + k - 1) % k;
+        for (const Batch& bt : e->plan.batches[c]) {
+            QuantIO io{hop_src(pg, s, k), A[w], pg ? B[w] : nullptr, e->arenas[pred].codes, e->arenas[pred].cbs,
+                       (float)k, e->arenas[w].codes, e->arenas[w].cbs, e->arenas[w].stats};
             TRY(launch_quant(bt, e->ws, io, st, &e->tr));
         }
-    for (uint32_t s = 0; s + 1 < k; ++s)
-        for (uint32_t w = 0; w < k; ++w) {
-            const uint32_t pred = (w + k - 1) % k;
-            const uint32_t recv_c = (w + k - s - 1) % k;
-            for (const Batch& bt : e->plan.batches[recv_c]) {
-                QuantIO io{hop_src(pg, s, k), A[w], pg ? B[w] : nullptr, e->arenas[pred].codes,
-                           e->arenas[pred].cbs, (float)k, e->arenas[w].codes, e->arenas[w].cbs, e->arenas[w].stats};
-                TRY(launch_quant(bt, e->ws, io, st, &e->tr));
-            }
+    }
+    return EMESH_OK;
+}
+
+// Worker w decodes the owner's final bytes of chunk c (+ Nesterov).
+int run_virtual_apply(emesh_engine* e, uint32_t c, uint32_t w, float* const* theta, float* const* buf,
+                      float* const* local_out, float* const* out, float lr, float mom) {
+    const uint32_t owner = (c + e->k - 1) % e->k;
+    for (const Batch& bt : e->plan.batches[c]) {
+        if (out) {
+            TRY(launch_apply(bt, 0, e->arenas[owner].codes, e->arenas[owner].cbs, nullptr, nullptr, nullptr, out[w],
+                             0.f, 0.f, e->s_comp, &e->tr));
+        } else {
+            TRY(launch_apply(bt, 1, e->arenas[owner].codes, e->arenas[owner].cbs, theta[w], buf[w],
+                             local_out ? local_out[w] : nullptr, nullptr, lr, mom, e->s_comp, &e->tr));
         }
-    // every worker decodes the owners' bytes (all-gather is zero-copy here)
-    for (uint32_t w = 0; w < k; ++w)
-        for (uint32_t c = 0; c < k; ++c) {
-            const uint32_t owner = (c + k - 1) % k;
-            for (const Batch& bt : e->plan.batches[c]) {
-                if (out) {
-                    TRY(launch_apply(bt, 0, e->arenas[owner].codes, e->arenas[owner].cbs, nullptr, nullptr, nullptr,
-                                     out[w], 0.f, 0.f, st, &e->tr));
-                } else {
-                    TRY(launch_apply(bt, 1, e->arenas[owner].codes, e->arenas[owner].cbs, theta[w], buf[w],
-                                     local_out ? local_out[w] : nullptr, nullptr, lr, mom, st, &e->tr));
-                }
-            }
-        }
+    }
+    return EMESH_OK;
+}
+
+int run_virtual(emesh_engine* e, const float* const* A, const float* const* B, float* const* theta, float* const* buf,
+                float* const* local_out, float* const* out, float lr, float mom) {
+    if (e->fp32) return run_virtual_f32(e, A, B, theta, buf, local_out, out, lr, mom);
+    for (uint32_t c = 0; c < e->k; ++c) {
+        TRY(run_virtual_chain(e, c, A, B));
+        for (uint32_t w = 0; w < e->k; ++w) TRY(run_virtual_apply(e, c, w, theta, buf, local_out, out, lr, mom));
+    }
     return EMESH_OK;
 }
 
@@ -1478,8 +1492,15 @@ int run_p2p_f32(emesh_engine* e, const float* A, const float* B, float* theta, f
     return EMESH_OK;
 }
 
+// Host-buffer pipelining hooks (outer_sync_host): called on the compute
+// stream before chunk c's inputs are first read (RS), before its decode, and
+// after its decode.
+struct HostPipe {
+    std::function<int(uint32_t)> before_rs, before_apply, after_apply;
+};
+
 int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float* buf, float* local_out, float* out,
-            float lr, float mom) {
+            float lr, float mom, const HostPipe* hp = nullptr) {
     if (e->fp32) return run_p2p_f32(e, A, B, theta, buf, local_out, out, lr, mom);
     const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
     const bool push_final = push_final_payload(e->plan.batches[succ][0]);
@@ -1508,6 +1529,7 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
         QuantIO io{pg ? kSrcAminusB : kSrcA, A, B, nullptr, nullptr, 1.f, nullptr, nullptr, ar.stats};
         to_succ(io);
         io.epoch = ep;
+        if (hp) TRY(hp->before_rs(r));
         mark(EMESH_OP_OWN, 0, true);
         TRY(launch_quant(P[r][0], e->ws, io, sc, &e->tr));
         mark(EMESH_OP_OWN, 0, false);
@@ -1531,6 +1553,7 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
                         io.flags[io.nflags++] = e->peers[q].ag_flag;
                     }
         }
+        if (hp) TRY(hp->before_rs(rc));
         mark(EMESH_OP_QUANT, (int)s, true);
         TRY(launch_quant(P[rc][0], e->ws, io, sc, &e->tr));
         mark(EMESH_OP_QUANT, (int)s, false);
@@ -1546,6 +1569,7 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
     for (uint32_t d = 0; d < k; ++d) {
         const uint32_t c = (succ + k - d) % k;  // succ = own chunk; then chunks owned by r-1, r-2, ...
         const uint32_t* flag = d == 0 ? nullptr : e->ag_flag;
+        if (hp) TRY(hp->before_apply(c));
         mark(EMESH_OP_APPLY, (int)d - 1, true);
         if (out)
             TRY(launch_apply(P[c][0], 0, e->peers[r].codes[par], e->peers[r].cbs[par], nullptr, nullptr, nullptr, out,
@@ -1554,6 +1578,7 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
             TRY(launch_apply(P[c][0], 1, e->peers[r].codes[par], e->peers[r].cbs[par], theta, buf, local_out, nullptr,
                              lr, mom, sc, &e->tr, flag, ep));
         mark(EMESH_OP_APPLY, (int)d - 1, false);
+        if (hp) TRY(hp->after_apply(c));
     }
     return EMESH_OK;
 }
@@ -1872,6 +1897,8 @@ int emesh_engine_destroy(emesh_engine* e) {
     if (e->ev_entry) cudaEventDestroy(e->ev_entry);
     if (e->ev_done) cudaEventDestroy(e->ev_done);
     if (e->ev_comm_done) cudaEventDestroy(e->ev_comm_done);
+    if (e->s_h2d) { cudaStreamSynchronize(e->s_h2d); cudaStreamDestroy(e->s_h2d); }
+    if (e->s_d2h) { cudaStreamSynchronize(e->s_d2h); cudaStreamDestroy(e->s_d2h); }
     if (e->s_comp) cudaStreamDestroy(e->s_comp);
     if (e->s_comm) cudaStreamDestroy(e->s_comm);
     delete e;
@@ -1984,6 +2011,146 @@ int emesh_engine_outer_sync(emesh_engine* e, float* const* theta_g, float* const
     return engine_exit(e, user);
 }
 
+// Host-buffer outer sync on k virtual workers, pipelined by chunk: the
+// inputs of chunk c (every worker's theta_g, theta_l, momentum over the
+// chunk's element runs) go up on one copy stream, the ring of chunk c runs
+// as soon as they landed, and its outputs come back on a second copy stream
+// while later chunks are still uploading — PCIe is full duplex, so the
+// round costs about max(upload, download) instead of their sum.
+static int outer_sync_host_pipelined(emesh_engine* e, float* const* theta_g, float* const* theta_l, float* const* buf,
+                              float lr, float mom, int write_local) {
+    const uint32_t k = e->k;
+    if (!e->s_h2d) CU(cudaStreamCreateWithFlags(&e->s_h2d, cudaStreamNonBlocking));
+    if (!e->s_d2h) CU(cudaStreamCreateWithFlags(&e->s_d2h, cudaStreamNonBlocking));
+    // ev[c]: chunk c's theta_g / theta_l of every worker landed; ev[k + c*k + w]:
+    // worker w's momentum of chunk c landed; ev[k + k*k + c*k + w]: its outputs are final
+    std::vector<cudaEvent_t> ev(k + 2 * k * k, nullptr);
+    for (auto& x : ev) CU(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    auto ev_theta = [&](uint32_t c) { return ev[c]; };
+    auto ev_buf = [&](uint32_t c, uint32_t w) { return ev[k + c * k + w]; };
+    auto ev_out = [&](uint32_t c, uint32_t w) { return ev[k + k * k + c * k + w]; };
+    int rc = EMESH_OK;
+    std::vector<std::vector<std::pair<uint64_t, uint64_t>>> runs(k);
+    for (uint32_t c = 0; c < k; ++c)  // the chunk's contiguous element runs, adjacent ones merged
+        for (const Batch& bt : e->plan.batches[c])
+            for (const auto& x : bt.eruns) {
+                auto& r = runs[c];
+                if (!r.empty() && r.back().first + r.back().second == x.first) r.back().second += x.second;
+                else if (x.second) r.push_back(x);
+            }
+    auto copy = [&](float* dst, const float* src, uint32_t c, cudaMemcpyKind kind, cudaStream_t st) {
+        for (const auto& x : runs[c])
+            if (cudaMemcpyAsync(dst + x.first, src + x.first, x.second * sizeof(float), kind, st) != cudaSuccess)
+                return fail(EMESH_ECUDA, "outer_sync_host: %s", cudaGetErrorString(cudaGetLastError()));
+        return (int)EMESH_OK;
+    };
+    auto record = [&](cudaEvent_t x, cudaStream_t st) {
+        return cudaEventRecord(x, st) == cudaSuccess ? (int)EMESH_OK : fail(EMESH_ECUDA, "event record");
+    };
+    auto wait = [&](cudaStream_t st, cudaEvent_t x) {
+        return cudaStreamWaitEvent(st, x, 0) == cudaSuccess ? (int)EMESH_OK : fail(EMESH_ECUDA, "stream wait");
+    };
+    // uploads in need order: the chunk's theta_g / theta_l (its RS chain), then its momentum worker by
+    // worker (each worker's decode + Nesterov), so the last bytes up gate only one worker's last decode
+    for (uint32_t c = 0; c < k && !rc; ++c) {
+        for (uint32_t w = 0; w < k && !rc; ++w) {
+            rc = copy(e->h_theta[w], theta_g[w], c, cudaMemcpyHostToDevice, e->s_h2d);
+            if (!rc) rc = copy(e->h_local[w], theta_l[w], c, cudaMemcpyHostToDevice, e->s_h2d);
+        }
+        if (!rc) rc = record(ev_theta(c), e->s_h2d);
+        for (uint32_t w = 0; w < k && !rc; ++w) {
+            rc = copy(e->h_buf[w], buf[w], c, cudaMemcpyHostToDevice, e->s_h2d);
+            if (!rc) rc = record(ev_buf(c, w), e->s_h2d);
+        }
+    }
+    for (uint32_t c = 0; c < k && !rc; ++c) {
+        if ((rc = wait(e->s_comp, ev_theta(c)))) break;
+        if ((rc = run_virtual_chain(e, c, e->h_theta.data(), e->h_local.data()))) break;
+        for (uint32_t w = 0; w < k && !rc; ++w) {
+            if ((rc = wait(e->s_comp, ev_buf(c, w)))) break;
+            if ((rc = run_virtual_apply(e, c, w, e->h_theta.data(), e->h_buf.data(),
+                                        write_local ? e->h_local.data() : nullptr, nullptr, lr, mom)))
+                break;
+            if ((rc = record(ev_out(c, w), e->s_comp)) || (rc = wait(e->s_d2h, ev_out(c, w)))) break;
+            rc = copy(theta_g[w], e->h_theta[w], c, cudaMemcpyDeviceToHost, e->s_d2h);
+            if (!rc) rc = copy(buf[w], e->h_buf[w], c, cudaMemcpyDeviceToHost, e->s_d2h);
+            if (!rc && write_local) rc = copy(theta_l[w], e->h_local[w], c, cudaMemcpyDeviceToHost, e->s_d2h);
+        }
+    }
+    cudaStreamSynchronize(e->s_h2d);
+    cudaStreamSynchronize(e->s_comp);
+    cudaStreamSynchronize(e->s_d2h);
+    for (auto x : ev) cudaEventDestroy(x);
+    if (rc) return rc;
+    return emesh_engine_check(e);
+}
+
+// Host-buffer outer sync, one worker per GPU (peer transport): theta_g /
+// theta_l go up chunk by chunk in the order the ring reads them (own chunk,
+// then r-1, r-2, ...), the momentum in decode order, and each chunk's
+// results come back on a second copy stream as soon as its decode ran.
+static int outer_sync_host_p2p(emesh_engine* e, float* theta_g, float* theta_l, float* buf, float lr, float mom,
+                               int write_local) {
+    const uint32_t k = e->k, r = e->rank;
+    if (!e->s_h2d) CU(cudaStreamCreateWithFlags(&e->s_h2d, cudaStreamNonBlocking));
+    if (!e->s_d2h) CU(cudaStreamCreateWithFlags(&e->s_d2h, cudaStreamNonBlocking));
+    std::vector<cudaEvent_t> ev(3 * k, nullptr);  // [c] theta landed, [k + c] momentum landed, [2k + c] decoded
+    for (auto& x : ev) CU(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    std::vector<std::vector<std::pair<uint64_t, uint64_t>>> runs(k);
+    for (uint32_t c = 0; c < k; ++c)
+        for (const Batch& bt : e->plan.batches[c])
+            for (const auto& x : bt.eruns) {
+                auto& v = runs[c];
+                if (!v.empty() && v.back().first + v.back().second == x.first) v.back().second += x.second;
+                else if (x.second) v.push_back(x);
+            }
+    auto copy = [&](float* dst, const float* src, uint32_t c, cudaMemcpyKind kind, cudaStream_t st) {
+        for (const auto& x : runs[c])
+            if (cudaMemcpyAsync(dst + x.first, src + x.first, x.second * sizeof(float), kind, st) != cudaSuccess)
+                return fail(EMESH_ECUDA, "outer_sync_host: %s", cudaGetErrorString(cudaGetLastError()));
+        return (int)EMESH_OK;
+    };
+    float* dg = e->h_theta[0];
+    float* dl = e->h_local[0];
+    float* db = e->h_buf[0];
+    int rc = EMESH_OK;
+    for (uint32_t i = 0; i < k && !rc; ++i) {  // RS read order: r, r-1, ..., r+1
+        const uint32_t c = (r + k - i) % k;
+        rc = copy(dg, theta_g, c, cudaMemcpyHostToDevice, e->s_h2d);
+        if (!rc) rc = copy(dl, theta_l, c, cudaMemcpyHostToDevice, e->s_h2d);
+        if (!rc && cudaEventRecord(ev[c], e->s_h2d) != cudaSuccess) rc = fail(EMESH_ECUDA, "event record");
+    }
+    for (uint32_t d = 0; d < k && !rc; ++d) {  // decode order: r+1, r, r-1, ...
+        const uint32_t c = (r + 1 + k - d) % k;
+        rc = copy(db, buf, c, cudaMemcpyHostToDevice, e->s_h2d);
+        if (!rc && cudaEventRecord(ev[k + c], e->s_h2d) != cudaSuccess) rc = fail(EMESH_ECUDA, "event record");
+    }
+    HostPipe hp;
+    hp.before_rs = [&](uint32_t c) {
+        return cudaStreamWaitEvent(e->s_comp, ev[c], 0) == cudaSuccess ? (int)EMESH_OK : fail(EMESH_ECUDA, "wait");
+    };
+    hp.before_apply = [&](uint32_t c) {
+        return cudaStreamWaitEvent(e->s_comp, ev[k + c], 0) == cudaSuccess ? (int)EMESH_OK
+                                                                              : fail(EMESH_ECUDA, "wait");
+    };
+    hp.after_apply = [&](uint32_t c) {
+        if (cudaEventRecord(ev[2 * k + c], e->s_comp) != cudaSuccess ||
+            cudaStreamWaitEvent(e->s_d2h, ev[2 * k + c], 0) != cudaSuccess)
+            return fail(EMESH_ECUDA, "event record");
+        int q = copy(theta_g, dg, c, cudaMemcpyDeviceToHost, e->s_d2h);
+        if (!q) q = copy(buf, db, c, cudaMemcpyDeviceToHost, e->s_d2h);
+        if (!q && write_local) q = copy(theta_l, dl, c, cudaMemcpyDeviceToHost, e->s_d2h);
+        return q;
+    };
+    // (no engine_enter: the compute stream must not wait for the whole upload, only per chunk)
+    if (!rc) rc = run_p2p(e, dg, dl, dg, db, write_local ? dl : nullptr, nullptr, lr, mom, &hp);
+    cudaStreamSynchronize(e->s_h2d);
+    const int crc = emesh_engine_check(e);  // bounded: a vanished peer surfaces as EMESH_ERING
+    cudaStreamSynchronize(e->s_d2h);
+    for (auto x : ev) cudaEventDestroy(x);
+    return rc ? rc : crc;
+}
+
 int emesh_engine_outer_sync_host(emesh_engine* e, float* const* theta_g, float* const* theta_l, float* const* buf,
                                  float lr, float mom, int write_local) {
     CU(cudaSetDevice(e->device));
@@ -1999,6 +2166,11 @@ int emesh_engine_outer_sync_host(emesh_engine* e, float* const* theta_g, float* 
             CU(cudaMalloc(&e->h_buf[w], bytes + 16));
         }
     }
+    static const bool serial = std::getenv("EMESH_HOST_SERIAL") != nullptr;  // A/B knob
+    if (e->virt && !e->fp32 && e->k > 1 && !serial)
+        return outer_sync_host_pipelined(e, theta_g, theta_l, buf, lr, mom, write_local);
+    if (!e->virt && !e->fp32 && e->k > 1 && e->transport == EMESH_TRANSPORT_P2P && !serial)
+        return outer_sync_host_p2p(e, theta_g[0], theta_l[0], buf[0], lr, mom, write_local);
     cudaStream_t st = e->s_comp;
     for (uint32_t w = 0; w < e->workers; ++w) {
         CU(cudaMemcpyAsync(e->h_theta[w], theta_g[w], bytes, cudaMemcpyHostToDevice, st));

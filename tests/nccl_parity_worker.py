@@ -58,6 +58,17 @@ def main():
             if not (np.array_equal(bits(tg.cpu().numpy()), bits(eg)) and np.array_equal(bits(tb.cpu().numpy()), bits(eb))):
                 print(f"rank {rank}: [{transport} {mode}] outer sync n={n} round {rnd} MISMATCH", flush=True)
                 ok = False
+        # a third round through the host-buffer entry point (chunk-pipelined copies)
+        ls = [(eg - O.uniform(n, 40, 1 + w, 0, 0, 2.0 ** -10)).astype(np.float32) for w in range(world)]
+        hg = torch.from_numpy(tg.cpu().numpy().copy()).pin_memory()
+        hb = torch.from_numpy(tb.cpu().numpy().copy()).pin_memory()
+        hl = torch.from_numpy(ls[rank].copy()).pin_memory()
+        eng.outer_sync_host([hg], [hl], [hb], E.HyperParams(), write_local=True)
+        eg, eb = O.outer_sync(eg, ls, eb, S, mode, 0.7, 0.9)
+        if not (np.array_equal(bits(hg.numpy()), bits(eg)) and np.array_equal(bits(hb.numpy()), bits(eb))
+                and np.array_equal(bits(hl.numpy()), bits(eg))):
+            print(f"rank {rank}: [{transport} {mode}] outer_sync_host n={n} MISMATCH", flush=True)
+            ok = False
         eng.close()
     # multi-tensor engine (config 5): one ReduceJob per tensor, chunks bucketed per hop
     sizes = [4096, 17, 0, 100_003, 1, 65_536, 3, 250_000]

@@ -143,8 +143,10 @@ def test_outer_sync_vs_oracle_two_rounds(E, oracle, k):
     eng.close()
 
 
-def test_outer_sync_host_api(E, oracle):
-    n, k, S = 100_000, 2, 4
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_outer_sync_host_api(E, oracle, k):
+    """Host buffers, chunk-pipelined copies (emesh_engine_outer_sync_host): bit-exact vs the oracle."""
+    n, S = 100_003, 4
     g = oracle.uniform(n, 8, 0)
     ls = [(g - oracle.uniform(n, 8, 1 + w, 0, 0, 2.0 ** -10)).astype(np.float32) for w in range(k)]
     b = oracle.uniform(n, 8, 7, 0, 0, 1e-3)
@@ -159,6 +161,32 @@ def test_outer_sync_host_api(E, oracle):
         assert np.array_equal(bits(hb[w].numpy()), bits(eb))
         assert np.array_equal(bits(hl[w].numpy()), bits(eg))
     eng.close()
+
+
+def test_outer_sync_host_multi_tensor_two_rounds(E):
+    """Host path over a multi-tensor plan (per-tensor chunk runs), two rounds: identical to the device path."""
+    sizes = [4096, 1_000_003, 17, 250_000, 4096 * 3]
+    n, k = sum(sizes), 4
+    gen = torch.Generator().manual_seed(3)
+    g0 = torch.randn(n, generator=gen)
+    ls = [[g0 - 1e-3 * torch.randn(n, generator=gen) for _ in range(k)] for _ in range(2)]
+    eng_h = E.RingEngine(n, k, opts=E.ReduceOptions(pipeline_subchunks=4), virtual=True, tensor_sizes=sizes)
+    eng_d = E.RingEngine(n, k, opts=E.ReduceOptions(pipeline_subchunks=4), virtual=True, tensor_sizes=sizes)
+    hg = [g0.clone().pin_memory() for _ in range(k)]
+    hb = [torch.zeros(n).pin_memory() for _ in range(k)]
+    dg = [g0.cuda() for _ in range(k)]
+    db = [torch.zeros(n, device="cuda") for _ in range(k)]
+    for rnd in range(2):
+        hl = [a.clone().pin_memory() for a in ls[rnd]]
+        dl = [a.cuda() for a in ls[rnd]]
+        eng_h.outer_sync_host(hg, hl, hb, E.HyperParams(), write_local=False)
+        eng_d.outer_sync(dg, dl, db, E.HyperParams(), write_local=False)
+        eng_d.check()
+        for w in range(k):
+            assert torch.equal(hg[w].view(torch.int32), dg[w].cpu().view(torch.int32)), (rnd, w)
+            assert torch.equal(hb[w].view(torch.int32), db[w].cpu().view(torch.int32)), (rnd, w)
+    eng_h.close()
+    eng_d.close()
 
 
 def test_full_size_properties_config1(E, oracle):
