@@ -19,6 +19,9 @@
 
 #include "emesh_b200.h"
 #include "kernels.cuh"
+#ifndef EMESH_BIN_L1PF_CARVEOUT
+#define EMESH_BIN_L1PF_CARVEOUT 50
+#endif
 
 using namespace emesh_b200;
 
@@ -538,6 +541,10 @@ int persistent_grid(const void* fn, uint32_t ntasks) {
         if (!per_sm) {
             if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQuantSmemBytes) != cudaSuccess)
                 return -1;
+#if EMESH_BIN_L1PF
+            // leave L1 room for the prefetched scratch lines (smem only as large as the CTAs need)
+            cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, EMESH_BIN_L1PF_CARVEOUT);
+#endif
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, kQuantSmemBytes) != cudaSuccess)
                 return -1;
             cache.push_back({fn, per_sm});

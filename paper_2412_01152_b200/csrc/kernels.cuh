@@ -653,6 +653,22 @@ struct BinParams {
 // common path has no data-dependent branches (invalid lanes add 0).
 // Per-warp limbs over a tile (see kLoBits): A += low bits | one count,
 // B += middle bits, C += high bits (only when nonzero: rare).
+#ifndef EMESH_BIN_L1PF
+#define EMESH_BIN_L1PF 0
+#endif
+// BIN's scratch reads. With EMESH_BIN_L1PF the warp prefetches its next
+// unit's 4 KB of scratch into L1 while it bins the current one, and the
+// loads go through L1 (each scratch line is written once, by STATS, before
+// the segment's statistics are published, and read once after: no stale L1
+// copy can exist within the launch).
+__device__ __forceinline__ float4 ld_scratch(const float4* p) {
+#if EMESH_BIN_L1PF
+    return *p;
+#else
+    return __ldcg(p);
+#endif
+}
+
 template <bool INTERIOR, bool FROM_SCRATCH>
 __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const SegInfo& si, uint64_t qbase,
                                          uint64_t hiel, const float4* xs, uint32_t* hw, const BinParams& p,
@@ -666,7 +682,7 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
         for (int jj = 0; jj < kHalf; ++jj) {
             const uint64_t q = qbase + (uint64_t)(h * kHalf + jj) * 32 + lane;
             const bool in = INTERIOR || q * 4 < hiel;
-            xv[jj] = !in ? make_float4(0.f, 0.f, 0.f, 0.f) : FROM_SCRATCH ? __ldcg(xs + q) : ld4(a.a, q);
+            xv[jj] = !in ? make_float4(0.f, 0.f, 0.f, 0.f) : FROM_SCRATCH ? ld_scratch(xs + q) : ld4(a.a, q);
         }
 #pragma unroll
         for (int pr = 0; pr < kHalf / 2; ++pr) {
@@ -815,6 +831,12 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
         if (u >= si.nunits) break;
         const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
         const bool interior = qbase * 4 >= si.lo && (qbase + kUnitSlots) * 4 <= hiel;  // warp-uniform
+#if EMESH_BIN_L1PF
+        if (FROM_SCRATCH && ui + 1 < kUnitsPerWarp && u + kWarps < si.nunits) {
+            const float4* nx = xs + qbase + (uint64_t)kWarps * kUnitSlots + lane * 8;  // one 128-B line per lane
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(nx));
+        }
+#endif
         if (degenerate) {  // sigma == 0: every code is 0 (quant.hpp:49-55)
             for (int j = 0; j < kSlotsPerLane; ++j) {
                 const uint64_t q = qbase + (uint64_t)j * 32 + lane;
