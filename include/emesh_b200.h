@@ -121,9 +121,11 @@ typedef struct {
                                    k chunks x min(S, len) segments per tensor, all tensors' chunk c
                                    reduced together ("bucketing") */
     uint32_t ntensors;
-    double step_timeout_s;      /* ReduceOptions.step_timeout (allreduce.hpp:59): a peer-transport wait that
-                                   exceeds it aborts the round; emesh_engine_check then returns EMESH_ERING
-                                   (RingFailureError). 0 = 30 s. */
+    double step_timeout_s;      /* ReduceOptions.step_timeout (allreduce.hpp:59): a wait on a peer that
+                                   exceeds it aborts the round and emesh_engine_check returns EMESH_ERING
+                                   (RingFailureError) — peer transport: the kernels' spin budget; NCCL
+                                   transport: the non-blocking communicator's enqueue / completion polls,
+                                   after which it is aborted. 0 = 30 s. */
 } emesh_engine_config;
 
 /* Transports of the one-process-per-GPU ring (k > 1, not virtual):
