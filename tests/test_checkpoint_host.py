@@ -149,3 +149,54 @@ def test_read_file_errors_without_device(capi, ck, tmp_path):
     p.write_bytes(bytes(bad))
     assert L.emesh_checkpoint_read_file(str(p).encode(), C.byref(v), None) == capi.EIO
     assert "hash mismatch" in capi.last_error()
+
+
+def test_random_mutations_match_reference(capi, ck):
+    """Seeded fuzz over the golden bytes (truncations, byte flips in the headers, u32 rewrites):
+    every verdict reached on the host equals emesh::decode_checkpoint's (bytes.hpp:52-92 reader,
+    tensor.hpp:122-154, checkpoint.hpp:49-66)."""
+    from oracle.pyoracle import Reference, have_reference
+    if not have_reference():
+        pytest.skip("oracle/_ref not built")
+    R = Reference()
+    L = capi.lib()
+    layout = layout_of(ck)
+    v, keep = view_of(capi, layout)
+    good = ck["encoded"].tobytes()
+    n = ck["sets"].shape[1]
+    rng = np.random.RandomState(1234)
+    # header byte positions: every tensor record's name length, name, rank and extents
+    hdr = []
+    pos = 8
+    for s_ in range(5):
+        if s_ == 2:
+            pos += 8
+        pos += 4
+        for nm, sh in layout:
+            rec = 4 + len(nm.encode()) + 4 + 4 * len(sh)
+            hdr.extend(range(pos, pos + rec))
+            pos += rec + 4 * (int(np.prod(sh)) if sh else 1)
+    checked = 0
+    for it in range(300):
+        b = bytearray(good)
+        kind = it % 3
+        if kind == 0:
+            b = b[: rng.randint(0, len(good))]
+        elif kind == 1:
+            for _ in range(rng.randint(1, 4)):
+                b[hdr[rng.randint(len(hdr))]] ^= 1 << rng.randint(8)
+        else:
+            at = hdr[rng.randint(len(hdr))]
+            b[at: at + 4] = int(rng.choice([0, 1, 9, 1 << 20, 1 << 28, 0xFFFFFFFF])).to_bytes(4, "little")
+        b = bytes(b)
+        rc = L.emesh_checkpoint_decode(b, len(b), C.byref(v), None)
+        ref_rc, ref_msg, *_ = R.decode_checkpoint(b, n)
+        if rc == capi.ECONFIG:  # structurally valid: the verdict needs the device (the reference decoded or
+            assert ref_rc in (0, 3), (it, ref_rc, ref_msg)  # found a non-finite value)
+            continue
+        if rc == capi.EDECODE and "differs from the destination" in capi.last_error():
+            assert ref_rc == 0 or ref_msg == "non-finite value in tensor payload", (it, ref_msg)
+            continue
+        assert (rc, capi.last_error()) == (ref_rc, ref_msg), it
+        checked += 1
+    assert checked > 150
