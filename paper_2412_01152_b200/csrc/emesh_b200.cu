@@ -20,7 +20,7 @@
 #include "emesh_b200.h"
 #include "kernels.cuh"
 #ifndef EMESH_BIN_L1PF_CARVEOUT
-#define EMESH_BIN_L1PF_CARVEOUT 50
+#define EMESH_BIN_L1PF_CARVEOUT 64
 #endif
 
 using namespace emesh_b200;
@@ -140,7 +140,9 @@ struct Plan {
                 const uint64_t nq = q_last - si.q0 + 1;
                 si.nunits = (uint32_t)((nq + kUnitSlots - 1) / kUnitSlots);
                 si.ncta = (si.nunits + kTileUnits - 1) / kTileUnits;
-                sq += nq;
+                // whole units: no 128-B scratch line (and no prefetched unit) is
+                // shared with another segment, whose STATS may not have run yet
+                sq += (nq + kUnitSlots - 1) / kUnitSlots * kUnitSlots;
                 if (first) { b.el_lo = g.lo; first = false; }
                 b.el_lo = std::min(b.el_lo, g.lo);
                 b.el_hi = std::max(b.el_hi, g.lo + g.len);

@@ -201,8 +201,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // ---------------------------------------------------------------------------
 // small helpers
 
+#ifndef EMESH_STREAM_NO_L1
+#define EMESH_STREAM_NO_L1 1
+#endif
+// Streaming (read-once) loads. EMESH_STREAM_NO_L1 (default): no L1
+// allocation, leaving L1 to the BIN scratch prefetch (EMESH_BIN_L1PF);
+// otherwise ld.global.cs (evict-first).
 __device__ __forceinline__ float4 ld4_stream(const float* p, uint64_t q) {
+#if EMESH_STREAM_NO_L1
+    float4 v;
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(reinterpret_cast<const float4*>(p) + q));
+    return v;
+#else
     return __ldcs(reinterpret_cast<const float4*>(p) + q);
+#endif
 }
 __device__ __forceinline__ float4 ld4(const float* p, uint64_t q) {
     return __ldg(reinterpret_cast<const float4*>(p) + q);
@@ -654,13 +668,14 @@ struct BinParams {
 // Per-warp limbs over a tile (see kLoBits): A += low bits | one count,
 // B += middle bits, C += high bits (only when nonzero: rare).
 #ifndef EMESH_BIN_L1PF
-#define EMESH_BIN_L1PF 0
+#define EMESH_BIN_L1PF 1
 #endif
-// BIN's scratch reads. With EMESH_BIN_L1PF the warp prefetches its next
-// unit's 4 KB of scratch into L1 while it bins the current one, and the
-// loads go through L1 (each scratch line is written once, by STATS, before
-// the segment's statistics are published, and read once after: no stale L1
-// copy can exist within the launch).
+// BIN's scratch reads. With EMESH_BIN_L1PF (default) the warp prefetches its
+// next unit's 4 KB of scratch into L1 while it bins the current one, and the
+// loads go through L1. Each scratch line belongs to exactly one segment
+// (segments own whole units of scratch, Plan::add_batch), is written once by
+// its STATS tiles before the segment's statistics are published, and only
+// read (or prefetched) after: no stale L1 copy can exist within the launch.
 __device__ __forceinline__ float4 ld_scratch(const float4* p) {
 #if EMESH_BIN_L1PF
     return *p;

@@ -12,6 +12,8 @@ print('$name', round(d['ms_per_step'], 3), d['roofline']['achieved'], {n: round(
 }
 run base
 run pf64 EMESH_LIB=build_var/libemesh_pf64.so
-run pfdef EMESH_LIB=build_var/libemesh_pfdef.so
+run pfna EMESH_LIB=build_var/libemesh_pfna.so
+run na EMESH_LIB=build_var/libemesh_na.so
 run base2
-run pf64b EMESH_LIB=build_var/libemesh_pf64.so
+run pfna2 EMESH_LIB=build_var/libemesh_pfna.so
+run na2 EMESH_LIB=build_var/libemesh_na.so
