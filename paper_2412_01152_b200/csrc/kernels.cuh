@@ -204,6 +204,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef EMESH_STREAM_NO_L1
 #define EMESH_STREAM_NO_L1 1
 #endif
+#ifndef EMESH_CODES_NO_L1
+#define EMESH_CODES_NO_L1 0
+#endif
+#ifndef EMESH_BIN_PF_FIRST
+#define EMESH_BIN_PF_FIRST 1
+#endif
 // Streaming (read-once) loads. EMESH_STREAM_NO_L1 (default): no L1
 // allocation, leaving L1 to the BIN scratch prefetch (EMESH_BIN_L1PF);
 // otherwise ld.global.cs (evict-first).
@@ -216,6 +222,15 @@ __device__ __forceinline__ float4 ld4_stream(const float* p, uint64_t q) {
     return v;
 #else
     return __ldcs(reinterpret_cast<const float4*>(p) + q);
+#endif
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
+#if EMESH_STREAM_NO_L1 && EMESH_CODES_NO_L1
+    uint32_t v;
+    asm volatile("ld.global.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+#else
+    return __ldcs(p);
 #endif
 }
 __device__ __forceinline__ float4 ld4(const float* p, uint64_t q) {
@@ -479,7 +494,7 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
                 const bool in = interior || q * 4 < hiel;
                 xa[jj] = in ? ld4_stream(a.a, q) : make_float4(0.f, 0.f, 0.f, 0.f);
                 if (SRC & kSrcAminusB) xb[jj] = in ? ld4_stream(a.b, q) : make_float4(0.f, 0.f, 0.f, 0.f);
-                if (SRC & kHasIn) c4[jj] = in ? __ldcs(reinterpret_cast<const uint32_t*>(a.in_codes) + q) : 0u;
+                if (SRC & kHasIn) c4[jj] = in ? ld_stream_u32(reinterpret_cast<const uint32_t*>(a.in_codes) + q) : 0u;
             }
 #pragma unroll
             for (int jj = 0; jj < kHalf; ++jj) {
@@ -814,6 +829,15 @@ template <bool FROM_SCRATCH>
 __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si, uint32_t tile) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const SegStat* st = &a.stats[si.slot];
+#if EMESH_BIN_L1PF && EMESH_BIN_PF_FIRST
+    if (FROM_SCRATCH) {  // the warp's first unit, while the tables load (the segment's scratch is complete)
+        const uint32_t u0 = tile * kTileUnits + warp;
+        if (u0 < si.nunits) {
+            const float4* p0 = reinterpret_cast<const float4*>(a.scratch) + si.sq0 + (uint64_t)u0 * kUnitSlots + lane * 8;
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(p0));
+        }
+    }
+#endif
     if (sm.bin_seg != (int32_t)s) {
         __syncthreads();
         const int b = threadIdx.x;

@@ -1,0 +1,18 @@
+# A/B on the default build: codes loads skip L1 (cna), BIN prefetches each tile's first unit (pff), both
+mkdir -p gpurun_out/ab2
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/ab2/build.log 2>&1 || exit 1
+run() {
+  name=$1; shift
+  env "$@" timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ab2/$name.json 2> gpurun_out/ab2/$name.err
+  python -c "
+import json
+d = json.loads(open('gpurun_out/ab2/$name.json').read().strip().splitlines()[-1])
+k = d['kernels']
+print('$name', round(d['ms_per_step'], 3), round(sum(v['ms_per_step'] for n, v in k.items() if n.startswith('quant')), 3))" || tail -3 gpurun_out/ab2/$name.err
+}
+for r in 1 2; do
+run base$r
+run cna$r EMESH_LIB=build_var/libemesh_cna.so
+run pff$r EMESH_LIB=build_var/libemesh_pff.so
+run both$r EMESH_LIB=build_var/libemesh_both.so
+done
