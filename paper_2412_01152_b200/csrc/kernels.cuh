@@ -224,6 +224,18 @@ __device__ __forceinline__ float4 ld4_stream(const float* p, uint64_t q) {
     return __ldcs(reinterpret_cast<const float4*>(p) + q);
 #endif
 }
+#ifndef EMESH_STATS_L1PF
+#define EMESH_STATS_L1PF 0
+#endif
+// STATS' theta loads: streamed past L1, or (EMESH_STATS_L1PF) through L1 after
+// a prefetch of the warp's next half-unit (read-only inputs of the launch).
+__device__ __forceinline__ float4 ld4_stats(const float* p, uint64_t q) {
+#if EMESH_STATS_L1PF
+    return reinterpret_cast<const float4*>(p)[q];
+#else
+    return ld4_stream(p, q);
+#endif
+}
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
 #if EMESH_STREAM_NO_L1 && EMESH_CODES_NO_L1
     uint32_t v;
@@ -488,12 +500,21 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
         for (int h = 0; h < 2; ++h) {
             float4 xa[kHalf], xb[kHalf];
             uint32_t c4[kHalf];
+#if EMESH_STATS_L1PF
+            {   // the warp's next half-unit of A (lanes 0-15) and B (lanes 16-31) into L1, 2 KB each
+                const bool more = h == 0 || (ui + 1 < kUnitsPerWarp && u + kWarps < si.nunits);
+                const uint64_t qn = h == 0 ? qbase + (uint64_t)kHalf * 32 : qbase + (uint64_t)kWarps * kUnitSlots;
+                const uint64_t ql = qn + (uint64_t)(lane & 15) * 8;
+                if (more && ql * 4 < hiel && ((SRC & kSrcAminusB) || lane < 16))
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const float4*>(lane < 16 ? a.a : a.b) + ql));
+            }
+#endif
 #pragma unroll
             for (int jj = 0; jj < kHalf; ++jj) {
                 const uint64_t q = qbase + (uint64_t)(h * kHalf + jj) * 32 + lane;
                 const bool in = interior || q * 4 < hiel;
-                xa[jj] = in ? ld4_stream(a.a, q) : make_float4(0.f, 0.f, 0.f, 0.f);
-                if (SRC & kSrcAminusB) xb[jj] = in ? ld4_stream(a.b, q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                xa[jj] = in ? ld4_stats(a.a, q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                if (SRC & kSrcAminusB) xb[jj] = in ? ld4_stats(a.b, q) : make_float4(0.f, 0.f, 0.f, 0.f);
                 if (SRC & kHasIn) c4[jj] = in ? ld_stream_u32(reinterpret_cast<const uint32_t*>(a.in_codes) + q) : 0u;
             }
 #pragma unroll
