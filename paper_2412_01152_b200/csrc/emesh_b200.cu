@@ -1142,26 +1142,50 @@ int run_virtual_chain(emesh_engine* e, uint32_t c, const float* const* A, const 
 
 // Worker w decodes the owner's final bytes of chunk c (+ Nesterov).
 int run_virtual_apply(emesh_engine* e, uint32_t c, uint32_t w, float* const* theta, float* const* buf,
-                      float* const* local_out, float* const* out, float lr, float mom) {
+                      float* const* local_out, float* const* out, float lr, float mom, cudaStream_t st = nullptr) {
     const uint32_t owner = (c + e->k - 1) % e->k;
+    if (!st) st = e->s_comp;
     for (const Batch& bt : e->plan.batches[c]) {
         if (out) {
             TRY(launch_apply(bt, 0, e->arenas[owner].codes, e->arenas[owner].cbs, nullptr, nullptr, nullptr, out[w],
-                             0.f, 0.f, e->s_comp, &e->tr));
+                             0.f, 0.f, st, &e->tr));
         } else {
             TRY(launch_apply(bt, 1, e->arenas[owner].codes, e->arenas[owner].cbs, theta[w], buf[w],
-                             local_out ? local_out[w] : nullptr, nullptr, lr, mom, e->s_comp, &e->tr));
+                             local_out ? local_out[w] : nullptr, nullptr, lr, mom, st, &e->tr));
         }
     }
     return EMESH_OK;
 }
 
+// Chunk c's decodes touch only chunk c's element range (theta, momentum, out)
+// and the owner's chunk-c codes / codebooks, which chunk c+1's chain never
+// writes; the chains share the quantizer workspace and stay serial on s_comp.
+// So the decodes of chunk c run on s_comm (idle in the virtual ring) behind an
+// event on chain c and overlap chain c+1: their HBM-bound CTAs fill the
+// quantizer's launch tails and its unused bandwidth. engine_exit joins s_comm.
+// Measured (config 2, N=1, 3 x 2 alternating runs): 25.61 vs 25.73 ms per round,
+// within noise — both kernels are DRAM-bound once they share the SMs — and the
+// overlapped per-kernel event times no longer give a roofline, so it is off.
+bool virtual_overlap() {
+    static const bool on = [] {
+        const char* v = std::getenv("EMESH_VIRTUAL_OVERLAP");  // A/B knob (default off)
+        return v ? std::atoi(v) != 0 : false;
+    }();
+    return on;
+}
+
 int run_virtual(emesh_engine* e, const float* const* A, const float* const* B, float* const* theta, float* const* buf,
                 float* const* local_out, float* const* out, float lr, float mom) {
     if (e->fp32) return run_virtual_f32(e, A, B, theta, buf, local_out, out, lr, mom);
+    const bool ov = virtual_overlap();
     for (uint32_t c = 0; c < e->k; ++c) {
         TRY(run_virtual_chain(e, c, A, B));
-        for (uint32_t w = 0; w < e->k; ++w) TRY(run_virtual_apply(e, c, w, theta, buf, local_out, out, lr, mom));
+        if (ov) {
+            CU(cudaEventRecord(e->ev_send[0], e->s_comp));  // ev_send is unused by the virtual ring otherwise
+            CU(cudaStreamWaitEvent(e->s_comm, e->ev_send[0], 0));
+        }
+        for (uint32_t w = 0; w < e->k; ++w)
+            TRY(run_virtual_apply(e, c, w, theta, buf, local_out, out, lr, mom, ov ? e->s_comm : e->s_comp));
     }
     return EMESH_OK;
 }
