@@ -93,6 +93,7 @@ struct Batch {
     uint64_t elems = 0;             // elements in the batch
     std::vector<std::pair<uint64_t, uint64_t>> eruns;  // contiguous element runs {lo, len} (transfers)
     uint32_t ncta = 0, nruns = 0, ntasks = 0;
+    uint32_t upw = kUnitsPerWarp;   // warp units per tile (tile_units_per_warp)
     size_t off_segs = 0, off_cta = 0, off_runs = 0;  // byte offsets into the table arena
     const SegInfo* d_segs = nullptr;
     const uint32_t* d_cta_seg = nullptr;
@@ -104,6 +105,21 @@ struct Batch {
         d_runs = reinterpret_cast<const uint4*>((char*)base + off_runs);
     }
 };
+
+// Tile shape per batch: 4 warp units (16K elements) per tile for large batches,
+// 2 (8K) for small ones, where twice the CTAs per segment halve the serial
+// STATS -> thresholds -> BIN chain. Measured at 2 GPUs (profiles/r01_u2_ab/):
+// 2-unit tiles take 0.101 vs 0.122 ms per round at 1 MB, 0.171 vs 0.183 ms at
+// 64 MB (8M-element batches), but are 2-4 % slower from 32M-element batches up.
+uint32_t tile_units_per_warp(uint64_t batch_elems) {
+    static const int force = [] {
+        const char* v = std::getenv("EMESH_TILE_UNITS");  // 2 / 4 force a shape; unset or 0: by size
+        return v ? std::atoi(v) : 0;
+    }();
+    if (force == 2 || force == 4) return (uint32_t)std::min(force, kUnitsPerWarp);
+    constexpr uint64_t kSmallBatchElems = 16ull << 20;
+    return batch_elems <= kSmallBatchElems ? (uint32_t)std::min(2, kUnitsPerWarp) : (uint32_t)kUnitsPerWarp;
+}
 
 struct Plan {
     uint64_t n = 0;
@@ -121,6 +137,11 @@ struct Plan {
         b.window = window;
         b.slot0 = s0;
         b.nseg = s1 - s0;
+        {
+            uint64_t tot = 0;
+            for (uint32_t s = s0; s < s1; ++s) tot += segs[s].len;
+            b.upw = tile_units_per_warp(tot);
+        }
         std::vector<SegInfo> infos;
         std::vector<uint32_t> cseg;
         bool first = true;
@@ -135,11 +156,12 @@ struct Plan {
             si.cta0 = (uint32_t)cseg.size();
             si.slot = s;
             si.in_slot = s;
+            si.upw = b.upw;
             if (g.len > 0) {
                 const uint64_t q_last = (g.lo + g.len - 1) >> 2;
                 const uint64_t nq = q_last - si.q0 + 1;
                 si.nunits = (uint32_t)((nq + kUnitSlots - 1) / kUnitSlots);
-                si.ncta = (si.nunits + kTileUnits - 1) / kTileUnits;
+                si.ncta = (si.nunits + kWarps * b.upw - 1) / (kWarps * b.upw);
                 // whole units: no 128-B scratch line (and no prefetched unit) is
                 // shared with another segment, whose STATS may not have run yet
                 sq += (nq + kUnitSlots - 1) / kUnitSlots * kUnitSlots;
@@ -675,7 +697,8 @@ int launch_apply(const Batch& bt, int mode, const uint8_t* codes, const float* c
     a.out = out;
     a.lr = lr;
     a.mom = mom;
-    const dim3 g(bt.ncta * kApplySplit), blk(kThreads);
+    a.upw = bt.upw;
+    const dim3 g(bt.ncta * bt.upw), blk(kThreads);
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
     if (mode == 0) k_apply<0><<<g, blk, 0, st>>>(a);
@@ -1015,7 +1038,8 @@ int launch_f32_hop(const Batch& bt, Workspace& ws, const F32IO& io, cudaStream_t
     if (io.nflags) CU(cudaMemsetAsync(ws.sync + kSyncReady, 0, (size_t)bt.nseg * sizeof(uint32_t), st));
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
-    const dim3 g(bt.ncta * kApplySplit), blk(kThreads);
+    a.upw = bt.upw;
+    const dim3 g(bt.ncta * bt.upw), blk(kThreads);
     const bool pg = io.b != nullptr, hin = io.in != nullptr;
     if (!hin) {
         if (pg) k_f32_hop<true, false, false><<<g, blk, 0, st>>>(a);
@@ -1056,7 +1080,8 @@ int launch_f32_apply(const Batch& bt, int mode, const float* pay, float* theta, 
     a.err = tr ? tr->err : nullptr;
     a.timeout_ns = tr ? tr->timeout_ns : 30ull * 1000000000ull;
     if (in_flag && !a.err) return fail(EMESH_ECONFIG, "peer wait without an error word");
-    const dim3 g(bt.ncta * kApplySplit), blk(kThreads);
+    a.upw = bt.upw;
+    const dim3 g(bt.ncta * bt.upw), blk(kThreads);
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
     if (mode == 0) k_f32_apply<0><<<g, blk, 0, st>>>(a, pay);

@@ -53,7 +53,9 @@ static_assert(kUnitsPerWarp == 2 || kUnitsPerWarp == 4, "limb layout sized for <
 constexpr int kLoBits = kUnitsPerWarp == 2 ? 9 : 7;
 constexpr int kCntShift = kUnitsPerWarp == 2 ? 20 : 19;
 constexpr int kMidEnd = kUnitsPerWarp == 2 ? 30 : 26;
-constexpr int kTileUnits = kWarps * kUnitsPerWarp;  // 16 units = 16384 elements per tile
+// The tile shape (kWarps * upw units: 16K or 8K elements) is chosen per batch at
+// run time (SegInfo::upw, Plan::add_batch): the limb layout above is sized for
+// the largest tile and stays exact for a smaller one (its bounds cap m).
 
 // Exact fixed-point encoding of one bucket's members for the codebook sums:
 // each member x maps to a non-negative integer r(x) < 2^42 with
@@ -100,7 +102,7 @@ struct SegInfo {
     uint32_t ncta;      // tiles
     uint32_t slot;      // global segment slot (stats / codebook index)
     uint32_t in_slot;   // slot of the incoming payload's codebook (== slot)
-    uint32_t pad;
+    uint32_t upw;       // warp units per tile (2 or 4, <= kUnitsPerWarp; one value per batch)
 };
 
 // Moments of a set of values around a pivot p: s = sum x, m2 = sum (x-p)^2,
@@ -490,8 +492,8 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
     double piv = 0.0;
     uint32_t cnt = 0;
     bool have_piv = false;
-    for (int ui = 0; ui < kUnitsPerWarp; ++ui) {
-        const uint32_t u = tile * kTileUnits + ui * kWarps + warp;  // segment-relative unit
+    for (int ui = 0; ui < (int)si.upw; ++ui) {
+        const uint32_t u = (tile * si.upw + ui) * kWarps + warp;  // segment-relative unit
         if (u >= si.nunits) break;
         const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
         const bool interior = qbase * 4 >= si.lo && (qbase + kUnitSlots) * 4 <= hiel;  // warp-uniform
@@ -502,7 +504,7 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
             uint32_t c4[kHalf];
 #if EMESH_STATS_L1PF
             {   // the warp's next half-unit of A (lanes 0-15) and B (lanes 16-31) into L1, 2 KB each
-                const bool more = h == 0 || (ui + 1 < kUnitsPerWarp && u + kWarps < si.nunits);
+                const bool more = h == 0 || (ui + 1 < (int)si.upw && u + kWarps < si.nunits);
                 const uint64_t qn = h == 0 ? qbase + (uint64_t)kHalf * 32 : qbase + (uint64_t)kWarps * kUnitSlots;
                 const uint64_t ql = qn + (uint64_t)(lane & 15) * 8;
                 if (more && ql * 4 < hiel && ((SRC & kSrcAminusB) || lane < 16))
@@ -852,7 +854,7 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
     const SegStat* st = &a.stats[si.slot];
 #if EMESH_BIN_L1PF && EMESH_BIN_PF_FIRST
     if (FROM_SCRATCH) {  // the warp's first unit, while the tables load (the segment's scratch is complete)
-        const uint32_t u0 = tile * kTileUnits + warp;
+        const uint32_t u0 = tile * si.upw * kWarps + warp;
         if (u0 < si.nunits) {
             const float4* p0 = reinterpret_cast<const float4*>(a.scratch) + si.sq0 + (uint64_t)u0 * kUnitSlots + lane * 8;
             asm volatile("prefetch.global.L1 [%0];" ::"l"(p0));
@@ -886,13 +888,13 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
     const float4* xs = reinterpret_cast<const float4*>(a.scratch) + ((int64_t)si.sq0 - (int64_t)si.q0);
     uint32_t nclip_lo = 0, nclip_hi = 0;
     const BinParams bpar{c_f, inv_w, lo_up, hi_dn, margin, one_m};
-    for (int ui = 0; ui < kUnitsPerWarp; ++ui) {
-        const uint32_t u = tile * kTileUnits + ui * kWarps + warp;
+    for (int ui = 0; ui < (int)si.upw; ++ui) {
+        const uint32_t u = (tile * si.upw + ui) * kWarps + warp;
         if (u >= si.nunits) break;
         const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
         const bool interior = qbase * 4 >= si.lo && (qbase + kUnitSlots) * 4 <= hiel;  // warp-uniform
 #if EMESH_BIN_L1PF
-        if (FROM_SCRATCH && ui + 1 < kUnitsPerWarp && u + kWarps < si.nunits) {
+        if (FROM_SCRATCH && ui + 1 < (int)si.upw && u + kWarps < si.nunits) {
             const float4* nx = xs + qbase + (uint64_t)kWarps * kUnitSlots + lane * 8;  // one 128-B line per lane
             asm volatile("prefetch.global.L1 [%0];" ::"l"(nx));
         }
@@ -1116,6 +1118,7 @@ struct ApplyArgs {
     const SegInfo* segs;
     const uint32_t* cta_seg;
     uint32_t ncta;
+    uint32_t upw;          // the batch's warp units per tile = CTAs per tile
     const uint8_t* codes;  // arena-indexed
     const float* cb;       // [slot][256]
     float* theta;          // theta_g, updated in place
@@ -1128,11 +1131,9 @@ struct ApplyArgs {
     uint32_t* err;            // sticky error word (kErrRingTimeout)
     unsigned long long timeout_ns;
 };
-#ifndef EMESH_APPLY_SPLIT
-#define EMESH_APPLY_SPLIT kUnitsPerWarp  // one unit per warp: measured best (k_apply 11.3 -> 11.0 ms per round)
-#endif
-constexpr int kApplySplit = EMESH_APPLY_SPLIT;               // k_apply CTAs per quantizer tile
-constexpr int kApplyUnits = kUnitsPerWarp / kApplySplit;     // units per warp in one k_apply CTA
+// k_apply-family CTAs: a.upw per quantizer tile, one unit per warp (measured
+// best: k_apply 11.3 -> 11.0 ms per round).
+constexpr int kApplyUnits = 1;  // units per warp in one k_apply CTA
 
 __device__ __forceinline__ void nesterov1(float& th, float& b, float d, float lr, float mom) {
     // optim.hpp:127-130, fp32, this exact association, no FMA
@@ -1146,7 +1147,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
     __shared__ float lut[kBuckets];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t tile = blockIdx.x / kApplySplit, part = blockIdx.x % kApplySplit;
+    const uint32_t tile = blockIdx.x / a.upw, part = blockIdx.x % a.upw;
     const SegInfo si = a.segs[a.cta_seg[tile]];
     if (a.in_flag) {
         if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.slot, a.epoch, a.err, a.timeout_ns);
@@ -1156,7 +1157,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
     __syncthreads();
     const uint64_t hiel = si.lo + si.len;
     for (int ui = 0; ui < kApplyUnits; ++ui) {
-    const uint32_t u = (tile - si.cta0) * kTileUnits + (part * kApplyUnits + ui) * kWarps + warp;
+    const uint32_t u = ((tile - si.cta0) * a.upw + part * kApplyUnits + ui) * kWarps + warp;
     if (u >= si.nunits) return;
     const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
 #pragma unroll 4
@@ -1202,13 +1203,14 @@ __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
 
 // ---------------------------------------------------------------------------
 // ReduceMode::fp32 ring (allreduce.hpp:120-164: raw fp32 payloads). One CTA
-// per half quantizer tile (like k_apply); segments are still the framing
+// per warp unit of a quantizer tile (like k_apply); segments are still the framing
 // unit (allreduce.hpp:326-336), and with the peer transport the last CTA of
 // a segment raises its arrival flags.
 
 struct F32HopArgs {
     const SegInfo* segs;
     const uint32_t* cta_seg;
+    uint32_t upw;              // the batch's warp units per tile = CTAs per tile
     const float* a;            // theta_g (PG) or the ring input
     const float* b;            // theta_l (PG) or nullptr
     const float* in;           // incoming partial sums (arena-indexed) or nullptr (hop 0)
@@ -1230,7 +1232,7 @@ struct F32HopArgs {
 template <bool PG, bool HAS_IN, bool DIV>
 __global__ void __launch_bounds__(kThreads) k_f32_hop(F32HopArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t tile = blockIdx.x / kApplySplit, part = blockIdx.x % kApplySplit;
+    const uint32_t tile = blockIdx.x / a.upw, part = blockIdx.x % a.upw;
     const uint32_t s = a.cta_seg[tile];
     const SegInfo si = a.segs[s];
     if (HAS_IN && a.in_flag) {
@@ -1239,7 +1241,7 @@ __global__ void __launch_bounds__(kThreads) k_f32_hop(F32HopArgs a) {
     }
     const uint64_t hiel = si.lo + si.len;
     for (int ui = 0; ui < kApplyUnits; ++ui) {
-        const uint32_t u = (tile - si.cta0) * kTileUnits + (part * kApplyUnits + ui) * kWarps + warp;
+        const uint32_t u = ((tile - si.cta0) * a.upw + part * kApplyUnits + ui) * kWarps + warp;
         if (u >= si.nunits) break;
         const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
 #pragma unroll 4
@@ -1279,7 +1281,7 @@ __global__ void __launch_bounds__(kThreads) k_f32_hop(F32HopArgs a) {
         __shared__ uint32_t last;
         __syncthreads();
         if (threadIdx.x == 0)
-            last = atom_add_acq_rel(a.seg_done + s, 1u) == si.ncta * kApplySplit - 1 ? 1u : 0u;
+            last = atom_add_acq_rel(a.seg_done + s, 1u) == si.ncta * a.upw - 1 ? 1u : 0u;
         __syncthreads();
         if (last && threadIdx.x == 0) {
             __threadfence_system();
@@ -1293,7 +1295,7 @@ __global__ void __launch_bounds__(kThreads) k_f32_hop(F32HopArgs a) {
 template <int MODE>
 __global__ void __launch_bounds__(kThreads) k_f32_apply(ApplyArgs a, const float* pay) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t tile = blockIdx.x / kApplySplit, part = blockIdx.x % kApplySplit;
+    const uint32_t tile = blockIdx.x / a.upw, part = blockIdx.x % a.upw;
     const SegInfo si = a.segs[a.cta_seg[tile]];
     if (a.in_flag) {
         if (threadIdx.x == 0) spin_until_ge_sys(a.in_flag + si.slot, a.epoch, a.err, a.timeout_ns);
@@ -1301,7 +1303,7 @@ __global__ void __launch_bounds__(kThreads) k_f32_apply(ApplyArgs a, const float
     }
     const uint64_t hiel = si.lo + si.len;
     for (int ui = 0; ui < kApplyUnits; ++ui) {
-        const uint32_t u = (tile - si.cta0) * kTileUnits + (part * kApplyUnits + ui) * kWarps + warp;
+        const uint32_t u = ((tile - si.cta0) * a.upw + part * kApplyUnits + ui) * kWarps + warp;
         if (u >= si.nunits) return;
         const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
 #pragma unroll 4
