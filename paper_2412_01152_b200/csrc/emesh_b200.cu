@@ -107,17 +107,20 @@ struct Batch {
 };
 
 // Tile shape per batch: 4 warp units (16K elements) per tile for large batches,
-// 2 (8K) for small ones, where twice the CTAs per segment halve the serial
-// STATS -> thresholds -> BIN chain. Measured at 2 GPUs (profiles/r01_u2_ab/):
-// 2-unit tiles take 0.101 vs 0.122 ms per round at 1 MB, 0.171 vs 0.183 ms at
-// 64 MB (8M-element batches), but are 2-4 % slower from 32M-element batches up.
+// 2 (8K) for small ones and 1 for tiny ones, where more CTAs per segment shorten
+// the serial STATS -> thresholds -> BIN chain. Measured at 2 GPUs
+// (profiles/r01_u2_ab/): 2-unit tiles take 0.101 vs 0.122 ms per round at 1 MB,
+// 0.171 vs 0.183 ms at 64 MB (8M-element batches), but are 2-4 % slower from
+// 32M-element batches up; 1-unit tiles (profiles/r01_tile1/) a further -8..-14 %
+// on <= 2M-element batches at 2 and 4 GPUs, mixed at 4M-8M.
 uint32_t tile_units_per_warp(uint64_t batch_elems) {
     static const int force = [] {
-        const char* v = std::getenv("EMESH_TILE_UNITS");  // 2 / 4 force a shape; unset or 0: by size
+        const char* v = std::getenv("EMESH_TILE_UNITS");  // 1 / 2 / 4 force a shape; unset or 0: by size
         return v ? std::atoi(v) : 0;
     }();
-    if (force == 2 || force == 4) return (uint32_t)std::min(force, kUnitsPerWarp);
-    constexpr uint64_t kSmallBatchElems = 16ull << 20;
+    if (force == 1 || force == 2 || force == 4) return (uint32_t)std::min(force, kUnitsPerWarp);
+    constexpr uint64_t kTinyBatchElems = 2ull << 20, kSmallBatchElems = 16ull << 20;
+    if (batch_elems <= kTinyBatchElems) return 1u;
     return batch_elems <= kSmallBatchElems ? (uint32_t)std::min(2, kUnitsPerWarp) : (uint32_t)kUnitsPerWarp;
 }
 
