@@ -948,6 +948,9 @@ struct emesh_engine {
     // CUDA IPC; codes / codebooks double-buffered by round parity; arrival
     // flags hold the round (epoch) number, so they never need resetting
     int transport = EMESH_TRANSPORT_NCCL;
+    // engine setup (communicator init, its first collectives' lazy connects)
+    // may take seconds at 3+ ranks: waits then get at least this budget
+    unsigned long long setup_floor_ns = 0;
     bool failed = false;             // a round failed (ring timeout / NCCL): abort, never wait for peers
     bool fp32 = false;               // ReduceMode::fp32 engine (raw fp32 payloads)
     std::vector<uint64_t> sizes;     // multi-tensor engine: one ReduceJob per tensor (config 5)
@@ -1228,6 +1231,10 @@ int run_virtual(emesh_engine* e, const float* const* A, const float* const* B, f
 // that may answer ncclInProgress is settled here against step_timeout; on
 // expiry the communicator is aborted and the round fails with EMESH_ERING
 // (allreduce.hpp:466-470), which allreduce_with_retry turns into a re-plan.
+double wait_budget_ns(const emesh_engine* e) {
+    return std::max((double)e->tr.timeout_ns, (double)e->setup_floor_ns);
+}
+
 int nccl_settle(emesh_engine* e, ncclResult_t r, const char* what) {
     const auto t0 = std::chrono::steady_clock::now();
     int spins = 0;
@@ -1235,12 +1242,12 @@ int nccl_settle(emesh_engine* e, ncclResult_t r, const char* what) {
         if (ncclCommGetAsyncError(e->comm, &r) != ncclSuccess) break;
         if (r != ncclInProgress) break;
         const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        if (waited * 1e9 > (double)e->tr.timeout_ns) {
+        if (waited * 1e9 > wait_budget_ns(e)) {
             e->failed = true;
             ncclCommAbort(e->comm);
             e->comm = nullptr;
             return fail(EMESH_ERING, "NCCL %s did not complete within step_timeout (%.1f s)", what,
-                        (double)e->tr.timeout_ns * 1e-9);
+                        wait_budget_ns(e) * 1e-9);
         }
         if (++spins > 1000) std::this_thread::sleep_for(std::chrono::microseconds(50));
     }
@@ -1281,7 +1288,7 @@ int nccl_drain(emesh_engine* e, std::initializer_list<cudaStream_t> streams, con
         if (e->comm) ncclCommGetAsyncError(e->comm, &ae);
         const bool err = ae != ncclSuccess && ae != ncclInProgress;
         const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        if (err || waited * 1e9 > (double)e->tr.timeout_ns) {
+        if (err || waited * 1e9 > wait_budget_ns(e)) {
             e->failed = true;
             if (e->comm) ncclCommAbort(e->comm);
             e->comm = nullptr;
@@ -1878,6 +1885,7 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
     if (e->k > 1 && (rc = engine_alloc(e))) return bail(rc);
     e->tr.err = e->ws.err;
     if (cfg->step_timeout_s > 0) e->tr.timeout_ns = (unsigned long long)(cfg->step_timeout_s * 1e9);
+    e->setup_floor_ns = 30ull * 1000000000ull;  // reset once the engine is up
     int lo_prio = 0, hi_prio = 0;
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
     if (cudaStreamCreateWithPriority(&e->s_comp, cudaStreamNonBlocking, lo_prio) != cudaSuccess ||
@@ -1932,6 +1940,7 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
             }
         }
     }
+    e->setup_floor_ns = 0;
     *out = e;
     return EMESH_OK;
 }
