@@ -319,6 +319,51 @@ int orc_ring_allreduce(const float* const* inputs, uint32_t k, uint64_t n, uint3
     return rc;
 }
 
+/* ---- one segment's reduce-scatter chain, transport-free ----------------
+ * The same arithmetic as orc_ring_allreduce restricted to ONE segment of
+ * chunk c: quantization is per segment (allreduce.hpp:326-336), so a
+ * segment's final payload depends only on that segment's elements of every
+ * worker. Chunk c leaves rank c at hop 0 and visits c+1, ..., c+k-1 = its
+ * owner (allreduce.hpp:411-426, owner :431): v = D_c; v = D_{c+t} + deq(Q(v))
+ * for t = 1..k-1 (:422); mean = v / (float)k (:435-439); final = Q(mean)
+ * (:441-443). D_w = theta_g - theta_l[w] (optim.hpp:108) when theta_g is
+ * given, else theta_l[w] is worker w's ring input itself.
+ * Outputs: codes (len), cb (256), stats (4: mu sigma lo width) of the final
+ * payload; mean_out (len, optional) = the owner's mean before quantization
+ * (input of the boundary-margin diagnostic). mode 0 (fp32) returns the fp32
+ * mean in mean_out only. Thread-safe (no globals): callers run segments in
+ * parallel. */
+int orc_segment_chain(const float* theta_g, const float* const* theta_l, uint32_t k, uint32_t c, uint64_t len,
+                      int mode, uint8_t* codes, float* cb, double* stats, float* mean_out) {
+    if (k == 0 || len == 0) return ORC_ESHAPE;
+    float* v = (float*)malloc(len * sizeof(float));
+    uint8_t* tc = (uint8_t*)malloc(len);
+    float tcb[NBUCKETS];
+    int rc = ORC_OK;
+    for (uint32_t t = 0; t < k && rc == ORC_OK; ++t) {
+        const uint32_t w = (c + t) % k;
+        const float* l = theta_l[w];
+        if (t > 0 && mode != 0) {  /* what the receiver decodes of the incoming payload */
+            rc = orc_quantize(v, len, tc, tcb, NULL);
+            if (rc != ORC_OK) break;
+            orc_dequantize(tc, tcb, len, v);
+        }
+        for (uint64_t i = 0; i < len; ++i) {
+            const float d = theta_g ? theta_g[i] - l[i] : l[i];
+            v[i] = t == 0 ? d : d + v[i];
+        }
+    }
+    if (rc == ORC_OK) {
+        const float divisor = (float)k;
+        for (uint64_t i = 0; i < len; ++i) v[i] = v[i] / divisor;
+        if (mean_out) memcpy(mean_out, v, len * sizeof(float));
+        if (mode != 0 && k > 1) rc = orc_quantize(v, len, codes, cb, stats);  /* k == 1: identity (:319) */
+    }
+    free(v);
+    free(tc);
+    return rc;
+}
+
 /* ---- one outer-sync round for k workers: trainer.hpp:355-382 ----------
  * theta_g: retained (global) params, identical on every worker, updated in
  * place; theta_l[w]: worker w's local params; buf: Nesterov buffer. Every

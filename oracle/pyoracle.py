@@ -75,6 +75,9 @@ class Oracle:
         L.orc_outer_sync.restype = C.c_int
         L.orc_outer_sync.argtypes = [_f32p, C.c_void_p, _f32p, C.c_uint32, C.c_uint64, C.c_uint32,
                                      C.c_int, C.c_float, C.c_float]
+        L.orc_segment_chain.restype = C.c_int
+        L.orc_segment_chain.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64, C.c_int,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_encode_quant_chunk.restype = C.c_uint64
         L.orc_encode_quant_chunk.argtypes = [_u8p, _f32p, C.c_uint32, _u8p]
         L.orc_decode_quant_chunk.restype = C.c_int
@@ -161,6 +164,34 @@ class Oracle:
         if with_payloads:
             return out[:n], codes[:n], cbs, stats
         return out[:n]
+
+    def segment_chain(self, theta_g, theta_ls, chunk, mode="int8", want_mean=False):
+        """One segment's reduce-scatter chain (emesh_oracle.c:orc_segment_chain): theta_g (or None: theta_ls
+        are the ring inputs) and every worker's slice of the segment; chunk = the segment's ring chunk.
+        Returns (codes, cb, stats, mean-or-None) of the owner's final payload."""
+        k = len(theta_ls)
+        ls = [np.ascontiguousarray(a, np.float32) for a in theta_ls]
+        n = len(ls[0])
+        g = None if theta_g is None else np.ascontiguousarray(theta_g, np.float32)
+        codes = np.empty(max(n, 1), np.uint8)
+        cb = np.zeros(256, np.float32)
+        st = np.zeros(4, np.float64)
+        mean = np.empty(max(n, 1), np.float32) if want_mean or mode != "int8" else None
+        arr = _ptr_array(ls)
+        rc = self.L.orc_segment_chain(None if g is None else g.ctypes.data, C.cast(arr, C.c_void_p), k, chunk, n,
+                                      1 if mode == "int8" else 0, codes.ctypes.data, cb.ctypes.data, st.ctypes.data,
+                                      None if mean is None else mean.ctypes.data)
+        if rc:
+            raise OracleError(rc, "segment_chain")
+        return codes[:n], cb, st, (mean[:n] if mean is not None else None)
+
+    def segment_chains(self, jobs, threads=None, want_mean=False):
+        """Many independent segment chains in parallel (ctypes releases the GIL): jobs = iterable of
+        (theta_g_slice | None, [theta_l slices], chunk). Returns the results in order."""
+        from concurrent.futures import ThreadPoolExecutor
+        threads = threads or max(1, min(64, os.cpu_count() or 1))
+        with ThreadPoolExecutor(threads) as ex:
+            return list(ex.map(lambda j: self.segment_chain(j[0], j[1], j[2], want_mean=want_mean), jobs))
 
     def outer_sync(self, theta_g, theta_ls, buf, S=4, mode="int8", lr=0.7, momentum=0.9):
         theta_g = np.array(theta_g, np.float32, copy=True)
