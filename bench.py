@@ -40,7 +40,10 @@ def parse():
     ap.add_argument("--window", type=float, default=0, help="pipelining window elems (0=auto)")
     ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "p2p"],
                     help="N>1 ring transport (auto: peer memory over NVLink when mappable, else NCCL)")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--parity-segments", type=int, default=8,
+                    help="segments of one extra (untimed) round re-derived by the oracle after the timed region")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=float, default=16e6, help="params per worker in the CPU sample")
@@ -162,7 +165,7 @@ def run_reference(args, rank, world):
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
         "config": config_block(args, k, int(args.n), "reference"),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, **host_info(),
                          "sample": f"{k} workers x {n} params/worker per round (bounded slice of the "
                                    f"{int(args.n)}-param workload), S={args.S}, TCP loopback ring, one node thread "
                                    f"+ one sender task per worker"},
@@ -201,7 +204,7 @@ def intellect1_tensor_sizes():
     return sizes + [d, vocab * d]
 
 
-def nvlink_block(world, k, n, S, ms, transport):
+def nvlink_block(world, k, n, S, ms, transport, measured=None):
     """per GPU per direction, the ring moves 2(k-1)/k B/param of codes + 2(k-1) S 1028 B of
     codebooks per round; averaged over the round (the transfers overlap the kernels, so this is a floor,
     not the link's busy rate). NVLink 5: 900 GB/s per direction per GPU."""
@@ -210,14 +213,115 @@ def nvlink_block(world, k, n, S, ms, transport):
     by = 2 * (k - 1) / k * n + 2 * (k - 1) * S * 1028
     gbs = by / (ms / 1e3) / 1e9
     return {"bytes_per_gpu_per_round": int(by), "avg_GBps_per_direction": round(gbs, 1), "peak_GBps": 900.0,
-            "frac_of_round": round(gbs / 900.0, 4), "transport": transport,
-            "note": "ring traffic averaged over the whole round; it overlaps the quantize/decode kernels"}
+            "frac_of_round": round(gbs / 900.0, 4), "transport": transport, "measured": measured,
+            "note": "algorithmic ring bytes averaged over the whole round; it overlaps the quantize/decode kernels"}
 
 
 def alg_bytes_per_param(k):
     # A(1) = 20, A(k>=2) = 24 + (2k-1)/k + 1 (theta_l write excluded)
     return 20.0 if k == 1 else 24.0 + (2 * k - 1) / k + 1.0
 
+
+def host_info():
+    """nproc and the CPU model of this host (the CPU baseline's hardware)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+class NvlinkCounters:
+    """NVLink data-throughput counters of one GPU from NVML (the driver's per-link hardware
+    counters, KiB, cumulative): user-data bytes sent / received over the timed region."""
+
+    TX, RX = 138, 139  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX
+
+    def __init__(self, index):
+        self.ok = False
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(index)
+            self.links = [l for l in range(18) if self._state(l)]
+            self.ok = bool(self.links)
+        except Exception as ex:  # reported as unavailable, never required
+            self.err = str(ex)[:120]
+
+    def _state(self, l):
+        try:
+            return self.N.nvmlDeviceGetNvLinkState(self.h, l) == 1
+        except Exception:
+            return False
+
+    def read(self):
+        if not self.ok:
+            return None
+        N = self.N
+        tx = rx = 0
+        for l in self.links:
+            vals = N.nvmlDeviceGetFieldValues(self.h, [(self.TX, l), (self.RX, l)])
+            tx += vals[0].value.ullVal
+            rx += vals[1].value.ullVal
+        return tx * 1024, rx * 1024
+
+
+def parity_round(eng, tg, tl, tb, hp, k, S, n, world, rank, nseg_pick):
+    """after the timed region, one more round whose sampled segments are
+    re-derived by the oracle (the checker only, like cpu_baseline): bit-exact codes, codebooks,
+    updated theta_g and momentum (oracle/parity.py)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from oracle import parity
+    from oracle.pyoracle import Oracle
+
+    lo, ln = eng.segments()
+    nseg = len(lo)
+    picks = sorted(set(int(round(i * (nseg - 1) / max(nseg_pick - 1, 1))) for i in range(min(nseg_pick, nseg))))
+    jobs = parity.segment_jobs(lo, ln, k, S, set(picks))
+    W = len(tg)
+    snap = {}
+    for j in jobs:  # inputs of the checked round, every worker's theta_l slice (gathered from the ranks)
+        sl = slice(j.lo, j.lo + j.length)
+        g0, b0 = tg[0][sl].clone(), tb[0][sl].clone()
+        if world > 1:
+            parts = [torch.empty_like(tl[0][sl]) for _ in range(world)]
+            dist.all_gather(parts, tl[0][sl].contiguous())
+        else:
+            parts = [t[sl].clone() for t in tl]
+        snap[j.slot] = (g0, parts, b0)
+    eng.outer_sync(tg, tl, tb, hp, write_local=False)
+    eng.check()
+    if rank != 0:
+        return None
+    owner_of = (lambda c: (c + k - 1) % k) if W > 1 else (lambda c: 0)
+    payloads = {}
+
+    def inputs(j):
+        g0, parts, b0 = snap[j.slot]
+        return g0.cpu().numpy(), [p.cpu().numpy() for p in parts], b0.cpu().numpy()
+
+    def gpu(j):
+        w = owner_of(j.chunk)
+        if w not in payloads:
+            payloads[w] = eng.payload(w)
+        codes, cbs, _ = payloads[w]
+        sl = slice(j.lo, j.lo + j.length)
+        return codes[sl], cbs[j.slot], tg[0][sl].cpu().numpy(), tb[0][sl].cpu().numpy()
+
+    for j in jobs:  # payload downloads on this thread (one per owner)
+        gpu(j)
+    rep = parity.check(Oracle(), jobs, k, inputs, gpu, hp.outer_lr, hp.outer_momentum)
+    d = rep.as_dict()
+    d["segment_slots"] = picks
+    d["segment_elems"] = int(max(int(x) for x in ln)) if nseg else 0
+    return d
 
 # ----------------------------------------------------------------- our arm
 
@@ -295,6 +399,7 @@ def main():
         return
 
     clk = ClockSampler(local_rank).__enter__()  # started early: nvidia-smi needs time to come up
+    nvl = NvlinkCounters(local_rank) if world > 1 else None
     for _ in range(args.warmup):
         step()
     eng.check()
@@ -305,11 +410,13 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     clk.start()
+    nv0 = nvl.read() if nvl else None
     ev0.record(stream)
     for _ in range(args.steps):
         step()
     ev1.record(stream)
     barrier()
+    nv1 = nvl.read() if nvl else None
     clk.stop()
     clk.__exit__()
     ms_local = ev0.elapsed_time(ev1)
@@ -373,6 +480,29 @@ def main():
     step_alg_gbs = W * n * alg_bytes_per_param(k) / (ms / 1e3) / 1e9
 
     # ---- e2e through the host-buffer C-ABI entry point (pinned host memory)
+    # ---- NVLink bytes this GPU moved during the timed region (NVML hardware counters)
+    nvl_meas = None
+    if nv0 is not None and nv1 is not None:
+        tx, rx = nv1[0] - nv0[0], nv1[1] - nv0[1]
+        v = torch.tensor([tx, rx], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        tx, rx = float(v[0]), float(v[1])
+        secs = ms * args.steps / 1e3
+        nvl_meas = {"source": "NVML NVLink data-throughput counters (per-link hardware counters), max over ranks",
+                    "tx_bytes_per_round": tx / args.steps, "rx_bytes_per_round": rx / args.steps,
+                    "tx_GBps_round_avg": round(tx / secs / 1e9, 1), "rx_GBps_round_avg": round(rx / secs / 1e9, 1)}
+    elif nvl is not None:
+        nvl_meas = {"unavailable": getattr(nvl, "err", "no active NVLink")}
+
+    # ---- parity of one more (untimed) round, sampled segments vs the oracle (checker only)
+    parity = None
+    if not args.no_parity and k > 1 and sizes is None:
+        try:
+            parity = parity_round(eng, tg, tl, tb, hp, k, args.S, n, world, rank, args.parity_segments)
+        except Exception as ex:
+            parity = {"error": str(ex)[:300]}
+
     e2e = None
     if not args.no_e2e:
         def pinned(x):  # straight into page-locked memory (no pageable staging copy)
@@ -403,6 +533,7 @@ def main():
             ns = int(args.cpu_sample)
             secs, kind = cpu_reference_round(ns, k, args.S)
             cpu = {"value": k * ns / secs, "unit": UNIT, "cores": min(os.cpu_count() or 1, 2 * k) if kind == "reference" else 1,
+                   **host_info(),
                    "kind": kind, "sample": f"one round, {k} workers x {ns} params/worker (slice of the workload), "
                                            f"S={args.S}, TCP loopback ring"}
         except Exception as ex:  # the baseline is reported, never required
@@ -417,7 +548,8 @@ def main():
             "hbm_alg_GBps_per_gpu": round(step_alg_gbs, 1),
             "hbm_frac_step": round(step_alg_gbs / hbm_peak, 4),
             "roofline": roofline, "roofline_other_kernels": roofline_others, "kernels": kernels,
-            "nvlink": nvlink_block(world, k, n, args.S, ms, eng.transport),
+            "nvlink": nvlink_block(world, k, n, args.S, ms, eng.transport, nvl_meas),
+            "parity": parity,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk.summary(),
         }

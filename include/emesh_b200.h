@@ -5,8 +5,10 @@
  * Drop-in boundary for the reference's C++ API in proj/include/emesh
  * (header-only C++20 library). Each entry point names the reference
  * interface it replaces. No torch types; plain pointers, sizes, CUDA
- * streams. Device pointers unless a name says _host. All fp32 arenas and
- * code arenas must be 16-byte aligned (cudaMalloc gives 256).
+ * streams. Device pointers unless a name says _host. fp32 arenas the
+ * quantizer reads (quantize input, ring input, theta_g / theta_l) must be
+ * 32-byte aligned and code arenas 8-byte aligned (256-bit loads; cudaMalloc
+ * gives 256); other fp32 arenas 16-byte aligned.
  *
  * Error convention (maps 1:1 onto the reference's exception hierarchy,
  * proj/include/emesh/errors.hpp:10-73): functions return EMESH_OK or an
@@ -166,15 +168,6 @@ typedef struct {
 uint64_t emesh_ring_schedule(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems, uint32_t rank,
                              emesh_ring_op* ops, uint64_t max_ops);
 
-/* Development aid: the persistent quantizer's task plan for one batch, as
- * runs of {first task, kind, segment, first tile}: kind 0 = STATS tiles,
- * 2 = BIN tiles (first tile | 1<<31 = descending), 1 / 3 = mixed run of
- * alternating STATS / BIN tasks (kind | BIN segment << 2; STATS segment;
- * first STATS tile | first BIN tile << 16; BIN tiles descending / ascending);
- * info = {ntasks, ncta, nseg, ncta of each segment...}. Host-only. */
-uint64_t emesh_debug_batch_runs(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems, uint32_t chunk,
-                                uint32_t window, uint32_t* runs4, uint64_t max_runs, uint32_t* info);
-
 /* NCCL unique id for emesh_engine_config.nccl_id (rank 0 creates, broadcast). */
 int emesh_nccl_unique_id(uint8_t out[128]);
 
@@ -226,12 +219,6 @@ int emesh_engine_payload(emesh_engine* e, uint32_t worker, const uint8_t** codes
  * stats (nseg*4 f64: mu, sigma, lo, width). Synchronizes the engine. */
 int emesh_engine_payload_host(emesh_engine* e, uint32_t worker, uint8_t* codes_host, float* codebooks_host,
                               double* stats_host);
-
-/* Development aid: per-task timeline of the persistent quantizer (records of
- * 4 x u64 globaltimer ns {start, ready, main-loop done, end} + 4 x u32
- * {kind, segment, tile, smid}). enable(0) turns it off. */
-int emesh_trace_enable(uint64_t records);
-uint64_t emesh_trace_read(void* host, uint64_t max_records);
 
 /* Number of kernels this engine launched since creation (for the bench's
  * gpu_launches claim). */

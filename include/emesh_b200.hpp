@@ -52,13 +52,13 @@ inline void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw FatalError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// RAII device buffer (16-byte aligned by cudaMalloc; a little slack for the
-// float4 grid the kernels read)
+// RAII device buffer (256-byte aligned by cudaMalloc; 32 bytes of slack for
+// the 32-byte octet grid the quantizer reads)
 template <typename T>
 class DeviceBuffer {
 public:
     explicit DeviceBuffer(size_t n) : n_(n) {
-        cuda_check(cudaMalloc(&p_, (n ? n : 1) * sizeof(T) + 16), "cudaMalloc");
+        cuda_check(cudaMalloc(&p_, (n ? n : 1) * sizeof(T) + 32), "cudaMalloc");
     }
     DeviceBuffer(const DeviceBuffer&) = delete;
     DeviceBuffer& operator=(const DeviceBuffer&) = delete;

@@ -20,12 +20,11 @@ EXPORTS = (
     "emesh_dequantize", "emesh_dequantize_segments",
     "emesh_encode_quant_chunk", "emesh_decode_quant_chunk",
     "emesh_pseudo_gradient", "emesh_nesterov_outer_step",
-    "emesh_adamw_step", "emesh_plan_segments", "emesh_plan_tensor_segments", "emesh_ring_schedule", "emesh_debug_batch_runs",
+    "emesh_adamw_step", "emesh_plan_segments", "emesh_plan_tensor_segments", "emesh_ring_schedule",
     "emesh_nccl_unique_id", "emesh_engine_create", "emesh_engine_destroy",
     "emesh_engine_segments", "emesh_engine_ring_allreduce", "emesh_engine_outer_sync",
     "emesh_engine_outer_sync_host", "emesh_engine_check", "emesh_engine_payload", "emesh_engine_payload_host",
     "emesh_engine_launches", "emesh_engine_profile", "emesh_engine_profile_read", "emesh_engine_timeline", "emesh_engine_transport",
-    "emesh_trace_enable", "emesh_trace_read",
     "emesh_checkpoint_encoded_size", "emesh_checkpoint_encode", "emesh_checkpoint_decode",
     "emesh_checkpoint_probe", "emesh_checkpoint_layout", "emesh_checkpoint_write_file",
     "emesh_checkpoint_read_file", "emesh_sha256",
@@ -114,7 +113,6 @@ def lib() -> C.CDLL:
         "emesh_adamw_step": (i32, [vp, vp, vp, vp, u64, u64] + [C.c_float] * 6 + [vp, vp]),
         "emesh_plan_tensor_segments": (u64, [vp, u32, u32, u32, vp, vp]),
         "emesh_ring_schedule": (u64, [u64, u32, u32, u64, u32, vp, u64]),
-        "emesh_debug_batch_runs": (u64, [u64, u32, u32, u64, u32, u32, vp, u64, vp]),
         "emesh_nccl_unique_id": (i32, [vp]),
         "emesh_engine_create": (i32, [P(EngineConfig), P(vp)]),
         "emesh_engine_destroy": (i32, [vp]),
@@ -126,8 +124,6 @@ def lib() -> C.CDLL:
         "emesh_engine_payload": (i32, [vp, u32, P(vp), P(vp), P(vp), P(u64)]),
         "emesh_engine_payload_host": (i32, [vp, u32, vp, vp, vp]),
         "emesh_engine_launches": (u64, [vp]),
-        "emesh_trace_enable": (i32, [u64]),
-        "emesh_trace_read": (u64, [vp, u64]),
         "emesh_engine_profile": (i32, [vp, i32]),
         "emesh_engine_profile_read": (i32, [vp, u32, P(u64), P(C.c_double), P(C.c_double)]),
         "emesh_engine_timeline": (u64, [vp, P(C.c_double), u64]),

@@ -19,9 +19,7 @@
 
 #include "emesh_b200.h"
 #include "kernels.cuh"
-#ifndef EMESH_BIN_L1PF_CARVEOUT
-#define EMESH_BIN_L1PF_CARVEOUT 64
-#endif
+#include "quant.cuh"
 
 using namespace emesh_b200;
 
@@ -81,10 +79,6 @@ struct Seg {
     uint64_t lo, len;
 };
 
-uint32_t quant_lag_tiles();
-bool bin_reverse();
-bool quant_mix();
-
 // One pipelining window: consecutive segments of one rank chunk.
 struct Batch {
     uint32_t chunk = 0, window = 0;
@@ -92,37 +86,20 @@ struct Batch {
     uint64_t el_lo = 0, el_hi = 0;  // element span [el_lo, el_hi) (contiguous for a flat arena)
     uint64_t elems = 0;             // elements in the batch
     std::vector<std::pair<uint64_t, uint64_t>> eruns;  // contiguous element runs {lo, len} (transfers)
-    uint32_t ncta = 0, nruns = 0, ntasks = 0;
-    uint32_t upw = kUnitsPerWarp;   // warp units per tile (tile_units_per_warp)
-    size_t off_segs = 0, off_cta = 0, off_runs = 0;  // byte offsets into the table arena
+    uint32_t ncta = 0;              // elementwise tiles (k_apply family)
+    uint32_t ntiles = 0;            // quantizer STATS tiles
+    uint32_t upw = 1;               // elementwise warp units per tile
+    size_t off_segs = 0, off_cta = 0, off_tiles = 0;  // byte offsets into the table arena
     const SegInfo* d_segs = nullptr;
     const uint32_t* d_cta_seg = nullptr;
-    const uint4* d_runs = nullptr;
+    const uint4* d_tile_seg = nullptr;
 
     void bind(void* base) {
         d_segs = reinterpret_cast<const SegInfo*>((char*)base + off_segs);
         d_cta_seg = reinterpret_cast<const uint32_t*>((char*)base + off_cta);
-        d_runs = reinterpret_cast<const uint4*>((char*)base + off_runs);
+        d_tile_seg = reinterpret_cast<const uint4*>((char*)base + off_tiles);
     }
 };
-
-// Tile shape per batch: 4 warp units (16K elements) per tile for large batches,
-// 2 (8K) for small ones and 1 for tiny ones, where more CTAs per segment shorten
-// the serial STATS -> thresholds -> BIN chain. Measured at 2 GPUs
-// (profiles/r01_u2_ab/): 2-unit tiles take 0.101 vs 0.122 ms per round at 1 MB,
-// 0.171 vs 0.183 ms at 64 MB (8M-element batches), but are 2-4 % slower from
-// 32M-element batches up; 1-unit tiles (profiles/r01_tile1/) a further -8..-14 %
-// on <= 2M-element batches at 2 and 4 GPUs, mixed at 4M-8M.
-uint32_t tile_units_per_warp(uint64_t batch_elems) {
-    static const int force = [] {
-        const char* v = std::getenv("EMESH_TILE_UNITS");  // 1 / 2 / 4 force a shape; unset or 0: by size
-        return v ? std::atoi(v) : 0;
-    }();
-    if (force == 1 || force == 2 || force == 4) return (uint32_t)std::min(force, kUnitsPerWarp);
-    constexpr uint64_t kTinyBatchElems = 2ull << 20, kSmallBatchElems = 16ull << 20;
-    if (batch_elems <= kTinyBatchElems) return 1u;
-    return batch_elems <= kSmallBatchElems ? (uint32_t)std::min(2, kUnitsPerWarp) : (uint32_t)kUnitsPerWarp;
-}
 
 struct Plan {
     uint64_t n = 0;
@@ -131,7 +108,7 @@ struct Plan {
     std::vector<std::vector<Batch>> batches;    // [chunk][window]
     std::vector<uint8_t> host_tables;
     void* d_tables = nullptr;
-    size_t max_cta = 0, max_segs = 0, max_slots = 0;
+    size_t max_cta = 0, max_segs = 0, max_oct = 0, max_tiles = 0;
 
     // Appends the device tables for one batch over segments [s0, s1).
     void add_batch(uint32_t chunk, uint32_t window, uint32_t s0, uint32_t s1) {
@@ -140,34 +117,33 @@ struct Plan {
         b.window = window;
         b.slot0 = s0;
         b.nseg = s1 - s0;
-        {
-            uint64_t tot = 0;
-            for (uint32_t s = s0; s < s1; ++s) tot += segs[s].len;
-            b.upw = tile_units_per_warp(tot);
-        }
         std::vector<SegInfo> infos;
         std::vector<uint32_t> cseg;
+        std::vector<uint4> tseg;  // quantizer STATS tile -> {segment, tile within it, first octet, octets}
         bool first = true;
-        uint64_t sq = 0;  // scratch float4 slots so far
+        uint64_t so = 0;  // overflow scratch octets so far
         for (uint32_t s = s0; s < s1; ++s) {
             const Seg& g = segs[s];
             SegInfo si{};
             si.lo = g.lo;
             si.len = g.len;
             si.q0 = g.lo >> 2;
-            si.sq0 = sq;
+            si.o0 = g.lo >> 3;
+            si.so0 = so;
             si.cta0 = (uint32_t)cseg.size();
+            si.t0 = (uint32_t)tseg.size();
             si.slot = s;
             si.in_slot = s;
             si.upw = b.upw;
             if (g.len > 0) {
-                const uint64_t q_last = (g.lo + g.len - 1) >> 2;
-                const uint64_t nq = q_last - si.q0 + 1;
+                const uint64_t nq = ((g.lo + g.len - 1) >> 2) - si.q0 + 1;
                 si.nunits = (uint32_t)((nq + kUnitSlots - 1) / kUnitSlots);
                 si.ncta = (si.nunits + kWarps * b.upw - 1) / (kWarps * b.upw);
-                // whole units: no 128-B scratch line (and no prefetched unit) is
-                // shared with another segment, whose STATS may not have run yet
-                sq += (nq + kUnitSlots - 1) / kUnitSlots * kUnitSlots;
+                const uint64_t no = ((g.lo + g.len - 1) >> 3) - si.o0 + 1;
+                si.nu8 = (uint32_t)((no + kUnitOct - 1) / kUnitOct);
+                si.ntile = (si.nu8 + kTileUnits - 1) / kTileUnits;
+                // whole units: no 128-B overflow line is shared with another segment
+                so += (uint64_t)si.nu8 * kUnitOct;
                 if (first) { b.el_lo = g.lo; first = false; }
                 b.el_lo = std::min(b.el_lo, g.lo);
                 b.el_hi = std::max(b.el_hi, g.lo + g.len);
@@ -178,86 +154,19 @@ struct Plan {
                     b.eruns.push_back({g.lo, g.len});
             }
             for (uint32_t t = 0; t < si.ncta; ++t) cseg.push_back((uint32_t)infos.size());
+            for (uint32_t t = 0; t < si.ntile; ++t) {
+                // the tile's octets [o, o + no) (for the L2 prefetch; an even count keeps the code range 16-B sized)
+                const uint64_t o = si.o0 + (uint64_t)t * kTileUnits * kUnitOct;
+                const uint64_t o_end = std::min<uint64_t>(si.o0 + (uint64_t)si.nu8 * kUnitOct, o + (uint64_t)kTileUnits * kUnitOct);
+                const uint64_t last = (g.lo + g.len - 1) >> 3;
+                uint64_t no = std::min<uint64_t>(o_end, last + 1) - o;
+                no = (no + 1) & ~uint64_t(1);
+                tseg.push_back(make_uint4((uint32_t)infos.size(), t, (uint32_t)o, (uint32_t)no));
+            }
             infos.push_back(si);
         }
         b.ncta = (uint32_t)cseg.size();
-        // persistent-kernel task order (see kernels.cuh): STATS tiles in
-        // segment order; the BIN tiles of s (in reverse tile order: the most
-        // recently written scratch is re-read first, while still in L2) become
-        // available `lag` tasks after its last STATS tile and are then
-        // interleaved 1:1 with the following STATS tiles, so every SM always
-        // runs a mix of the HBM-bound STATS and the issue-bound BIN work.
-        // Compressed into runs {first task, kind | bin segment << 2, segment,
-        // first tile}: plain runs (one kind) and mixed runs (S, B, S, B, ...).
-        std::vector<uint4> runs;
-        {
-            const uint32_t lag = quant_lag_tiles();
-            struct Task { uint32_t kind, seg, tile; };
-            std::vector<Task> order;
-            order.reserve(2 * (size_t)b.ncta);
-            struct Pending { uint32_t seg, next, left, at; };
-            std::vector<Pending> bq;
-            size_t hb = 0;
-            const bool mix = quant_mix();
-            auto bin_ready = [&]() { return hb < bq.size() && order.size() >= bq[hb].at; };
-            auto pop_bin = [&]() {
-                Pending& pb = bq[hb];
-                order.push_back({kTaskBin, pb.seg, pb.next});
-                if (bin_reverse()) --pb.next; else ++pb.next;
-                if (--pb.left == 0) ++hb;
-            };
-            for (uint32_t i = 0; i < infos.size(); ++i) {
-                for (uint32_t t = 0; t < infos[i].ncta; ++t) {
-                    order.push_back({kTaskStats, i, t});
-                    if (mix) {
-                        if (bin_ready()) pop_bin();
-                    } else {  // whole-segment BIN blocks (no interleaving)
-                        while (bin_ready()) pop_bin();
-                    }
-                }
-                if (infos[i].ncta)
-                    bq.push_back({i, bin_reverse() ? infos[i].ncta - 1 : 0u, infos[i].ncta,
-                                  (uint32_t)order.size() + lag});
-            }
-            while (hb < bq.size()) pop_bin();
-            b.ntasks = (uint32_t)order.size();
-            const int dir = bin_reverse() ? -1 : 1;
-            size_t p0 = 0;
-            while (p0 < order.size()) {
-                const Task& t0 = order[p0];
-                // mixed run: S(a, i), B(b, j), S(a, i+1), B(b, j+dir), ...
-                size_t q = p0;
-                if (t0.kind == kTaskStats && p0 + 1 < order.size() && order[p0 + 1].kind == kTaskBin) {
-                    const Task& t1 = order[p0 + 1];
-                    while (q + 1 < order.size()) {
-                        const uint32_t i = (uint32_t)((q - p0) / 2);
-                        const Task& s0 = order[q];
-                        const Task& s1 = order[q + 1];
-                        if (s0.kind != kTaskStats || s0.seg != t0.seg || s0.tile != t0.tile + i) break;
-                        if (s1.kind != kTaskBin || s1.seg != t1.seg || (int64_t)s1.tile != (int64_t)t1.tile + dir * (int64_t)i) break;
-                        q += 2;
-                    }
-                    if (q - p0 >= 4 && t0.tile < 0x10000u && t1.tile < 0x10000u) {
-                        runs.push_back(make_uint4((uint32_t)p0, (dir < 0 ? kTaskMixRev : kTaskMixFwd) | (t1.seg << 2), t0.seg,
-                                                  t0.tile | (t1.tile << 16)));
-                        p0 = q;
-                        continue;
-                    }
-                    q = p0;
-                }
-                // plain run of one kind and segment, tiles +1 (STATS) / +dir (BIN)
-                const int step = t0.kind == kTaskBin ? dir : 1;
-                q = p0 + 1;
-                while (q < order.size() && order[q].kind == t0.kind && order[q].seg == t0.seg &&
-                       (int64_t)order[q].tile == (int64_t)t0.tile + step * (int64_t)(q - p0))
-                    ++q;
-                runs.push_back(make_uint4((uint32_t)p0, t0.kind, t0.seg,
-                                          step < 0 ? 0x80000000u | t0.tile : t0.tile));
-                p0 = q;
-            }
-        }
-        b.nruns = (uint32_t)runs.size();
-
+        b.ntiles = (uint32_t)tseg.size();
         auto append = [&](const void* p, size_t bytes) {
             size_t off = (host_tables.size() + 15) & ~size_t(15);
             host_tables.resize(off + bytes);
@@ -266,11 +175,11 @@ struct Plan {
         };
         b.off_segs = append(infos.data(), infos.size() * sizeof(SegInfo));
         b.off_cta = append(cseg.data(), cseg.size() * sizeof(uint32_t));
-        b.off_runs = append(runs.data(), runs.size() * sizeof(uint4));
-
+        b.off_tiles = append(tseg.data(), tseg.size() * sizeof(uint4));
         max_cta = std::max<size_t>(max_cta, b.ncta);
+        max_tiles = std::max<size_t>(max_tiles, b.ntiles);
         max_segs = std::max<size_t>(max_segs, b.nseg);
-        max_slots = std::max<size_t>(max_slots, sq);
+        max_oct = std::max<size_t>(max_oct, so);
         batches[chunk].push_back(b);
     }
 
@@ -289,33 +198,6 @@ struct Plan {
 };
 
 constexpr uint64_t kDefaultWindow = (uint64_t)16 << 20;  // elements per pipelining window
-
-int persistent_grid(const void* fn, uint32_t ntasks);
-// Lag between a segment's last STATS tile and its first BIN tile in the task
-// order: one persistent grid (the stats root publishes within about one
-// tile time; longer lags push scratch x out of L2).
-bool quant_mix() {
-    static const bool r = [] {
-        const char* e = std::getenv("EMESH_QUANT_MIX");  // tuning knob
-        return e ? std::atoi(e) != 0 : true;
-    }();
-    return r;
-}
-bool bin_reverse() {
-    static const bool r = [] {
-        const char* e = std::getenv("EMESH_BIN_REVERSE");  // tuning knob
-        return e ? std::atoi(e) != 0 : true;
-    }();
-    return r;
-}
-uint32_t quant_lag_tiles() {
-    const int g = persistent_grid((const void*)k_quant<kSrcAminusB | kHasIn>, 1u << 30);
-    static const double mult = [] {
-        const char* e = std::getenv("EMESH_QUANT_LAG");  // tuning knob, in persistent grids
-        return e ? std::atof(e) : 1.5;
-    }();
-    return (uint32_t)(std::max(1.0, mult * (g > 0 ? g : 512)));
-}
 
 // Ring plan: k chunks, min(S, len) subs each, windows of G segments.
 Plan make_ring_plan(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems) {
@@ -414,52 +296,50 @@ Plan make_list_plan(const uint64_t* lo, const uint64_t* len, uint32_t nseg) {
 
 // Device scratch shared by every batch launched on one stream.
 struct Workspace {
-    float* scratch = nullptr;
-    StatP* leaf_stat = nullptr;
-    SegAcc* acc = nullptr;  // zero between launches (self-cleaning, see SegAcc)
+    float* scratch = nullptr;    // quantizer overflow x (octets of 8 floats)
+    StatP* leaf_stat = nullptr;  // per quantizer tile
+    uint32_t* ovf = nullptr;     // per quantizer tile: overflow lists
+    SegAcc* acc = nullptr;       // zero between launches (self-cleaning, see SegAcc)
     uint32_t* seg_flags = nullptr;
     uint32_t* sync = nullptr;
     uint32_t* err = nullptr;
-    size_t cap_slots = 0, cap_cta = 0, cap_segs = 0;
+    size_t cap_oct = 0, cap_tiles = 0, cap_segs = 0;
 
     template <typename T>
-    static int grow(T*& p, size_t& cap, size_t want, size_t elems_per, bool zero) {
-        if (want <= cap && p) return EMESH_OK;
+    static int grow(T*& p, size_t want_bytes, bool zero) {
         if (p) CU(cudaFree(p));
-        const size_t bytes = std::max<size_t>(want, 1) * elems_per * sizeof(T);
+        p = nullptr;
+        const size_t bytes = std::max<size_t>(want_bytes, 16);
         CU(cudaMalloc(&p, bytes));
         if (zero) CU(cudaMemset(p, 0, bytes));
         return EMESH_OK;
     }
 
-    int reserve(size_t slots, size_t ctas, size_t segs) {
+    int reserve(size_t oct, size_t tiles, size_t segs) {
         if (!err) {
             CU(cudaMalloc(&err, sizeof(uint32_t)));
             CU(cudaMemset(err, 0, sizeof(uint32_t)));
         }
-        if (slots > cap_slots || !scratch) {
-            size_t c = 0;
-            TRY(grow(scratch, c, slots, 4, false));
-            cap_slots = std::max<size_t>(slots, 1);
+        if (oct > cap_oct || !scratch) {
+            TRY(grow(scratch, oct * 32, false));
+            cap_oct = std::max<size_t>(oct, 1);
         }
-        if (ctas > cap_cta || !leaf_stat) {
-            size_t c = 0;
-            TRY(grow(leaf_stat, c, ctas, 1, false));
-            cap_cta = std::max<size_t>(ctas, 1);
+        if (tiles > cap_tiles || !leaf_stat) {
+            TRY(grow(leaf_stat, tiles * sizeof(StatP), false));
+            TRY(grow(ovf, tiles * sizeof(uint32_t), false));
+            cap_tiles = std::max<size_t>(tiles, 1);
         }
         if (segs > cap_segs || !seg_flags) {
-            size_t c = 0;
-            TRY(grow(seg_flags, c, segs, 1, true));
-            c = 0;
-            TRY(grow(acc, c, segs, 1, true));
-            c = 0;
-            TRY(grow(sync, c, kSyncReady + 3 * segs, 1, true));
+            TRY(grow(seg_flags, segs * sizeof(uint32_t), true));
+            TRY(grow(acc, segs * sizeof(SegAcc), true));
+            TRY(grow(sync, (kSyncReady + kSyPerSeg * segs) * sizeof(uint32_t), true));
             cap_segs = std::max<size_t>(segs, 1);
         }
         return EMESH_OK;
     }
     void release() {
-        cudaFree(scratch); cudaFree(leaf_stat); cudaFree(acc); cudaFree(seg_flags); cudaFree(sync); cudaFree(err);
+        cudaFree(scratch); cudaFree(leaf_stat); cudaFree(ovf); cudaFree(acc); cudaFree(seg_flags); cudaFree(sync);
+        cudaFree(err);
         *this = Workspace();
     }
 };
@@ -547,49 +427,30 @@ struct Tracker {
 };
 Tracker g_codec_tracker;
 
-// Optional task trace (development aid): emesh_trace_enable / emesh_trace_read.
-struct TraceBuf {
-    TraceRec* buf = nullptr;
-    uint32_t* n = nullptr;
-    size_t cap = 0;
-} g_trace;
-
-// Co-resident grid of the persistent quantizer (occupancy x SMs, capped at the task count).
-int persistent_grid(const void* fn, uint32_t ntasks) {
-    static std::mutex mu;
-    static std::vector<std::pair<const void*, int>> cache;
+// SMs of this device (cached per device).
+int sm_count() {
+    static int cache[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
-    int per_sm = 0;
-    {
-        std::lock_guard<std::mutex> g(mu);
-        for (auto& kv : cache)
-            if (kv.first == fn) per_sm = kv.second;
-        if (!per_sm) {
-            if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQuantSmemBytes) != cudaSuccess)
-                return -1;
-#if EMESH_BIN_L1PF
-            // leave L1 room for the prefetched scratch lines (smem only as large as the CTAs need)
-            cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, EMESH_BIN_L1PF_CARVEOUT);
-#endif
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, kQuantSmemBytes) != cudaSuccess)
-                return -1;
-            cache.push_back({fn, per_sm});
-        }
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = sms;
     }
-    int sms = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const long long want = (long long)per_sm * sms;
-    return (int)std::max<long long>(1, std::min<long long>(want, ntasks));
+    return cache[dev];
 }
 
+// Segment-resident quantizer (quant.cuh): one persistent 512-thread CTA per
+// SM. `reserve_sms` SMs stay free for NCCL's kernels (NCCL transport) so the
+// ring's transfers overlap this kernel.
 int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t st, Tracker* tr,
-                 uint32_t reserve_ctas = 0) {
-    if (bt.ncta == 0) return EMESH_OK;
-    QuantArgs a{};
+                 uint32_t reserve_sms = 0) {
+    if (bt.ntiles == 0) return EMESH_OK;
+    Q2Args a{};
     a.segs = bt.d_segs;
-    a.cta_seg = bt.d_cta_seg;
-    a.ncta = bt.ncta;
+    a.tile_seg = bt.d_tile_seg;
+    a.ntiles = bt.ntiles;
     a.nseg = bt.nseg;
     a.a = io.a;
     a.b = io.b;
@@ -617,12 +478,6 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     }
     for (uint32_t f = 0; f < io.nflags; ++f) a.sflag[f] = io.flags[f];
     a.nflag = io.nflags;
-    a.remote = io.nx > 0 ? 1u : 0u;
-    static const bool tile_fence = [] {
-        const char* v = std::getenv("EMESH_P2P_TILE_FENCE");  // tuning knob
-        return v ? std::atoi(v) != 0 : false;
-    }();
-    if (a.remote && tile_fence) a.remote |= 2u;
     a.in_flag = io.in_flag;
     a.epoch = io.epoch;
     a.timeout_ns = tr ? tr->timeout_ns : 30ull * 1000000000ull;
@@ -631,14 +486,9 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     a.acc = ws.acc;
     a.seg_flags = ws.seg_flags;
     a.err = ws.err;
-    a.runs = bt.d_runs;
-    a.nruns = bt.nruns;
-    a.ntasks = bt.ntasks;
     a.sync = ws.sync;
-    a.trace = g_trace.buf;
-    a.trace_n = g_trace.n;
-    a.trace_cap = (uint32_t)g_trace.cap;
-    CU(cudaMemsetAsync(ws.sync, 0, (kSyncReady + 3 * (size_t)bt.nseg) * sizeof(uint32_t), st));
+    a.ovf = ws.ovf;
+    CU(cudaMemsetAsync(ws.sync, 0, (kSyncReady + kSyPerSeg * (size_t)bt.nseg) * sizeof(uint32_t), st));
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
     void* args[] = {&a};
@@ -652,17 +502,24 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
         case kSrcAminusB | kHasIn | kDivK: fn = (const void*)k_quant<kSrcAminusB | kHasIn | kDivK>; break;
         default: return fail(EMESH_ECONFIG, "unsupported producer %d", io.src);
     }
-    // A plain launch suffices: a task is claimed only by a running CTA and only
-    // ever waits on tasks claimed before it, so progress never depends on
-    // co-residency. `reserve` CTA slots stay free for NCCL's kernels so the
-    // ring's transfers overlap this kernel.
-    int grid = persistent_grid(fn, bt.ntasks);
-    if (grid <= 0) return fail(EMESH_ECUDA, "k_quant: occupancy query failed");
-    grid = std::max(1, grid - (int)reserve_ctas);
+    {
+        static std::mutex mu;
+        static std::vector<const void*> configured;
+        std::lock_guard<std::mutex> g(mu);
+        if (std::find(configured.begin(), configured.end(), fn) == configured.end()) {
+            CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQ2SmemBytes));
+            configured.push_back(fn);
+        }
+    }
+    // A plain launch suffices: a CTA waits only when every STATS tile is
+    // claimed (quant.cuh), so progress never depends on co-residency.
+    const int sms = sm_count();
+    int grid = std::max(1, sms - (int)std::min<uint32_t>(reserve_sms, (uint32_t)sms - 1));
+    grid = std::min<int>(grid, (int)bt.ntiles);
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(grid);
-    lc.blockDim = dim3(kThreads);
-    lc.dynamicSmemBytes = kQuantSmemBytes;
+    lc.blockDim = dim3(kQThreads);
+    lc.dynamicSmemBytes = kQ2SmemBytes;
     lc.stream = st;
     CU(cudaLaunchKernelExC(&lc, fn, args));
     if (tr) tr->launches += 1;
@@ -725,6 +582,8 @@ int flat_grid(uint64_t n) {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+// the quantizer moves 32-byte octets (256-bit loads) and 8-byte code words
+bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
 
 // Process-global workspace for the standalone codec entry points.
 std::mutex g_codec_mu;
@@ -746,14 +605,14 @@ int emesh_abi_version(void) { return 1; }
 int emesh_quantize_segments(const float* x, const uint64_t* seg_lo, const uint64_t* seg_len, uint32_t nseg,
                             uint8_t* codes, float* codebooks, double* stats, emesh_stream_t stream) {
     if (nseg == 0) return EMESH_OK;
-    if (!aligned16(x) || (reinterpret_cast<uintptr_t>(codes) & 3u))
-        return fail(EMESH_ESHAPE, "quantize: x must be 16-byte and codes 4-byte aligned");
+    if (!aligned32(x) || (reinterpret_cast<uintptr_t>(codes) & 7u))
+        return fail(EMESH_ESHAPE, "quantize: x must be 32-byte and codes 8-byte aligned");
     for (uint32_t i = 0; i < nseg; ++i)
         if (seg_len[i] == 0) return fail(EMESH_ESHAPE, "quantize: empty chunk");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     std::lock_guard<std::mutex> g(g_codec_mu);
     Plan p = make_list_plan(seg_lo, seg_len, nseg);
-    TRY(g_codec_ws.reserve(p.max_slots, p.max_cta, p.max_segs));
+    TRY(g_codec_ws.reserve(p.max_oct, p.max_tiles, p.max_segs));
     // stream-ordered tables + stats (freed in stream order)
     void* d_tables = nullptr;
     SegStat* d_stats = nullptr;
@@ -771,27 +630,6 @@ int emesh_quantize_segments(const float* x, const uint64_t* seg_lo, const uint64
     CU(cudaFreeAsync(d_tables, st));
     CU(cudaFreeAsync(d_stats, st));
     return EMESH_OK;
-}
-
-int emesh_trace_enable(uint64_t records) {
-    if (g_trace.buf) { cudaFree(g_trace.buf); cudaFree(g_trace.n); g_trace = TraceBuf(); }
-    if (!records) return EMESH_OK;
-    CU(cudaMalloc(&g_trace.buf, records * sizeof(TraceRec)));
-    CU(cudaMalloc(&g_trace.n, sizeof(uint32_t)));
-    CU(cudaMemset(g_trace.n, 0, sizeof(uint32_t)));
-    g_trace.cap = records;
-    return EMESH_OK;
-}
-
-uint64_t emesh_trace_read(void* host, uint64_t max_records) {
-    if (!g_trace.buf) return 0;
-    cudaDeviceSynchronize();
-    uint32_t n = 0;
-    cudaMemcpy(&n, g_trace.n, sizeof n, cudaMemcpyDeviceToHost);
-    const uint64_t m = std::min<uint64_t>({(uint64_t)n, (uint64_t)g_trace.cap, max_records});
-    if (host && m) cudaMemcpy(host, g_trace.buf, m * sizeof(TraceRec), cudaMemcpyDeviceToHost);
-    cudaMemset(g_trace.n, 0, sizeof(uint32_t));
-    return m;
 }
 
 int emesh_codec_check(emesh_stream_t stream) {
@@ -937,7 +775,7 @@ struct emesh_engine {
     cudaEvent_t ev_entry = nullptr, ev_done = nullptr, ev_comm_done = nullptr;
     std::vector<cudaEvent_t> ev_send, ev_recv;  // per window
     std::vector<emesh_ring_op> schedule;        // NCCL mode program (build_schedule)
-    uint32_t reserve_ctas = 0;                  // quantizer CTA slots left to NCCL (NCCL mode)
+    uint32_t reserve_sms = 8;                   // SMs the quantizer leaves to NCCL's kernels (NCCL transport)
     struct Arena {
         uint8_t* codes = nullptr;
         float* cbs = nullptr;
@@ -1001,7 +839,7 @@ int engine_alloc(emesh_engine* e) {
         e->pay.assign(e->workers, nullptr);
         for (auto& p : e->pay) CU(cudaMalloc(&p, n * sizeof(float) + 16));
     }
-    TRY(e->ws.reserve(e->plan.max_slots, e->plan.max_cta, e->plan.max_segs));
+    TRY(e->ws.reserve(e->plan.max_oct, e->plan.max_tiles, e->plan.max_segs));
     return EMESH_OK;
 }
 
@@ -1188,35 +1026,12 @@ int run_virtual_apply(emesh_engine* e, uint32_t c, uint32_t w, float* const* the
     return EMESH_OK;
 }
 
-// Chunk c's decodes touch only chunk c's element range (theta, momentum, out)
-// and the owner's chunk-c codes / codebooks, which chunk c+1's chain never
-// writes; the chains share the quantizer workspace and stay serial on s_comp.
-// So the decodes of chunk c run on s_comm (idle in the virtual ring) behind an
-// event on chain c and overlap chain c+1: their HBM-bound CTAs fill the
-// quantizer's launch tails and its unused bandwidth. engine_exit joins s_comm.
-// Measured (config 2, N=1, 3 x 2 alternating runs): 25.61 vs 25.73 ms per round,
-// within noise — both kernels are DRAM-bound once they share the SMs — and the
-// overlapped per-kernel event times no longer give a roofline, so it is off.
-bool virtual_overlap() {
-    static const bool on = [] {
-        const char* v = std::getenv("EMESH_VIRTUAL_OVERLAP");  // A/B knob (default off)
-        return v ? std::atoi(v) != 0 : false;
-    }();
-    return on;
-}
-
 int run_virtual(emesh_engine* e, const float* const* A, const float* const* B, float* const* theta, float* const* buf,
                 float* const* local_out, float* const* out, float lr, float mom) {
     if (e->fp32) return run_virtual_f32(e, A, B, theta, buf, local_out, out, lr, mom);
-    const bool ov = virtual_overlap();
     for (uint32_t c = 0; c < e->k; ++c) {
         TRY(run_virtual_chain(e, c, A, B));
-        if (ov) {
-            CU(cudaEventRecord(e->ev_send[0], e->s_comp));  // ev_send is unused by the virtual ring otherwise
-            CU(cudaStreamWaitEvent(e->s_comm, e->ev_send[0], 0));
-        }
-        for (uint32_t w = 0; w < e->k; ++w)
-            TRY(run_virtual_apply(e, c, w, theta, buf, local_out, out, lr, mom, ov ? e->s_comm : e->s_comp));
+        for (uint32_t w = 0; w < e->k; ++w) TRY(run_virtual_apply(e, c, w, theta, buf, local_out, out, lr, mom));
     }
     return EMESH_OK;
 }
@@ -1402,7 +1217,7 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
                     TRY(launch_f32_hop(P[o.recv_chunk][j], e->ws, io, sc, &e->tr));
                 } else {
                     QuantIO io{pg ? kSrcAminusB : kSrcA, A, B, nullptr, nullptr, 1.f, ar.codes, ar.cbs, ar.stats};
-                    TRY(launch_quant(P[o.recv_chunk][j], e->ws, io, sc, &e->tr, e->reserve_ctas));
+                    TRY(launch_quant(P[o.recv_chunk][j], e->ws, io, sc, &e->tr, e->reserve_sms));
                 }
                 CU(cudaEventRecord(e->ev_send[j], sc));
                 break;
@@ -1425,7 +1240,7 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
                 } else {
                     QuantIO io{hop_src(pg, (uint32_t)o.hop, k), A, B, ar.codes, ar.cbs, (float)k, ar.codes, ar.cbs,
                                ar.stats};
-                    TRY(launch_quant(P[o.recv_chunk][j], e->ws, io, sc, &e->tr, e->reserve_ctas));
+                    TRY(launch_quant(P[o.recv_chunk][j], e->ws, io, sc, &e->tr, e->reserve_sms));
                 }
                 CU(cudaEventRecord(e->ev_send[j], sc));
                 break;
@@ -1797,26 +1612,6 @@ uint64_t emesh_plan_tensor_segments(const uint64_t* sizes, uint32_t nt, uint32_t
     return p.segs.size();
 }
 
-uint64_t emesh_debug_batch_runs(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems, uint32_t chunk,
-                                uint32_t window, uint32_t* out4, uint64_t max_runs, uint32_t* ntasks_ncta) {
-    if (k == 0 || chunk >= k) return 0;
-    Plan p = make_ring_plan(n, k, S ? S : 4, window_elems ? window_elems : kDefaultWindow);
-    if (window >= p.batches[chunk].size()) return 0;
-    const Batch& b = p.batches[chunk][window];
-    const uint4* r = reinterpret_cast<const uint4*>(p.host_tables.data() + b.off_runs);
-    for (uint32_t i = 0; i < b.nruns && i < max_runs; ++i) {
-        out4[4 * i] = r[i].x; out4[4 * i + 1] = r[i].y; out4[4 * i + 2] = r[i].z; out4[4 * i + 3] = r[i].w;
-    }
-    if (ntasks_ncta) {
-        ntasks_ncta[0] = b.ntasks;
-        ntasks_ncta[1] = b.ncta;
-        ntasks_ncta[2] = b.nseg;
-        const SegInfo* si = reinterpret_cast<const SegInfo*>(p.host_tables.data() + b.off_segs);
-        for (uint32_t i = 0; i < b.nseg; ++i) ntasks_ncta[3 + i] = si[i].ncta;
-    }
-    return b.nruns;
-}
-
 uint64_t emesh_ring_schedule(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems, uint32_t rank,
                              emesh_ring_op* ops, uint64_t max_ops) {
     if (k == 0 || rank >= k) return 0;
@@ -1902,8 +1697,6 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
     }
     if (!virt && e->k > 1) {
         e->schedule = build_schedule(e->plan, e->rank);
-        const char* rs = std::getenv("EMESH_NCCL_RESERVE_CTAS");
-        e->reserve_ctas = rs ? (uint32_t)std::atoi(rs) : 0u;
         ncclUniqueId id;
         std::memcpy(&id, cfg->nccl_id, sizeof id);
         ncclConfig_t ncfg = NCCL_CONFIG_INITIALIZER;
@@ -1927,7 +1720,7 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
             e->plan.release();
             e->plan = mkplan(nccl_window);
             e->windows = (uint32_t)e->plan.batches[0].size();
-            if ((rc = e->plan.upload()) || (rc = e->ws.reserve(e->plan.max_slots, e->plan.max_cta, e->plan.max_segs)))
+            if ((rc = e->plan.upload()) || (rc = e->ws.reserve(e->plan.max_oct, e->plan.max_tiles, e->plan.max_segs)))
                 return bail(rc);
             e->schedule = build_schedule(e->plan, e->rank);
             for (auto ev : e->ev_send) cudaEventDestroy(ev);
@@ -2036,7 +1829,7 @@ int emesh_engine_ring_allreduce(emesh_engine* e, const float* const* input, floa
                                 emesh_stream_t stream) {
     cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
     for (uint32_t w = 0; w < e->workers; ++w)
-        if (!aligned16(input[w]) || !aligned16(output[w])) return fail(EMESH_ESHAPE, "arenas must be 16-byte aligned");
+        if (!aligned32(input[w]) || !aligned16(output[w])) return fail(EMESH_ESHAPE, "arenas must be 32-byte aligned");
     TRY(engine_enter(e, user));
     if (e->k == 1) {
         // allreduce.hpp:319: identity, zero communication
@@ -2055,8 +1848,8 @@ int emesh_engine_outer_sync(emesh_engine* e, float* const* theta_g, float* const
                             float lr, float mom, int write_local, emesh_stream_t stream) {
     cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
     for (uint32_t w = 0; w < e->workers; ++w)
-        if (!aligned16(theta_g[w]) || !aligned16(theta_l[w]) || !aligned16(buf[w]))
-            return fail(EMESH_ESHAPE, "arenas must be 16-byte aligned");
+        if (!aligned32(theta_g[w]) || !aligned32(theta_l[w]) || !aligned16(buf[w]))
+            return fail(EMESH_ESHAPE, "arenas must be 32-byte aligned");
     TRY(engine_enter(e, user));
     if (e->k == 1) {
         // k == 1: avg = delta exactly (allreduce.hpp:319); PG + Nesterov fused, 20 B/param
@@ -2236,10 +2029,9 @@ int emesh_engine_outer_sync_host(emesh_engine* e, float* const* theta_g, float* 
             CU(cudaMalloc(&e->h_buf[w], bytes + 16));
         }
     }
-    static const bool serial = std::getenv("EMESH_HOST_SERIAL") != nullptr;  // A/B knob
-    if (e->virt && !e->fp32 && e->k > 1 && !serial)
+    if (e->virt && !e->fp32 && e->k > 1)
         return outer_sync_host_pipelined(e, theta_g, theta_l, buf, lr, mom, write_local);
-    if (!e->virt && !e->fp32 && e->k > 1 && e->transport == EMESH_TRANSPORT_P2P && !serial)
+    if (!e->virt && !e->fp32 && e->k > 1 && e->transport == EMESH_TRANSPORT_P2P)
         return outer_sync_host_p2p(e, theta_g[0], theta_l[0], buf[0], lr, mom, write_local);
     cudaStream_t st = e->s_comp;
     for (uint32_t w = 0; w < e->workers; ++w) {

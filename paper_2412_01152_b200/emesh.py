@@ -83,10 +83,10 @@ def _dev_f32(t: torch.Tensor, what: str) -> torch.Tensor:
 
 
 def _aligned_empty(n: int, dtype, device) -> torch.Tensor:
-    """Fresh allocations are 256-B aligned by the caching allocator; pad by 16
-    so float4 reads of the last slot stay inside the allocation."""
+    """Fresh allocations are 512-B aligned by the caching allocator; pad by 32
+    so the quantizer's 32-byte octet reads of the last slot stay inside the allocation."""
     itemsize = torch.empty((), dtype=dtype).element_size()
-    pad = max(1, 16 // itemsize)
+    pad = max(1, 32 // itemsize)
     return torch.empty(n + pad, dtype=dtype, device=device)[:n]
 
 
@@ -115,7 +115,7 @@ def quantize(values: torch.Tensor, stream=None) -> QuantChunk:
     n = values.numel()
     if n == 0:
         raise ShapeError("quantize: empty chunk")
-    if values.data_ptr() % 16:
+    if values.data_ptr() % 32:  # the quantizer reads 32-byte octets
         values = values.clone()
     dev = values.device
     codes = _aligned_empty(n, torch.uint8, dev)

@@ -136,46 +136,3 @@ def test_plan_tensor_segments_match_per_tensor_oracle(capi, oracle, sizes, k, S)
     assert [(int(a), int(b)) for a, b in zip(lo, ln)] == want
     assert int(ln.sum()) == sum(sizes)
 
-
-def _decode_runs(runs, t):
-    """Task t of the quantizer's run table -> (kind, segment, tile) (kernels.cuh decode_run)."""
-    lo = int(np.searchsorted(runs[:, 0], t, side="right")) - 1
-    x, y, z, w = (int(v) for v in runs[lo])
-    off, kk = t - x, y & 3
-    if kk in (1, 3):  # mixed run: STATS / BIN alternating
-        i = off >> 1
-        if off & 1:
-            return 2, y >> 2, ((w >> 16) - i) if kk == 1 else ((w >> 16) + i)
-        return 0, z, (w & 0xFFFF) + i
-    tile = ((w & 0x7FFFFFFF) - off) if (w & 0x80000000) else w + off
-    return y, z, tile
-
-
-@pytest.mark.parametrize("n,k,S", [(1_000_000_000, 4, 16), (1_000_000_000, 4, 64), (100_003, 4, 4),
-                                   (50_000_000, 4, 16), (10_211_381_248, 8, 80)])
-def test_quantizer_task_plan_invariants(capi, n, k, S):
-    """The persistent quantizer's task order (emesh_debug_batch_runs, whole-chunk batch): every tile's
-    STATS and BIN task appear exactly once, and a segment's BIN tasks all follow its last STATS task
-    (the only wait in the kernel: progress never depends on co-residency)."""
-    L = capi.lib()
-    runs = np.zeros((1 << 16) * 4, np.uint32)
-    info = np.zeros(1 << 16, np.uint32)
-    nr = L.emesh_debug_batch_runs(n, k, S, 1 << 62, 0, 0, runs.ctypes.data, 1 << 16, info.ctypes.data)
-    assert 0 < nr < (1 << 16)
-    r = runs[: 4 * nr].reshape(-1, 4).astype(np.int64)
-    ntasks, _, nseg = (int(v) for v in info[:3])
-    nct = info[3:3 + nseg]
-    seen_s, seen_b, stats_done = set(), set(), {}
-    for t in range(ntasks):
-        kind, s, tile = _decode_runs(r, t)
-        assert 0 <= s < nseg and 0 <= tile < nct[s]
-        if kind == 0:
-            assert (s, tile) not in seen_s
-            seen_s.add((s, tile))
-            stats_done[s] = stats_done.get(s, 0) + 1
-        else:
-            assert kind == 2 and (s, tile) not in seen_b
-            seen_b.add((s, tile))
-            assert stats_done.get(s, 0) == nct[s], (t, s)
-    want = {(s, t) for s in range(nseg) for t in range(int(nct[s]))}
-    assert seen_s == want and seen_b == want

@@ -1,0 +1,79 @@
+"""Bit-exact parity at the sizes the bench runs: whole
+rounds whose segments exceed what one SM keeps on chip (the quantizer's
+overflow path), and the full config-2 round (1B params/worker, 4 workers,
+S = 16: 64 segments of 15.6M elements), every segment re-derived by the
+oracle's transport-free chain (oracle/parity.py) and compared bit for bit:
+final codes, codebooks, updated theta_g and Nesterov momentum."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def E():
+    import paper_2412_01152_b200 as E
+    return E
+
+
+def _synthetic(n, k, dev, seed):
+    """bench.py's synthetic replicas: theta_g ~ U[-1,1), theta_l = theta_g - 2^-10 U, b = 0.1 U (round 2 state)."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    tg = torch.empty(n + 8, device=dev)[:n].uniform_(-1.0, 1.0, generator=g)
+    tls = []
+    for _ in range(k):
+        l = torch.empty(n + 8, device=dev)[:n].uniform_(-1.0, 1.0, generator=g)
+        tls.append(l.mul_(-(2.0 ** -10)).add_(tg))
+    b = torch.empty(n + 8, device=dev)[:n].uniform_(-0.1, 0.1, generator=g)
+    return tg, tls, b
+
+
+def _round_and_check(E, oracle, n, k, S, seed=3, picks=None):
+    from oracle import parity
+
+    dev = torch.device("cuda:0")
+    tg0, tls, b0 = _synthetic(n, k, dev, seed)
+    eng = E.RingEngine(n, k, opts=E.ReduceOptions(pipeline_subchunks=S), virtual=True)
+    tg = [tg0.clone() for _ in range(k)]
+    tb = [b0.clone() for _ in range(k)]
+    eng.outer_sync(tg, tls, tb, E.HyperParams(), write_local=False)
+    eng.check()
+    lo, ln = eng.segments()
+    jobs = parity.segment_jobs(lo, ln, k, S, picks)
+    payloads = [eng.payload(w) for w in range(k)]  # chunk c's final payload lives in worker (c-1)%k's arena
+    # every worker ends with the same theta_g / momentum
+    for w in range(1, k):
+        assert torch.equal(tg[w], tg[0]) and torch.equal(tb[w], tb[0]), w
+
+    def inputs(j):
+        sl = slice(j.lo, j.lo + j.length)
+        return tg0[sl].cpu().numpy(), [t[sl].cpu().numpy() for t in tls], b0[sl].cpu().numpy()
+
+    def gpu(j):
+        sl = slice(j.lo, j.lo + j.length)
+        codes, cbs, _ = payloads[(j.chunk + k - 1) % k]
+        return codes[sl], cbs[j.slot], tg[0][sl].cpu().numpy(), tb[0][sl].cpu().numpy()
+
+    rep = parity.check(oracle, jobs, k, inputs, gpu)
+    eng.close()
+    return rep
+
+
+@pytest.mark.parametrize("n,k,S", [(80_000_000, 4, 1), (48_000_011, 2, 2)])
+def test_segments_beyond_on_chip_capacity(E, oracle, n, k, S):
+    """20M / 12M-element segments: more x than the SMs hold on chip, so tiles overflow to the
+    global scratch and are binned by other CTAs; still bit-exact."""
+    rep = _round_and_check(E, oracle, n, k, S)
+    assert rep.ok(), rep.as_dict()
+    assert rep.checked_segments == k * S
+
+
+def test_config2_full_round_bit_exact(E, oracle):
+    """BASELINE config 2 as the bench runs it: 1B params/worker, 4 workers, S = 16; all 64
+    segments (4.0e9 quantized elements on the host, threaded over segments)."""
+    rep = _round_and_check(E, oracle, 1_000_000_000, 4, 16, seed=1)
+    assert rep.checked_segments == 64 and rep.elements == 1_000_000_000
+    assert rep.ok(), rep.as_dict()
