@@ -35,7 +35,9 @@ enum {
     EMESH_ENCCL = 5,    /* NCCL failure (the transport; emesh::LinkError analogue) */
     EMESH_ERING = 6,    /* emesh::RingFailureError (collective aborted) */
     EMESH_ECONFIG = 7,  /* emesh::ConfigError (invalid plan/options) */
-    EMESH_EIO = 8       /* emesh::Error (checkpoint file I/O, integrity hash mismatch) */
+    EMESH_EIO = 8,      /* emesh::Error (checkpoint file I/O, integrity hash mismatch) */
+    EMESH_ESTALE = 9,   /* emesh::StalePlanError (a ring peer runs a newer plan epoch, allreduce.hpp:272) */
+    EMESH_EPROTO = 10   /* emesh::Error "ring protocol violation" (unexpected chunk header, allreduce.hpp:280) */
 };
 
 #define EMESH_BUCKETS 256
@@ -128,6 +130,9 @@ typedef struct {
                                    (RingFailureError) — peer transport: the kernels' spin budget; NCCL
                                    transport: the non-blocking communicator's enqueue / completion polls,
                                    after which it is aborted. 0 = 30 s. */
+    uint32_t plan_epoch;        /* RingPlan.epoch (allreduce.hpp:25-45): carried in every payload's ChunkMsg
+                                   header and compared at engine setup; a peer with a newer epoch ->
+                                   EMESH_ESTALE (StalePlanError) */
 } emesh_engine_config;
 
 /* Transports of the one-process-per-GPU ring (k > 1, not virtual):
@@ -205,8 +210,24 @@ int emesh_engine_outer_sync_host(emesh_engine* e, float* const* theta_g, float* 
                                  int write_local);
 
 /* Synchronizes the engine; EMESH_ENUMERIC if a quantize saw non-finite data
- * since the last check (the reference's NumericError, quant.hpp:31). */
+ * since the last check (the reference's NumericError, quant.hpp:31).
+ * Ring failures (peer transport; allreduce.hpp:247-305, :341-359, :466-472):
+ * EMESH_ERING (RingFailureError: a peer stalled past step_timeout or a
+ * poisoned flag swept the failure around the ring), EMESH_ESTALE
+ * (StalePlanError), EMESH_EPROTO (protocol violation). A failed round
+ * commits NOTHING on any rank (theta_g / momentum / theta_l untouched), so
+ * allreduce_with_retry can restart from the same state; the engine is then
+ * unusable (rebuild it over the survivors). */
 int emesh_engine_check(emesh_engine* e);
+
+/* The rank the last failed round names as the culprit (the predecessor whose
+ * reduce-scatter payload or the owner whose final payload never arrived, or
+ * the one a poisoned flag names); -1 when unknown. RingFailureError.failed_node. */
+int emesh_engine_failed_rank(const emesh_engine* e);
+
+/* ReduceJob.id of the engine's next round (ChunkMsg job id; default: the
+ * engine's round counter). */
+int emesh_engine_set_job(emesh_engine* e, uint64_t job_id);
 
 /* Device views of a local worker's final payload arenas after a round:
  * codes (n bytes, arena-indexed) and codebooks (nseg x 256). In NCCL mode

@@ -44,6 +44,8 @@ inline void check(int rc) {
         case EMESH_ECONFIG: throw ConfigError(what);
         case EMESH_ERING: throw RingFailureError("", what);
         case EMESH_ENCCL: throw RingFailureError("", what);
+        case EMESH_ESTALE: throw StalePlanError(0, what);
+        case EMESH_EPROTO: throw Error(what);
         default: throw FatalError(what);
     }
 }
@@ -220,7 +222,7 @@ public:
                const uint8_t* nccl_id /* 128 B, rank 0's emesh_nccl_unique_id; nullptr when local */,
                uint32_t local_workers = 1, int device = -1)
         : n_(n), k_(static_cast<uint32_t>(plan.order.size())), mode_(mode),
-          workers_(local_workers > 1 ? local_workers : 1) {
+          workers_(local_workers > 1 ? local_workers : 1), order_(plan.order), plan_epoch_(plan.epoch) {
         emesh_engine_config cfg{};
         cfg.n = n;
         cfg.k = k_;
@@ -232,6 +234,7 @@ public:
         cfg.transport = EMESH_TRANSPORT_AUTO;
         cfg.reduce_fp32 = mode == ReduceMode::fp32 ? 1u : 0u;
         cfg.step_timeout_s = opts.step_timeout;
+        cfg.plan_epoch = plan.epoch;
         S_ = opts.pipeline_subchunks ? opts.pipeline_subchunks : 4;
         check(emesh_engine_create(&cfg, &e_));
     }
@@ -265,8 +268,8 @@ public:
             pin.push_back(bi->get());
             pout.push_back(bo->get());
         }
-        check(emesh_engine_ring_allreduce(e_, pin.data(), pout.data(), nullptr));
-        check(emesh_engine_check(e_));
+        round_check(emesh_engine_ring_allreduce(e_, pin.data(), pout.data(), nullptr));
+        round_check(emesh_engine_check(e_));
         for (uint32_t w = 0; w < workers_; ++w) {
             res[w].resize(n_);
             if (n_) cuda_check(cudaMemcpy(res[w].data(), pout[w], n_ * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
@@ -292,7 +295,7 @@ public:
             pl.push_back(l[w].data());
             pb.push_back(b[w].data());
         }
-        check(emesh_engine_outer_sync_host(e_, pg.data(), pl.data(), pb.data(), hp.outer_lr, hp.outer_momentum, 1));
+        round_check(emesh_engine_outer_sync_host(e_, pg.data(), pl.data(), pb.data(), hp.outer_lr, hp.outer_momentum, 1));
         for (uint32_t w = 0; w < workers_; ++w) {
             retained[w]->unflatten(g[w]);
             local[w]->unflatten(l[w]);
@@ -327,6 +330,20 @@ public:
         return out;
     }
 
+    // A round's status as the reference raises it (allreduce.hpp:466-472): RingFailureError naming
+    // the culprit node of the plan (emesh_engine_failed_rank), StalePlanError, or check()'s mapping.
+    // A failed round committed nothing (the engine's commit gate), so a retry restarts from the
+    // same retained / local / momentum state.
+    void round_check(int rc) const {
+        if (rc == EMESH_ERING) {
+            const int who = emesh_engine_failed_rank(e_);
+            throw RingFailureError(who >= 0 && static_cast<size_t>(who) < order_.size() ? order_[who] : std::string(),
+                                   emesh_last_error());
+        }
+        if (rc == EMESH_ESTALE) throw StalePlanError(plan_epoch_ + 1, emesh_last_error());
+        check(rc);
+    }
+
 private:
     uint64_t subs_in_chunk(uint32_t c) const {
         const uint64_t clen = n_ / k_ + (c < n_ % k_ ? 1 : 0);
@@ -339,6 +356,49 @@ private:
     uint32_t k_;
     ReduceMode mode_;
     uint32_t workers_;
+    std::vector<std::string> order_;
+    uint32_t plan_epoch_ = 0;
 };
+
+// allreduce.hpp:485-518 `allreduce_with_retry` over GPU ring engines:
+// builds one engine per membership epoch (make_engine(plan) -> an engine
+// with ring_allreduce(std::vector<ReduceJob>) like b200::RingEngine; the
+// caller exchanges the NCCL id among plan.order), reports the culprit of a
+// RingFailureError, waits for the mesh to commit the eviction and restarts
+// from the preserved input; a StalePlanError refetches the mesh. `mesh` is
+// the reference's MeshClient (report_failure, wait_epoch_change, fetch_mesh)
+// or anything with those members.
+template <class MakeEngine, class Mesh>
+RetryResult allreduce_with_retry(MakeEngine&& make_engine, Mesh& mesh, MeshState mesh_state, const std::string& self_id,
+                                 const ReduceJob& job, const ReduceOptions& opts) {
+    uint32_t failures = 0;
+    for (;;) {
+        if (mesh_state.find(self_id) == nullptr) throw FatalError("this node is no longer in the mesh");
+        if (mesh_state.members.size() < 1) throw FatalError("no participants left");
+        RingPlan plan = RingPlan::from_mesh(mesh_state, self_id, job.id);
+        try {
+            auto engine = make_engine(plan);
+            RetryResult out;
+            out.value = std::move(engine->ring_allreduce(std::vector<ReduceJob>{job})[0]);
+            out.participants = static_cast<uint32_t>(plan.order.size());
+            out.attempts = failures;
+            out.epoch = mesh_state.epoch;
+            return out;
+        } catch (const RingFailureError& rf) {
+            failures += 1;
+            if (failures > opts.max_retries) throw FatalError("all-reduce retries exhausted: " + std::string(rf.what()));
+            if (!rf.failed_node.empty() && rf.failed_node != self_id) mesh.report_failure(rf.failed_node);
+            try {
+                mesh_state = mesh.wait_epoch_change(mesh_state.epoch, opts.evict_wait);
+            } catch (const TimeoutError&) {
+                mesh_state = mesh.fetch_mesh();  // maybe it changed and we missed it
+            }
+        } catch (const StalePlanError&) {
+            failures += 1;
+            if (failures > opts.max_retries) throw FatalError("all-reduce retries exhausted");
+            mesh_state = mesh.fetch_mesh();
+        }
+    }
+}
 
 }  // namespace emesh::b200

@@ -10,6 +10,7 @@ from . import emesh  # noqa: F401
 from .emesh import (  # noqa: F401
     ConfigError, DecodeError, Error, FatalError, HyperParams, ModelParams, NesterovState, NumericError,
     QuantChunk, ReduceJob, ReduceMode, ReduceOptions, RingEngine, RingFailureError, RingPlan, ShapeError,
+    StalePlanError,
     compute_pseudo_gradient, decode_quant_chunk, dequantize, dequantize_into, encode_quant_chunk,
     nesterov_outer_step, quantize, quantize_segments, codec_check, ring_allreduce, segment_table,
     MeshState, RetryResult, allreduce_with_retry, plan_tensor_segments, AdamWState, adamw_step,

@@ -25,12 +25,13 @@ EXPORTS = (
     "emesh_engine_segments", "emesh_engine_ring_allreduce", "emesh_engine_outer_sync",
     "emesh_engine_outer_sync_host", "emesh_engine_check", "emesh_engine_payload", "emesh_engine_payload_host",
     "emesh_engine_launches", "emesh_engine_profile", "emesh_engine_profile_read", "emesh_engine_timeline", "emesh_engine_transport",
+    "emesh_engine_failed_rank", "emesh_engine_set_job",
     "emesh_checkpoint_encoded_size", "emesh_checkpoint_encode", "emesh_checkpoint_decode",
     "emesh_checkpoint_probe", "emesh_checkpoint_layout", "emesh_checkpoint_write_file",
     "emesh_checkpoint_read_file", "emesh_sha256",
 )
 
-OK, ESHAPE, ENUMERIC, EDECODE, ECUDA, ENCCL, ERING, ECONFIG, EIO = range(9)
+OK, ESHAPE, ENUMERIC, EDECODE, ECUDA, ENCCL, ERING, ECONFIG, EIO, ESTALE, EPROTO = range(11)
 
 
 class EngineConfig(C.Structure):
@@ -48,6 +49,7 @@ class EngineConfig(C.Structure):
         ("tensor_numel", C.c_void_p),
         ("ntensors", C.c_uint32),
         ("step_timeout_s", C.c_double),
+        ("plan_epoch", C.c_uint32),
     ]
 
 
@@ -107,6 +109,8 @@ def lib() -> C.CDLL:
         "emesh_dequantize_segments": (i32, [vp, vp, P(u64), P(u64), u32, vp, vp]),
         "emesh_encode_quant_chunk": (u64, [vp, vp, u32, vp]),
         "emesh_decode_quant_chunk": (i32, [vp, u64, vp, vp, P(u32)]),
+        "emesh_engine_failed_rank": (i32, [vp]),
+        "emesh_engine_set_job": (i32, [vp, u64]),
         "emesh_pseudo_gradient": (i32, [vp, vp, vp, u64, vp]),
         "emesh_nesterov_outer_step": (i32, [vp, vp, vp, u64, f32, f32, vp]),
         "emesh_plan_segments": (u64, [u64, u32, u32, vp, vp]),

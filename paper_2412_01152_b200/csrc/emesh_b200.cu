@@ -135,6 +135,7 @@ struct Plan {
             si.slot = s;
             si.in_slot = s;
             si.upw = b.upw;
+            si.chunk = chunk;
             if (g.len > 0) {
                 const uint64_t nq = ((g.lo + g.len - 1) >> 2) - si.q0 + 1;
                 si.nunits = (uint32_t)((nq + kUnitSlots - 1) / kUnitSlots);
@@ -316,9 +317,9 @@ struct Workspace {
     }
 
     int reserve(size_t oct, size_t tiles, size_t segs) {
-        if (!err) {
-            CU(cudaMalloc(&err, sizeof(uint32_t)));
-            CU(cudaMemset(err, 0, sizeof(uint32_t)));
+        if (!err) {  // [0] sticky bits, [1] culprit rank + 1 (kernels.cuh ring_fail)
+            CU(cudaMalloc(&err, 4 * sizeof(uint32_t)));
+            CU(cudaMemset(err, 0, 4 * sizeof(uint32_t)));
         }
         if (oct > cap_oct || !scratch) {
             TRY(grow(scratch, oct * 32, false));
@@ -367,6 +368,12 @@ struct QuantIO {
     uint32_t* flags[kMaxDest] = {};
     const uint32_t* in_flag = nullptr;
     uint32_t epoch = 0;
+    // ChunkMsg headers (peer transport): one per destination (nullptr: none), the incoming ones
+    ChunkHdr* hdr_out[kMaxDest] = {};  // parallel to the destinations: [0] = out (when local_out), then x_*
+    const ChunkHdr* in_hdr = nullptr;
+    HdrRef hdr{};
+    uint32_t phase_out = kPhaseRS;
+    uint32_t culprit_in = kNoCulprit;
 };
 
 enum ProfKind : int {
@@ -488,6 +495,11 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     a.err = ws.err;
     a.sync = ws.sync;
     a.ovf = ws.ovf;
+    for (uint32_t d = 0; d < a.ndest; ++d) a.dhdr[d] = io.hdr_out[d];
+    a.in_hdr = io.in_hdr;
+    a.hdr = io.hdr;
+    a.phase_out = io.phase_out;
+    a.culprit_in = io.culprit_in;
     CU(cudaMemsetAsync(ws.sync, 0, (kSyncReady + kSyPerSeg * (size_t)bt.nseg) * sizeof(uint32_t), st));
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
@@ -538,14 +550,11 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
 
 int launch_apply(const Batch& bt, int mode, const uint8_t* codes, const float* cb, float* theta, float* buf,
                  float* theta_local, float* out, float lr, float mom, cudaStream_t st, Tracker* tr,
-                 const uint32_t* in_flag = nullptr, uint32_t epoch = 0) {
+                 const uint32_t* gate = nullptr, uint32_t epoch = 0) {
     if (bt.ncta == 0) return EMESH_OK;
     ApplyArgs a{};
-    a.in_flag = in_flag;
+    a.gate = gate;
     a.epoch = epoch;
-    a.err = tr ? tr->err : nullptr;
-    a.timeout_ns = tr ? tr->timeout_ns : 30ull * 1000000000ull;
-    if (in_flag && !a.err) return fail(EMESH_ECONFIG, "peer wait without an error word");
     a.segs = bt.d_segs;
     a.cta_seg = bt.d_cta_seg;
     a.ncta = bt.ncta;
@@ -805,14 +814,25 @@ struct emesh_engine {
         float* pay[2] = {nullptr, nullptr};
         uint32_t* rs_flag = nullptr;
         uint32_t* ag_flag = nullptr;
+        ChunkHdr* hdr[2] = {nullptr, nullptr};  // ChunkMsg headers by slot, per round parity
+        uint32_t* done = nullptr;              // [k] owners' done words
     };
+    // round commit (peer transport): this rank's done source word, gate word, slot metadata
+    ChunkHdr* hdr_alt = nullptr;  // parity-1 headers (parity 0: hdr0)
+    ChunkHdr* hdr0 = nullptr;
+    uint32_t* done = nullptr;     // [k], written by the owners' copy engines
+    uint32_t* done_src = nullptr; // this rank's done value (k_done_value)
+    uint32_t* gate = nullptr;     // the gate word the decode kernels check (k_round_gate)
+    uint2* meta = nullptr;        // by slot: {ring chunk, elements}
+    // NCCL transport's gate: page-locked host word mapped into the device; the host sets it to
+    // the round number when it enqueues a round and to 0 when it aborts the communicator
+    volatile uint32_t* h_gate = nullptr;
+    uint32_t* d_gate = nullptr;
+    uint32_t plan_epoch = 0;      // RingPlan epoch (ChunkMsg epoch)
+    unsigned long long job = 0;   // ReduceJob id of the next round (ChunkMsg job)
+    bool job_set = false;
+    int32_t culprit = -1;         // failed rank reported by the last failed round (-1: unknown)
     std::vector<Peer> peers;  // [rank]; own rank: local pointers
-    // all-gather arrival flags are written by the copy engine from page-locked
-    // host words holding the round number (per round parity): no kernel is
-    // involved, so a GPU whose SMs are all busy waiting for its peers' flags
-    // can never hold back the flags those peers wait for
-    uint32_t* h_epoch[2] = {nullptr, nullptr};
-    cudaEvent_t ev_flags[2] = {nullptr, nullptr};
     // device mirrors for the host-buffer entry point
     std::vector<float*> h_theta, h_local, h_buf;
     Tracker tr;
@@ -856,6 +876,11 @@ struct F32IO {
     uint32_t* flags[kMaxDest] = {};
     const uint32_t* in_flag = nullptr;
     uint32_t epoch = 0;
+    ChunkHdr* hdr_out[kMaxDest] = {};  // parallel to dst
+    const ChunkHdr* in_hdr = nullptr;
+    HdrRef hdr{};
+    uint32_t phase_out = kPhaseRS;
+    uint32_t culprit_in = kNoCulprit;
 };
 
 int launch_f32_hop(const Batch& bt, Workspace& ws, const F32IO& io, cudaStream_t st, Tracker* tr) {
@@ -879,6 +904,11 @@ int launch_f32_hop(const Batch& bt, Workspace& ws, const F32IO& io, cudaStream_t
     a.epoch = io.epoch;
     a.timeout_ns = tr ? tr->timeout_ns : 30ull * 1000000000ull;
     a.nseg = bt.nseg;
+    for (uint32_t d = 0; d < io.ndest; ++d) a.dhdr[d] = io.hdr_out[d];
+    a.in_hdr = io.in_hdr;
+    a.hdr = io.hdr;
+    a.phase_out = (uint8_t)io.phase_out;
+    a.culprit_in = io.culprit_in;
     if (io.nflags) CU(cudaMemsetAsync(ws.sync + kSyncReady, 0, (size_t)bt.nseg * sizeof(uint32_t), st));
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
@@ -906,7 +936,7 @@ int launch_f32_hop(const Batch& bt, Workspace& ws, const F32IO& io, cudaStream_t
 }
 
 int launch_f32_apply(const Batch& bt, int mode, const float* pay, float* theta, float* buf, float* theta_local,
-                     float* out, float lr, float mom, cudaStream_t st, Tracker* tr, const uint32_t* in_flag = nullptr,
+                     float* out, float lr, float mom, cudaStream_t st, Tracker* tr, const uint32_t* gate = nullptr,
                      uint32_t epoch = 0) {
     if (bt.ncta == 0) return EMESH_OK;
     ApplyArgs a{};
@@ -919,11 +949,8 @@ int launch_f32_apply(const Batch& bt, int mode, const float* pay, float* theta, 
     a.out = out;
     a.lr = lr;
     a.mom = mom;
-    a.in_flag = in_flag;
+    a.gate = gate;
     a.epoch = epoch;
-    a.err = tr ? tr->err : nullptr;
-    a.timeout_ns = tr ? tr->timeout_ns : 30ull * 1000000000ull;
-    if (in_flag && !a.err) return fail(EMESH_ECONFIG, "peer wait without an error word");
     a.upw = bt.upw;
     const dim3 g(bt.ncta * bt.upw), blk(kThreads);
     const bool prof = tr && tr->prof;
@@ -1059,6 +1086,7 @@ int nccl_settle(emesh_engine* e, ncclResult_t r, const char* what) {
         const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (waited * 1e9 > wait_budget_ns(e)) {
             e->failed = true;
+            if (e->h_gate) *e->h_gate = 0u;  // nothing of this round may commit
             ncclCommAbort(e->comm);
             e->comm = nullptr;
             return fail(EMESH_ERING, "NCCL %s did not complete within step_timeout (%.1f s)", what,
@@ -1068,6 +1096,7 @@ int nccl_settle(emesh_engine* e, ncclResult_t r, const char* what) {
     }
     if (r != ncclSuccess) {
         e->failed = true;
+        if (e->h_gate) *e->h_gate = 0u;
         ncclCommAbort(e->comm);
         e->comm = nullptr;
         return fail(EMESH_ENCCL, "NCCL %s: %s", what, ncclGetErrorString(r));
@@ -1105,6 +1134,8 @@ int nccl_drain(emesh_engine* e, std::initializer_list<cudaStream_t> streams, con
         const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (err || waited * 1e9 > wait_budget_ns(e)) {
             e->failed = true;
+            if (e->h_gate) *e->h_gate = 0u;  // the decodes still queued behind the aborted transfers skip
+            e->culprit = (int32_t)((e->rank + e->k - 1) % e->k);  // every receive of the NCCL ring is from the predecessor
             if (e->comm) ncclCommAbort(e->comm);
             e->comm = nullptr;
             for (cudaStream_t st : streams) cudaStreamSynchronize(st);
@@ -1175,14 +1206,18 @@ std::vector<emesh_ring_op> build_schedule(const Plan& P, uint32_t r) {
             op(EMESH_OP_QUANT, 0, (int32_t)s, j, -1, recv_c);
         }
     }
+    // all-gather: forward the final bytes k-1 hops, THEN decode: a round commits (Nesterov writes
+    // theta / momentum) only once every final payload arrived, so a failed round leaves the state
+    // untouched for allreduce_with_retry (trainer.hpp:375-381 applies Nesterov after the all-reduce)
     const int32_t own = (int32_t)((r + 1) % k);
-    for (uint32_t j = 0; j < W; ++j) op(EMESH_OP_APPLY, 1, -1, j, -1, own);
     for (uint32_t s = 0; s + 1 < k; ++s) {
         const int32_t send_c = (int32_t)((r + 1 + k - s) % k), recv_c = (int32_t)((r + k - s) % k);
-        for (uint32_t j = 0; j < W; ++j) {
-            op(EMESH_OP_XFER, 1, (int32_t)s, j, send_c, recv_c);
-            op(EMESH_OP_APPLY, 1, (int32_t)s, j, -1, recv_c);
-        }
+        for (uint32_t j = 0; j < W; ++j) op(EMESH_OP_XFER, 1, (int32_t)s, j, send_c, recv_c);
+    }
+    for (uint32_t j = 0; j < W; ++j) op(EMESH_OP_APPLY, 1, -1, j, -1, own);
+    for (uint32_t s = 0; s + 1 < k; ++s) {
+        const int32_t recv_c = (int32_t)((r + k - s) % k);
+        for (uint32_t j = 0; j < W; ++j) op(EMESH_OP_APPLY, 1, (int32_t)s, j, -1, recv_c);
     }
     return ops;
 }
@@ -1194,6 +1229,8 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
     auto& ar = e->arenas[0];
     cudaStream_t sc = e->s_comp, sm = e->s_comm;
     if (!e->comm) return fail(EMESH_ERING, "NCCL communicator was aborted by an earlier ring failure");
+    const uint32_t ep = ++e->epoch;
+    *e->h_gate = ep;  // the decodes commit unless the host aborts the communicator (nccl_abort)
     const auto& P = e->plan.batches;
     const uint32_t W = (uint32_t)P[0].size();
     for (uint32_t c = 1; c < k; ++c)
@@ -1249,13 +1286,13 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
                 if (o.hop >= 0) CU(cudaStreamWaitEvent(sc, e->ev_recv[j], 0));
                 if (e->fp32)
                     TRY(launch_f32_apply(P[o.recv_chunk][j], out ? 0 : 1, e->pay[0], theta, buf, local_out, out, lr, mom,
-                                         sc, &e->tr));
+                                         sc, &e->tr, e->d_gate, ep));
                 else if (out)
                     TRY(launch_apply(P[o.recv_chunk][j], 0, ar.codes, ar.cbs, nullptr, nullptr, nullptr, out, 0.f, 0.f,
-                                     sc, &e->tr));
+                                     sc, &e->tr, e->d_gate, ep));
                 else
                     TRY(launch_apply(P[o.recv_chunk][j], 1, ar.codes, ar.cbs, theta, buf, local_out, nullptr, lr, mom,
-                                     sc, &e->tr));
+                                     sc, &e->tr, e->d_gate, ep));
                 break;
             default:
                 return fail(EMESH_ECONFIG, "bad schedule op");
@@ -1281,15 +1318,11 @@ constexpr uint64_t kMinDmaElems = (uint64_t)32 << 20;
 bool push_final_payload(const Batch& fb) { return fb.eruns.size() > kMaxDmaRuns || fb.elems < kMinDmaElems; }
 
 // Owner's final chunk -> every other rank by DMA (see run_p2p), in segment
-// groups, each followed by its arrival flags.
-int p2p_allgather(emesh_engine* e, int par, uint32_t ep) {
+// groups: codes (or fp32 means), codebooks and ChunkMsg headers. The owner's
+// done word follows in stream order (p2p_commit).
+int p2p_allgather(emesh_engine* e, int par) {
     const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
     cudaStream_t cm = e->s_comm;
-    // the host words of this parity were last read by the copies two rounds ago
-    CU(cudaEventSynchronize(e->ev_flags[par]));
-    std::fill(e->h_epoch[par], e->h_epoch[par] + e->plan.segs.size(), ep);
-    CU(cudaEventRecord(e->ev_send[0], e->s_comp));
-    CU(cudaStreamWaitEvent(cm, e->ev_send[0], 0));
     const Batch& fb = e->plan.batches[succ][0];
     const uint32_t groups = std::min<uint32_t>(fb.nseg, 4);
     for (uint32_t g = 0; g < groups; ++g) {
@@ -1298,10 +1331,10 @@ int p2p_allgather(emesh_engine* e, int par, uint32_t ep) {
         if (s1 == s0) continue;
         std::vector<std::pair<uint64_t, uint64_t>> runs;  // contiguous element runs of the group
         for (uint32_t s = s0; s < s1; ++s) {
-            const Seg& g = e->plan.segs[s];
-            if (!g.len) continue;
-            if (!runs.empty() && runs.back().first + runs.back().second == g.lo) runs.back().second += g.len;
-            else runs.push_back({g.lo, g.len});
+            const Seg& sg = e->plan.segs[s];
+            if (!sg.len) continue;
+            if (!runs.empty() && runs.back().first + runs.back().second == sg.lo) runs.back().second += sg.len;
+            else runs.push_back({sg.lo, sg.len});
         }
         for (uint32_t d = 1; d < k; ++d) {
             const uint32_t q = (r + d) % k;
@@ -1317,31 +1350,77 @@ int p2p_allgather(emesh_engine* e, int par, uint32_t ep) {
                                    e->peers[r].cbs[par] + (size_t)s0 * kBuckets,
                                    (size_t)(s1 - s0) * kBuckets * sizeof(float), cudaMemcpyDeviceToDevice, cm));
             }
-            CU(cudaMemcpyAsync(e->peers[q].ag_flag + s0, e->h_epoch[par] + s0, (size_t)(s1 - s0) * sizeof(uint32_t),
-                               cudaMemcpyHostToDevice, cm));  // after this group's bytes (stream order)
+            CU(cudaMemcpyAsync(e->peers[q].hdr[par] + s0, e->peers[r].hdr[par] + s0, (size_t)(s1 - s0) * sizeof(ChunkHdr),
+                               cudaMemcpyDeviceToDevice, cm));
         }
     }
-    CU(cudaEventRecord(e->ev_flags[par], cm));
     return EMESH_OK;
 }
+
+// The round's commit (peer transport), after this rank's last quantizer:
+// k_done_value turns this rank's error word into its done value (the round,
+// or poison naming the culprit); the copy engines deliver the owner's final
+// payload (unless the quantizer stored it itself) and then the done word to
+// every peer; k_round_gate waits for every other owner's done word,
+// validates the final payloads' headers and publishes the gate word that
+// every decode kernel of the round checks. A round that failed anywhere
+// therefore commits nowhere (theta / momentum untouched) and every rank
+// reports it.
+int p2p_commit(emesh_engine* e, int par, uint32_t ep, bool push_final) {
+    const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
+    cudaStream_t sc = e->s_comp, cm = e->s_comm;
+    k_done_value<<<1, 32, 0, sc>>>(e->ws.err, ep, e->done_src);
+    e->tr.launches += 1;
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(e->ev_send[0], sc));
+    CU(cudaStreamWaitEvent(cm, e->ev_send[0], 0));
+    if (!push_final) TRY(p2p_allgather(e, par));
+    for (uint32_t d = 1; d < k; ++d) {  // after the payload (stream order)
+        const uint32_t q = (r + d) % k;
+        CU(cudaMemcpyAsync(e->peers[q].done + r, e->done_src, sizeof(uint32_t), cudaMemcpyDeviceToDevice, cm));
+    }
+    GateArgs g{};
+    g.done = e->done;
+    g.gate = e->gate;
+    g.err = e->ws.err;
+    g.hdr = e->peers[r].hdr[par];
+    g.meta = e->meta;
+    g.want = HdrRef{e->job, e->plan_epoch, (uint8_t)(e->fp32 ? 0 : 1)};
+    g.k = k;
+    g.rank = r;
+    g.own_chunk = succ;
+    g.nslots = (uint32_t)e->plan.segs.size();
+    g.epoch = ep;
+    g.timeout_ns = (unsigned long long)wait_budget_ns(e);
+    g.ag_flag = push_final ? e->ag_flag : nullptr;
+    k_round_gate<<<1, kThreads, 0, sc>>>(g);
+    e->tr.launches += 1;
+    CU(cudaGetLastError());
+    return EMESH_OK;
+}
+
+HdrRef round_hdr(const emesh_engine* e) { return HdrRef{e->job, e->plan_epoch, (uint8_t)(e->fp32 ? 0 : 1)}; }
 
 // ReduceMode::fp32 over the peer transport: the same ring with raw fp32
 // partial sums stored into the successor's payload arena.
 int run_p2p_f32(emesh_engine* e, const float* A, const float* B, float* theta, float* buf, float* local_out,
                 float* out, float lr, float mom) {
-    const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
-    const uint32_t ep = ++e->epoch;
+    const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k, pred = (r + k - 1) % k;
+    const uint32_t ep = e->epoch;
     const int par = (int)(ep & 1u);
     cudaStream_t sc = e->s_comp;
     const auto& P = e->plan.batches;
     const bool push_final = push_final_payload(P[succ][0]);
+    const HdrRef H = round_hdr(e);
     {
         F32IO io{A, B, nullptr};
         io.ndest = 1;
         io.dst[0] = e->peers[succ].pay[par];
+        io.hdr_out[0] = e->peers[succ].hdr[par];
         io.nflags = 1;
         io.flags[0] = e->peers[succ].rs_flag;
         io.epoch = ep;
+        io.hdr = H;
         TRY(launch_f32_hop(P[r][0], e->ws, io, sc, &e->tr));
     }
     for (uint32_t s = 0; s + 1 < k; ++s) {
@@ -1349,28 +1428,35 @@ int run_p2p_f32(emesh_engine* e, const float* A, const float* B, float* theta, f
         const bool fin = s + 2 == k;
         F32IO io{A, B, e->peers[r].pay[par], fin, (float)k};
         io.in_flag = e->rs_flag;
+        io.in_hdr = e->peers[r].hdr[par];
+        io.culprit_in = pred;
         io.epoch = ep;
+        io.hdr = H;
         io.ndest = 1;
         if (fin) {
             io.dst[0] = e->peers[r].pay[par];
+            io.hdr_out[0] = e->peers[r].hdr[par];
+            io.phase_out = kPhaseAG;
             if (push_final)
                 for (uint32_t q = 0; q < k; ++q)
                     if (q != r) {
+                        io.hdr_out[io.ndest] = e->peers[q].hdr[par];
                         io.dst[io.ndest++] = e->peers[q].pay[par];
                         io.flags[io.nflags++] = e->peers[q].ag_flag;
                     }
         } else {
             io.dst[0] = e->peers[succ].pay[par];
+            io.hdr_out[0] = e->peers[succ].hdr[par];
             io.nflags = 1;
             io.flags[0] = e->peers[succ].rs_flag;
         }
         TRY(launch_f32_hop(P[rc][0], e->ws, io, sc, &e->tr));
     }
-    if (!push_final) TRY(p2p_allgather(e, par, ep));
+    TRY(p2p_commit(e, par, ep, push_final));
     for (uint32_t d = 0; d < k; ++d) {
         const uint32_t c = (succ + k - d) % k;
         TRY(launch_f32_apply(P[c][0], out ? 0 : 1, e->peers[r].pay[par], theta, buf, local_out, out, lr, mom, sc,
-                             &e->tr, d == 0 ? nullptr : e->ag_flag, ep));
+                             &e->tr, e->gate, ep));
     }
     return EMESH_OK;
 }
@@ -1384,15 +1470,19 @@ struct HostPipe {
 
 int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float* buf, float* local_out, float* out,
             float lr, float mom, const HostPipe* hp = nullptr) {
+    if (e->failed) return fail(EMESH_ERING, "engine unusable after a failed round (rebuild it over the survivors)");
+    const uint32_t ep = ++e->epoch;
+    if (!e->job_set) e->job = ep;  // ReduceJob id of this round (ChunkMsg job): the round number by default
+    e->job_set = false;
     if (e->fp32) return run_p2p_f32(e, A, B, theta, buf, local_out, out, lr, mom);
-    const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
+    const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k, pred = (r + k - 1) % k;
     const bool push_final = push_final_payload(e->plan.batches[succ][0]);
     const bool pg = B != nullptr;
-    const uint32_t ep = ++e->epoch;
     const int par = (int)(ep & 1u);
     auto& ar = e->arenas[0];
     cudaStream_t sc = e->s_comp;
     const auto& P = e->plan.batches;
+    const HdrRef H = round_hdr(e);
     for (uint32_t c = 0; c < k; ++c)
         if (P[c].size() != 1) return fail(EMESH_ECONFIG, "peer transport expects one batch per chunk");
     auto mark = [&](int kind, int hop, bool begin) {
@@ -1405,6 +1495,7 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
         io.nx = 1;
         io.x_codes[0] = e->peers[succ].codes[par];
         io.x_cb[0] = e->peers[succ].cbs[par];
+        io.hdr_out[0] = e->peers[succ].hdr[par];
         io.nflags = 1;
         io.flags[0] = e->peers[succ].rs_flag;
     };
@@ -1412,6 +1503,7 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
         QuantIO io{pg ? kSrcAminusB : kSrcA, A, B, nullptr, nullptr, 1.f, nullptr, nullptr, ar.stats};
         to_succ(io);
         io.epoch = ep;
+        io.hdr = H;
         if (hp) TRY(hp->before_rs(r));
         mark(EMESH_OP_OWN, 0, true);
         TRY(launch_quant(P[r][0], e->ws, io, sc, &e->tr));
@@ -1422,17 +1514,23 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
         QuantIO io{hop_src(pg, s, k), A, B, e->peers[r].codes[par], e->peers[r].cbs[par], (float)k,
                    e->peers[r].codes[par], e->peers[r].cbs[par], ar.stats};
         io.in_flag = e->rs_flag;
+        io.in_hdr = e->peers[r].hdr[par];
+        io.culprit_in = pred;
         io.epoch = ep;
+        io.hdr = H;
         if (s + 2 < k) {
             to_succ(io);
         } else {  // owner: final payload local; the copy engines deliver it to every other rank
             io.local_out = true;
+            io.hdr_out[0] = e->peers[r].hdr[par];
+            io.phase_out = kPhaseAG;
             if (push_final)  // many small runs (multi-tensor): the quantizer stores to every rank itself
                 for (uint32_t q = 0; q < k; ++q)
                     if (q != r) {
                         io.x_codes[io.nx] = e->peers[q].codes[par];
                         io.x_cb[io.nx] = e->peers[q].cbs[par];
                         ++io.nx;
+                        io.hdr_out[io.nx] = e->peers[q].hdr[par];
                         io.flags[io.nflags++] = e->peers[q].ag_flag;
                     }
         }
@@ -1441,36 +1539,35 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
         TRY(launch_quant(P[rc][0], e->ws, io, sc, &e->tr));
         mark(EMESH_OP_QUANT, (int)s, false);
     }
-    // all-gather: the owner's final bytes to every rank by DMA over NVLink
-    // (allreduce.hpp:446-464 forwards the same bytes hop by hop), in segment
-    // groups so receivers start decoding while the rest streams; a group's
-    // arrival flags are raised after its bytes (stream order). Runs on the
-    // comm stream, overlapping this rank's own decode.
-    if (!push_final) TRY(p2p_allgather(e, par, ep));
-    // decode every chunk: own final first, then the others as their owners'
-    // copies land (per-segment ag_flag waits inside k_apply)
+    // all-gather (the owner's final bytes to every rank, allreduce.hpp:446-464 forwards the same
+    // bytes hop by hop) + the commit gate
+    TRY(p2p_commit(e, par, ep, push_final));
+    // decode every chunk (own final first); each decode commits only through the gate
     for (uint32_t d = 0; d < k; ++d) {
         const uint32_t c = (succ + k - d) % k;  // succ = own chunk; then chunks owned by r-1, r-2, ...
-        const uint32_t* flag = d == 0 ? nullptr : e->ag_flag;
         if (hp) TRY(hp->before_apply(c));
         mark(EMESH_OP_APPLY, (int)d - 1, true);
         if (out)
             TRY(launch_apply(P[c][0], 0, e->peers[r].codes[par], e->peers[r].cbs[par], nullptr, nullptr, nullptr, out,
-                             0.f, 0.f, sc, &e->tr, flag, ep));
+                             0.f, 0.f, sc, &e->tr, e->gate, ep));
         else
             TRY(launch_apply(P[c][0], 1, e->peers[r].codes[par], e->peers[r].cbs[par], theta, buf, local_out, nullptr,
-                             lr, mom, sc, &e->tr, flag, ep));
+                             lr, mom, sc, &e->tr, e->gate, ep));
         mark(EMESH_OP_APPLY, (int)d - 1, false);
         if (hp) TRY(hp->after_apply(c));
     }
     return EMESH_OK;
 }
 
-// Map every rank's parity arenas and flags (CUDA IPC handles all-gathered
-// over the NCCL communicator). Returns false (and leaves the engine on NCCL)
-// unless every rank mapped every peer.
-bool setup_p2p(emesh_engine* e) {
+// Map every rank's parity arenas, headers and flags (CUDA IPC handles
+// all-gathered over the NCCL communicator, with each rank's plan epoch).
+// Returns false (and leaves the engine on NCCL) unless every rank mapped
+// every peer; sets *stale when a peer runs a newer plan epoch
+// (StalePlanError, allreduce.hpp:272) or an older one (its ring attempt is
+// stale: RingFailureError on this side).
+bool setup_p2p(emesh_engine* e, int* stale) {
     const uint32_t k = e->k, r = e->rank;
+    *stale = 0;
     if (k > (uint32_t)kMaxDest) return false;
     const uint64_t n = e->plan.n;
     const size_t nslots = e->plan.segs.size();
@@ -1479,20 +1576,34 @@ bool setup_p2p(emesh_engine* e) {
               cudaMalloc(&e->cbs_alt, nslots * kBuckets * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&e->rs_flag, nslots * sizeof(uint32_t)) == cudaSuccess &&
               cudaMalloc(&e->ag_flag, nslots * sizeof(uint32_t)) == cudaSuccess &&
+              cudaMalloc(&e->hdr0, nslots * sizeof(ChunkHdr)) == cudaSuccess &&
+              cudaMalloc(&e->hdr_alt, nslots * sizeof(ChunkHdr)) == cudaSuccess &&
+              cudaMalloc(&e->done, 64 * sizeof(uint32_t)) == cudaSuccess &&
+              cudaMalloc(&e->done_src, 16 * sizeof(uint32_t)) == cudaSuccess &&
+              cudaMalloc(&e->gate, 16 * sizeof(uint32_t)) == cudaSuccess &&
+              cudaMalloc(&e->meta, nslots * sizeof(uint2)) == cudaSuccess &&
               cudaMemset(e->rs_flag, 0, nslots * sizeof(uint32_t)) == cudaSuccess &&
               cudaMemset(e->ag_flag, 0, nslots * sizeof(uint32_t)) == cudaSuccess &&
-              cudaMallocHost(&e->h_epoch[0], nslots * sizeof(uint32_t)) == cudaSuccess &&
-              cudaMallocHost(&e->h_epoch[1], nslots * sizeof(uint32_t)) == cudaSuccess &&
-              cudaEventCreateWithFlags(&e->ev_flags[0], cudaEventDisableTiming) == cudaSuccess &&
-              cudaEventCreateWithFlags(&e->ev_flags[1], cudaEventDisableTiming) == cudaSuccess;
-    constexpr int kH = 8;
-    constexpr size_t kRec = kH * sizeof(cudaIpcMemHandle_t);
+              cudaMemset(e->hdr0, 0, nslots * sizeof(ChunkHdr)) == cudaSuccess &&
+              cudaMemset(e->hdr_alt, 0, nslots * sizeof(ChunkHdr)) == cudaSuccess &&
+              cudaMemset(e->done, 0, 64 * sizeof(uint32_t)) == cudaSuccess &&
+              cudaMemset(e->gate, 0, 16 * sizeof(uint32_t)) == cudaSuccess;
+    if (ok) {  // by slot: {ring chunk, elements} (the gate's header checks)
+        std::vector<uint2> meta(nslots);
+        for (uint32_t c = 0; c < k; ++c)
+            for (const Batch& bt : e->plan.batches[c])
+                for (uint32_t s = bt.slot0; s < bt.slot0 + bt.nseg; ++s) meta[s] = make_uint2(c, (uint32_t)e->plan.segs[s].len);
+        ok = cudaMemcpy(e->meta, meta.data(), nslots * sizeof(uint2), cudaMemcpyHostToDevice) == cudaSuccess;
+    }
+    constexpr int kH = 11;
+    constexpr size_t kRec = kH * sizeof(cudaIpcMemHandle_t) + 64;  // + plan epoch
     std::vector<uint8_t> mine(kRec, 0), all(kRec * k, 0);
     void* bufs[kH] = {e->arenas[0].codes, e->codes_alt, e->arenas[0].cbs, e->cbs_alt, e->rs_flag, e->ag_flag,
-                      e->fp32 ? e->pay[0] : nullptr, e->pay_alt};
-    const int nh = e->fp32 ? 8 : 6;  // every rank runs the same mode
+                      e->hdr0, e->hdr_alt, e->done, e->fp32 ? e->pay[0] : nullptr, e->pay_alt};
+    const int nh = e->fp32 ? 11 : 9;  // every rank runs the same mode
     for (int h = 0; ok && h < nh; ++h)
         ok = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data()) + h, bufs[h]) == cudaSuccess;
+    std::memcpy(mine.data() + kH * sizeof(cudaIpcMemHandle_t), &e->plan_epoch, sizeof(uint32_t));
     // all-gather the handle records (and everyone's ok) over NCCL
     uint8_t* d = nullptr;
     int* d_ok = nullptr;
@@ -1504,9 +1615,23 @@ bool setup_p2p(emesh_engine* e) {
                   cudaMemcpyAsync(all.data(), d + kRec, kRec * k, cudaMemcpyDeviceToHost, e->s_comm) == cudaSuccess &&
                   nccl_drain(e, {e->s_comm}, "p2p handle exchange") == EMESH_OK;
     }
+    if (comm_ok)
+        for (uint32_t q = 0; q < k; ++q) {
+            uint32_t pe = 0;
+            std::memcpy(&pe, all.data() + q * kRec + kH * sizeof(cudaIpcMemHandle_t), sizeof pe);
+            if (pe > e->plan_epoch) *stale = 1;                     // this rank's plan is behind
+            else if (pe < e->plan_epoch && *stale == 0) *stale = -1;  // a peer's plan is behind
+        }
     e->peers.assign(k, emesh_engine::Peer{});
-    e->peers[r] = emesh_engine::Peer{{e->arenas[0].codes, e->codes_alt}, {e->arenas[0].cbs, e->cbs_alt},
-                                     {e->fp32 ? e->pay[0] : nullptr, e->pay_alt}, e->rs_flag, e->ag_flag};
+    {
+        auto& me = e->peers[r];
+        me.codes[0] = e->arenas[0].codes; me.codes[1] = e->codes_alt;
+        me.cbs[0] = e->arenas[0].cbs; me.cbs[1] = e->cbs_alt;
+        me.pay[0] = e->fp32 ? e->pay[0] : nullptr; me.pay[1] = e->pay_alt;
+        me.rs_flag = e->rs_flag; me.ag_flag = e->ag_flag;
+        me.hdr[0] = e->hdr0; me.hdr[1] = e->hdr_alt;
+        me.done = e->done;
+    }
     for (uint32_t q = 0; ok && comm_ok && q < k; ++q) {
         if (q == r) continue;
         void* ptr[kH] = {};
@@ -1519,7 +1644,9 @@ bool setup_p2p(emesh_engine* e) {
         pq.codes[0] = (uint8_t*)ptr[0]; pq.codes[1] = (uint8_t*)ptr[1];
         pq.cbs[0] = (float*)ptr[2]; pq.cbs[1] = (float*)ptr[3];
         pq.rs_flag = (uint32_t*)ptr[4]; pq.ag_flag = (uint32_t*)ptr[5];
-        pq.pay[0] = (float*)ptr[6]; pq.pay[1] = (float*)ptr[7];
+        pq.hdr[0] = (ChunkHdr*)ptr[6]; pq.hdr[1] = (ChunkHdr*)ptr[7];
+        pq.done = (uint32_t*)ptr[8];
+        pq.pay[0] = (float*)ptr[9]; pq.pay[1] = (float*)ptr[10];
     }
     cudaGetLastError();  // clear a failed open, if any
     // agree: every rank must have mapped every peer
@@ -1541,26 +1668,23 @@ void teardown_p2p(emesh_engine* e) {
     for (uint32_t q = 0; q < e->peers.size(); ++q) {
         if (q == e->rank) continue;
         auto& pq = e->peers[q];
-        void* ptrs[] = {pq.codes[0], pq.codes[1], pq.cbs[0], pq.cbs[1], pq.rs_flag, pq.ag_flag, pq.pay[0], pq.pay[1]};
+        void* ptrs[] = {pq.codes[0], pq.codes[1], pq.cbs[0], pq.cbs[1], pq.rs_flag, pq.ag_flag,
+                        pq.hdr[0], pq.hdr[1], pq.done, pq.pay[0], pq.pay[1]};
         for (void* p : ptrs)
             if (p) cudaIpcCloseMemHandle(p);
     }
     e->peers.clear();
-    for (int p = 0; p < 2; ++p) {
-        if (e->h_epoch[p]) cudaFreeHost(e->h_epoch[p]);
-        if (e->ev_flags[p]) cudaEventDestroy(e->ev_flags[p]);
-        e->h_epoch[p] = nullptr;
-        e->ev_flags[p] = nullptr;
-    }
-    cudaFree(e->codes_alt);
-    cudaFree(e->cbs_alt);
-    cudaFree(e->pay_alt);
-    e->pay_alt = nullptr;
-    cudaFree(e->rs_flag);
-    cudaFree(e->ag_flag);
+    void* own[] = {e->codes_alt, e->cbs_alt, e->pay_alt, e->rs_flag, e->ag_flag, e->hdr0, e->hdr_alt,
+                   e->done, e->done_src, e->gate, e->meta};
+    for (void* p : own)
+        if (p) cudaFree(p);
     e->codes_alt = nullptr;
     e->cbs_alt = nullptr;
+    e->pay_alt = nullptr;
     e->rs_flag = e->ag_flag = nullptr;
+    e->hdr0 = e->hdr_alt = nullptr;
+    e->done = e->done_src = e->gate = nullptr;
+    e->meta = nullptr;
     cudaGetLastError();
 }
 
@@ -1680,6 +1804,7 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
     if (e->k > 1 && (rc = engine_alloc(e))) return bail(rc);
     e->tr.err = e->ws.err;
     if (cfg->step_timeout_s > 0) e->tr.timeout_ns = (unsigned long long)(cfg->step_timeout_s * 1e9);
+    e->plan_epoch = cfg->plan_epoch;
     e->setup_floor_ns = 30ull * 1000000000ull;  // reset once the engine is up
     int lo_prio = 0, hi_prio = 0;
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
@@ -1696,6 +1821,14 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
         cudaEventCreateWithFlags(&e->ev_recv[j], cudaEventDisableTiming);
     }
     if (!virt && e->k > 1) {
+        {   // the NCCL transport's commit gate: a page-locked host word the decode kernels read
+            void* h = nullptr;
+            if (cudaHostAlloc(&h, 64, cudaHostAllocMapped) != cudaSuccess ||
+                cudaHostGetDevicePointer((void**)&e->d_gate, h, 0) != cudaSuccess)
+                return bail(fail(EMESH_ECUDA, "gate word allocation"));
+            e->h_gate = static_cast<volatile uint32_t*>(h);
+            *e->h_gate = 0u;
+        }
         e->schedule = build_schedule(e->plan, e->rank);
         ncclUniqueId id;
         std::memcpy(&id, cfg->nccl_id, sizeof id);
@@ -1706,7 +1839,15 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
             return bail(fail(EMESH_ENCCL, "ncclCommInitRankConfig: %s", ncclGetErrorString(r)));
         if ((rc = nccl_settle(e, r, "ncclCommInitRankConfig"))) return bail(rc);
         e->transport = EMESH_TRANSPORT_NCCL;
-        if (try_p2p && setup_p2p(e)) {
+        int stale = 0;
+        const bool mapped = try_p2p && setup_p2p(e, &stale);
+        if (stale) {  // the ranks disagree on the plan epoch (allreduce.hpp:272)
+            if (mapped) teardown_p2p(e);
+            e->failed = true;
+            if (stale > 0) return bail(fail(EMESH_ESTALE, "a ring peer runs a newer plan epoch"));
+            return bail(fail(EMESH_ERING, "a ring peer runs an older plan epoch (stale attempt)"));
+        }
+        if (mapped) {
             e->transport = EMESH_TRANSPORT_P2P;
             // NCCL only bootstrapped the mappings: release it now, while every
             // rank is here, so teardown never depends on a peer being alive
@@ -1748,6 +1889,7 @@ int emesh_engine_destroy(emesh_engine* e) {
     teardown_p2p(e);
     nccl_close(e);  // aborts when a round failed: peers may be gone
     for (auto& a : e->arenas) { cudaFree(a.codes); cudaFree(a.cbs); cudaFree(a.stats); }
+    if (e->h_gate) cudaFreeHost(const_cast<uint32_t*>(e->h_gate));
     for (auto* p : e->pay) cudaFree(p);
     for (auto* p : e->h_theta) cudaFree(p);
     for (auto* p : e->h_local) cudaFree(p);
@@ -2062,17 +2204,34 @@ int emesh_engine_check(emesh_engine* e) {
     CU(cudaStreamSynchronize(e->s_comp));
     CU(cudaStreamSynchronize(e->s_comm));
     if (!e->ws.err) return EMESH_OK;
-    uint32_t v = 0;
-    CU(cudaMemcpy(&v, e->ws.err, sizeof v, cudaMemcpyDeviceToHost));
-    if (v) {
-        CU(cudaMemset(e->ws.err, 0, sizeof(uint32_t)));
-        if (v & kErrRingTimeout) {  // allreduce.hpp:466-470: a peer stopped mid-collective
+    uint32_t v[2] = {0, 0};
+    CU(cudaMemcpy(v, e->ws.err, sizeof v, cudaMemcpyDeviceToHost));
+    if (v[0]) {
+        CU(cudaMemset(e->ws.err, 0, 2 * sizeof(uint32_t)));
+        if (v[0] & kErrRing) {  // the round failed on some rank: nothing was committed (k_round_gate)
             e->failed = true;
-            return fail(EMESH_ERING, "ring step timed out waiting for a peer's payload (step_timeout %.1f s)",
-                        (double)e->tr.timeout_ns * 1e-9);
+            e->culprit = (v[1] && (v[1] - 1) != kNoCulprit) ? (int32_t)(v[1] - 1) : -1;
+            char who[48] = "unknown";
+            if (e->culprit >= 0) snprintf(who, sizeof who, "rank %d", e->culprit);
+            if (v[0] & kErrStale)  // allreduce.hpp:272
+                return fail(EMESH_ESTALE, "newer plan epoch on the ring (culprit %s)", who);
+            if (v[0] & kErrProto)  // allreduce.hpp:280-281
+                return fail(EMESH_EPROTO, "ring protocol violation: unexpected chunk header (from %s)", who);
+            // allreduce.hpp:466-470: a peer stopped or aborted mid-collective
+            return fail(EMESH_ERING, "ring step failed: a peer stalled past step_timeout (%.1f s) or aborted; culprit %s",
+                        (double)e->tr.timeout_ns * 1e-9, who);
         }
         return fail(EMESH_ENUMERIC, "quantize: non-finite input");
     }
+    return EMESH_OK;
+}
+
+int emesh_engine_failed_rank(const emesh_engine* e) { return e ? e->culprit : -1; }
+
+int emesh_engine_set_job(emesh_engine* e, uint64_t job_id) {
+    if (!e) return fail(EMESH_ECONFIG, "null engine");
+    e->job = job_id;
+    e->job_set = true;
     return EMESH_OK;
 }
 

@@ -528,6 +528,7 @@ struct GateArgs {
     uint32_t* err;
     const ChunkHdr* hdr;   // final-payload headers by slot (this rank's arena)
     const uint2* meta;     // by slot: {ring chunk, elements}
+    const uint32_t* ag_flag;  // by slot, when the owners' quantizers stored the final payloads themselves
     HdrRef want;
     uint32_t k, rank, own_chunk, nslots, epoch;
     unsigned long long timeout_ns;
@@ -540,7 +541,11 @@ __global__ void __launch_bounds__(kThreads) k_round_gate(GateArgs a) {
         for (uint32_t s = t; s < a.nslots; s += blockDim.x) {
             const uint2 m = a.meta[s];
             if (m.x == a.own_chunk || m.y == 0) continue;
-            check_hdr(a.hdr + s, a.want, m.x, m.y, kPhaseAG, a.err, (m.x + a.k - 1) % a.k);
+            const uint32_t owner = (m.x + a.k - 1) % a.k;
+            // the owner's quantizer stored this payload itself: its per-segment flag (system-scope
+            // release after the stores) makes the bytes visible here
+            if (a.ag_flag && !spin_until_ge_sys(a.ag_flag + s, a.epoch, a.err, a.timeout_ns, owner)) continue;
+            check_hdr(a.hdr + s, a.want, m.x, m.y, kPhaseAG, a.err, owner);
         }
     }
     __syncthreads();

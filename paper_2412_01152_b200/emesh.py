@@ -44,7 +44,15 @@ class ConfigError(Error):
 
 
 class RingFailureError(Error):
-    """emesh::RingFailureError"""
+    """emesh::RingFailureError (errors.hpp): ``failed_node`` names the culprit when known."""
+
+    def __init__(self, msg: str = "", failed_node: str = ""):
+        super().__init__(msg)
+        self.failed_node = failed_node
+
+
+class StalePlanError(Error):
+    """emesh::StalePlanError: a ring peer runs a newer plan epoch (allreduce.hpp:272)."""
 
 
 class FatalError(Error):
@@ -62,7 +70,7 @@ class NcclError(RingFailureError):
 _ERRS = {
     _capi.ESHAPE: ShapeError, _capi.ENUMERIC: NumericError, _capi.EDECODE: DecodeError,
     _capi.ECUDA: CudaError, _capi.ENCCL: NcclError, _capi.ERING: RingFailureError,
-    _capi.ECONFIG: ConfigError, _capi.EIO: Error,
+    _capi.ECONFIG: ConfigError, _capi.EIO: Error, _capi.ESTALE: StalePlanError, _capi.EPROTO: Error,
 }
 
 
@@ -597,8 +605,12 @@ class RingEngine:
 
     def __init__(self, n: int, k: int, rank: int = 0, opts: Optional[ReduceOptions] = None, virtual: bool = False,
                  nccl_id: Optional[bytes] = None, window_elems: int = 0, device: Optional[int] = None,
-                 transport: str = "auto", mode: "ReduceMode" = None, tensor_sizes: Optional[Sequence[int]] = None):
+                 transport: str = "auto", mode: "ReduceMode" = None, tensor_sizes: Optional[Sequence[int]] = None,
+                 plan: Optional["RingPlan"] = None):
         opts = opts or ReduceOptions()
+        # RingPlan (allreduce.hpp:25-45): its epoch goes into every payload's ChunkMsg header; its
+        # order names the culprit of a failed round (RingFailureError.failed_node)
+        self.plan = plan
         if opts.pipeline_subchunks < 1:
             raise ConfigError("pipeline_subchunks must be >= 1")
         self.n, self.k, self.rank = int(n), int(k), int(rank)
@@ -618,6 +630,7 @@ class RingEngine:
         self.mode = ReduceMode.int8 if mode is None else ReduceMode(mode)
         cfg.reduce_fp32 = 1 if self.mode == ReduceMode.fp32 else 0
         cfg.step_timeout_s = float(opts.step_timeout)
+        cfg.plan_epoch = int(plan.epoch) if plan is not None else 0
         self._sizes = None
         if tensor_sizes is not None:  # one ReduceJob per tensor (config 5)
             self._sizes = np.ascontiguousarray(np.asarray(tensor_sizes, dtype=np.uint64))
@@ -698,7 +711,7 @@ class RingEngine:
 
     def ring_allreduce(self, inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor], stream=None) -> None:
         """allreduce.hpp:314 in this engine's ReduceMode, stream-ordered."""
-        _check(_capi.lib().emesh_engine_ring_allreduce(self._h, self._ptrs(inputs, "input"),
+        self._rc(_capi.lib().emesh_engine_ring_allreduce(self._h, self._ptrs(inputs, "input"),
                                                        self._ptrs(outputs, "output"), _stream(stream)))
 
     def outer_sync(self, theta_g: Sequence[torch.Tensor], theta_l: Sequence[torch.Tensor],
@@ -706,7 +719,7 @@ class RingEngine:
                    stream=None) -> None:
         """trainer.hpp:355-382: PG -> ring all-reduce (this engine's ReduceMode) -> Nesterov, in place."""
         hp = hp or HyperParams()
-        _check(_capi.lib().emesh_engine_outer_sync(self._h, self._ptrs(theta_g, "theta_g"),
+        self._rc(_capi.lib().emesh_engine_outer_sync(self._h, self._ptrs(theta_g, "theta_g"),
                                                    self._ptrs(theta_l, "theta_l"), self._ptrs(momentum, "momentum"),
                                                    hp.outer_lr, hp.outer_momentum, 1 if write_local else 0,
                                                    _stream(stream)))
@@ -724,12 +737,28 @@ class RingEngine:
                     raise ShapeError("host buffers must be contiguous CPU float32 of length n")
             return _capi.ptr_array([t.data_ptr() for t in ts])
 
-        _check(_capi.lib().emesh_engine_outer_sync_host(self._h, ptrs(theta_g), ptrs(theta_l), ptrs(momentum),
+        self._rc(_capi.lib().emesh_engine_outer_sync_host(self._h, ptrs(theta_g), ptrs(theta_l), ptrs(momentum),
                                                         hp.outer_lr, hp.outer_momentum, 1 if write_local else 0))
 
+    def _rc(self, rc: int) -> None:
+        """_check, with the culprit of a failed round (emesh_engine_failed_rank) as
+        RingFailureError.failed_node (allreduce.hpp:466-470)."""
+        if rc == _capi.ERING:
+            who = int(_capi.lib().emesh_engine_failed_rank(self._h))
+            node = ""
+            if who >= 0:
+                node = self.plan.order[who] if self.plan is not None and who < len(self.plan.order) else str(who)
+            raise RingFailureError(_capi.last_error(), failed_node=node)
+        _check(rc)
+
     def check(self) -> None:
-        """Synchronize; raise NumericError if any quantize saw non-finite data."""
-        _check(_capi.lib().emesh_engine_check(self._h))
+        """Synchronize; raise NumericError if any quantize saw non-finite data, RingFailureError
+        (with failed_node) / StalePlanError if the round failed (then nothing was committed)."""
+        self._rc(_capi.lib().emesh_engine_check(self._h))
+
+    def set_job(self, job_id: int) -> None:
+        """ReduceJob.id of the next round (the ChunkMsg job id every payload carries)."""
+        _check(_capi.lib().emesh_engine_set_job(self._h, int(job_id)))
 
     def payload(self, worker: int = 0):
         """Host copies (codes u8[n], codebooks f32[nseg,256], stats f64[nseg,4]
@@ -779,6 +808,11 @@ def allreduce_with_retry(make_engine, mesh, mesh_state: MeshState, self_id: str,
                 mesh_state = mesh.wait_epoch_change(mesh_state.epoch, opts.evict_wait)
             except TimeoutError:
                 mesh_state = mesh.fetch_mesh()  # maybe it changed and we missed it
+        except StalePlanError as sp:  # allreduce.hpp:512-515: this node's plan is behind
+            failures += 1
+            if failures > opts.max_retries:
+                raise FatalError("all-reduce retries exhausted") from sp
+            mesh_state = mesh.fetch_mesh()
         finally:
             if eng is not None and hasattr(eng, "close"):
                 eng.close()
