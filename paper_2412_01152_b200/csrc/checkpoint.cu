@@ -26,6 +26,7 @@
 #include <deque>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "emesh_b200.h"
@@ -389,6 +390,48 @@ uint64_t first_nonfinite_host(const uint8_t* b, const Parsed& P, uint64_t limit)
     return ~0ull;
 }
 
+// Any non-finite float in the tensor payloads, scanned on the host before a
+// single byte reaches the caller's arenas (a malformed checkpoint must leave
+// the destination untouched, like the reference's decode_checkpoint, which
+// returns by value): exponent-field test on the raw words, split over threads.
+bool any_nonfinite_host(const uint8_t* b, const Parsed& P) {
+    std::vector<std::pair<uint64_t, uint64_t>> ranges;  // byte ranges of every tensor payload
+    uint64_t total = 0;
+    for (const auto& set : P.set)
+        for (const auto& t : set)
+            if (t.numel) {
+                ranges.push_back({t.data_off, 4 * t.numel});
+                total += 4 * t.numel;
+            }
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    const unsigned nt = total < (64ull << 20) ? 1u : hw;
+    std::vector<int> bad(nt, 0);
+    auto scan = [&](unsigned w) {
+        const uint64_t lo = total * w / nt, hi = total * (w + 1) / nt;  // this thread's share of the bytes
+        uint64_t pos = 0;
+        for (const auto& r : ranges) {
+            const uint64_t a = std::max(lo, pos), e = std::min(hi, pos + r.second);
+            pos += r.second;
+            if (a >= e) continue;
+            const uint64_t a4 = (a - (pos - r.second)) & ~uint64_t(3), e4 = e - (pos - r.second);
+            for (uint64_t o = a4; o + 4 <= e4; o += 4) {
+                uint32_t u;
+                std::memcpy(&u, b + r.first + o, 4);
+                if ((u & 0x7f800000u) == 0x7f800000u) { bad[w] = 1; return; }
+            }
+        }
+    };
+    if (nt == 1) scan(0);
+    else {
+        std::vector<std::thread> th;
+        for (unsigned w = 0; w < nt; ++w) th.emplace_back(scan, w);
+        for (auto& t : th) t.join();
+    }
+    for (int v : bad)
+        if (v) return true;
+    return false;
+}
+
 int check_layout(const Layout& L, const std::vector<TensorRec>& got) {
     if (got.size() != L.t.size())
         return set_error(EMESH_EDECODE, fmt("checkpoint holds %zu tensors, the destination arenas %zu", got.size(),
@@ -475,6 +518,7 @@ int decode_into(const uint8_t* b, uint64_t len, emesh_checkpoint* ck, cudaStream
         return set_error(P.err.code, P.err.msg);
     }
     if ((rc = check_layout(L, P.set[0]))) return rc;
+    if (any_nonfinite_host(b, P)) return set_error(EMESH_EDECODE, "non-finite value in tensor payload");
     if ((rc = upload_and_scan(b, P, ck, L, st))) return rc;
     ck->outer_step = P.outer_step;
     ck->adam_step = P.adam_step;

@@ -1142,7 +1142,7 @@ int nccl_drain(emesh_engine* e, std::initializer_list<cudaStream_t> streams, con
             cudaGetLastError();
             if (err) return fail(EMESH_ERING, "%s: NCCL ring failed: %s", what, ncclGetErrorString(ae));
             return fail(EMESH_ERING, "%s: NCCL ring step timed out (step_timeout %.1f s)", what,
-                        (double)e->tr.timeout_ns * 1e-9);
+                        wait_budget_ns(e) * 1e-9);
         }
         std::this_thread::sleep_for(std::chrono::microseconds(100));
     }
@@ -1805,7 +1805,9 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
     e->tr.err = e->ws.err;
     if (cfg->step_timeout_s > 0) e->tr.timeout_ns = (unsigned long long)(cfg->step_timeout_s * 1e9);
     e->plan_epoch = cfg->plan_epoch;
-    e->setup_floor_ns = 30ull * 1000000000ull;  // reset once the engine is up
+    // setup waits (communicator init, the first round's lazy NCCL connects) get at least 30 s;
+    // the floor is dropped once a round has drained successfully (emesh_engine_check)
+    e->setup_floor_ns = 30ull * 1000000000ull;
     int lo_prio = 0, hi_prio = 0;
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
     if (cudaStreamCreateWithPriority(&e->s_comp, cudaStreamNonBlocking, lo_prio) != cudaSuccess ||
@@ -1874,7 +1876,6 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
             }
         }
     }
-    e->setup_floor_ns = 0;
     *out = e;
     return EMESH_OK;
 }
@@ -2205,6 +2206,7 @@ int emesh_engine_check(emesh_engine* e) {
     CU(cudaStreamSynchronize(e->s_comm));
     if (!e->ws.err) return EMESH_OK;
     uint32_t v[2] = {0, 0};
+    e->setup_floor_ns = 0;  // a round drained: later waits get step_timeout alone
     CU(cudaMemcpy(v, e->ws.err, sizeof v, cudaMemcpyDeviceToHost));
     if (v[0]) {
         CU(cudaMemset(e->ws.err, 0, 2 * sizeof(uint32_t)));

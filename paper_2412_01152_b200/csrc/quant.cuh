@@ -96,6 +96,14 @@ struct QHeld {
     uint32_t seg, tile, slot;
 };
 
+// One step of a CTA (thread 0's decision, broadcast through shared memory).
+struct QStep {
+    uint32_t kind;                     // kQTaskStep / kQTaskFinStats / kQTaskFinCb / kQTaskExit
+    uint32_t s_seg, s_tile, s_slot;    // STATS tile (s_seg == kNone: none)
+    uint32_t b_seg, b_tile, b_slot;    // BIN tile (b_seg == kNone: none)
+};
+constexpr uint32_t kNone = 0xffffffffu;
+
 struct Q2Smem {
     uint32_t hist[kQHists][kBuckets + 1][3];  // per warp pair; row 256: sink
     double2 bsk[kBuckets];                    // per bucket {s, K}: fixed point m = x * s + K (kInfoWide)
@@ -108,18 +116,18 @@ struct Q2Smem {
     uint32_t degenerate;
     uint32_t flag;
     uint32_t tbase;                           // TMEM base address
-    uint32_t kind, seg, tile, slot;           // decided task
     uint32_t ovf_seg;                         // lowest segment that may still hold unclaimed overflow tiles
     uint32_t freemask;                        // free on-chip slots
     uint32_t qh, qn;                          // held on-chip tiles (FIFO)
     QHeld q[kQSlots];
     int32_t lut_seg, bin_seg;
     uint32_t pf_o, pf_no;                     // next STATS tile's octets (L2 prefetch)
+    QStep step;
 };
 constexpr size_t kQ2SmemX = (size_t)kQSmemSlots * kQWarps * 4096;
 constexpr size_t kQ2SmemBytes = sizeof(Q2Smem) + 16 + kQ2SmemX;
 
-enum : uint32_t { kQTaskStats = 0, kQTaskBin = 1, kQTaskExit = 2, kQTaskFinStats = 3, kQTaskFinCb = 4 };
+enum : uint32_t { kQTaskStep = 1, kQTaskExit = 2, kQTaskFinStats = 3, kQTaskFinCb = 4 };
 
 // ---------------------------------------------------------------------------
 // tensor memory (tcgen05) as the on-chip x store
@@ -180,175 +188,187 @@ __device__ __forceinline__ void red_shared_add_relaxed(uint32_t* p, uint32_t v) 
 }
 
 // ---------------------------------------------------------------------------
-// STATS tile
+// tensor-memory halves (16 columns = octets j = 2h, 2h + 1 of a warp unit)
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* x) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};" ::"r"(taddr),
+        "f"(x[0]), "f"(x[1]), "f"(x[2]), "f"(x[3]), "f"(x[4]), "f"(x[5]), "f"(x[6]), "f"(x[7]), "f"(x[8]), "f"(x[9]),
+        "f"(x[10]), "f"(x[11]), "f"(x[12]), "f"(x[13]), "f"(x[14]), "f"(x[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* x) {
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, "
+        "[%16];"
+        : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]), "=f"(x[6]), "=f"(x[7]), "=f"(x[8]),
+          "=f"(x[9]), "=f"(x[10]), "=f"(x[11]), "=f"(x[12]), "=f"(x[13]), "=f"(x[14]), "=f"(x[15])
+        : "r"(taddr)
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Where a warp unit's x lives between its STATS and BIN passes.
+struct QSlotRef {
+    uint32_t slot;    // < kQTmemSlots: TMEM; < kQSlots: smem; kSlotGlobal: overflow scratch
+    uint32_t taddr;   // TMEM address of the unit's 32 columns
+    float4* sp;       // smem unit (256 float4: [j][lane] low half, [j][32 + lane] high half)
+    float* gp;        // overflow scratch of the segment, arena-indexed by element
+};
+
+__device__ __forceinline__ QSlotRef q2_slot(const Q2Args& a, const Q2Smem& sm, float4* xsm, const SegInfo& si,
+                                            uint32_t slot) {
+    const int warp = threadIdx.x >> 5;
+    QSlotRef r;
+    r.slot = slot;
+    r.taddr = sm.tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 128u * (uint32_t)(warp >> 2) + 32u * (slot & 3u);
+    r.sp = xsm + ((size_t)(((slot < kQSlots ? slot : kQTmemSlots) - kQTmemSlots) * kQWarps + warp) * 4) * 64;
+    r.gp = a.scratch + ((int64_t)si.so0 - (int64_t)si.o0) * 8;
+    return r;
+}
+
+// x of octets j = 2h, 2h + 1 (16 values per lane) into / out of the slot
+__device__ __forceinline__ void q2_put_half(const QSlotRef& r, uint64_t obase, int h, const float* x) {
+    const int lane = threadIdx.x & 31;
+    if (r.slot < kQTmemSlots) {
+        tmem_st16(r.taddr + 16u * (uint32_t)h, x);
+    } else if (r.slot < kQSlots) {
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            const int j = 2 * h + jj;
+            r.sp[j * 64 + lane] = make_float4(x[8 * jj], x[8 * jj + 1], x[8 * jj + 2], x[8 * jj + 3]);
+            r.sp[j * 64 + 32 + lane] = make_float4(x[8 * jj + 4], x[8 * jj + 5], x[8 * jj + 6], x[8 * jj + 7]);
+        }
+    } else {
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) st8_f32(r.gp + (obase + (uint64_t)(2 * h + jj) * 32 + lane) * 8, &x[8 * jj]);
+    }
+}
+__device__ __forceinline__ void q2_get_half(const QSlotRef& r, uint64_t obase, int h, float* x) {
+    const int lane = threadIdx.x & 31;
+    if (r.slot < kQTmemSlots) {
+        tmem_ld16(r.taddr + 16u * (uint32_t)h, x);
+    } else if (r.slot < kQSlots) {
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            const int j = 2 * h + jj;
+            const float4 v0 = r.sp[j * 64 + lane], v1 = r.sp[j * 64 + 32 + lane];
+            x[8 * jj] = v0.x; x[8 * jj + 1] = v0.y; x[8 * jj + 2] = v0.z; x[8 * jj + 3] = v0.w;
+            x[8 * jj + 4] = v1.x; x[8 * jj + 5] = v1.y; x[8 * jj + 6] = v1.z; x[8 * jj + 7] = v1.w;
+        }
+    } else {
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) ld8_f32(r.gp + (obase + (uint64_t)(2 * h + jj) * 32 + lane) * 8, &x[8 * jj]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// STATS: the fused producer (PG / hop add / owner mean) + moments, per half unit
+
+// Per-lane moments around a pivot (its first in-segment value), fp64.
+struct QMoments {
+    double s0, s1, d0, d1, q0, q1, piv;
+    uint32_t cnt;
+    bool have;
+};
 
 template <int SRC>
-__device__ __forceinline__ void q2_stats_unit(const Q2Args& a, Q2Smem& sm, const SegInfo& si, uint32_t u,
-                                              float (&x)[32], StatP& p) {
+struct QLoads {
+    float a[16];
+    float b[(SRC & kSrcAminusB) ? 16 : 1];
+    uint2 c[2];
+};
+
+template <int SRC>
+__device__ __forceinline__ void q2_stats_load(const Q2Args& a, uint64_t obase, uint64_t hiel, bool interior, int h,
+                                              QLoads<SRC>& L) {
     const int lane = threadIdx.x & 31;
-    const uint64_t hiel = si.lo + si.len;
-    const uint64_t obase = si.o0 + (uint64_t)u * kUnitOct;
-    const bool interior = obase * 8 >= si.lo && (obase + kUnitOct) * 8 <= hiel;
-    float xb[32];
-    uint2 cw[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const uint64_t o = obase + (uint64_t)j * 32 + lane;
-        const bool in = interior || o * 8 < hiel;  // octets past the segment end: not loaded
-        if (in) {
-            ld8_stream(a.a + o * 8, &x[8 * j]);
-            if (SRC & kSrcAminusB) ld8_stream(a.b + o * 8, &xb[8 * j]);
-            if (SRC & kHasIn) cw[j] = ld8_codes(a.in_codes + o * 8);
+    for (int jj = 0; jj < 2; ++jj) {
+        const uint64_t o = obase + (uint64_t)(2 * h + jj) * 32 + lane;
+        if (interior || o * 8 < hiel) {  // octets past the segment end are not loaded
+            ld8_stream(a.a + o * 8, &L.a[8 * jj]);
+            if (SRC & kSrcAminusB) ld8_stream(a.b + o * 8, &L.b[8 * jj]);
+            if (SRC & kHasIn) L.c[jj] = ld8_codes(a.in_codes + o * 8);
         } else {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) x[8 * j + e] = 0.f, xb[8 * j + e] = 0.f;
-            cw[j] = make_uint2(0u, 0u);
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            float v = x[8 * j + e];
-            if (SRC & kSrcAminusB) v = __fsub_rn(v, xb[8 * j + e]);
-            if (SRC & kHasIn) {
-                const uint32_t w = e < 4 ? cw[j].x : cw[j].y;
-                v = __fadd_rn(v, sm.lut[(w >> (8 * (e & 3))) & 0xffu]);
+            for (int e = 0; e < 8; ++e) {
+                L.a[8 * jj + e] = 0.f;
+                if (SRC & kSrcAminusB) L.b[8 * jj + e] = 0.f;
             }
-            if (SRC & kDivK) v = a.inv_divisor != 0.f ? __fmul_rn(v, a.inv_divisor) : __fdiv_rn(v, a.divisor);
-            x[8 * j + e] = v;
+            L.c[jj] = make_uint2(0u, 0u);
         }
     }
-    // moments around the lane's pivot (its first in-segment value), fp64
-    double s0 = 0.0, s1 = 0.0, d0 = 0.0, d1 = 0.0, q0 = 0.0, q1 = 0.0, piv = 0.0;
-    uint32_t cnt = 0;
-    if (interior) {
-        piv = (double)x[0];
+}
+
+// x = producer(loads) in place (L.a), accumulated into the lane's moments.
+template <int SRC>
+__device__ __forceinline__ void q2_stats_finish(const Q2Args& a, const Q2Smem& sm, const SegInfo& si, uint64_t obase,
+                                                bool interior, int h, QLoads<SRC>& L, QMoments& m) {
+    const int lane = threadIdx.x & 31;
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-            const double x0 = (double)x[i], x1 = (double)x[i + 1];
-            const double v0 = __dsub_rn(x0, piv), v1 = __dsub_rn(x1, piv);
-            s0 = __dadd_rn(s0, x0);
-            s1 = __dadd_rn(s1, x1);
-            d0 = __dadd_rn(d0, v0);
-            d1 = __dadd_rn(d1, v1);
-            q0 = __fma_rn(v0, v0, q0);
-            q1 = __fma_rn(v1, v1, q1);
+    for (int i = 0; i < 16; ++i) {
+        float v = L.a[i];
+        if (SRC & kSrcAminusB) v = __fsub_rn(v, L.b[i]);  // optim.hpp:108
+        if (SRC & kHasIn) {                                // allreduce.hpp:422
+            const uint32_t w = (i & 7) < 4 ? L.c[i >> 3].x : L.c[i >> 3].y;
+            v = __fadd_rn(v, sm.lut[(w >> (8 * (i & 3))) & 0xffu]);
         }
-        cnt = 32;
-    } else {
-        bool have = false;
+        if (SRC & kDivK) v = a.inv_divisor != 0.f ? __fmul_rn(v, a.inv_divisor) : __fdiv_rn(v, a.divisor);  // :439
+        L.a[i] = v;
+    }
+    if (interior) {
+        if (!m.have) {
+            m.piv = (double)L.a[0];
+            m.have = true;
+        }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint64_t e0 = (obase + (uint64_t)j * 32 + lane) * 8;
+        for (int i = 0; i < 16; i += 2) {
+            const double x0 = (double)L.a[i], x1 = (double)L.a[i + 1];
+            const double v0 = __dsub_rn(x0, m.piv), v1 = __dsub_rn(x1, m.piv);
+            m.s0 = __dadd_rn(m.s0, x0);
+            m.s1 = __dadd_rn(m.s1, x1);
+            m.d0 = __dadd_rn(m.d0, v0);
+            m.d1 = __dadd_rn(m.d1, v1);
+            m.q0 = __fma_rn(v0, v0, m.q0);
+            m.q1 = __fma_rn(v1, v1, m.q1);
+        }
+        m.cnt += 16;
+    } else {
+        const uint64_t hiel = si.lo + si.len;
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            const uint64_t e0 = (obase + (uint64_t)(2 * h + jj) * 32 + lane) * 8;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 if (e0 + e >= si.lo && e0 + e < hiel) {
-                    const double xd = (double)x[8 * j + e];
-                    if (!have) { piv = xd; have = true; }
-                    const double dv = __dsub_rn(xd, piv);
-                    s0 = __dadd_rn(s0, xd);
-                    d0 = __dadd_rn(d0, dv);
-                    q0 = __fma_rn(dv, dv, q0);
-                    cnt += 1;
+                    const double xd = (double)L.a[8 * jj + e];
+                    if (!m.have) {
+                        m.piv = xd;
+                        m.have = true;
+                    }
+                    const double dv = __dsub_rn(xd, m.piv);
+                    m.s0 = __dadd_rn(m.s0, xd);
+                    m.d0 = __dadd_rn(m.d0, dv);
+                    m.q0 = __fma_rn(dv, dv, m.q0);
+                    m.cnt += 1;
                 }
             }
         }
     }
-    p = StatP{__dadd_rn(s0, s1), __dadd_rn(q0, q1), __dadd_rn(d0, d1), piv, (uint64_t)cnt};
 }
 
 __device__ void q2_finalize_stats(const Q2Args& a, Q2Smem& sm, uint32_t s, const SegInfo& si);
+__device__ void q2_finalize_codebook(const Q2Args& a, uint32_t s, const SegInfo& si);
 
 // Deferred arrival of a tile on its segment's counter: the atomic's result is
-// only looked at in thread 0's next decision, so no block ever waits on it.
+// only looked at in thread 0's next decision, so no block waits on it.
 struct QArrive {
     uint32_t kind;  // kQTaskFinStats / kQTaskFinCb when pending, else 0
     uint32_t seg, last, old;
 };
-
-template <int SRC>
-__device__ void q2_stats_tile(const Q2Args& a, Q2Smem& sm, float4* xsm, uint32_t s, uint32_t tile,
-                              uint32_t slot, QArrive& arr) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const SegInfo si = a.segs[s];
-    uint32_t* sy = a.sync + kSyncReady + kSyPerSeg * s;
-    uint32_t ovf_i = 0;
-    if (threadIdx.x == 0 && slot == kSlotGlobal) ovf_i = atomicAdd(sy + kSyOvfCount, 1u);  // used at the end
-#ifndef EMESH_Q_NOPF
-    {   // the NEXT STATS tile's inputs into L2 (whole 128-B lines: the compiler lowers these to bulk
-        // prefetches, which need aligned addresses): its loads then hit L2 while HBM streams the
-        // tile after it
-        const uint64_t o0 = sm.pf_o, o1 = (uint64_t)sm.pf_o + sm.pf_no;
-        const uint64_t t0 = (o0 * 32) & ~127ull, t1 = (o1 * 32 + 127) & ~127ull;
-        for (uint64_t l = t0 + 128ull * threadIdx.x; l < t1; l += 128ull * kQThreads) {
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(a.a) + l));
-            if (SRC & kSrcAminusB) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(a.b) + l));
-        }
-        if (SRC & kHasIn) {
-            const uint64_t c0 = (o0 * 8) & ~127ull, c1 = (o1 * 8 + 127) & ~127ull;
-            for (uint64_t l = c0 + 128ull * threadIdx.x; l < c1; l += 128ull * kQThreads)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(a.in_codes + l));
-        }
-    }
-#endif
-    if (SRC & kHasIn) {
-        if (sm.lut_seg != (int32_t)s) {  // CTA-uniform
-            if (a.in_flag) {  // peer transport: the predecessor's payload of s must have landed
-                if (threadIdx.x == 0 &&
-                    spin_until_ge_sys(a.in_flag + si.in_slot, a.epoch, a.err, a.timeout_ns, a.culprit_in) && a.in_hdr)
-                    check_hdr(a.in_hdr + si.in_slot, a.hdr, si.chunk, (uint32_t)si.len, kPhaseRS, a.err, a.culprit_in);
-                __syncthreads();
-            }
-            if (threadIdx.x < kBuckets) sm.lut[threadIdx.x] = __ldcg(a.in_cb + (uint64_t)si.in_slot * kBuckets + threadIdx.x);
-            __syncthreads();
-            if (threadIdx.x == 0) sm.lut_seg = (int32_t)s;
-        }
-    }
-    const uint32_t u = tile * kTileUnits + warp;
-    StatP p{0.0, 0.0, 0.0, 0.0, 0};
-    if (u < si.nu8) {
-        float x[32];
-        q2_stats_unit<SRC>(a, sm, si, u, x, p);
-        if (slot < kQTmemSlots) {
-            const uint32_t tq = sm.tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 128u * (uint32_t)(warp >> 2);
-            tmem_st32(tq + 32u * slot, x);
-        } else if (slot < kQSlots) {
-            float4* d = xsm + ((size_t)((slot - kQTmemSlots) * kQWarps + warp) * 4) * 64;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                d[j * 64 + lane] = make_float4(x[8 * j], x[8 * j + 1], x[8 * j + 2], x[8 * j + 3]);
-                d[j * 64 + 32 + lane] = make_float4(x[8 * j + 4], x[8 * j + 5], x[8 * j + 6], x[8 * j + 7]);
-            }
-        } else {  // overflow: the segment's scratch octets
-            float* xs = a.scratch + ((int64_t)si.so0 - (int64_t)si.o0) * 8;
-            const uint64_t obase = si.o0 + (uint64_t)u * kUnitOct;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) st8_f32(xs + (obase + (uint64_t)j * 32 + lane) * 8, &x[8 * j]);
-        }
-    }
-    p = warp_merge(p);
-    if (lane == 0) {
-        sm.wp[warp] = p;
-        if (!isfinite(p.s) || !isfinite(p.m2)) {  // finite fp32 inputs cannot overflow an fp64 sum
-            atomicOr(&a.seg_flags[s], kFlagNonFinite);
-            atomicOr(a.err, 1u);
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        StatP t = sm.wp[0];
-        for (int w = 1; w < kQWarps; ++w) t = statp_merge(t, sm.wp[w]);
-        a.leaf_stat[si.t0 + tile] = t;
-        if (slot == kSlotGlobal) a.ovf[si.t0 + ovf_i] = tile;  // for BIN by any CTA (published below)
-        // acq_rel: publishes this leaf (and overflow entry); the last tile to arrive acquires all
-        // and finalizes the segment (deferred: see QArrive)
-        arr.kind = kQTaskFinStats;
-        arr.seg = s;
-        arr.last = si.ntile - 1;
-        arr.old = atom_add_acq_rel(sy + kSyStats, 1u);
-    }
-}
 
 // Run by the last STATS tile of s: merge the leaves in a fixed order, then
 // mu / sigma / lo / hi / width (quant.hpp:33-59), the exact threshold table
@@ -432,9 +452,7 @@ __device__ void q2_finalize_stats(const Q2Args& a, Q2Smem& sm, uint32_t s, const
 }
 
 // ---------------------------------------------------------------------------
-// BIN tile
-
-__device__ void q2_finalize_codebook(const Q2Args& a, uint32_t s, const SegInfo& si);
+// BIN
 
 // Bins one octet group of 8 values (codes + exact bucket sums).
 template <bool INTERIOR>
@@ -521,133 +539,6 @@ __device__ __forceinline__ void q2_bin_octet(const Q2Args& a, Q2Smem& sm, const 
     }
 }
 
-__device__ void q2_bin_tile(const Q2Args& a, Q2Smem& sm, const float4* xsm, uint32_t s, uint32_t tile,
-                            uint32_t slot, QArrive& arr) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const SegInfo si = a.segs[s];
-    const SegStat* st = &a.stats[si.slot];
-    if (sm.bin_seg != (int32_t)s) {  // CTA-uniform: load the segment's tables
-        __syncthreads();
-        const int b = threadIdx.x;
-        if (b < kBuckets) {
-            sm.thr[b] = b == 0 ? -INFINITY : __ldcg(&st->thr[b]);
-            const uint32_t info = __ldcg(&st->binfo[b]);
-            // s = high word of info (low bits zero), K = 2^52 (+ 2^41 for a wide bucket)
-            sm.bsk[b] = make_double2(__hiloint2double((int)(info & ~kInfoWide), 0),
-                                     __hiloint2double((int)(0x43300000u | ((info & kInfoWide) << 9)), 0));
-        } else if (b == kBuckets) {
-            sm.thr[kBuckets] = INFINITY;
-            sm.thr[kBuckets + 1] = __ldcg(&st->lo_up);
-            const float margin = __ldcg(&st->margin);
-            sm.bp[0] = __ldcg(&st->c_f);
-            sm.bp[1] = __ldcg(&st->inv_w_f);
-            sm.bp[2] = __ldcg(&st->lo_up);
-            sm.bp[3] = __ldcg(&st->hi_dn);
-            sm.bp[4] = margin;
-            sm.bp[5] = 1.f - margin;
-            sm.degenerate = (__ldcg(&st->flags) & kFlagDegenerate) != 0;
-            sm.bin_seg = (int32_t)s;
-        }
-        __syncthreads();
-    }
-    const uint32_t u = tile * kTileUnits + warp;
-    uint32_t nclip_lo = 0, nclip_hi = 0;
-    if (u < si.nu8) {
-        float x[32];
-        const uint64_t obase = si.o0 + (uint64_t)u * kUnitOct;
-        if (slot < kQTmemSlots) {
-            const uint32_t tq = sm.tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 128u * (uint32_t)(warp >> 2);
-            tmem_ld32(tq + 32u * slot, x);
-        } else if (slot < kQSlots) {
-            const float4* d = xsm + ((size_t)((slot - kQTmemSlots) * kQWarps + warp) * 4) * 64;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float4 v0 = d[j * 64 + lane], v1 = d[j * 64 + 32 + lane];
-                x[8 * j] = v0.x; x[8 * j + 1] = v0.y; x[8 * j + 2] = v0.z; x[8 * j + 3] = v0.w;
-                x[8 * j + 4] = v1.x; x[8 * j + 5] = v1.y; x[8 * j + 6] = v1.z; x[8 * j + 7] = v1.w;
-            }
-        } else {
-            const float* xs = a.scratch + ((int64_t)si.so0 - (int64_t)si.o0) * 8;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) ld8_f32(xs + (obase + (uint64_t)j * 32 + lane) * 8, &x[8 * j]);
-        }
-        const uint64_t hiel = si.lo + si.len;
-        const bool interior = obase * 8 >= si.lo && (obase + kUnitOct) * 8 <= hiel;
-        uint32_t* hw = &sm.hist[warp >> 1][0][0];
-        if (sm.degenerate) {  // sigma == 0: every code is 0 (quant.hpp:49-55)
-#pragma unroll 1
-            for (int j = 0; j < 4; ++j) {
-                const uint64_t o = obase + (uint64_t)j * 32 + lane;
-                for (int e = 0; e < 8; ++e)
-                    if (o * 8 + e >= si.lo && o * 8 + e < hiel)
-                        for (uint32_t d = 0; d < a.ndest; ++d) a.dcodes[d][o * 8 + e] = 0;
-            }
-        } else if (interior) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                q2_bin_octet<true>(a, sm, &x[8 * j], obase + (uint64_t)j * 32 + lane, si, hw, nclip_lo, nclip_hi);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                q2_bin_octet<false>(a, sm, &x[8 * j], obase + (uint64_t)j * 32 + lane, si, hw, nclip_lo, nclip_hi);
-        }
-        if (slot == kSlotGlobal && interior) {
-            // consumed (read exactly once): drop the unit's scratch lines from L2 without write-back
-            const float* xs = a.scratch + ((int64_t)si.so0 - (int64_t)si.o0) * 8;
-            const uintptr_t lo_b = reinterpret_cast<uintptr_t>(xs + obase * 8);
-#pragma unroll
-            for (int r = 0; r < 1; ++r)
-                asm volatile("discard.global.L2 [%0], 128;" ::"l"(lo_b + (uintptr_t)lane * 128) : "memory");
-        }
-    }
-    nclip_lo = warp_sum_u(nclip_lo);
-    nclip_hi = warp_sum_u(nclip_hi);
-    if (threadIdx.x < 2) sm.clip[threadIdx.x] = 0u;
-    __syncthreads();
-    if (lane == 0 && (nclip_lo | nclip_hi)) {
-        atomicAdd(&sm.clip[0], nclip_lo);
-        atomicAdd(&sm.clip[1], nclip_hi);
-    }
-    __syncthreads();
-    if (threadIdx.x < kBuckets) {  // tile histogram (exact integers, order-free) -> segment accumulator
-        const int b = threadIdx.x;
-        unsigned long long r = 0;
-        uint32_t cn = 0;
-#pragma unroll
-        for (int h = 0; h < kQHists; ++h) {
-            const uint32_t A = sm.hist[h][b][0], B = sm.hist[h][b][1], Cc = sm.hist[h][b][2];
-            r += (unsigned long long)(A & ((1u << kQCntShift) - 1u)) + ((unsigned long long)B << kQLoBits) +
-                 ((unsigned long long)Cc << kQMidEnd);
-            cn += A >> kQCntShift;
-            sm.hist[h][b][0] = 0u;
-            sm.hist[h][b][1] = 0u;
-            sm.hist[h][b][2] = 0u;
-        }
-        SegAcc* acc = &a.acc[s];
-        if (cn) {
-            atomicAdd(&acc->rlo[b], r & 0xffffffffull);
-            if (r >> 32) atomicAdd(&acc->rhi[b], r >> 32);
-            atomicAdd(&acc->cnt[b], (unsigned long long)cn);
-        }
-        if (b < 2 && sm.clip[b]) atomicAdd(&acc->clip[b], (unsigned long long)sm.clip[b]);
-    } else if (threadIdx.x < kBuckets + kQHists) {  // the sink rows
-        const int h = threadIdx.x - kBuckets;
-        sm.hist[h][kBuckets][0] = 0u;
-        sm.hist[h][kBuckets][1] = 0u;
-        sm.hist[h][kBuckets][2] = 0u;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        // acq_rel: releases this CTA's accumulator atomics and code stores; the last tile acquires
-        // all and writes the codebook (deferred: see QArrive)
-        arr.kind = kQTaskFinCb;
-        arr.seg = s;
-        arr.last = si.ntile - 1;
-        arr.old = atom_add_acq_rel(a.sync + kSyncReady + kSyPerSeg * s + kSyBins, 1u);
-        if (slot < kQSlots) sm.freemask |= 1u << slot;
-    }
-}
-
 // Run by the last BIN tile of s: the codebook from the exact bucket sums
 // (quant.hpp:78-85); re-zeroes the accumulator; raises the arrival flags.
 __device__ void q2_finalize_codebook(const Q2Args& a, uint32_t s, const SegInfo& si) {
@@ -690,7 +581,196 @@ __device__ void q2_finalize_codebook(const Q2Args& a, uint32_t s, const SegInfo&
 }
 
 // ---------------------------------------------------------------------------
-// scheduler (thread 0): next task of this CTA
+// One fused step of a CTA: a STATS tile and a BIN tile side by side. Every
+// warp, per half unit: issue the STATS loads, bin its BIN half unit (pure
+// compute on on-chip x) while they fly, then finish the STATS half and park
+// its x. The block synchronizes twice per step (tile leaf + histogram flush).
+
+
+// BIN: the segment's tables into shared memory (CTA-wide; at segment changes only)
+__device__ void q2_bin_tables(const Q2Args& a, Q2Smem& sm, uint32_t s, const SegInfo& si) {
+    const SegStat* st = &a.stats[si.slot];
+    __syncthreads();
+    const int b = threadIdx.x;
+    if (b < kBuckets) {
+        sm.thr[b] = b == 0 ? -INFINITY : __ldcg(&st->thr[b]);
+        const uint32_t info = __ldcg(&st->binfo[b]);
+        // s = high word of info (low bits zero), K = 2^52 (+ 2^41 for a wide bucket)
+        sm.bsk[b] = make_double2(__hiloint2double((int)(info & ~kInfoWide), 0),
+                                 __hiloint2double((int)(0x43300000u | ((info & kInfoWide) << 9)), 0));
+    } else if (b == kBuckets) {
+        sm.thr[kBuckets] = INFINITY;
+        sm.thr[kBuckets + 1] = __ldcg(&st->lo_up);
+        const float margin = __ldcg(&st->margin);
+        sm.bp[0] = __ldcg(&st->c_f);
+        sm.bp[1] = __ldcg(&st->inv_w_f);
+        sm.bp[2] = __ldcg(&st->lo_up);
+        sm.bp[3] = __ldcg(&st->hi_dn);
+        sm.bp[4] = margin;
+        sm.bp[5] = 1.f - margin;
+        sm.degenerate = (__ldcg(&st->flags) & kFlagDegenerate) != 0;
+        sm.bin_seg = (int32_t)s;
+    }
+    __syncthreads();
+}
+
+// STATS: the incoming codebook of segment s (hop add), after the peer flag (CTA-wide)
+__device__ void q2_stats_lut(const Q2Args& a, Q2Smem& sm, uint32_t s, const SegInfo& si) {
+    __syncthreads();
+    if (a.in_flag) {  // peer transport: the predecessor's payload of s must have landed intact
+        if (threadIdx.x == 0 &&
+            spin_until_ge_sys(a.in_flag + si.in_slot, a.epoch, a.err, a.timeout_ns, a.culprit_in) && a.in_hdr)
+            check_hdr(a.in_hdr + si.in_slot, a.hdr, si.chunk, (uint32_t)si.len, kPhaseRS, a.err, a.culprit_in);
+        __syncthreads();
+    }
+    if (threadIdx.x < kBuckets) sm.lut[threadIdx.x] = __ldcg(a.in_cb + (uint64_t)si.in_slot * kBuckets + threadIdx.x);
+    if (threadIdx.x == 0) sm.lut_seg = (int32_t)s;
+    __syncthreads();
+}
+
+template <int SRC>
+__device__ void q2_step(const Q2Args& a, Q2Smem& sm, float4* xsm, const QStep& t, QArrive (&arr)[2]) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool do_s = t.s_seg != kNone, do_b = t.b_seg != kNone;
+    SegInfo ss{}, sb{};
+    if (do_s) ss = a.segs[t.s_seg];
+    if (do_b) sb = a.segs[t.b_seg];
+    if (do_b && sm.bin_seg != (int32_t)t.b_seg) q2_bin_tables(a, sm, t.b_seg, sb);
+    if ((SRC & kHasIn) && do_s && sm.lut_seg != (int32_t)t.s_seg) q2_stats_lut(a, sm, t.s_seg, ss);
+    uint32_t ovf_i = 0;  // overflow slot of the STATS tile: claimed now, used at the end
+    if (do_s && threadIdx.x == 0 && t.s_slot == kSlotGlobal)
+        ovf_i = atomicAdd(a.sync + kSyncReady + kSyPerSeg * t.s_seg + kSyOvfCount, 1u);
+#ifndef EMESH_Q_NOPF
+    if (do_s) {  // the NEXT STATS tile's inputs into L2 (whole 128-B lines): its loads then hit L2
+        const uint64_t o0 = sm.pf_o, o1 = (uint64_t)sm.pf_o + sm.pf_no;
+        const uint64_t t0 = (o0 * 32) & ~127ull, t1 = (o1 * 32 + 127) & ~127ull;
+        for (uint64_t l = t0 + 128ull * threadIdx.x; l < t1; l += 128ull * kQThreads) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(a.a) + l));
+            if (SRC & kSrcAminusB) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(a.b) + l));
+        }
+        if (SRC & kHasIn) {
+            const uint64_t c0 = (o0 * 8) & ~127ull, c1 = (o1 * 8 + 127) & ~127ull;
+            for (uint64_t l = c0 + 128ull * threadIdx.x; l < c1; l += 128ull * kQThreads)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(a.in_codes + l));
+        }
+    }
+#endif
+    const uint32_t us = t.s_tile * kTileUnits + warp, ub = t.b_tile * kTileUnits + warp;
+    const bool vs = do_s && us < ss.nu8, vb = do_b && ub < sb.nu8;
+    const uint64_t hs = ss.lo + ss.len, hb = sb.lo + sb.len;
+    const uint64_t os = ss.o0 + (uint64_t)us * kUnitOct, ob = sb.o0 + (uint64_t)ub * kUnitOct;
+    const bool is = vs && os * 8 >= ss.lo && (os + kUnitOct) * 8 <= hs;
+    const bool ib = vb && ob * 8 >= sb.lo && (ob + kUnitOct) * 8 <= hb;
+    const QSlotRef rs = q2_slot(a, sm, xsm, ss, t.s_slot), rb = q2_slot(a, sm, xsm, sb, t.b_slot);
+    QMoments m{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0u, false};
+    uint32_t nclip_lo = 0, nclip_hi = 0;
+    uint32_t* hw = &sm.hist[warp >> 1][0][0];
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+        QLoads<SRC> L;
+        if (vs) q2_stats_load<SRC>(a, os, hs, is, h, L);
+        if (vb) {  // bin this half while the loads fly
+            float y[16];
+            q2_get_half(rb, ob, h, y);
+            if (sm.degenerate) {  // sigma == 0: every code is 0 (quant.hpp:49-55)
+                for (int jj = 0; jj < 2; ++jj) {
+                    const uint64_t o = ob + (uint64_t)(2 * h + jj) * 32 + lane;
+                    for (int e = 0; e < 8; ++e)
+                        if (o * 8 + e >= sb.lo && o * 8 + e < hb)
+                            for (uint32_t d = 0; d < a.ndest; ++d) a.dcodes[d][o * 8 + e] = 0;
+                }
+            } else if (ib) {
+                q2_bin_octet<true>(a, sm, &y[0], ob + (uint64_t)(2 * h) * 32 + lane, sb, hw, nclip_lo, nclip_hi);
+                q2_bin_octet<true>(a, sm, &y[8], ob + (uint64_t)(2 * h + 1) * 32 + lane, sb, hw, nclip_lo, nclip_hi);
+            } else {
+                q2_bin_octet<false>(a, sm, &y[0], ob + (uint64_t)(2 * h) * 32 + lane, sb, hw, nclip_lo, nclip_hi);
+                q2_bin_octet<false>(a, sm, &y[8], ob + (uint64_t)(2 * h + 1) * 32 + lane, sb, hw, nclip_lo, nclip_hi);
+            }
+        }
+        if (vs) {
+            q2_stats_finish<SRC>(a, sm, ss, os, is, h, L, m);
+            q2_put_half(rs, os, h, L.a);
+        }
+    }
+    if (vb && t.b_slot == kSlotGlobal && ib) {
+        // consumed (read exactly once): drop the unit's scratch lines from L2 without write-back
+        const uintptr_t lo_b = reinterpret_cast<uintptr_t>(rb.gp + ob * 8);
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(lo_b + (uintptr_t)lane * 128) : "memory");
+    }
+    if (do_s) {
+        StatP p{__dadd_rn(m.s0, m.s1), __dadd_rn(m.q0, m.q1), __dadd_rn(m.d0, m.d1), m.piv, (uint64_t)m.cnt};
+        p = warp_merge(p);
+        if (lane == 0) {
+            sm.wp[warp] = p;
+            if (!isfinite(p.s) || !isfinite(p.m2)) {  // finite fp32 inputs cannot overflow an fp64 sum
+                atomicOr(&a.seg_flags[t.s_seg], kFlagNonFinite);
+                atomicOr(a.err, kErrNonFinite);
+            }
+        }
+    }
+    if (do_b) {
+        nclip_lo = warp_sum_u(nclip_lo);
+        nclip_hi = warp_sum_u(nclip_hi);
+        if (lane == 0 && (nclip_lo | nclip_hi)) {
+            atomicAdd(&sm.clip[0], nclip_lo);
+            atomicAdd(&sm.clip[1], nclip_hi);
+        }
+    }
+    __syncthreads();
+    if (do_s && threadIdx.x == 0) {
+        StatP tl = sm.wp[0];
+        for (int w = 1; w < kQWarps; ++w) tl = statp_merge(tl, sm.wp[w]);
+        a.leaf_stat[ss.t0 + t.s_tile] = tl;
+        if (t.s_slot == kSlotGlobal) a.ovf[ss.t0 + ovf_i] = t.s_tile;  // for BIN by any CTA (published below)
+        // acq_rel: publishes the leaf, the overflow entry and (bar.sync + cumulativity) the block's
+        // scratch stores; the last tile to arrive finalizes the segment (deferred: QArrive)
+        arr[0] = QArrive{kQTaskFinStats, t.s_seg, ss.ntile - 1,
+                         atom_add_acq_rel(a.sync + kSyncReady + kSyPerSeg * t.s_seg + kSyStats, 1u)};
+    }
+    if (do_b) {
+        if (threadIdx.x < kBuckets) {  // tile histogram (exact integers, order-free) -> segment accumulator
+            const int b = threadIdx.x;
+            unsigned long long r = 0;
+            uint32_t cn = 0;
+#pragma unroll
+            for (int hh = 0; hh < kQHists; ++hh) {
+                const uint32_t A = sm.hist[hh][b][0], B = sm.hist[hh][b][1], Cc = sm.hist[hh][b][2];
+                r += (unsigned long long)(A & ((1u << kQCntShift) - 1u)) + ((unsigned long long)B << kQLoBits) +
+                     ((unsigned long long)Cc << kQMidEnd);
+                cn += A >> kQCntShift;
+                sm.hist[hh][b][0] = 0u;
+                sm.hist[hh][b][1] = 0u;
+                sm.hist[hh][b][2] = 0u;
+            }
+            SegAcc* acc = &a.acc[t.b_seg];
+            if (cn) {
+                atomicAdd(&acc->rlo[b], r & 0xffffffffull);
+                if (r >> 32) atomicAdd(&acc->rhi[b], r >> 32);
+                atomicAdd(&acc->cnt[b], (unsigned long long)cn);
+            }
+            if (b < 2) {
+                if (sm.clip[b]) atomicAdd(&acc->clip[b], (unsigned long long)sm.clip[b]);
+                sm.clip[b] = 0u;
+            }
+        } else if (threadIdx.x < kBuckets + kQHists) {  // the sink rows
+            const int hh = threadIdx.x - kBuckets;
+            sm.hist[hh][kBuckets][0] = 0u;
+            sm.hist[hh][kBuckets][1] = 0u;
+            sm.hist[hh][kBuckets][2] = 0u;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            // acq_rel: releases the block's accumulator atomics and code stores; the last tile
+            // acquires all and writes the codebook (deferred: QArrive)
+            arr[1] = QArrive{kQTaskFinCb, t.b_seg, sb.ntile - 1,
+                             atom_add_acq_rel(a.sync + kSyncReady + kSyPerSeg * t.b_seg + kSyBins, 1u)};
+            if (t.b_slot < kQSlots) sm.freemask |= 1u << t.b_slot;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// scheduler (thread 0): the next step of this CTA
 
 __device__ __forceinline__ bool q2_ready(const Q2Args& a, uint32_t s) {
     return ld_acquire(a.sync + kSyncReady + kSyPerSeg * s + kSyReady) != 0u;
@@ -701,13 +781,12 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
     return v;
 }
 
-// Thread 0's scheduler state, kept in registers across tasks. Every global
-// access the next decision needs is issued one task ahead, so a decision
-// never waits on a memory round trip in the common case: the STATS claims
-// run three tiles ahead (c1: next to run, its {segment, tile} loaded; c2:
-// the one after, its table entry in flight; c3: its claim atomic in flight)
-// and the ready flag of the oldest held tile's segment is polled (relaxed)
-// during the task.
+// Thread 0's scheduler state, kept in registers across steps. Every global
+// access a decision needs is issued one step ahead, so a decision never
+// waits on a memory round trip in the common case: the STATS claims run
+// three tiles ahead (c1: next to run, its table entry loaded; c2: the one
+// after, its entry in flight; c3: its claim atomic in flight) and the ready
+// flag of the oldest held tile's segment is polled (relaxed) during the step.
 struct QSched {
     uint32_t c1;       // claimed STATS tile to run next (>= ntiles: none left)
     uint4 ts1;         // its {segment, tile, first octet, octets}
@@ -717,7 +796,6 @@ struct QSched {
     uint32_t poll_seg; // segment whose ready flag `poll` holds (~0u: none)
     uint32_t poll;
     uint32_t ready_seg;  // a segment known ready (flags are monotone within a launch)
-    bool last_stats;
 };
 
 __device__ __forceinline__ bool q2_known_ready(const Q2Args& a, QSched& q, uint32_t s) {
@@ -733,32 +811,30 @@ __device__ __forceinline__ bool q2_known_ready(const Q2Args& a, QSched& q, uint3
     return r;
 }
 
-__device__ void q2_decide(const Q2Args& a, Q2Smem& sm, QSched& q, QArrive& arr) {
-    if (arr.kind) {  // the previous tile's arrival: the last tile of its segment finalizes it
-        const uint32_t k = arr.kind;
-        arr.kind = 0;
-        if (arr.old == arr.last) {
-            sm.kind = k;
-            sm.seg = arr.seg;
-            return;
-        }
-    }
-    for (;;) {
-        const bool stats_left = q.c1 < a.ntiles;
-        if (!stats_left || q.last_stats) {
-            // 1) the oldest tile held on chip, when its segment is ready
-            if (sm.qn > 0) {
-                const QHeld h = sm.q[sm.qh];
-                if (q2_known_ready(a, q, h.seg)) {
-                    sm.kind = kQTaskBin; sm.seg = h.seg; sm.tile = h.tile; sm.slot = h.slot;
-                    sm.qh = (sm.qh + 1) % kQSlots;
-                    sm.qn -= 1;
-                    q.last_stats = false;
-                    break;
-                }
+__device__ void q2_decide(const Q2Args& a, Q2Smem& sm, QSched& q, QArrive (&arr)[2], QStep& t) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+        if (arr[i].kind) {  // a tile's deferred arrival: the last tile of a segment finalizes it
+            const uint32_t k = arr[i].kind;
+            arr[i].kind = 0;
+            if (arr[i].old == arr[i].last) {
+                t.kind = k;
+                t.s_seg = arr[i].seg;
+                return;
             }
-            // 2) an overflow tile of a ready segment (any CTA may bin those)
-            bool got = false;
+        }
+    for (;;) {
+        t.kind = kQTaskStep;
+        t.s_seg = t.b_seg = kNone;
+        t.s_slot = t.b_slot = kSlotGlobal;
+        // BIN: the oldest tile held on chip when its segment is ready, else an overflow tile of a
+        // ready segment (any CTA may bin those)
+        if (sm.qn > 0 && q2_known_ready(a, q, sm.q[sm.qh].seg)) {
+            const QHeld hd = sm.q[sm.qh];
+            t.b_seg = hd.seg; t.b_tile = hd.tile; t.b_slot = hd.slot;
+            sm.qh = (sm.qh + 1) % kQSlots;
+            sm.qn -= 1;
+        } else {
             while (sm.ovf_seg < a.nseg) {
                 const uint32_t s = sm.ovf_seg;
                 if (__ldg(&a.segs[s].ntile) == 0) {  // empty segment (a chunk shorter than S): no tiles
@@ -771,20 +847,18 @@ __device__ void q2_decide(const Q2Args& a, Q2Smem& sm, QSched& q, QArrive& arr) 
                 if (cnt && __ldcg(sy + kSyOvfClaim) < cnt) {
                     const uint32_t i = atomicAdd(sy + kSyOvfClaim, 1u);
                     if (i < cnt) {
-                        sm.kind = kQTaskBin; sm.seg = s; sm.tile = __ldcg(a.ovf + a.segs[s].t0 + i);
-                        sm.slot = kSlotGlobal;
-                        q.last_stats = false;
-                        got = true;
+                        t.b_seg = s; t.b_tile = __ldcg(a.ovf + a.segs[s].t0 + i);
+                        t.b_slot = kSlotGlobal;
                         break;
                     }
                 }
                 sm.ovf_seg = s + 1;
             }
-            if (got) break;
         }
-        if (stats_left) {
-            sm.kind = kQTaskStats; sm.seg = q.ts1.x; sm.tile = q.ts1.y;
-            // an on-chip slot when one is free (then held for BIN in FIFO order), else the overflow scratch
+        // STATS: the claimed tile, on chip when a slot is free (the BIN tile's slot frees at the
+        // end of this step), else in the overflow scratch
+        if (q.c1 < a.ntiles) {
+            t.s_seg = q.ts1.x; t.s_tile = q.ts1.y;
             uint32_t slot = kSlotGlobal;
             if (sm.freemask) {
                 slot = __ffs(sm.freemask) - 1;
@@ -792,21 +866,20 @@ __device__ void q2_decide(const Q2Args& a, Q2Smem& sm, QSched& q, QArrive& arr) 
                 sm.q[(sm.qh + sm.qn) % kQSlots] = QHeld{q.ts1.x, q.ts1.y, slot};
                 sm.qn += 1;
             }
-            sm.slot = slot;
-            q.last_stats = true;
-            // advance the claim pipeline (every value used here arrived during an earlier task)
+            t.s_slot = slot;
+            // advance the claim pipeline (every value used here arrived during an earlier step)
             q.c1 = q.c2;
             q.ts1 = q.ts2;
             q.c2 = q.c3;
-            q.ts2 = q.c2 < a.ntiles ? __ldg(a.tile_seg + q.c2) : make_uint4(0u, 0u, 0u, 0u);  // used a task later
-            q.c3 = atomicAdd(a.sync, 1u);                                                      // used a task later
-            // the next STATS tile's octet range, prefetched into L2 by the whole block during this tile
+            q.ts2 = q.c2 < a.ntiles ? __ldg(a.tile_seg + q.c2) : make_uint4(0u, 0u, 0u, 0u);  // used a step later
+            q.c3 = atomicAdd(a.sync, 1u);                                                      // used a step later
+            // the next STATS tile's octets, prefetched into L2 by the block during this step
             sm.pf_o = q.c1 < a.ntiles ? q.ts1.z : 0u;
             sm.pf_no = q.c1 < a.ntiles ? q.ts1.w : 0u;
-            break;
         }
+        if (t.s_seg != kNone || t.b_seg != kNone) return;
         if (sm.qn == 0 && sm.ovf_seg >= a.nseg) {
-            sm.kind = kQTaskExit;
+            t.kind = kQTaskExit;
             return;
         }
         // nothing runnable: wait for the oldest pending segment's statistics (every STATS tile
@@ -820,7 +893,7 @@ __device__ void q2_decide(const Q2Args& a, Q2Smem& sm, QSched& q, QArrive& arr) 
     }
 }
 
-// Issued right after a decision, consumed at the next one (latency hidden by the task).
+// Issued right after a decision, consumed at the next one (latency hidden by the step).
 __device__ __forceinline__ void q2_prefetch(const Q2Args& a, const Q2Smem& sm, QSched& q) {
     if (sm.qn > 0) {
         const uint32_t s = sm.q[sm.qh].seg;
@@ -844,7 +917,8 @@ __global__ void __launch_bounds__(kQThreads, 1) k_quant(Q2Args a) {
     }
     for (uint32_t i = threadIdx.x; i < kQHists * (kBuckets + 1) * 3; i += kQThreads) (&sm.hist[0][0][0])[i] = 0u;
     QSched q{};
-    QArrive arr{};
+    QArrive arr[2] = {};
+    QStep t{};
     if (threadIdx.x == 0) {
         q.c1 = atomicAdd(a.sync, 1u);
         q.ts1 = q.c1 < a.ntiles ? __ldg(a.tile_seg + q.c1) : make_uint4(0u, 0u, 0u, 0u);
@@ -853,7 +927,6 @@ __global__ void __launch_bounds__(kQThreads, 1) k_quant(Q2Args a) {
         q.c3 = atomicAdd(a.sync, 1u);
         q.poll_seg = ~0u;
         q.ready_seg = ~0u;
-        q.last_stats = false;
         sm.ovf_seg = 0;
         sm.freemask = (1u << kQSlots) - 1u;
         sm.qh = 0;
@@ -861,22 +934,23 @@ __global__ void __launch_bounds__(kQThreads, 1) k_quant(Q2Args a) {
         sm.lut_seg = -1;
         sm.bin_seg = -1;
         sm.pf_no = 0;
+        sm.clip[0] = sm.clip[1] = 0u;
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     for (;;) {
         if (threadIdx.x == 0) {
-            q2_decide(a, sm, q, arr);
+            q2_decide(a, sm, q, arr, t);
             q2_prefetch(a, sm, q);
+            sm.step = t;
         }
         __syncthreads();
-        const uint32_t kind = sm.kind, s = sm.seg, tile = sm.tile, slot = sm.slot;
-        if (kind == kQTaskExit) break;
-        if (kind == kQTaskStats) q2_stats_tile<SRC>(a, sm, xsm, s, tile, slot, arr);
-        else if (kind == kQTaskBin) q2_bin_tile(a, sm, xsm, s, tile, slot, arr);
-        else if (kind == kQTaskFinStats) q2_finalize_stats(a, sm, s, a.segs[s]);
-        else q2_finalize_codebook(a, s, a.segs[s]);
+        const QStep st = sm.step;
+        if (st.kind == kQTaskExit) break;
+        if (st.kind == kQTaskStep) q2_step<SRC>(a, sm, xsm, st, arr);
+        else if (st.kind == kQTaskFinStats) q2_finalize_stats(a, sm, st.s_seg, a.segs[st.s_seg]);
+        else q2_finalize_codebook(a, st.s_seg, a.segs[st.s_seg]);
         __syncthreads();
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
