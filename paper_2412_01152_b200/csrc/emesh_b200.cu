@@ -478,6 +478,7 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     }
     if (io.nflags > (uint32_t)kMaxDest || a.ndest + io.nx > (uint32_t)kMaxDest)
         return fail(EMESH_ECONFIG, "too many quantizer destinations");
+    if (a.ndest + io.nx == 0) return fail(EMESH_ECONFIG, "quantizer without a destination");
     for (uint32_t d = 0; d < io.nx; ++d) {
         a.dcodes[a.ndest] = io.x_codes[d];
         a.dcb[a.ndest] = io.x_cb[d];
@@ -526,7 +527,7 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     // A plain launch suffices: a CTA waits only when every STATS tile is
     // claimed (quant.cuh), so progress never depends on co-residency.
     const int sms = sm_count();
-    int grid = std::max(1, sms - (int)std::min<uint32_t>(reserve_sms, (uint32_t)sms - 1));
+    int grid = std::max(1, sms - (int)std::min<uint32_t>(reserve_sms, (uint32_t)sms - 1)) * kQCtasPerSm;
     grid = std::min<int>(grid, (int)bt.ntiles);
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(grid);

@@ -35,7 +35,12 @@
 
 namespace emesh_b200 {
 
-constexpr int kQWarps = 16;
+#ifndef EMESH_QWARPS
+#define EMESH_QWARPS 16
+#endif
+constexpr int kQWarps = EMESH_QWARPS;       // warps per CTA (CTAs per SM: 16 / kQWarps)
+constexpr int kQCtasPerSm = 16 / kQWarps;
+constexpr int kQTmemCols = 128 * kQWarps / 4;  // this CTA's share of the SM's 512 TMEM columns
 constexpr int kQThreads = kQWarps * 32;  // 512
 constexpr int kQTmemSlots = 4;           // 4 x 32 TMEM columns per warp (its quadrant's 128-column share)
 #ifndef EMESH_QSMEM_SLOTS
@@ -186,6 +191,11 @@ __device__ __forceinline__ void ld8_f32(const float* p, float* v) {
 __device__ __forceinline__ void red_shared_add_relaxed(uint32_t* p, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v));
 }
+__device__ __forceinline__ void red_shared_add_nz_relaxed(uint32_t* p, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q red.shared.add.u32 [%0], %1;\n\t}" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(p)),
+                 "r"(v));
+}
 
 // ---------------------------------------------------------------------------
 // tensor-memory halves (16 columns = octets j = 2h, 2h + 1 of a warp unit)
@@ -319,6 +329,13 @@ __device__ __forceinline__ void q2_stats_finish(const Q2Args& a, const Q2Smem& s
         if (SRC & kDivK) v = a.inv_divisor != 0.f ? __fmul_rn(v, a.inv_divisor) : __fdiv_rn(v, a.divisor);  // :439
         L.a[i] = v;
     }
+#ifdef EMESH_Q_ABL_NOMOM  // ablation (timing only): no fp64 moments
+    if (true) {
+        m.s0 = __dadd_rn(m.s0, (double)(L.a[0] + L.a[15]));
+        m.cnt += 16;
+        return;
+    }
+#endif
     if (interior) {
         if (!m.have) {
             m.piv = (double)L.a[0];
@@ -523,18 +540,23 @@ __device__ __forceinline__ void q2_bin_octet(const Q2Args& a, Q2Smem& sm, const 
         red_shared_add_relaxed(hc, (rlo[i] & ((1u << kQLoBits) - 1u)) | (1u << kQCntShift));
         red_shared_add_relaxed(hc + 1, (rlo[i] >> kQLoBits) & ((1u << (kQMidEnd - kQLoBits)) - 1u));
         const uint32_t rc = __funnelshift_r(rlo[i], rhi[i], kQMidEnd) & ((1u << (42 - kQMidEnd)) - 1u);
-        if (rc) red_shared_add_relaxed(hc + 2, rc);
+        red_shared_add_nz_relaxed(hc + 2, rc);  // predicated: the high limb is rarely nonzero
     }
     const uint32_t p0 = __byte_perm(__byte_perm(cc[0], cc[1], 0x0040), __byte_perm(cc[2], cc[3], 0x0040), 0x5410);
     const uint32_t p1 = __byte_perm(__byte_perm(cc[4], cc[5], 0x0040), __byte_perm(cc[6], cc[7], 0x0040), 0x5410);
-    for (uint32_t d = 0; d < a.ndest; ++d) {
-        uint8_t* oc = a.dcodes[d] + o * 8;
-        if (INTERIOR || vmask == 0xffu) {
-            *reinterpret_cast<uint2*>(oc) = make_uint2(p0, p1);
-        } else if (vmask) {
+    if (INTERIOR) {
+        *reinterpret_cast<uint2*>(a.dcodes[0] + o * 8) = make_uint2(p0, p1);
+        for (uint32_t d = 1; d < a.ndest; ++d) *reinterpret_cast<uint2*>(a.dcodes[d] + o * 8) = make_uint2(p0, p1);
+    } else {
+        for (uint32_t d = 0; d < a.ndest; ++d) {
+            uint8_t* oc = a.dcodes[d] + o * 8;
+            if (vmask == 0xffu) {
+                *reinterpret_cast<uint2*>(oc) = make_uint2(p0, p1);
+            } else if (vmask) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-                if (vmask & (1u << e)) oc[e] = (uint8_t)((e < 4 ? p0 : p1) >> (8 * (e & 3)));
+                for (int e = 0; e < 8; ++e)
+                    if (vmask & (1u << e)) oc[e] = (uint8_t)((e < 4 ? p0 : p1) >> (8 * (e & 3)));
+            }
         }
     }
 }
@@ -598,7 +620,8 @@ __device__ void q2_bin_tables(const Q2Args& a, Q2Smem& sm, uint32_t s, const Seg
         // s = high word of info (low bits zero), K = 2^52 (+ 2^41 for a wide bucket)
         sm.bsk[b] = make_double2(__hiloint2double((int)(info & ~kInfoWide), 0),
                                  __hiloint2double((int)(0x43300000u | ((info & kInfoWide) << 9)), 0));
-    } else if (b == kBuckets) {
+    }
+    if (b == kQThreads - 1) {  // (the last thread: 256 of them may all be busy with buckets above)
         sm.thr[kBuckets] = INFINITY;
         sm.thr[kBuckets + 1] = __ldcg(&st->lo_up);
         const float margin = __ldcg(&st->margin);
@@ -679,6 +702,11 @@ __device__ void q2_step(const Q2Args& a, Q2Smem& sm, float4* xsm, const QStep& t
                         if (o * 8 + e >= sb.lo && o * 8 + e < hb)
                             for (uint32_t d = 0; d < a.ndest; ++d) a.dcodes[d][o * 8 + e] = 0;
                 }
+#ifdef EMESH_Q_ABL_NOBIN  // ablation (timing only): the BIN pass reads x and stores codes, nothing else
+            } else if (true) {
+                const uint32_t p0 = __float_as_uint(y[0]) ^ __float_as_uint(y[15]);
+                *reinterpret_cast<uint2*>(a.dcodes[0] + (ob + (uint64_t)(2 * h) * 32 + lane) * 8) = make_uint2(p0, p0);
+#endif
             } else if (ib) {
                 q2_bin_octet<true>(a, sm, &y[0], ob + (uint64_t)(2 * h) * 32 + lane, sb, hw, nclip_lo, nclip_hi);
                 q2_bin_octet<true>(a, sm, &y[8], ob + (uint64_t)(2 * h + 1) * 32 + lane, sb, hw, nclip_lo, nclip_hi);
@@ -724,8 +752,12 @@ __device__ void q2_step(const Q2Args& a, Q2Smem& sm, float4* xsm, const QStep& t
         if (t.s_slot == kSlotGlobal) a.ovf[ss.t0 + ovf_i] = t.s_tile;  // for BIN by any CTA (published below)
         // acq_rel: publishes the leaf, the overflow entry and (bar.sync + cumulativity) the block's
         // scratch stores; the last tile to arrive finalizes the segment (deferred: QArrive)
+#ifdef EMESH_Q_ABL_RELAXED
+        arr[0] = QArrive{kQTaskFinStats, t.s_seg, ss.ntile - 1, atomicAdd(a.sync + kSyncReady + kSyPerSeg * t.s_seg + kSyStats, 1u)};
+#else
         arr[0] = QArrive{kQTaskFinStats, t.s_seg, ss.ntile - 1,
                          atom_add_acq_rel(a.sync + kSyncReady + kSyPerSeg * t.s_seg + kSyStats, 1u)};
+#endif
     }
     if (do_b) {
         if (threadIdx.x < kBuckets) {  // tile histogram (exact integers, order-free) -> segment accumulator
@@ -752,8 +784,9 @@ __device__ void q2_step(const Q2Args& a, Q2Smem& sm, float4* xsm, const QStep& t
                 if (sm.clip[b]) atomicAdd(&acc->clip[b], (unsigned long long)sm.clip[b]);
                 sm.clip[b] = 0u;
             }
-        } else if (threadIdx.x < kBuckets + kQHists) {  // the sink rows
-            const int hh = threadIdx.x - kBuckets;
+        }
+        if (threadIdx.x >= kQThreads - kQHists) {  // the sink rows
+            const int hh = threadIdx.x - (kQThreads - kQHists);
             sm.hist[hh][kBuckets][0] = 0u;
             sm.hist[hh][kBuckets][1] = 0u;
             sm.hist[hh][kBuckets][2] = 0u;
@@ -762,8 +795,12 @@ __device__ void q2_step(const Q2Args& a, Q2Smem& sm, float4* xsm, const QStep& t
         if (threadIdx.x == 0) {
             // acq_rel: releases the block's accumulator atomics and code stores; the last tile
             // acquires all and writes the codebook (deferred: QArrive)
+#ifdef EMESH_Q_ABL_RELAXED
+            arr[1] = QArrive{kQTaskFinCb, t.b_seg, sb.ntile - 1, atomicAdd(a.sync + kSyncReady + kSyPerSeg * t.b_seg + kSyBins, 1u)};
+#else
             arr[1] = QArrive{kQTaskFinCb, t.b_seg, sb.ntile - 1,
                              atom_add_acq_rel(a.sync + kSyncReady + kSyPerSeg * t.b_seg + kSyBins, 1u)};
+#endif
             if (t.b_slot < kQSlots) sm.freemask |= 1u << t.b_slot;
         }
     }
@@ -793,22 +830,20 @@ struct QSched {
     uint32_t c2;       // the claim after c1
     uint4 ts2;         // its table entry
     uint32_t c3;       // the claim after c2
-    uint32_t poll_seg; // segment whose ready flag `poll` holds (~0u: none)
-    uint32_t poll;
-    uint32_t ready_seg;  // a segment known ready (flags are monotone within a launch)
+    uint32_t ready_upto;  // segments [0, ready_upto) are known ready (published in order, mostly)
+    uint32_t poll;        // relaxed read of segment ready_upto's flag (1 for an empty segment)
+    uint32_t ready_seg;   // a segment found ready out of order (blocking wait)
 };
 
-__device__ __forceinline__ bool q2_known_ready(const Q2Args& a, QSched& q, uint32_t s) {
-    if (q.ready_seg == s) return true;
-    bool r;
-    if (q.poll_seg == s && q.poll != 0u) {
-        __threadfence();  // acquire: the relaxed poll saw the release of SegStat(s)
-        r = true;
-    } else {
-        r = q2_ready(a, s);
+// Known ready without a memory round trip: the flag polled during the last step
+// (one segment per decision; flags are monotone within a launch).
+__device__ __forceinline__ bool q2_known_ready(QSched& q, uint32_t s) { return s < q.ready_upto || s == q.ready_seg; }
+__device__ __forceinline__ void q2_advance_ready(const Q2Args& a, QSched& q) {
+    if (q.ready_upto < a.nseg && q.poll) {
+        __threadfence();  // acquire: the relaxed poll saw the release of SegStat(ready_upto)
+        q.ready_upto += 1;
+        q.poll = 0;
     }
-    if (r) q.ready_seg = s;
-    return r;
 }
 
 __device__ void q2_decide(const Q2Args& a, Q2Smem& sm, QSched& q, QArrive (&arr)[2], QStep& t) {
@@ -823,13 +858,14 @@ __device__ void q2_decide(const Q2Args& a, Q2Smem& sm, QSched& q, QArrive (&arr)
                 return;
             }
         }
+    q2_advance_ready(a, q);
     for (;;) {
         t.kind = kQTaskStep;
         t.s_seg = t.b_seg = kNone;
         t.s_slot = t.b_slot = kSlotGlobal;
         // BIN: the oldest tile held on chip when its segment is ready, else an overflow tile of a
         // ready segment (any CTA may bin those)
-        if (sm.qn > 0 && q2_known_ready(a, q, sm.q[sm.qh].seg)) {
+        if (sm.qn > 0 && q2_known_ready(q, sm.q[sm.qh].seg)) {
             const QHeld hd = sm.q[sm.qh];
             t.b_seg = hd.seg; t.b_tile = hd.tile; t.b_slot = hd.slot;
             sm.qh = (sm.qh + 1) % kQSlots;
@@ -841,7 +877,7 @@ __device__ void q2_decide(const Q2Args& a, Q2Smem& sm, QSched& q, QArrive (&arr)
                     sm.ovf_seg = s + 1;
                     continue;
                 }
-                if (!q2_known_ready(a, q, s)) break;
+                if (!q2_known_ready(q, s)) break;
                 uint32_t* sy = a.sync + kSyncReady + kSyPerSeg * s;
                 const uint32_t cnt = __ldcg(sy + kSyOvfCount);
                 if (cnt && __ldcg(sy + kSyOvfClaim) < cnt) {
@@ -890,29 +926,31 @@ __device__ void q2_decide(const Q2Args& a, Q2Smem& sm, QSched& q, QArrive (&arr)
             __nanosleep(ns);
             ns = ns < 1024 ? 2 * ns : ns;
         }
-    }
-}
-
-// Issued right after a decision, consumed at the next one (latency hidden by the step).
-__device__ __forceinline__ void q2_prefetch(const Q2Args& a, const Q2Smem& sm, QSched& q) {
-    if (sm.qn > 0) {
-        const uint32_t s = sm.q[sm.qh].seg;
-        if (s != q.ready_seg) {
-            q.poll_seg = s;
-            q.poll = ld_relaxed(a.sync + kSyncReady + kSyPerSeg * s + kSyReady);
+        q.ready_seg = s;
+        if (s == q.ready_upto) {
+            q.ready_upto += 1;
+            q.poll = 0;
         }
     }
 }
 
+// Issued right after a decision, consumed at the next one (latency hidden by the step).
+__device__ __forceinline__ void q2_prefetch(const Q2Args& a, QSched& q) {
+    if (q.ready_upto < a.nseg && !q.poll)
+        q.poll = __ldg(&a.segs[q.ready_upto].ntile) == 0
+                     ? 1u
+                     : ld_relaxed(a.sync + kSyncReady + kSyPerSeg * q.ready_upto + kSyReady);
+}
+
 template <int SRC>
-__global__ void __launch_bounds__(kQThreads, 1) k_quant(Q2Args a) {
+__global__ void __launch_bounds__(kQThreads, kQCtasPerSm) k_quant(Q2Args a) {
     extern __shared__ __align__(16) unsigned char qraw[];
     Q2Smem& sm = *reinterpret_cast<Q2Smem*>(qraw);
     float4* xsm = reinterpret_cast<float4*>(qraw + ((sizeof(Q2Smem) + 15) & ~size_t(15)));
     const int warp = threadIdx.x >> 5;
-    if (warp == 0) {  // the whole tensor memory of this SM (one CTA per SM)
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-            (uint32_t)__cvta_generic_to_shared(&sm.tbase)));
+    if (warp == 0) {  // this CTA's share of the SM's tensor memory
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&sm.tbase)), "n"(kQTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     for (uint32_t i = threadIdx.x; i < kQHists * (kBuckets + 1) * 3; i += kQThreads) (&sm.hist[0][0][0])[i] = 0u;
@@ -925,7 +963,8 @@ __global__ void __launch_bounds__(kQThreads, 1) k_quant(Q2Args a) {
         q.c2 = atomicAdd(a.sync, 1u);
         q.ts2 = q.c2 < a.ntiles ? __ldg(a.tile_seg + q.c2) : make_uint4(0u, 0u, 0u, 0u);
         q.c3 = atomicAdd(a.sync, 1u);
-        q.poll_seg = ~0u;
+        q.ready_upto = 0;
+        q.poll = 0;
         q.ready_seg = ~0u;
         sm.ovf_seg = 0;
         sm.freemask = (1u << kQSlots) - 1u;
@@ -942,7 +981,7 @@ __global__ void __launch_bounds__(kQThreads, 1) k_quant(Q2Args a) {
     for (;;) {
         if (threadIdx.x == 0) {
             q2_decide(a, sm, q, arr, t);
-            q2_prefetch(a, sm, q);
+            q2_prefetch(a, q);
             sm.step = t;
         }
         __syncthreads();
@@ -956,7 +995,7 @@ __global__ void __launch_bounds__(kQThreads, 1) k_quant(Q2Args a) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(sm.tbase));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tbase), "n"(kQTmemCols));
 }
 
 }  // namespace emesh_b200

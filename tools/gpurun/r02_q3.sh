@@ -1,0 +1,11 @@
+mkdir -p gpurun_out/r02i
+echo "== repro"; timeout 120 python tools/repro.py 2>&1 | tail -4
+timeout 900 python -m pytest tests/test_gpu_scale.py -x -q --timeout 400 > gpurun_out/r02i/scale.txt 2>&1; echo "scale rc=$?"; tail -3 gpurun_out/r02i/scale.txt
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 200 > gpurun_out/r02i/gpu_tests.txt 2>&1; echo "tests rc=$?"
+tail -5 gpurun_out/r02i/gpu_tests.txt
+for v in default nopf; do
+  L=""; [ $v = nopf ] && L="EMESH_LIB=build_var/libnopf.so"
+  env $L timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r02i/bench_$v.json 2> gpurun_out/r02i/bench_$v.err; echo "bench $v rc=$?"
+  python -c "
+import json;d=json.loads(open('gpurun_out/r02i/bench_$v.json').read().strip().splitlines()[-1]);print(d['ms_per_step'],d['value'],d['roofline']['frac'],d['roofline']['avg_launch_ms'],{k:v['ms_per_step'] for k,v in d['kernels'].items()}, d.get('parity'))"
+done
