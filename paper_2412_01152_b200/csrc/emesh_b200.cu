@@ -87,17 +87,18 @@ struct Batch {
     uint64_t elems = 0;             // elements in the batch
     std::vector<std::pair<uint64_t, uint64_t>> eruns;  // contiguous element runs {lo, len} (transfers)
     uint32_t ncta = 0;              // elementwise tiles (k_apply family)
-    uint32_t ntiles = 0;            // quantizer STATS tiles
+    uint32_t nunits = 0;            // quantizer warp units (1024 elements each)
+    uint32_t nblocks = 0;           // quantizer leaf blocks
     uint32_t upw = 1;               // elementwise warp units per tile
-    size_t off_segs = 0, off_cta = 0, off_tiles = 0;  // byte offsets into the table arena
+    size_t off_segs = 0, off_cta = 0, off_u0 = 0;  // byte offsets into the table arena
     const SegInfo* d_segs = nullptr;
     const uint32_t* d_cta_seg = nullptr;
-    const uint4* d_tile_seg = nullptr;
+    const uint32_t* d_seg_u0 = nullptr;  // [nseg + 1] first unit of each segment
 
     void bind(void* base) {
         d_segs = reinterpret_cast<const SegInfo*>((char*)base + off_segs);
         d_cta_seg = reinterpret_cast<const uint32_t*>((char*)base + off_cta);
-        d_tile_seg = reinterpret_cast<const uint4*>((char*)base + off_tiles);
+        d_seg_u0 = reinterpret_cast<const uint32_t*>((char*)base + off_u0);
     }
 };
 
@@ -108,7 +109,7 @@ struct Plan {
     std::vector<std::vector<Batch>> batches;    // [chunk][window]
     std::vector<uint8_t> host_tables;
     void* d_tables = nullptr;
-    size_t max_cta = 0, max_segs = 0, max_oct = 0, max_tiles = 0;
+    size_t max_cta = 0, max_segs = 0, max_oct = 0, max_units = 0, max_blocks = 0;
 
     // Appends the device tables for one batch over segments [s0, s1).
     void add_batch(uint32_t chunk, uint32_t window, uint32_t s0, uint32_t s1) {
@@ -118,10 +119,10 @@ struct Plan {
         b.slot0 = s0;
         b.nseg = s1 - s0;
         std::vector<SegInfo> infos;
-        std::vector<uint32_t> cseg;
-        std::vector<uint4> tseg;  // quantizer STATS tile -> {segment, tile within it, first octet, octets}
+        std::vector<uint32_t> cseg, segu0;
         bool first = true;
-        uint64_t so = 0;  // overflow scratch octets so far
+        uint64_t so = 0;     // overflow scratch octets so far
+        uint32_t units = 0, blocks = 0;
         for (uint32_t s = s0; s < s1; ++s) {
             const Seg& g = segs[s];
             SegInfo si{};
@@ -131,7 +132,8 @@ struct Plan {
             si.o0 = g.lo >> 3;
             si.so0 = so;
             si.cta0 = (uint32_t)cseg.size();
-            si.t0 = (uint32_t)tseg.size();
+            si.u0 = units;
+            si.b0 = blocks;
             si.slot = s;
             si.in_slot = s;
             si.upw = b.upw;
@@ -142,7 +144,7 @@ struct Plan {
                 si.ncta = (si.nunits + kWarps * b.upw - 1) / (kWarps * b.upw);
                 const uint64_t no = ((g.lo + g.len - 1) >> 3) - si.o0 + 1;
                 si.nu8 = (uint32_t)((no + kUnitOct - 1) / kUnitOct);
-                si.ntile = (si.nu8 + kTileUnits - 1) / kTileUnits;
+                si.nblk = (si.nu8 + kBlkUnits - 1) / kBlkUnits;
                 // whole units: no 128-B overflow line is shared with another segment
                 so += (uint64_t)si.nu8 * kUnitOct;
                 if (first) { b.el_lo = g.lo; first = false; }
@@ -155,19 +157,15 @@ struct Plan {
                     b.eruns.push_back({g.lo, g.len});
             }
             for (uint32_t t = 0; t < si.ncta; ++t) cseg.push_back((uint32_t)infos.size());
-            for (uint32_t t = 0; t < si.ntile; ++t) {
-                // the tile's octets [o, o + no) (for the L2 prefetch; an even count keeps the code range 16-B sized)
-                const uint64_t o = si.o0 + (uint64_t)t * kTileUnits * kUnitOct;
-                const uint64_t o_end = std::min<uint64_t>(si.o0 + (uint64_t)si.nu8 * kUnitOct, o + (uint64_t)kTileUnits * kUnitOct);
-                const uint64_t last = (g.lo + g.len - 1) >> 3;
-                uint64_t no = std::min<uint64_t>(o_end, last + 1) - o;
-                no = (no + 1) & ~uint64_t(1);
-                tseg.push_back(make_uint4((uint32_t)infos.size(), t, (uint32_t)o, (uint32_t)no));
-            }
+            segu0.push_back(units);
+            units += si.nu8;
+            blocks += si.nblk;
             infos.push_back(si);
         }
+        segu0.push_back(units);
         b.ncta = (uint32_t)cseg.size();
-        b.ntiles = (uint32_t)tseg.size();
+        b.nunits = units;
+        b.nblocks = blocks;
         auto append = [&](const void* p, size_t bytes) {
             size_t off = (host_tables.size() + 15) & ~size_t(15);
             host_tables.resize(off + bytes);
@@ -176,9 +174,10 @@ struct Plan {
         };
         b.off_segs = append(infos.data(), infos.size() * sizeof(SegInfo));
         b.off_cta = append(cseg.data(), cseg.size() * sizeof(uint32_t));
-        b.off_tiles = append(tseg.data(), tseg.size() * sizeof(uint4));
+        b.off_u0 = append(segu0.data(), segu0.size() * sizeof(uint32_t));
         max_cta = std::max<size_t>(max_cta, b.ncta);
-        max_tiles = std::max<size_t>(max_tiles, b.ntiles);
+        max_units = std::max<size_t>(max_units, b.nunits);
+        max_blocks = std::max<size_t>(max_blocks, b.nblocks);
         max_segs = std::max<size_t>(max_segs, b.nseg);
         max_oct = std::max<size_t>(max_oct, so);
         batches[chunk].push_back(b);
@@ -298,13 +297,14 @@ Plan make_list_plan(const uint64_t* lo, const uint64_t* len, uint32_t nseg) {
 // Device scratch shared by every batch launched on one stream.
 struct Workspace {
     float* scratch = nullptr;    // quantizer overflow x (octets of 8 floats)
-    StatP* leaf_stat = nullptr;  // per quantizer tile
-    uint32_t* ovf = nullptr;     // per quantizer tile: overflow lists
+    StatP* leaf_stat = nullptr;  // per quantizer unit: moment leaves
+    uint32_t* ovf = nullptr;     // per quantizer unit: overflow lists
+    StatP* blk_leaf = nullptr;   // per quantizer leaf block
     SegAcc* acc = nullptr;       // zero between launches (self-cleaning, see SegAcc)
     uint32_t* seg_flags = nullptr;
     uint32_t* sync = nullptr;
     uint32_t* err = nullptr;
-    size_t cap_oct = 0, cap_tiles = 0, cap_segs = 0;
+    size_t cap_oct = 0, cap_units = 0, cap_blocks = 0, cap_segs = 0;
 
     template <typename T>
     static int grow(T*& p, size_t want_bytes, bool zero) {
@@ -316,7 +316,7 @@ struct Workspace {
         return EMESH_OK;
     }
 
-    int reserve(size_t oct, size_t tiles, size_t segs) {
+    int reserve(size_t oct, size_t units, size_t blocks, size_t segs) {
         if (!err) {  // [0] sticky bits, [1] culprit rank + 1 (kernels.cuh ring_fail)
             CU(cudaMalloc(&err, 4 * sizeof(uint32_t)));
             CU(cudaMemset(err, 0, 4 * sizeof(uint32_t)));
@@ -325,22 +325,25 @@ struct Workspace {
             TRY(grow(scratch, oct * 32, false));
             cap_oct = std::max<size_t>(oct, 1);
         }
-        if (tiles > cap_tiles || !leaf_stat) {
-            TRY(grow(leaf_stat, tiles * sizeof(StatP), false));
-            TRY(grow(ovf, tiles * sizeof(uint32_t), false));
-            cap_tiles = std::max<size_t>(tiles, 1);
+        if (units > cap_units || !leaf_stat) {
+            TRY(grow(leaf_stat, units * sizeof(StatP), false));
+            TRY(grow(ovf, units * sizeof(uint32_t), false));
+            cap_units = std::max<size_t>(units, 1);
         }
-        if (segs > cap_segs || !seg_flags) {
-            TRY(grow(seg_flags, segs * sizeof(uint32_t), true));
-            TRY(grow(acc, segs * sizeof(SegAcc), true));
-            TRY(grow(sync, (kSyncReady + kSyPerSeg * segs) * sizeof(uint32_t), true));
-            cap_segs = std::max<size_t>(segs, 1);
+        if (blocks > cap_blocks || segs > cap_segs || !seg_flags) {
+            TRY(grow(blk_leaf, std::max<size_t>(blocks, 1) * sizeof(StatP), false));
+            TRY(grow(seg_flags, std::max(segs, cap_segs) * sizeof(uint32_t), true));
+            TRY(grow(acc, std::max(segs, cap_segs) * sizeof(SegAcc), true));
+            TRY(grow(sync, (kSyncReady + kSyPerSeg * std::max(segs, cap_segs) + std::max(blocks, cap_blocks)) *
+                               sizeof(uint32_t), true));
+            cap_segs = std::max<size_t>(std::max(segs, cap_segs), 1);
+            cap_blocks = std::max<size_t>(std::max(blocks, cap_blocks), 1);
         }
         return EMESH_OK;
     }
     void release() {
-        cudaFree(scratch); cudaFree(leaf_stat); cudaFree(ovf); cudaFree(acc); cudaFree(seg_flags); cudaFree(sync);
-        cudaFree(err);
+        cudaFree(scratch); cudaFree(leaf_stat); cudaFree(ovf); cudaFree(blk_leaf); cudaFree(acc); cudaFree(seg_flags);
+        cudaFree(sync); cudaFree(err);
         *this = Workspace();
     }
 };
@@ -453,11 +456,11 @@ int sm_count() {
 // ring's transfers overlap this kernel.
 int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t st, Tracker* tr,
                  uint32_t reserve_sms = 0) {
-    if (bt.ntiles == 0) return EMESH_OK;
+    if (bt.nunits == 0) return EMESH_OK;
     Q2Args a{};
     a.segs = bt.d_segs;
-    a.tile_seg = bt.d_tile_seg;
-    a.ntiles = bt.ntiles;
+    a.seg_u0 = bt.d_seg_u0;
+    a.nunits = bt.nunits;
     a.nseg = bt.nseg;
     a.a = io.a;
     a.b = io.b;
@@ -490,7 +493,8 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     a.epoch = io.epoch;
     a.timeout_ns = tr ? tr->timeout_ns : 30ull * 1000000000ull;
     a.stats = io.stats;
-    a.leaf_stat = ws.leaf_stat;
+    a.leaf = ws.leaf_stat;
+    a.blk_leaf = ws.blk_leaf;
     a.acc = ws.acc;
     a.seg_flags = ws.seg_flags;
     a.err = ws.err;
@@ -501,7 +505,7 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     a.hdr = io.hdr;
     a.phase_out = io.phase_out;
     a.culprit_in = io.culprit_in;
-    CU(cudaMemsetAsync(ws.sync, 0, (kSyncReady + kSyPerSeg * (size_t)bt.nseg) * sizeof(uint32_t), st));
+    CU(cudaMemsetAsync(ws.sync, 0, (kSyncReady + kSyPerSeg * (size_t)bt.nseg + bt.nblocks) * sizeof(uint32_t), st));
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
     void* args[] = {&a};
@@ -527,8 +531,8 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     // A plain launch suffices: a CTA waits only when every STATS tile is
     // claimed (quant.cuh), so progress never depends on co-residency.
     const int sms = sm_count();
-    int grid = std::max(1, sms - (int)std::min<uint32_t>(reserve_sms, (uint32_t)sms - 1)) * kQCtasPerSm;
-    grid = std::min<int>(grid, (int)bt.ntiles);
+    int grid = std::max(1, sms - (int)std::min<uint32_t>(reserve_sms, (uint32_t)sms - 1));
+    grid = std::min<int>(grid, (int)((bt.nunits + kQWarps * kQuad - 1) / (kQWarps * kQuad)));
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(grid);
     lc.blockDim = dim3(kQThreads);
@@ -622,7 +626,7 @@ int emesh_quantize_segments(const float* x, const uint64_t* seg_lo, const uint64
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     std::lock_guard<std::mutex> g(g_codec_mu);
     Plan p = make_list_plan(seg_lo, seg_len, nseg);
-    TRY(g_codec_ws.reserve(p.max_oct, p.max_tiles, p.max_segs));
+    TRY(g_codec_ws.reserve(p.max_oct, p.max_units, p.max_blocks, p.max_segs));
     // stream-ordered tables + stats (freed in stream order)
     void* d_tables = nullptr;
     SegStat* d_stats = nullptr;
@@ -860,7 +864,7 @@ int engine_alloc(emesh_engine* e) {
         e->pay.assign(e->workers, nullptr);
         for (auto& p : e->pay) CU(cudaMalloc(&p, n * sizeof(float) + 16));
     }
-    TRY(e->ws.reserve(e->plan.max_oct, e->plan.max_tiles, e->plan.max_segs));
+    TRY(e->ws.reserve(e->plan.max_oct, e->plan.max_units, e->plan.max_blocks, e->plan.max_segs));
     return EMESH_OK;
 }
 
@@ -1864,7 +1868,7 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
             e->plan.release();
             e->plan = mkplan(nccl_window);
             e->windows = (uint32_t)e->plan.batches[0].size();
-            if ((rc = e->plan.upload()) || (rc = e->ws.reserve(e->plan.max_oct, e->plan.max_tiles, e->plan.max_segs)))
+            if ((rc = e->plan.upload()) || (rc = e->ws.reserve(e->plan.max_oct, e->plan.max_units, e->plan.max_blocks, e->plan.max_segs)))
                 return bail(rc);
             e->schedule = build_schedule(e->plan, e->rank);
             for (auto ev : e->ev_send) cudaEventDestroy(ev);

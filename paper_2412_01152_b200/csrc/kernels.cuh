@@ -85,8 +85,9 @@ struct SegInfo {
     uint32_t cta0;      // first elementwise tile (batch-relative)
     uint32_t ncta;      // elementwise tiles
     uint32_t nu8;       // octet-grid warp units (quantizer)
-    uint32_t t0;        // first quantizer tile (batch-relative): leaf_stat / overflow list index
-    uint32_t ntile;     // quantizer tiles (16 warp units each)
+    uint32_t u0;        // first quantizer unit (batch-relative): leaf / overflow list index
+    uint32_t b0;        // first quantizer leaf block (batch-relative)
+    uint32_t nblk;      // quantizer leaf blocks (64 units each)
     uint32_t slot;      // global segment slot (stats / codebook index)
     uint32_t in_slot;   // slot of the incoming payload's codebook (== slot)
     uint32_t upw;       // elementwise warp units per tile (one value per batch)
