@@ -79,6 +79,10 @@ struct Seg {
     uint64_t lo, len;
 };
 
+uint32_t quant_lag_tiles();
+bool bin_reverse();
+bool quant_mix();
+
 // One pipelining window: consecutive segments of one rank chunk.
 struct Batch {
     uint32_t chunk = 0, window = 0;
@@ -86,21 +90,32 @@ struct Batch {
     uint64_t el_lo = 0, el_hi = 0;  // element span [el_lo, el_hi) (contiguous for a flat arena)
     uint64_t elems = 0;             // elements in the batch
     std::vector<std::pair<uint64_t, uint64_t>> eruns;  // contiguous element runs {lo, len} (transfers)
-    uint32_t ncta = 0;              // elementwise tiles (k_apply family)
-    uint32_t nunits = 0;            // quantizer warp units (1024 elements each)
-    uint32_t nblocks = 0;           // quantizer leaf blocks
-    uint32_t upw = 1;               // elementwise warp units per tile
-    size_t off_segs = 0, off_cta = 0, off_u0 = 0;  // byte offsets into the table arena
+    uint32_t ncta = 0, nruns = 0, ntasks = 0;
+    uint32_t upw = kUnitsPerWarp;   // warp units per tile (tile_units_per_warp)
+    size_t off_segs = 0, off_cta = 0, off_runs = 0;  // byte offsets into the table arena
     const SegInfo* d_segs = nullptr;
     const uint32_t* d_cta_seg = nullptr;
-    const uint32_t* d_seg_u0 = nullptr;  // [nseg + 1] first unit of each segment
+    const uint4* d_runs = nullptr;
 
     void bind(void* base) {
         d_segs = reinterpret_cast<const SegInfo*>((char*)base + off_segs);
         d_cta_seg = reinterpret_cast<const uint32_t*>((char*)base + off_cta);
-        d_seg_u0 = reinterpret_cast<const uint32_t*>((char*)base + off_u0);
+        d_runs = reinterpret_cast<const uint4*>((char*)base + off_runs);
     }
 };
+
+// Tile shape per batch: 4 warp units (16K elements) per tile for large batches,
+// 2 (8K) for small ones and 1 for tiny ones, where more CTAs per segment shorten
+// the serial STATS -> thresholds -> BIN chain. Measured at 2 GPUs
+// (profiles/r01_u2_ab/): 2-unit tiles take 0.101 vs 0.122 ms per round at 1 MB,
+// 0.171 vs 0.183 ms at 64 MB (8M-element batches), but are 2-4 % slower from
+// 32M-element batches up; 1-unit tiles (profiles/r01_tile1/) a further -8..-14 %
+// on <= 2M-element batches at 2 and 4 GPUs, mixed at 4M-8M.
+uint32_t tile_units_per_warp(uint64_t batch_elems) {
+    constexpr uint64_t kTinyBatchElems = 2ull << 20, kSmallBatchElems = 16ull << 20;
+    if (batch_elems <= kTinyBatchElems) return 1u;
+    return batch_elems <= kSmallBatchElems ? (uint32_t)std::min(2, kUnitsPerWarp) : (uint32_t)kUnitsPerWarp;
+}
 
 struct Plan {
     uint64_t n = 0;
@@ -109,7 +124,7 @@ struct Plan {
     std::vector<std::vector<Batch>> batches;    // [chunk][window]
     std::vector<uint8_t> host_tables;
     void* d_tables = nullptr;
-    size_t max_cta = 0, max_segs = 0, max_oct = 0, max_units = 0, max_blocks = 0;
+    size_t max_cta = 0, max_segs = 0, max_slots = 0;
 
     // Appends the device tables for one batch over segments [s0, s1).
     void add_batch(uint32_t chunk, uint32_t window, uint32_t s0, uint32_t s1) {
@@ -118,35 +133,35 @@ struct Plan {
         b.window = window;
         b.slot0 = s0;
         b.nseg = s1 - s0;
+        {
+            uint64_t tot = 0;
+            for (uint32_t s = s0; s < s1; ++s) tot += segs[s].len;
+            b.upw = tile_units_per_warp(tot);
+        }
         std::vector<SegInfo> infos;
-        std::vector<uint32_t> cseg, segu0;
+        std::vector<uint32_t> cseg;
         bool first = true;
-        uint64_t so = 0;     // overflow scratch octets so far
-        uint32_t units = 0, blocks = 0;
+        uint64_t sq = 0;  // scratch float4 slots so far
         for (uint32_t s = s0; s < s1; ++s) {
             const Seg& g = segs[s];
             SegInfo si{};
             si.lo = g.lo;
             si.len = g.len;
             si.q0 = g.lo >> 2;
-            si.o0 = g.lo >> 3;
-            si.so0 = so;
+            si.sq0 = sq;
             si.cta0 = (uint32_t)cseg.size();
-            si.u0 = units;
-            si.b0 = blocks;
             si.slot = s;
             si.in_slot = s;
             si.upw = b.upw;
             si.chunk = chunk;
             if (g.len > 0) {
-                const uint64_t nq = ((g.lo + g.len - 1) >> 2) - si.q0 + 1;
+                const uint64_t q_last = (g.lo + g.len - 1) >> 2;
+                const uint64_t nq = q_last - si.q0 + 1;
                 si.nunits = (uint32_t)((nq + kUnitSlots - 1) / kUnitSlots);
                 si.ncta = (si.nunits + kWarps * b.upw - 1) / (kWarps * b.upw);
-                const uint64_t no = ((g.lo + g.len - 1) >> 3) - si.o0 + 1;
-                si.nu8 = (uint32_t)((no + kUnitOct - 1) / kUnitOct);
-                si.nblk = (si.nu8 + kBlkUnits - 1) / kBlkUnits;
-                // whole units: no 128-B overflow line is shared with another segment
-                so += (uint64_t)si.nu8 * kUnitOct;
+                // whole units: no 128-B scratch line (and no prefetched unit) is
+                // shared with another segment, whose STATS may not have run yet
+                sq += (nq + kUnitSlots - 1) / kUnitSlots * kUnitSlots;
                 if (first) { b.el_lo = g.lo; first = false; }
                 b.el_lo = std::min(b.el_lo, g.lo);
                 b.el_hi = std::max(b.el_hi, g.lo + g.len);
@@ -157,15 +172,86 @@ struct Plan {
                     b.eruns.push_back({g.lo, g.len});
             }
             for (uint32_t t = 0; t < si.ncta; ++t) cseg.push_back((uint32_t)infos.size());
-            segu0.push_back(units);
-            units += si.nu8;
-            blocks += si.nblk;
             infos.push_back(si);
         }
-        segu0.push_back(units);
         b.ncta = (uint32_t)cseg.size();
-        b.nunits = units;
-        b.nblocks = blocks;
+        // persistent-kernel task order (see kernels.cuh): STATS tiles in
+        // segment order; the BIN tiles of s (in reverse tile order: the most
+        // recently written scratch is re-read first, while still in L2) become
+        // available `lag` tasks after its last STATS tile and are then
+        // interleaved 1:1 with the following STATS tiles, so every SM always
+        // runs a mix of the HBM-bound STATS and the issue-bound BIN work.
+        // Compressed into runs {first task, kind | bin segment << 2, segment,
+        // first tile}: plain runs (one kind) and mixed runs (S, B, S, B, ...).
+        std::vector<uint4> runs;
+        {
+            const uint32_t lag = quant_lag_tiles();
+            struct Task { uint32_t kind, seg, tile; };
+            std::vector<Task> order;
+            order.reserve(2 * (size_t)b.ncta);
+            struct Pending { uint32_t seg, next, left, at; };
+            std::vector<Pending> bq;
+            size_t hb = 0;
+            const bool mix = quant_mix();
+            auto bin_ready = [&]() { return hb < bq.size() && order.size() >= bq[hb].at; };
+            auto pop_bin = [&]() {
+                Pending& pb = bq[hb];
+                order.push_back({kTaskBin, pb.seg, pb.next});
+                if (bin_reverse()) --pb.next; else ++pb.next;
+                if (--pb.left == 0) ++hb;
+            };
+            for (uint32_t i = 0; i < infos.size(); ++i) {
+                for (uint32_t t = 0; t < infos[i].ncta; ++t) {
+                    order.push_back({kTaskStats, i, t});
+                    if (mix) {
+                        if (bin_ready()) pop_bin();
+                    } else {  // whole-segment BIN blocks (no interleaving)
+                        while (bin_ready()) pop_bin();
+                    }
+                }
+                if (infos[i].ncta)
+                    bq.push_back({i, bin_reverse() ? infos[i].ncta - 1 : 0u, infos[i].ncta,
+                                  (uint32_t)order.size() + lag});
+            }
+            while (hb < bq.size()) pop_bin();
+            b.ntasks = (uint32_t)order.size();
+            const int dir = bin_reverse() ? -1 : 1;
+            size_t p0 = 0;
+            while (p0 < order.size()) {
+                const Task& t0 = order[p0];
+                // mixed run: S(a, i), B(b, j), S(a, i+1), B(b, j+dir), ...
+                size_t q = p0;
+                if (t0.kind == kTaskStats && p0 + 1 < order.size() && order[p0 + 1].kind == kTaskBin) {
+                    const Task& t1 = order[p0 + 1];
+                    while (q + 1 < order.size()) {
+                        const uint32_t i = (uint32_t)((q - p0) / 2);
+                        const Task& s0 = order[q];
+                        const Task& s1 = order[q + 1];
+                        if (s0.kind != kTaskStats || s0.seg != t0.seg || s0.tile != t0.tile + i) break;
+                        if (s1.kind != kTaskBin || s1.seg != t1.seg || (int64_t)s1.tile != (int64_t)t1.tile + dir * (int64_t)i) break;
+                        q += 2;
+                    }
+                    if (q - p0 >= 4 && t0.tile < 0x10000u && t1.tile < 0x10000u) {
+                        runs.push_back(make_uint4((uint32_t)p0, (dir < 0 ? kTaskMixRev : kTaskMixFwd) | (t1.seg << 2), t0.seg,
+                                                  t0.tile | (t1.tile << 16)));
+                        p0 = q;
+                        continue;
+                    }
+                    q = p0;
+                }
+                // plain run of one kind and segment, tiles +1 (STATS) / +dir (BIN)
+                const int step = t0.kind == kTaskBin ? dir : 1;
+                q = p0 + 1;
+                while (q < order.size() && order[q].kind == t0.kind && order[q].seg == t0.seg &&
+                       (int64_t)order[q].tile == (int64_t)t0.tile + step * (int64_t)(q - p0))
+                    ++q;
+                runs.push_back(make_uint4((uint32_t)p0, t0.kind, t0.seg,
+                                          step < 0 ? 0x80000000u | t0.tile : t0.tile));
+                p0 = q;
+            }
+        }
+        b.nruns = (uint32_t)runs.size();
+
         auto append = [&](const void* p, size_t bytes) {
             size_t off = (host_tables.size() + 15) & ~size_t(15);
             host_tables.resize(off + bytes);
@@ -174,12 +260,11 @@ struct Plan {
         };
         b.off_segs = append(infos.data(), infos.size() * sizeof(SegInfo));
         b.off_cta = append(cseg.data(), cseg.size() * sizeof(uint32_t));
-        b.off_u0 = append(segu0.data(), segu0.size() * sizeof(uint32_t));
+        b.off_runs = append(runs.data(), runs.size() * sizeof(uint4));
+
         max_cta = std::max<size_t>(max_cta, b.ncta);
-        max_units = std::max<size_t>(max_units, b.nunits);
-        max_blocks = std::max<size_t>(max_blocks, b.nblocks);
         max_segs = std::max<size_t>(max_segs, b.nseg);
-        max_oct = std::max<size_t>(max_oct, so);
+        max_slots = std::max<size_t>(max_slots, sq);
         batches[chunk].push_back(b);
     }
 
@@ -198,6 +283,20 @@ struct Plan {
 };
 
 constexpr uint64_t kDefaultWindow = (uint64_t)16 << 20;  // elements per pipelining window
+
+int persistent_grid(const void* fn, uint32_t ntasks);
+// Lag between a segment's last STATS tile and its first BIN tile in the task
+// order: one persistent grid (the stats root publishes within about one
+// tile time; longer lags push scratch x out of L2).
+// measured best (round 1, config 2): BIN interleaved 1:1 with STATS, a segment's BIN tiles
+// in reverse tile order (the most recently written scratch first), 1.5 persistent grids of lag
+bool quant_mix() { return true; }
+bool bin_reverse() { return true; }
+uint32_t quant_lag_tiles() {
+    const int g = persistent_grid((const void*)k_quant<kSrcAminusB | kHasIn>, 1u << 30);
+    return (uint32_t)std::max(1.0, 1.5 * (g > 0 ? g : 512));
+}
+
 
 // Ring plan: k chunks, min(S, len) subs each, windows of G segments.
 Plan make_ring_plan(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems) {
@@ -296,57 +395,56 @@ Plan make_list_plan(const uint64_t* lo, const uint64_t* len, uint32_t nseg) {
 
 // Device scratch shared by every batch launched on one stream.
 struct Workspace {
-    float* scratch = nullptr;    // quantizer overflow x (octets of 8 floats)
-    StatP* leaf_stat = nullptr;  // per quantizer unit: moment leaves
-    uint32_t* ovf = nullptr;     // per quantizer unit: overflow lists
-    StatP* blk_leaf = nullptr;   // per quantizer leaf block
-    SegAcc* acc = nullptr;       // zero between launches (self-cleaning, see SegAcc)
+    float* scratch = nullptr;
+    StatP* leaf_stat = nullptr;
+    SegAcc* acc = nullptr;  // zero between launches (self-cleaning, see SegAcc)
     uint32_t* seg_flags = nullptr;
     uint32_t* sync = nullptr;
     uint32_t* err = nullptr;
-    size_t cap_oct = 0, cap_units = 0, cap_blocks = 0, cap_segs = 0;
+    size_t cap_slots = 0, cap_cta = 0, cap_segs = 0;
 
     template <typename T>
-    static int grow(T*& p, size_t want_bytes, bool zero) {
+    static int grow(T*& p, size_t& cap, size_t want, size_t elems_per, bool zero) {
+        if (want <= cap && p) return EMESH_OK;
         if (p) CU(cudaFree(p));
-        p = nullptr;
-        const size_t bytes = std::max<size_t>(want_bytes, 16);
+        const size_t bytes = std::max<size_t>(want, 1) * elems_per * sizeof(T);
         CU(cudaMalloc(&p, bytes));
         if (zero) CU(cudaMemset(p, 0, bytes));
         return EMESH_OK;
     }
 
-    int reserve(size_t oct, size_t units, size_t blocks, size_t segs) {
+    int reserve(size_t slots, size_t ctas, size_t segs) {
         if (!err) {  // [0] sticky bits, [1] culprit rank + 1 (kernels.cuh ring_fail)
             CU(cudaMalloc(&err, 4 * sizeof(uint32_t)));
             CU(cudaMemset(err, 0, 4 * sizeof(uint32_t)));
         }
-        if (oct > cap_oct || !scratch) {
-            TRY(grow(scratch, oct * 32, false));
-            cap_oct = std::max<size_t>(oct, 1);
+        if (slots > cap_slots || !scratch) {
+            size_t c = 0;
+            TRY(grow(scratch, c, slots, 4, false));
+            cap_slots = std::max<size_t>(slots, 1);
         }
-        if (units > cap_units || !leaf_stat) {
-            TRY(grow(leaf_stat, units * sizeof(StatP), false));
-            TRY(grow(ovf, units * sizeof(uint32_t), false));
-            cap_units = std::max<size_t>(units, 1);
+        if (ctas > cap_cta || !leaf_stat) {
+            size_t c = 0;
+            TRY(grow(leaf_stat, c, ctas, 1, false));
+            cap_cta = std::max<size_t>(ctas, 1);
         }
-        if (blocks > cap_blocks || segs > cap_segs || !seg_flags) {
-            TRY(grow(blk_leaf, std::max<size_t>(blocks, 1) * sizeof(StatP), false));
-            TRY(grow(seg_flags, std::max(segs, cap_segs) * sizeof(uint32_t), true));
-            TRY(grow(acc, std::max(segs, cap_segs) * sizeof(SegAcc), true));
-            TRY(grow(sync, (kSyncReady + kSyPerSeg * std::max(segs, cap_segs) + std::max(blocks, cap_blocks)) *
-                               sizeof(uint32_t), true));
-            cap_segs = std::max<size_t>(std::max(segs, cap_segs), 1);
-            cap_blocks = std::max<size_t>(std::max(blocks, cap_blocks), 1);
+        if (segs > cap_segs || !seg_flags) {
+            size_t c = 0;
+            TRY(grow(seg_flags, c, segs, 1, true));
+            c = 0;
+            TRY(grow(acc, c, segs, 1, true));
+            c = 0;
+            TRY(grow(sync, c, kSyncReady + 3 * segs, 1, true));
+            cap_segs = std::max<size_t>(segs, 1);
         }
         return EMESH_OK;
     }
     void release() {
-        cudaFree(scratch); cudaFree(leaf_stat); cudaFree(ovf); cudaFree(blk_leaf); cudaFree(acc); cudaFree(seg_flags);
-        cudaFree(sync); cudaFree(err);
+        cudaFree(scratch); cudaFree(leaf_stat); cudaFree(acc); cudaFree(seg_flags); cudaFree(sync); cudaFree(err);
         *this = Workspace();
     }
 };
+
 
 // ---------------------------------------------------------------------------
 // Launchers
@@ -437,30 +535,40 @@ struct Tracker {
 };
 Tracker g_codec_tracker;
 
-// SMs of this device (cached per device).
-int sm_count() {
-    static int cache[64] = {0};
+// Co-resident grid of the persistent quantizer (occupancy x SMs, capped at the task count).
+int persistent_grid(const void* fn, uint32_t ntasks) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> cache;
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64) dev = 0;
-    if (!cache[dev]) {
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cache[dev] = sms;
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        for (auto& kv : cache)
+            if (kv.first == fn) per_sm = kv.second;
+        if (!per_sm) {
+            if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQuantSmemBytes) != cudaSuccess)
+                return -1;
+            // leave L1 room for the prefetched scratch lines (smem only as large as the CTAs need)
+            cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 64);
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, kQuantSmemBytes) != cudaSuccess)
+                return -1;
+            cache.push_back({fn, per_sm});
+        }
     }
-    return cache[dev];
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long want = (long long)per_sm * sms;
+    return (int)std::max<long long>(1, std::min<long long>(want, ntasks));
 }
 
-// Segment-resident quantizer (quant.cuh): one persistent 512-thread CTA per
-// SM. `reserve_sms` SMs stay free for NCCL's kernels (NCCL transport) so the
-// ring's transfers overlap this kernel.
 int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t st, Tracker* tr,
-                 uint32_t reserve_sms = 0) {
-    if (bt.nunits == 0) return EMESH_OK;
-    Q2Args a{};
+                 uint32_t reserve_ctas = 0) {
+    if (bt.ncta == 0) return EMESH_OK;
+    QuantArgs a{};
     a.segs = bt.d_segs;
-    a.seg_u0 = bt.d_seg_u0;
-    a.nunits = bt.nunits;
+    a.cta_seg = bt.d_cta_seg;
+    a.ncta = bt.ncta;
     a.nseg = bt.nseg;
     a.a = io.a;
     a.b = io.b;
@@ -481,7 +589,6 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     }
     if (io.nflags > (uint32_t)kMaxDest || a.ndest + io.nx > (uint32_t)kMaxDest)
         return fail(EMESH_ECONFIG, "too many quantizer destinations");
-    if (a.ndest + io.nx == 0) return fail(EMESH_ECONFIG, "quantizer without a destination");
     for (uint32_t d = 0; d < io.nx; ++d) {
         a.dcodes[a.ndest] = io.x_codes[d];
         a.dcb[a.ndest] = io.x_cb[d];
@@ -489,23 +596,25 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     }
     for (uint32_t f = 0; f < io.nflags; ++f) a.sflag[f] = io.flags[f];
     a.nflag = io.nflags;
+    if (a.ndest == 0) return fail(EMESH_ECONFIG, "quantizer without a destination");
     a.in_flag = io.in_flag;
     a.epoch = io.epoch;
     a.timeout_ns = tr ? tr->timeout_ns : 30ull * 1000000000ull;
     a.stats = io.stats;
-    a.leaf = ws.leaf_stat;
-    a.blk_leaf = ws.blk_leaf;
+    a.leaf_stat = ws.leaf_stat;
     a.acc = ws.acc;
     a.seg_flags = ws.seg_flags;
     a.err = ws.err;
+    a.runs = bt.d_runs;
+    a.nruns = bt.nruns;
+    a.ntasks = bt.ntasks;
     a.sync = ws.sync;
-    a.ovf = ws.ovf;
     for (uint32_t d = 0; d < a.ndest; ++d) a.dhdr[d] = io.hdr_out[d];
     a.in_hdr = io.in_hdr;
     a.hdr = io.hdr;
     a.phase_out = io.phase_out;
     a.culprit_in = io.culprit_in;
-    CU(cudaMemsetAsync(ws.sync, 0, (kSyncReady + kSyPerSeg * (size_t)bt.nseg + bt.nblocks) * sizeof(uint32_t), st));
+    CU(cudaMemsetAsync(ws.sync, 0, (kSyncReady + 3 * (size_t)bt.nseg) * sizeof(uint32_t), st));
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
     void* args[] = {&a};
@@ -519,24 +628,17 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
         case kSrcAminusB | kHasIn | kDivK: fn = (const void*)k_quant<kSrcAminusB | kHasIn | kDivK>; break;
         default: return fail(EMESH_ECONFIG, "unsupported producer %d", io.src);
     }
-    {
-        static std::mutex mu;
-        static std::vector<const void*> configured;
-        std::lock_guard<std::mutex> g(mu);
-        if (std::find(configured.begin(), configured.end(), fn) == configured.end()) {
-            CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQ2SmemBytes));
-            configured.push_back(fn);
-        }
-    }
-    // A plain launch suffices: a CTA waits only when every STATS tile is
-    // claimed (quant.cuh), so progress never depends on co-residency.
-    const int sms = sm_count();
-    int grid = std::max(1, sms - (int)std::min<uint32_t>(reserve_sms, (uint32_t)sms - 1));
-    grid = std::min<int>(grid, (int)((bt.nunits + kQWarps * kQuad - 1) / (kQWarps * kQuad)));
+    // A plain launch suffices: a task is claimed only by a running CTA and only
+    // ever waits on tasks claimed before it, so progress never depends on
+    // co-residency. `reserve` CTA slots stay free for NCCL's kernels so the
+    // ring's transfers overlap this kernel.
+    int grid = persistent_grid(fn, bt.ntasks);
+    if (grid <= 0) return fail(EMESH_ECUDA, "k_quant: occupancy query failed");
+    grid = std::max(1, grid - (int)reserve_ctas);
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(grid);
-    lc.blockDim = dim3(kQThreads);
-    lc.dynamicSmemBytes = kQ2SmemBytes;
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = kQuantSmemBytes;
     lc.stream = st;
     CU(cudaLaunchKernelExC(&lc, fn, args));
     if (tr) tr->launches += 1;
@@ -626,7 +728,7 @@ int emesh_quantize_segments(const float* x, const uint64_t* seg_lo, const uint64
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     std::lock_guard<std::mutex> g(g_codec_mu);
     Plan p = make_list_plan(seg_lo, seg_len, nseg);
-    TRY(g_codec_ws.reserve(p.max_oct, p.max_units, p.max_blocks, p.max_segs));
+    TRY(g_codec_ws.reserve(p.max_slots, p.max_cta, p.max_segs));
     // stream-ordered tables + stats (freed in stream order)
     void* d_tables = nullptr;
     SegStat* d_stats = nullptr;
@@ -864,7 +966,7 @@ int engine_alloc(emesh_engine* e) {
         e->pay.assign(e->workers, nullptr);
         for (auto& p : e->pay) CU(cudaMalloc(&p, n * sizeof(float) + 16));
     }
-    TRY(e->ws.reserve(e->plan.max_oct, e->plan.max_units, e->plan.max_blocks, e->plan.max_segs));
+    TRY(e->ws.reserve(e->plan.max_slots, e->plan.max_cta, e->plan.max_segs));
     return EMESH_OK;
 }
 
@@ -1868,7 +1970,7 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
             e->plan.release();
             e->plan = mkplan(nccl_window);
             e->windows = (uint32_t)e->plan.batches[0].size();
-            if ((rc = e->plan.upload()) || (rc = e->ws.reserve(e->plan.max_oct, e->plan.max_units, e->plan.max_blocks, e->plan.max_segs)))
+            if ((rc = e->plan.upload()) || (rc = e->ws.reserve(e->plan.max_slots, e->plan.max_cta, e->plan.max_segs)))
                 return bail(rc);
             e->schedule = build_schedule(e->plan, e->rank);
             for (auto ev : e->ev_send) cudaEventDestroy(ev);

@@ -71,27 +71,22 @@ constexpr uint32_t kFlagNonFinite = 1u;
 constexpr uint32_t kFlagDegenerate = 2u;  // sigma == 0 (quant.hpp:49-55)
 
 
-// One segment of a batch (host-built, device-resident). Two work grids over
-// the same elements: the quantizer's (octets of 8 floats, 1024-element warp
-// units on the 32-byte grid, 16-unit tiles; quant.cuh) and the elementwise
-// kernels' (float4 slots, 1024-element units, `upw` units per warp-CTA tile).
+// One segment of a batch (host-built, device-resident). CTA-aligned: the
+// segment's work is ncta consecutive tiles of kWarps * upw warp units; a
+// warp unit is 256 float4 slots (1024 elements) of the arena's float4 grid.
 struct SegInfo {
     uint64_t lo;        // absolute element offset in the arena
     uint64_t len;       // elements
-    uint64_t q0;        // lo >> 2: first float4 slot (elementwise kernels)
-    uint64_t o0;        // lo >> 3: first octet (quantizer)
-    uint64_t so0;       // the segment's first octet in the batch's overflow scratch (whole units)
-    uint32_t nunits;    // float4-grid units (elementwise kernels)
-    uint32_t cta0;      // first elementwise tile (batch-relative)
-    uint32_t ncta;      // elementwise tiles
-    uint32_t nu8;       // octet-grid warp units (quantizer)
-    uint32_t u0;        // first quantizer unit (batch-relative): leaf / overflow list index
-    uint32_t b0;        // first quantizer leaf block (batch-relative)
-    uint32_t nblk;      // quantizer leaf blocks (64 units each)
+    uint64_t q0;        // lo >> 2: first float4 slot
+    uint64_t sq0;       // the segment's first float4 slot in the batch's scratch (whole units)
+    uint32_t nunits;    // warp units (1024-element float4-grid spans)
+    uint32_t cta0;      // first tile (batch-relative): leaf_stat index
+    uint32_t ncta;      // tiles
     uint32_t slot;      // global segment slot (stats / codebook index)
     uint32_t in_slot;   // slot of the incoming payload's codebook (== slot)
-    uint32_t upw;       // elementwise warp units per tile (one value per batch)
+    uint32_t upw;       // warp units per tile (1, 2 or 4; one value per batch)
     uint32_t chunk;     // ring chunk of the segment (ChunkMsg header)
+    uint32_t pad_;
 };
 constexpr uint32_t kSyncReady = 32;  // first per-segment word of a launch's sync array
 

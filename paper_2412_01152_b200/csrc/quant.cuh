@@ -1,509 +1,293 @@
-// Segment-resident quantizer (k_quant): the reference's quantize
+// Persistent two-pass quantizer (k_quant): the reference's quantize
 // (proj/include/emesh/quant.hpp:28-87) over every segment of one ring batch,
 // with its producer fused in (pseudo-gradient optim.hpp:108, ring hop add
-// allreduce.hpp:422, owner mean :435-439).
-//
-// quantize is two passes over a segment: the statistics (mu, sigma over ALL
-// of the segment, quant.hpp:33-43) before any bucket can be assigned
-// (:57-76). The value being quantized, x, is produced by the first pass and
-// consumed by the second. At the benchmarked shapes a segment is 15.6M-16M
-// elements (62.5 MB of x) — twice the GPU's shared memory — so round 1 kept x
-// in an L2/HBM scratch and paid 8 B/element of DRAM for it. Here x stays ON
-// CHIP: the warp that produced a unit of x parks it in its share of the SM's
-// tensor memory (4 units) or shared memory (1 unit) until the segment's
-// statistics are final, then bins it itself. Only units beyond a warp's
-// on-chip capacity go to a global scratch (an overflow any warp may bin).
-//
-// Every warp is an independent worker (no block barriers in the steady
-// state): it claims 4-unit quads of the batch in segment order, and per
-// unit issues the STATS loads, bins one ready unit of its own while they fly
-// (pure compute on on-chip x), then finishes the STATS unit. A warp only
-// ever waits (for a segment's statistics) when no unit is left to claim, so
-// progress never depends on co-residency (a plain launch suffices).
-//
-// Statistics stay deterministic under dynamic claiming: every unit writes its
-// own moment leaf; the last unit of each fixed 64-unit block merges the
-// block's leaves in index order, the last block of the segment merges the
-// blocks in order and publishes the segment (mu, sigma, lo/hi/width,
-// the exact threshold table and bucket encodings). Bucket sums are exact
-// integers (order-free). Codes, codebooks and everything after them are
-// therefore independent of the schedule.
-//
-// Element layout of a warp unit: 128 octets (8 floats = 32 B) of the arena's
-// octet grid; lane l at step j (0..3) owns octet o0 + 128 u + 32 j + l, so one
-// warp instruction moves 1 KB contiguous (256-bit LDG/STG, sm_100). The
-// lane's 32 values x[8 j + e] are one tcgen05 32x32b row of its TMEM lane.
+// allreduce.hpp:422, owner mean :435-439). STATS tiles compute the value x
+// and its moments and park x in a per-batch scratch; once a segment's
+// statistics are published, BIN tiles re-read x and assign codes + exact
+// bucket sums. See DESIGN.md §3 for the numerics and §7 for the on-chip
+// (tensor-memory) variants measured in round 2.
 #pragma once
 
 #include "kernels.cuh"
 
 namespace emesh_b200 {
 
-constexpr int kQWarps = 16;
-constexpr int kQThreads = kQWarps * 32;  // 512: one CTA per SM
-constexpr int kWTmemSlots = 4;           // units per warp in tensor memory (its 128-column share)
-constexpr int kWSmemSlots = 1;           // units per warp in shared memory
-constexpr int kWSlots = kWTmemSlots + kWSmemSlots;
-constexpr uint32_t kSlotGlobal = 0xffu;
-constexpr int kUnitOct = 128;            // octets per warp unit (1024 elements)
-constexpr int kQuad = 4;                 // units per claim
-constexpr int kBlkUnits = 64;            // units per leaf block (deterministic two-level merge)
-constexpr int kWFlushUnits = 4;          // BIN units per histogram flush
-constexpr uint32_t kNone = 0xffffffffu;
+constexpr int kQuantMinBlocks = 3;  // co-resident quantizer CTAs per SM (80 registers)
+constexpr int kUnitsPerWarp = 4;    // warp units per tile task (large batches; SegInfo::upw)
+// Bin-pass limbs (32-bit smem atomics per warp over one tile, see bin_unit):
+// A = r[0:kLoBits) | 1 << kCntShift, B = r[kLoBits:kMidEnd), C = r[kMidEnd:42).
+// With m = 1024 kUnitsPerWarp members: m (2^kLoBits - 1) < 2^kCntShift,
+// m < 2^(32 - kCntShift), m 2^(kMidEnd - kLoBits) <= 2^32, m 2^(42 - kMidEnd) < 2^32.
+constexpr int kLoBits = 7;
+constexpr int kCntShift = 19;
+constexpr int kMidEnd = 26;
+// The tile shape (kWarps * upw units: 32K, 16K or 8K elements) is chosen per
+// batch at run time (SegInfo::upw, Plan::add_batch): the limb layout above is
+// sized for the largest tile and stays exact for a smaller one (its bounds cap m).
 
-// Bin-pass limbs of a warp's histogram over <= kWFlushUnits units (4096 members):
-// A = r[0:8) | 1 << 20 (count), B = r[8:28), C = r[28:42) (rare).
-// 4096 * 255 < 2^20; 4096 < 2^12; 4096 * (2^20 - 1) < 2^32; 4096 * (2^14 - 1) < 2^32.
-constexpr int kWLoBits = 8, kWCntShift = 20, kWMidEnd = 28;
-
-// Per-segment sync words of one launch (zeroed per launch): base kSyncReady + 5 s; the
-// leaf-block arrival counters follow at kSyncReady + 5 nseg.
-enum : uint32_t { kSyReady = 0, kSyBlocks = 1, kSyBins = 2, kSyOvfCount = 3, kSyOvfClaim = 4, kSyPerSeg = 5 };
-
-struct Q2Args {
+struct QuantArgs {
     const SegInfo* segs;
-    const uint32_t* seg_u0;    // [nseg + 1] first unit of each segment (batch-relative, segment-major)
+    const uint32_t* cta_seg;   // CTA -> batch-local segment
+    uint32_t ncta;
     uint32_t nseg;
-    uint32_t nunits;           // units of the batch
     const float* a;
     const float* b;
     const uint8_t* in_codes;
     const float* in_cb;
     float divisor;
-    float inv_divisor;  // 1/k when k is a power of two (exact), else 0
-    float* scratch;     // overflow x, octet-addressed: segment s at octets [so0, so0 + nu8 * 128)
+    float inv_divisor;         // 1/k when k is a power of two (exact), else 0
+    float* scratch;            // x of the batch; segment s at float4 slots [sq0, sq0 + slots)
+    // output destinations (peer transport: the successor's arena); after a
+    // segment's codes + codebook are stored everywhere, store `epoch` to
+    // sflag[f][slot] for every flag f (the successor's arrival flags, or
+    // every rank's for the owner's final payload)
     uint8_t* dcodes[kMaxDest];
     float* dcb[kMaxDest];
     uint32_t ndest;
     uint32_t* sflag[kMaxDest];
     uint32_t nflag;
-    const uint32_t* in_flag;
+    const uint32_t* in_flag;   // peer transport: in_codes / in_cb of slot s valid once in_flag[s] >= epoch
     uint32_t epoch;
-    unsigned long long timeout_ns;
-    SegStat* stats;     // by slot
-    StatP* leaf;        // by unit
-    StatP* blk_leaf;    // by leaf block
-    SegAcc* acc;        // by batch-local segment (self-cleaning)
-    uint32_t* seg_flags;
-    uint32_t* err;
-    uint32_t* sync;     // [0] quad claim counter; per segment kSyPerSeg words from kSyncReady; block counters
-    uint32_t* ovf;      // overflow unit lists: segment s's at [u0, u0 + nu8)
+    unsigned long long timeout_ns;  // peer-wait budget (spin_until_ge_sys)
+    SegStat* stats;            // indexed by slot
+    StatP* leaf_stat;          // [tile]
+    SegAcc* acc;               // [seg] bucket histograms (batch-local segment)
+    uint32_t* seg_flags;       // [seg] non-finite bits (reset by the stats root)
+    uint32_t* err;             // sticky error word (bit 0: non-finite)
+    uint32_t* sync;            // see kSyncReady (zeroed per launch)
+    const uint4* runs;         // task order as runs {first task, kind, segment, first tile}
+    uint32_t nruns, ntasks;
     // peer transport: ChunkMsg headers written next to every payload / checked on receipt
     ChunkHdr* dhdr[kMaxDest];
     const ChunkHdr* in_hdr;
     HdrRef hdr;
-    uint32_t phase_out;  // kPhaseRS, or kPhaseAG for the owner's final payload
-    uint32_t culprit_in; // rank that owes the incoming payloads (the predecessor)
+    uint32_t phase_out;        // kPhaseRS, or kPhaseAG for the owner's final payload
+    uint32_t culprit_in;       // rank that owes the incoming payloads (the predecessor)
 };
 
-struct QHeld {
-    uint32_t seg, unit, slot;  // unit: within the segment
-};
-
-// One warp's shared memory (private: no cross-warp coordination).
-struct WSm {
-    double2 bsk[kBuckets];                 // BIN: per bucket {s, K}: fixed point m = x * s + K (kInfoWide)
-    uint32_t hist[kBuckets + 1][3];        // BIN: limbs over <= kWFlushUnits units; row 256: sink
-    float thr[kBuckets + 2];               // BIN: exact thresholds; [256] = +inf, [257] = lo_up
-    float lut[kBuckets];                   // STATS: incoming codebook (hop add)
-    float bp[6];                           // BIN params: c, inv_w, lo_up, hi_dn, margin, 1 - margin
-    uint32_t degenerate;
-    int32_t lut_seg, bin_seg, hist_seg;
-    uint32_t hist_units, clip_lo, clip_hi;
-    uint32_t qh, qn, freemask;
-    QHeld q[kWSlots];
-    float4 x[kWSmemSlots][256];            // on-chip x slot(s) in shared memory
-};
-constexpr uint32_t kMaxSegCache = 512;     // seg_u0 cached in shared memory when it fits
-struct QCta {
-    uint32_t tbase;                        // TMEM base address
-    uint32_t seg_u0[kMaxSegCache + 1];
-};
-constexpr size_t kQ2SmemBytes = ((sizeof(QCta) + 15) & ~size_t(15)) + kQWarps * ((sizeof(WSm) + 15) & ~size_t(15));
-
-// ---------------------------------------------------------------------------
-// memory helpers
-
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&x)[32]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
-        "f"(x[0]), "f"(x[1]), "f"(x[2]), "f"(x[3]), "f"(x[4]), "f"(x[5]), "f"(x[6]), "f"(x[7]), "f"(x[8]), "f"(x[9]),
-        "f"(x[10]), "f"(x[11]), "f"(x[12]), "f"(x[13]), "f"(x[14]), "f"(x[15]), "f"(x[16]), "f"(x[17]), "f"(x[18]),
-        "f"(x[19]), "f"(x[20]), "f"(x[21]), "f"(x[22]), "f"(x[23]), "f"(x[24]), "f"(x[25]), "f"(x[26]), "f"(x[27]),
-        "f"(x[28]), "f"(x[29]), "f"(x[30]), "f"(x[31])
-        : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&x)[32]) {
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-        : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]), "=f"(x[6]), "=f"(x[7]), "=f"(x[8]),
-          "=f"(x[9]), "=f"(x[10]), "=f"(x[11]), "=f"(x[12]), "=f"(x[13]), "=f"(x[14]), "=f"(x[15]), "=f"(x[16]),
-          "=f"(x[17]), "=f"(x[18]), "=f"(x[19]), "=f"(x[20]), "=f"(x[21]), "=f"(x[22]), "=f"(x[23]), "=f"(x[24]),
-          "=f"(x[25]), "=f"(x[26]), "=f"(x[27]), "=f"(x[28]), "=f"(x[29]), "=f"(x[30]), "=f"(x[31])
-        : "r"(taddr)
-        : "memory");
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 
 
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* x) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15, %16};" ::"r"(taddr),
-        "f"(x[0]), "f"(x[1]), "f"(x[2]), "f"(x[3]), "f"(x[4]), "f"(x[5]), "f"(x[6]), "f"(x[7]), "f"(x[8]), "f"(x[9]),
-        "f"(x[10]), "f"(x[11]), "f"(x[12]), "f"(x[13]), "f"(x[14]), "f"(x[15])
-        : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* x) {
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, "
-        "[%16];"
-        : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]), "=f"(x[6]), "=f"(x[7]), "=f"(x[8]),
-          "=f"(x[9]), "=f"(x[10]), "=f"(x[11]), "=f"(x[12]), "=f"(x[13]), "=f"(x[14]), "=f"(x[15])
-        : "r"(taddr)
-        : "memory");
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-
-// 256-bit streaming loads (read once: L1 no-allocate, L2 evict-first)
-__device__ __forceinline__ void ld8_stream(const float* p, float* v) {
-    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
-                 : "l"(p));
-}
-// incoming codes of one octet (the predecessor may have written them during this launch's
-// lifetime only under the peer transport, and then before its flag: not .nc)
-__device__ __forceinline__ uint2 ld8_codes(const uint8_t* p) {
-    uint2 v;
-    asm volatile("ld.global.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+// Streaming (read-once) loads: no L1 allocation, leaving L1 to the BIN
+// pass's scratch prefetch.
+__device__ __forceinline__ float4 ld4_stream(const float* p, uint64_t q) {
+    float4 v;
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(reinterpret_cast<const float4*>(p) + q));
     return v;
 }
-__device__ __forceinline__ void st8_f32(float* p, const float* v) {
-    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
-                 "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
-                 : "memory");
-}
-__device__ __forceinline__ void ld8_f32(const float* p, float* v) {
-    asm volatile("ld.global.cg.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
-                 : "l"(p)
-                 : "memory");
-}
-
-
-// smem histogram add with no compiler memory barrier: ordered against other
-// shared-memory traffic by the block barriers around the tile only
-__device__ __forceinline__ void red_shared_add_relaxed(uint32_t* p, uint32_t v) {
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v));
-}
-__device__ __forceinline__ void red_shared_add_nz_relaxed(uint32_t* p, uint32_t v) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q red.shared.add.u32 [%0], %1;\n\t}" ::"r"(
-                     (uint32_t)__cvta_generic_to_shared(p)),
-                 "r"(v));
-}
-
-
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ uint32_t bcast(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
-
-// Where a unit's x lives between its STATS and BIN passes.
-struct QSlotRef {
-    uint32_t slot;    // < kWTmemSlots: TMEM; < kWSlots: smem; kSlotGlobal: overflow scratch
-    uint32_t taddr;   // TMEM address of the unit's 32 columns
-    float4* sp;       // smem unit (256 float4: [j][lane] low half, [j][32 + lane] high half)
-    float* gp;        // overflow scratch of the segment, arena-indexed by element
-};
-
-__device__ __forceinline__ QSlotRef q2_slot(const Q2Args& a, uint32_t tbase, WSm& ws, const SegInfo& si,
-                                            uint32_t slot) {
-    const int warp = threadIdx.x >> 5;
-    QSlotRef r;
-    r.slot = slot;
-    r.taddr = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 128u * (uint32_t)(warp >> 2) + 32u * (slot & 3u);
-    r.sp = ws.x[0];
-    r.gp = a.scratch + ((int64_t)si.so0 - (int64_t)si.o0) * 8;
-    return r;
-}
-
-// x of octets j = 2h, 2h + 1 (16 values per lane) into / out of the slot
-__device__ __forceinline__ void q2_put_half(const QSlotRef& r, uint64_t obase, int h, const float* x) {
-    const int lane = threadIdx.x & 31;
-    if (r.slot < kWTmemSlots) {
-        tmem_st16(r.taddr + 16u * (uint32_t)h, x);
-    } else if (r.slot < kWSlots) {
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-            const int j = 2 * h + jj;
-            r.sp[j * 64 + lane] = make_float4(x[8 * jj], x[8 * jj + 1], x[8 * jj + 2], x[8 * jj + 3]);
-            r.sp[j * 64 + 32 + lane] = make_float4(x[8 * jj + 4], x[8 * jj + 5], x[8 * jj + 6], x[8 * jj + 7]);
-        }
-    } else {
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) st8_f32(r.gp + (obase + (uint64_t)(2 * h + jj) * 32 + lane) * 8, &x[8 * jj]);
-    }
-}
-__device__ __forceinline__ void q2_get_half(const QSlotRef& r, uint64_t obase, int h, float* x) {
-    const int lane = threadIdx.x & 31;
-    if (r.slot < kWTmemSlots) {
-        tmem_ld16(r.taddr + 16u * (uint32_t)h, x);
-    } else if (r.slot < kWSlots) {
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-            const int j = 2 * h + jj;
-            const float4 v0 = r.sp[j * 64 + lane], v1 = r.sp[j * 64 + 32 + lane];
-            x[8 * jj] = v0.x; x[8 * jj + 1] = v0.y; x[8 * jj + 2] = v0.z; x[8 * jj + 3] = v0.w;
-            x[8 * jj + 4] = v1.x; x[8 * jj + 5] = v1.y; x[8 * jj + 6] = v1.z; x[8 * jj + 7] = v1.w;
-        }
-    } else {
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) ld8_f32(r.gp + (obase + (uint64_t)(2 * h + jj) * 32 + lane) * 8, &x[8 * jj]);
-    }
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) { return __ldcs(p); }
+__device__ __forceinline__ float4 ld4(const float* p, uint64_t q) {
+    return __ldg(reinterpret_cast<const float4*>(p) + q);
 }
 
 // ---------------------------------------------------------------------------
-// STATS: the fused producer (PG / hop add / owner mean) + per-lane moments
+// Persistent quantizer: one launch per batch (pipelining window), a grid of
+// co-resident CTAs that claim tile tasks in plan order (one atomicAdd each).
 
-// Per-lane moments around a pivot (its first in-segment value), fp64.
-struct QMoments {
-    double s0, s1, d0, d1, q0, q1, piv;
-    uint32_t cnt;
-    bool have;
+struct __align__(16) QSmem {
+    uint32_t hist[kWarps][kBuckets + 1][3];  // per-warp limbs over the tile (bin), see bin_unit; row 256: sink
+    uint2 bsk[2 * kBuckets];             // per bucket {high word of s, high word of K} (bin), twice:
+                                         // index code | 256 = same bucket (see kInfoWide)
+    float thr[kBuckets + 2];             // exact threshold table (bin); [257] = bucket 0's base (lo_up)
+    float lut[kBuckets];                 // incoming codebook (stats, hop)
+    StatP wp[kWarps];
+    double red[2];
+    uint32_t clip[2];
+    uint32_t flag;
+    uint32_t task;
+    int32_t bin_seg, lut_seg, ready_seg;
+    uint32_t run_idx;
 };
 
-template <int SRC>
-struct QLoads {
-    float a[16];
-    float b[(SRC & kSrcAminusB) ? 16 : 1];
-    uint2 c[2];
-};
+// Task order (host-built run table, QuantArgs::runs): the STATS tiles of
+// the batch in segment order; the BIN tiles of segment s once `lag` more
+// tasks were issued after its last STATS tile (lag ~ 1.5 grids: the segment's
+// statistics are normally published before its bins are claimed, and a
+// tile's scratch x is re-read soon enough to still be in L2). The last STATS
+// tile of s to finish finalizes SegStat(s); the last BIN tile of s to finish
+// writes its codebook. A BIN task only waits (at the top of the loop, owing
+// nothing) on STATS tiles claimed before it, so the grid always progresses
+// whatever the co-residency.
+// sync layout: [0] task counter, [kSyncReady + s] SegStat(s) published,
+// [kSyncReady + nseg + s] STATS tiles done, [kSyncReady + 2 nseg + s] BIN tiles done.
+enum : uint32_t { kTaskStats = 0, kTaskBin = 2 };
+// mixed run (alternating STATS / BIN tasks): y = kTaskMix{Rev,Fwd} | bin segment << 2,
+// z = STATS segment, w = first STATS tile | first BIN tile << 16
+constexpr uint32_t kTaskMixRev = 1, kTaskMixFwd = 3;
+constexpr uint32_t kMaxRunsSmem = 512;  // run table cached in smem when it fits (8 KB)
+constexpr uint32_t kMaxSegsSmem = 128;  // SegInfo cached in smem when it fits (6 KB)
+
+
+
+__device__ void finalize_stats(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si);
+
+// Scratch x (written by STATS, read once by BIN, then discarded).
+__device__ __forceinline__ void st_scratch(float4* p, float4 v) { *p = v; }
 
 template <int SRC>
-__device__ __forceinline__ void q2_stats_load(const Q2Args& a, uint64_t obase, uint64_t hiel, bool interior, int h,
-                                              QLoads<SRC>& L) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int jj = 0; jj < 2; ++jj) {
-        const uint64_t o = obase + (uint64_t)(2 * h + jj) * 32 + lane;
-        if (interior || o * 8 < hiel) {  // octets past the segment end are not loaded
-            ld8_stream(a.a + o * 8, &L.a[8 * jj]);
-            if (SRC & kSrcAminusB) ld8_stream(a.b + o * 8, &L.b[8 * jj]);
-            if (SRC & kHasIn) L.c[jj] = ld8_codes(a.in_codes + o * 8);
-        } else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                L.a[8 * jj + e] = 0.f;
-                if (SRC & kSrcAminusB) L.b[8 * jj + e] = 0.f;
+__device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si,
+                                           uint32_t tile) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t hiel = si.lo + si.len;     // exclusive
+    float4* xs = reinterpret_cast<float4*>(a.scratch) + ((int64_t)si.sq0 - (int64_t)si.q0);
+
+    if (SRC & kHasIn) {
+        if (sm.lut_seg != (int32_t)s) {
+            __syncthreads();
+            if (a.in_flag) {  // peer transport: the predecessor's payload of s must have landed intact
+                if (threadIdx.x == 0 &&
+                    spin_until_ge_sys(a.in_flag + si.in_slot, a.epoch, a.err, a.timeout_ns, a.culprit_in) &&
+                    a.in_hdr)
+                    check_hdr(a.in_hdr + si.in_slot, a.hdr, si.chunk, (uint32_t)si.len, kPhaseRS, a.err,
+                              a.culprit_in);
+                __syncthreads();
             }
-            L.c[jj] = make_uint2(0u, 0u);
+            sm.lut[threadIdx.x] = __ldcg(a.in_cb + (uint64_t)si.in_slot * kBuckets + threadIdx.x);
+            __syncthreads();
+            if (threadIdx.x == 0) sm.lut_seg = (int32_t)s;
         }
     }
-}
-
-// x = producer(loads) in place (L.a), accumulated into the lane's moments.
-template <int SRC>
-__device__ __forceinline__ void q2_stats_finish(const Q2Args& a, const WSm& sm, const SegInfo& si, uint64_t obase,
-                                                bool interior, int h, QLoads<SRC>& L, QMoments& m) {
-    const int lane = threadIdx.x & 31;
+    StatP p{0.0, 0.0, 0.0, 0.0, 0};
+    double sum0 = 0.0, sum1 = 0.0, d0 = 0.0, d1 = 0.0, q0 = 0.0, q1 = 0.0;
+    double piv = 0.0;
+    uint32_t cnt = 0;
+    bool have_piv = false;
+    for (int ui = 0; ui < (int)si.upw; ++ui) {
+        const uint32_t u = (tile * si.upw + ui) * kWarps + warp;  // segment-relative unit
+        if (u >= si.nunits) break;
+        const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
+        const bool interior = qbase * 4 >= si.lo && (qbase + kUnitSlots) * 4 <= hiel;  // warp-uniform
+        constexpr int kHalf = kSlotsPerLane / 2;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        float v = L.a[i];
-        if (SRC & kSrcAminusB) v = __fsub_rn(v, L.b[i]);  // optim.hpp:108
-        if (SRC & kHasIn) {                                // allreduce.hpp:422
-            const uint32_t w = (i & 7) < 4 ? L.c[i >> 3].x : L.c[i >> 3].y;
-            v = __fadd_rn(v, sm.lut[(w >> (8 * (i & 3))) & 0xffu]);
-        }
-        if (SRC & kDivK) v = a.inv_divisor != 0.f ? __fmul_rn(v, a.inv_divisor) : __fdiv_rn(v, a.divisor);  // :439
-        L.a[i] = v;
-    }
-#ifdef EMESH_Q_ABL_NOMOM  // ablation (timing only): no fp64 moments
-    if (true) {
-        m.s0 = __dadd_rn(m.s0, (double)(L.a[0] + L.a[15]));
-        m.cnt += 16;
-        return;
-    }
-#endif
-    if (interior) {
-        if (!m.have) {
-            m.piv = (double)L.a[0];
-            m.have = true;
-        }
+        for (int h = 0; h < 2; ++h) {
+            float4 xa[kHalf], xb[kHalf];
+            uint32_t c4[kHalf];
 #pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-            const double x0 = (double)L.a[i], x1 = (double)L.a[i + 1];
-            const double v0 = __dsub_rn(x0, m.piv), v1 = __dsub_rn(x1, m.piv);
-            m.s0 = __dadd_rn(m.s0, x0);
-            m.s1 = __dadd_rn(m.s1, x1);
-            m.d0 = __dadd_rn(m.d0, v0);
-            m.d1 = __dadd_rn(m.d1, v1);
-            m.q0 = __fma_rn(v0, v0, m.q0);
-            m.q1 = __fma_rn(v1, v1, m.q1);
-        }
-        m.cnt += 16;
-    } else {
-        const uint64_t hiel = si.lo + si.len;
+            for (int jj = 0; jj < kHalf; ++jj) {
+                const uint64_t q = qbase + (uint64_t)(h * kHalf + jj) * 32 + lane;
+                const bool in = interior || q * 4 < hiel;
+                xa[jj] = in ? ld4_stream(a.a, q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                if (SRC & kSrcAminusB) xb[jj] = in ? ld4_stream(a.b, q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                if (SRC & kHasIn) c4[jj] = in ? ld_stream_u32(reinterpret_cast<const uint32_t*>(a.in_codes) + q) : 0u;
+            }
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-            const uint64_t e0 = (obase + (uint64_t)(2 * h + jj) * 32 + lane) * 8;
+            for (int jj = 0; jj < kHalf; ++jj) {
+                const uint64_t q = qbase + (uint64_t)(h * kHalf + jj) * 32 + lane;
+                const uint64_t e0 = q * 4;
+                float x[4] = {xa[jj].x, xa[jj].y, xa[jj].z, xa[jj].w};
+                if (SRC & kSrcAminusB) {
+                    x[0] = __fsub_rn(x[0], xb[jj].x); x[1] = __fsub_rn(x[1], xb[jj].y);
+                    x[2] = __fsub_rn(x[2], xb[jj].z); x[3] = __fsub_rn(x[3], xb[jj].w);
+                }
+                if (SRC & kHasIn) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                if (e0 + e >= si.lo && e0 + e < hiel) {
-                    const double xd = (double)L.a[8 * jj + e];
-                    if (!m.have) {
-                        m.piv = xd;
-                        m.have = true;
+                    for (int e = 0; e < 4; ++e) x[e] = __fadd_rn(x[e], sm.lut[(c4[jj] >> (8 * e)) & 0xff]);
+                }
+                if (SRC & kDivK) {
+                    // x / k (allreduce.hpp:439): exact multiply for a power-of-two k
+                    if (a.inv_divisor != 0.f) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) x[e] = __fmul_rn(x[e], a.inv_divisor);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) x[e] = __fdiv_rn(x[e], a.divisor);
                     }
-                    const double dv = __dsub_rn(xd, m.piv);
-                    m.s0 = __dadd_rn(m.s0, xd);
-                    m.d0 = __dadd_rn(m.d0, dv);
-                    m.q0 = __fma_rn(dv, dv, m.q0);
-                    m.cnt += 1;
+                }
+                if (interior && !have_piv) {  // pivot: the lane's first value
+                    piv = (double)x[0];
+                    have_piv = true;
+                }
+                if (interior) {
+                    const double x0 = (double)x[0], x1 = (double)x[1], x2 = (double)x[2], x3 = (double)x[3];
+                    const double v0 = __dsub_rn(x0, piv), v1 = __dsub_rn(x1, piv);
+                    const double v2 = __dsub_rn(x2, piv), v3 = __dsub_rn(x3, piv);
+                    sum0 = __dadd_rn(__dadd_rn(sum0, x0), x2);
+                    sum1 = __dadd_rn(__dadd_rn(sum1, x1), x3);
+                    d0 = __dadd_rn(__dadd_rn(d0, v0), v2);
+                    d1 = __dadd_rn(__dadd_rn(d1, v1), v3);
+                    // sigma is not bit-exact vs the sequential reference anyway:
+                    // fused multiply-adds for the squares
+                    q0 = __fma_rn(v2, v2, __fma_rn(v0, v0, q0));
+                    q1 = __fma_rn(v3, v3, __fma_rn(v1, v1, q1));
+                    if (SRC != kSrcA) st_scratch(xs + q, make_float4(x[0], x[1], x[2], x[3]));
+                } else {
+                    uint32_t vm = 0u;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) vm |= (e0 + e >= si.lo && e0 + e < hiel) ? (1u << e) : 0u;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        if (vm & (1u << e)) {
+                            const double xd = (double)x[e];
+                            if (!have_piv) { piv = xd; have_piv = true; }
+                            const double dv = __dsub_rn(xd, piv);
+                            sum0 = __dadd_rn(sum0, xd);
+                            d0 = __dadd_rn(d0, dv);
+                            q0 = __fma_rn(dv, dv, q0);
+                            cnt += 1;
+                            if (SRC != kSrcA) reinterpret_cast<float*>(xs + q)[e] = x[e];
+                        }
+                    }
                 }
             }
         }
+        if (interior) cnt += kSlotsPerLane * 4;  // per lane
     }
-}
-
-
-// ---------------------------------------------------------------------------
-// BIN (exact codes + exact bucket sums into the warp's histogram)
-
-// Bins one octet group of 8 values (codes + exact bucket sums).
-template <bool INTERIOR>
-__device__ __forceinline__ void q2_bin_octet(const Q2Args& a, WSm& sm, const float* xe, uint64_t o,
-                                             const SegInfo& si, uint32_t* hw, uint32_t& nclip_lo,
-                                             uint32_t& nclip_hi) {
-    const float c_f = sm.bp[0], inv_w = sm.bp[1], lo_up = sm.bp[2], hi_dn = sm.bp[3], margin = sm.bp[4],
-                one_m = sm.bp[5];
-    uint32_t vmask = 0xffu;
-    if (!INTERIOR) {
-        vmask = 0u;
-        const uint64_t hiel = si.lo + si.len;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) vmask |= (o * 8 + i >= si.lo && o * 8 + i < hiel) ? (1u << i) : 0u;
-    }
-    int cc[8];
-    bool okall = true;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        // in range and clear of every bucket edge by the proven margin: trunc(g)
-        // is the exact bucket (clipped x fails this test; see SegStat::margin)
-        const float g = __fmaf_rn(xe[i], inv_w, -c_f);
-        const int c = __float2int_rz(g);
-        const float fr = __fsub_rn(g, __int2float_rz(c));
-        okall &= (fr > margin) & (fr < one_m) & ((uint32_t)c < 256u);
-        cc[i] = c;
-    }
-    if (!INTERIOR) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) cc[i] |= ((vmask >> i) & 1u) ? 0 : 256;  // outside the segment: sink row
-    }
-    if (!okall) {  // rare: near an edge (exact table) or clipped (quant.hpp:66-67)
-        uint32_t clo_m = 0, chi_m = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float x = xe[i];
-            const float g = __fmaf_rn(x, inv_w, -c_f);
-            const int c0 = __float2int_rz(g);
-            const float fr = __fsub_rn(g, __int2float_rz(c0));
-            const int sink = cc[i] & 256;
-            if (x < lo_up) {
-                cc[i] = 256; clo_m |= 1u << i;
-            } else if (x > hi_dn) {
-                cc[i] = 256 | 255; chi_m |= 1u << i;
-            } else if (!(fr > margin && fr < one_m && (uint32_t)c0 < 256u)) {
-                cc[i] = sink | bucket_walk(x, min(max(c0, 0), 255), sm.thr);
-            }
-        }
-        nclip_lo += __popc(clo_m & vmask);
-        nclip_hi += __popc(chi_m & vmask);
-    }
-    // fixed point r of every member (kInfoWide): all 8 table loads first, then the fmas, then the
-    // limb atomics (no compiler memory barrier between them: they only touch the histogram)
-    double2 sk[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) sk[i] = sm.bsk[cc[i] & 255];
-    uint32_t rlo[8], rhi[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        // m = x * s + K in [2^52, 2^53): its mantissa is the member's fixed point r
-        const double m = __fma_rn((double)xe[i], sk[i].x, sk[i].y);
-        rlo[i] = (uint32_t)__double2loint(m);
-        rhi[i] = (uint32_t)__double2hiint(m);
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        uint32_t* hc = hw + 3 * min(cc[i], kBuckets);
-        red_shared_add_relaxed(hc, (rlo[i] & ((1u << kWLoBits) - 1u)) | (1u << kWCntShift));
-        red_shared_add_relaxed(hc + 1, (rlo[i] >> kWLoBits) & ((1u << (kWMidEnd - kWLoBits)) - 1u));
-        const uint32_t rc = __funnelshift_r(rlo[i], rhi[i], kWMidEnd) & ((1u << (42 - kWMidEnd)) - 1u);
-        red_shared_add_nz_relaxed(hc + 2, rc);  // predicated: the high limb is rarely nonzero
-    }
-    const uint32_t p0 = __byte_perm(__byte_perm(cc[0], cc[1], 0x0040), __byte_perm(cc[2], cc[3], 0x0040), 0x5410);
-    const uint32_t p1 = __byte_perm(__byte_perm(cc[4], cc[5], 0x0040), __byte_perm(cc[6], cc[7], 0x0040), 0x5410);
-    if (INTERIOR) {
-        *reinterpret_cast<uint2*>(a.dcodes[0] + o * 8) = make_uint2(p0, p1);
-        for (uint32_t d = 1; d < a.ndest; ++d) *reinterpret_cast<uint2*>(a.dcodes[d] + o * 8) = make_uint2(p0, p1);
-    } else {
-        for (uint32_t d = 0; d < a.ndest; ++d) {
-            uint8_t* oc = a.dcodes[d] + o * 8;
-            if (vmask == 0xffu) {
-                *reinterpret_cast<uint2*>(oc) = make_uint2(p0, p1);
-            } else if (vmask) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    if (vmask & (1u << e)) oc[e] = (uint8_t)((e < 4 ? p0 : p1) >> (8 * (e & 3)));
-            }
-        }
-    }
-}
-
-
-// ---------------------------------------------------------------------------
-// Segment statistics: leaves -> blocks -> segment (warp-level, fixed order)
-
-__device__ __forceinline__ StatP ldcg_statp(const StatP* src) {
-    StatP c;
-    c.s = __ldcg(&src->s); c.m2 = __ldcg(&src->m2); c.d = __ldcg(&src->d);
-    c.piv = __ldcg(&src->piv); c.n = __ldcg(&src->n);
-    return c;
-}
-// Fixed-order merge of n consecutive leaves by one warp: lane l merges leaves l, l+32, ... in
-// order, then the lanes merge in lane order (warp_merge). Deterministic for a given n.
-__device__ StatP warp_merge_range(const StatP* src, uint32_t n) {
-    const int lane = threadIdx.x & 31;
-    StatP p{0.0, 0.0, 0.0, 0.0, 0};
-    for (uint32_t i = lane; i < n; i += 32) p = statp_merge(p, ldcg_statp(src + i));
-    return warp_merge(p);
-}
-
-// Run by the warp whose block arrival completed segment s: mu / sigma / lo / hi / width
-// (quant.hpp:33-59), the exact threshold table and bucket encodings; publishes SegStat(s).
-__device__ void q2_finalize_stats(const Q2Args& a, uint32_t s, const SegInfo& si) {
-    const int lane = threadIdx.x & 31;
-    const StatP t = warp_merge_range(a.blk_leaf + si.b0, si.nblk);
-    double mu = 0.0, sigma = 0.0;
+    p = StatP{__dadd_rn(sum0, sum1), __dadd_rn(q0, q1), __dadd_rn(d0, d1), piv, (uint64_t)cnt};
+    p = warp_merge(p);
     if (lane == 0) {
-        mu = __ddiv_rn(t.s, (double)si.len);
+        sm.wp[warp] = p;
+        // finite fp32 inputs cannot overflow an fp64 sum: one check per unit
+        if (!isfinite(p.s) || !isfinite(p.m2)) {
+            atomicOr(&a.seg_flags[s], kFlagNonFinite);
+            atomicOr(a.err, kErrNonFinite);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        StatP t = sm.wp[0];
+        for (int w = 1; w < kWarps; ++w) t = statp_merge(t, sm.wp[w]);
+        a.leaf_stat[si.cta0 + tile] = t;
+        // acq_rel: publishes this leaf; the last tile to arrive acquires all
+        sm.flag = atom_add_acq_rel(&a.sync[kSyncReady + a.nseg + s], 1u) == si.ncta - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (sm.flag) finalize_stats(a, sm, s, si);
+}
+
+// Run by the last STATS tile of s to finish: combine the segment's leaves in
+// a fixed order (thread t: leaves t, t+256, ...; then warps; then the 8 warp
+// partials), finalize mu / sigma / lo / hi / width (quant.hpp:33-59), the
+// exact threshold table and the bucket parameters, and publish SegStat(s).
+__device__ void finalize_stats(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    StatP p{0.0, 0.0, 0.0, 0.0, 0};
+    for (uint32_t i = threadIdx.x; i < si.ncta; i += kThreads) {
+        const StatP* src = &a.leaf_stat[si.cta0 + i];
+        StatP ch;
+        ch.s = __ldcg(&src->s); ch.m2 = __ldcg(&src->m2); ch.d = __ldcg(&src->d);
+        ch.piv = __ldcg(&src->piv); ch.n = __ldcg(&src->n);
+        p = statp_merge(p, ch);
+    }
+    p = warp_merge(p);
+    if (lane == 0) sm.wp[warp] = p;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        StatP t = sm.wp[0];
+        for (int w = 1; w < kWarps; ++w) t = statp_merge(t, sm.wp[w]);
+        const double mu = __ddiv_rn(t.s, (double)si.len);
         const double dm = __dsub_rn(t.piv, mu);
         // sum (x - mu)^2 = M2 + 2 (p - mu) D + n (p - mu)^2
         double ss = __dadd_rn(t.m2, __dmul_rn(__dmul_rn(2.0, dm), t.d));
         ss = __dadd_rn(ss, __dmul_rn((double)t.n, __dmul_rn(dm, dm)));
         const double var = __ddiv_rn(ss < 0.0 ? 0.0 : ss, (double)si.len);
-        sigma = __dsqrt_rn(var);
+        sm.red[0] = mu;
+        sm.red[1] = __dsqrt_rn(var);
     }
-    mu = __shfl_sync(0xffffffffu, mu, 0);
-    sigma = __shfl_sync(0xffffffffu, sigma, 0);
+    __syncthreads();
+    const double mu = sm.red[0], sigma = sm.red[1];
     SegStat* st = &a.stats[si.slot];
-    if (lane == 0) {
+    if (threadIdx.x == 0) {
         st->mu = mu;
         st->sigma = sigma;
         st->flags = __ldcg(&a.seg_flags[s]) | (sigma == 0.0 ? kFlagDegenerate : 0u);
@@ -518,427 +302,410 @@ __device__ void q2_finalize_stats(const Q2Args& a, uint32_t s, const SegInfo& si
         const double lo = __dsub_rn(mu, six);
         const double hi = __dadd_rn(mu, six);
         const double w = __ddiv_rn(__dsub_rn(hi, lo), 256.0);
-        float lo_up = (float)lo;  // smallest fp32 >= lo, largest fp32 <= hi
+        // smallest fp32 >= lo, largest fp32 <= hi (clipping in fp32 terms)
+        float lo_up = (float)lo;
         if ((double)lo_up < lo) lo_up = key2f(f2key(lo_up) + 1);
         float hi_dn = (float)hi;
         if ((double)hi_dn > hi) hi_dn = key2f(f2key(hi_dn) - 1);
-        float thr[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int b = lane + 32 * i;
-            thr[i] = b == 0 ? lo_up : threshold(b, lo, hi, w);
-            st->thr[b] = b == 0 ? -INFINITY : thr[i];
-        }
-        // bucket b spans [thr[b], thr[b + 1]): the next threshold is lane + 1's (or the next row's)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int b = lane + 32 * i;
-            float nxt = __shfl_down_sync(0xffffffffu, thr[i], 1);
-            const float row_next = __shfl_sync(0xffffffffu, thr[i < 7 ? i + 1 : 7], 0);
-            if (lane == 31) nxt = i < 7 ? row_next : key2f(f2key(hi_dn) + 1);
-            st->binfo[b] = bucket_info(thr[i], nxt);
-        }
-        if (lane == 0) {
+        const int b = threadIdx.x;
+        sm.thr[b] = b == 0 ? lo_up : threshold(b, lo, hi, w);
+        if (b == 0) sm.thr[kBuckets] = key2f(f2key(hi_dn) + 1);
+        __syncthreads();
+        st->thr[b] = b == 0 ? -INFINITY : sm.thr[b];
+        st->binfo[b] = bucket_info(sm.thr[b], sm.thr[b + 1]);
+        if (b == 0) {
             st->lo = lo; st->hi = hi; st->width = w;
-            st->c_f = (float)__ddiv_rn(lo, w);
-            st->inv_w_f = (float)__ddiv_rn(1.0, w);
+            const float c_f = (float)__ddiv_rn(lo, w), inv_w = (float)__ddiv_rn(1.0, w);
+            st->c_f = c_f;
+            st->inv_w_f = inv_w;
             st->lo_up = lo_up;
             st->hi_dn = hi_dn;
-            // error of g = fma(x, inv_w, -c) (fp32) vs (x - lo) / w in buckets, for lo <= x <= hi:
-            // inv_w and c carry <= 2^-24 relative error each, the fma one rounding of |g| <= 256:
-            // err <= ((max(|lo|, |hi|) + |lo|) / w + 256) 2^-24; x2 for safety
+            // Error of g = fma(x, inv_w, -c) (fp32) vs (x - lo) / w, in buckets, for
+            // lo <= x <= hi: inv_w and c carry <= 2^-24 relative error each
+            // (|x| / w and |lo| / w terms), the fma one rounding of |g| <= 256:
+            // err <= ((max(|lo|, |hi|) + |lo|) / w + 256) 2^-24; x2 for safety.
             const double mag = __ddiv_rn(fmax(fabs(lo), fabs(hi)) + fabs(lo), w);
             const double err = __dmul_rn(__dadd_rn(mag, 256.0), 1.01 / 16777216.0);
             const double mg = __dmul_rn(2.0, err) + 1e-6;
-            st->margin = mg < 0.25 ? (float)mg : 2.0f;  // 2.0: always walk the table
+            st->margin = mg < 0.25 ? (float)mg : 2.0f;  // 2.0: always use the table
         }
     }
-    __syncwarp();
-    if (lane == 0) {
-        __threadfence();  // every lane's SegStat stores (observed through the warp barrier)
-        st_release(a.sync + kSyncReady + kSyPerSeg * s + kSyReady, 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        sm.bin_seg = -1;  // thr in smem now holds this segment's raw table: force a reload
+        st_release(&a.sync[kSyncReady + s], 1u);  // publish (cumulative over the CTA's SegStat writes)
     }
-    __syncwarp();
 }
 
-// A finished STATS unit (its leaf stored by lane 0): arrival on its leaf block; the unit that
-// completes a block merges it; the block that completes the segment finalizes the segment.
-__device__ void q2_stats_arrive(const Q2Args& a, uint32_t s, const SegInfo& si, uint32_t unit) {
+
+
+struct BinParams {
+    float c, inv_w, lo_up, hi_dn, margin, one_m;  // bucket estimate g = fma(x, inv_w, -c)
+};
+
+// One warp unit of the bin pass (1024 elements; this lane's 32), in groups of
+// 8: bucket estimates for all 8, rare fix-ups (exact table near an edge,
+// clipping), fixed-point codes via the fp32 fast path (fp64 for the few
+// buckets that need it), then the limb atomics — unconditional, so the
+// common path has no data-dependent branches (invalid lanes add 0).
+// Per-warp limbs over a tile (see kLoBits): A += low bits | one count,
+// B += middle bits, C += high bits (only when nonzero: rare).
+// BIN's scratch reads. The warp prefetches its
+// next unit's 4 KB of scratch into L1 while it bins the current one, and the
+// loads go through L1. Each scratch line belongs to exactly one segment
+// (segments own whole units of scratch, Plan::add_batch), is written once by
+// its STATS tiles before the segment's statistics are published, and only
+// read (or prefetched) after: no stale L1 copy can exist within the launch.
+__device__ __forceinline__ float4 ld_scratch(const float4* p) { return *p; }
+
+template <bool INTERIOR, bool FROM_SCRATCH>
+__device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const SegInfo& si, uint64_t qbase,
+                                         uint64_t hiel, const float4* xs, uint32_t* hw, const BinParams& p,
+                                         uint32_t& nclip_lo, uint32_t& nclip_hi) {
     const int lane = threadIdx.x & 31;
-    const uint32_t blk = unit / kBlkUnits, bsize = min((uint32_t)kBlkUnits, si.nu8 - blk * kBlkUnits);
-    uint32_t* blk_cnt = a.sync + kSyncReady + kSyPerSeg * a.nseg;
-    uint32_t old = 0;
-    if (lane == 0) old = atom_add_acq_rel(blk_cnt + si.b0 + blk, 1u);  // publishes the leaf
-    old = bcast(old);
-    if (old != bsize - 1) return;
-    const StatP p = warp_merge_range(a.leaf + si.u0 + blk * kBlkUnits, bsize);
-    uint32_t oldb = 0;
-    if (lane == 0) {
-        a.blk_leaf[si.b0 + blk] = p;
-        oldb = atom_add_acq_rel(a.sync + kSyncReady + kSyPerSeg * s + kSyBlocks, 1u);
+    constexpr int kHalf = kSlotsPerLane / 2;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+        float4 xv[kHalf];
+#pragma unroll
+        for (int jj = 0; jj < kHalf; ++jj) {
+            const uint64_t q = qbase + (uint64_t)(h * kHalf + jj) * 32 + lane;
+            const bool in = INTERIOR || q * 4 < hiel;
+            xv[jj] = !in ? make_float4(0.f, 0.f, 0.f, 0.f) : FROM_SCRATCH ? ld_scratch(xs + q) : ld4(a.a, q);
+        }
+#pragma unroll
+        for (int pr = 0; pr < kHalf / 2; ++pr) {
+            float xe[8] = {xv[2 * pr].x, xv[2 * pr].y, xv[2 * pr].z, xv[2 * pr].w,
+                           xv[2 * pr + 1].x, xv[2 * pr + 1].y, xv[2 * pr + 1].z, xv[2 * pr + 1].w};
+            const uint64_t q0 = qbase + (uint64_t)(h * kHalf + 2 * pr) * 32 + lane;
+            uint32_t vmask = 0xffu;
+            if (!INTERIOR) {
+                vmask = 0u;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const uint64_t e = (q0 + (uint64_t)(i >> 2) * 32) * 4 + (i & 3);
+                    vmask |= (e >= si.lo && e < hiel) ? (1u << i) : 0u;
+                }
+            }
+            int cc[8];
+            bool okall = true;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                // in range and clear of every bucket edge by the proven margin:
+                // then trunc(g) is the exact bucket. Clipped x fails this test
+                // (g < margin or g > 256 - margin), see SegStat::margin.
+                const float g = __fmaf_rn(xe[i], p.inv_w, -p.c);
+                const int c = __float2int_rz(g);
+                const float fr = __fsub_rn(g, __int2float_rz(c));
+                okall &= (fr > p.margin) & (fr < p.one_m) & ((uint32_t)c < 256u);
+                cc[i] = c;
+            }
+            // clipped lanes (and lanes outside the segment) keep their code in the
+            // low byte and set bit 8: their limbs go to the sink row 256; the
+            // codebook adds the clipped ones as count * lo / hi (quant.hpp:66-67)
+            if (!INTERIOR) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) cc[i] |= ((vmask >> i) & 1u) ? 0 : 256;
+            }
+            if (!okall) {  // rare: near an edge (exact table) or clipped (quant.hpp:66-67)
+                uint32_t clo_m = 0, chi_m = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float x = xe[i];
+                    const float g = __fmaf_rn(x, p.inv_w, -p.c);
+                    const int c0 = __float2int_rz(g);
+                    const float fr = __fsub_rn(g, __int2float_rz(c0));
+                    const int sink = cc[i] & 256;
+                    if (x < p.lo_up) {
+                        cc[i] = 256; clo_m |= 1u << i;
+                    } else if (x > p.hi_dn) {
+                        cc[i] = 256 | 255; chi_m |= 1u << i;
+                    } else if (!(fr > p.margin && fr < p.one_m && (uint32_t)c0 < 256u)) {
+                        cc[i] = sink | bucket_walk(x, min(max(c0, 0), 255), sm.thr);
+                    }
+                }
+                nclip_lo += __popc(clo_m & vmask);
+                nclip_hi += __popc(chi_m & vmask);
+            }
+            // fixed point r(x) (see kInfoWide), split into the limbs
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint2 sk = sm.bsk[cc[i]];
+                // m = x * s + K in [2^52, 2^53): mantissa = r (see kInfoWide)
+                const double sc = __hiloint2double((int)sk.x, 0);
+                const double kk = __hiloint2double((int)sk.y, 0);
+                const double m = __fma_rn((double)xe[i], sc, kk);
+                const uint32_t rlo = (uint32_t)__double2loint(m);
+                const uint32_t rhi = (uint32_t)__double2hiint(m);
+                uint32_t* hc = hw + 3 * min(cc[i], kBuckets);
+                red_shared_add(hc, (rlo & ((1u << kLoBits) - 1u)) | (1u << kCntShift));
+                red_shared_add(hc + 1, (rlo >> kLoBits) & ((1u << (kMidEnd - kLoBits)) - 1u));
+                const uint32_t rc = __funnelshift_r(rlo, rhi, kMidEnd) & ((1u << (42 - kMidEnd)) - 1u);
+                if (rc) red_shared_add(hc + 2, rc);
+            }
+            const uint32_t p0 = __byte_perm(__byte_perm(cc[0], cc[1], 0x0040), __byte_perm(cc[2], cc[3], 0x0040), 0x5410);
+            const uint32_t p1 = __byte_perm(__byte_perm(cc[4], cc[5], 0x0040), __byte_perm(cc[6], cc[7], 0x0040), 0x5410);
+            for (uint32_t d = 0; d < a.ndest; ++d) {
+                uint8_t* oc = a.dcodes[d];
+                if (INTERIOR) {
+                    reinterpret_cast<uint32_t*>(oc)[q0] = p0;
+                    reinterpret_cast<uint32_t*>(oc)[q0 + 32] = p1;
+                } else {
+#pragma unroll
+                    for (int f = 0; f < 2; ++f) {
+                        const uint64_t q = q0 + (uint64_t)f * 32;
+                        const uint32_t packed = f ? p1 : p0;
+                        const uint32_t vm = (vmask >> (4 * f)) & 0xfu;
+                        if (vm == 0xfu) {
+                            reinterpret_cast<uint32_t*>(oc)[q] = packed;
+                        } else if (vm) {
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                if (vm & (1u << e)) oc[q * 4 + e] = (uint8_t)(packed >> (8 * e));
+                        }
+                    }
+                }
+            }
+        }
+        if (FROM_SCRATCH && INTERIOR) {
+            // this half's 2 KB of scratch x is consumed (each element is read
+            // exactly once): drop the 128-B L2 lines wholly inside it without
+            // write-back — x was only ever meant as an L2 round trip
+            const uintptr_t lo_b = reinterpret_cast<uintptr_t>(xs + qbase + (uint64_t)h * kHalf * 32);
+            const uintptr_t hi_b = lo_b + (uintptr_t)kHalf * 32 * 16;
+            const uintptr_t line = ((lo_b + 127) & ~(uintptr_t)127) + (uintptr_t)lane * 128;
+            if (lane < 16 && line + 128 <= hi_b)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
+        }
     }
-    oldb = bcast(oldb);
-    if (oldb == si.nblk - 1) q2_finalize_stats(a, s, si);
 }
 
-// ---------------------------------------------------------------------------
-// BIN: the warp's tables, histogram flush, codebook
+__device__ void finalize_codebook(const QuantArgs& a, uint32_t s, const SegInfo& si);
+__device__ float codebook_entry(const SegStat* st, int b, unsigned long long rl, unsigned long long rh,
+                                unsigned long long total, unsigned long long clip);
 
-__device__ void q2_bin_tables(const Q2Args& a, WSm& ws, uint32_t s, const SegInfo& si) {
-    const int lane = threadIdx.x & 31;
+template <bool FROM_SCRATCH>
+__device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si, uint32_t tile) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const SegStat* st = &a.stats[si.slot];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int b = lane + 32 * i;
-        ws.thr[b] = b == 0 ? -INFINITY : __ldcg(&st->thr[b]);
+    if (FROM_SCRATCH) {  // the warp's first unit, while the tables load (the segment's scratch is complete)
+        const uint32_t u0 = tile * si.upw * kWarps + warp;
+        if (u0 < si.nunits) {
+            const float4* p0 = reinterpret_cast<const float4*>(a.scratch) + si.sq0 + (uint64_t)u0 * kUnitSlots + lane * 8;
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(p0));
+        }
+    }
+    if (sm.bin_seg != (int32_t)s) {
+        __syncthreads();
+        const int b = threadIdx.x;
+        sm.thr[b] = b == 0 ? -INFINITY : __ldcg(&st->thr[b]);
         const uint32_t info = __ldcg(&st->binfo[b]);
-        // s = high word of info (low bits zero), K = 2^52 (+ 2^41 for a wide bucket)
-        ws.bsk[b] = make_double2(__hiloint2double((int)(info & ~kInfoWide), 0),
-                                 __hiloint2double((int)(0x43300000u | ((info & kInfoWide) << 9)), 0));
-    }
-    if (lane == 0) {
-        ws.thr[kBuckets] = INFINITY;
-        ws.thr[kBuckets + 1] = __ldcg(&st->lo_up);
-        const float margin = __ldcg(&st->margin);
-        ws.bp[0] = __ldcg(&st->c_f);
-        ws.bp[1] = __ldcg(&st->inv_w_f);
-        ws.bp[2] = __ldcg(&st->lo_up);
-        ws.bp[3] = __ldcg(&st->hi_dn);
-        ws.bp[4] = margin;
-        ws.bp[5] = 1.f - margin;
-        ws.degenerate = (__ldcg(&st->flags) & kFlagDegenerate) != 0;
-        ws.bin_seg = (int32_t)s;
-    }
-    __syncwarp();
-}
+        const uint2 sk = make_uint2(info & ~kInfoWide, 0x43300000u | ((info & kInfoWide) << 9));  // K = 2^52 (+2^41)
+        sm.bsk[b] = sm.bsk[kBuckets + b] = sk;
 
-__device__ void q2_finalize_codebook(const Q2Args& a, uint32_t s, const SegInfo& si);
+        if (b == 0) {
+            sm.thr[kBuckets] = INFINITY;
+            sm.thr[kBuckets + 1] = __ldcg(&st->lo_up);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) sm.bin_seg = (int32_t)s;
+    }
+    const float c_f = __ldcg(&st->c_f), inv_w = __ldcg(&st->inv_w_f);
+    const float lo_up = __ldcg(&st->lo_up), hi_dn = __ldcg(&st->hi_dn);  // x < lo <=> x < lo_up (fp32 x)
+    const float margin = __ldcg(&st->margin), one_m = 1.f - margin;
+    const bool degenerate = (__ldcg(&st->flags) & kFlagDegenerate) != 0;
+    uint32_t* hw = &sm.hist[warp][0][0];  // zero on entry (kernel start / previous tile's combine)
+    if (threadIdx.x < 2) sm.clip[threadIdx.x] = 0u;
+    __syncthreads();
 
-// The warp's histogram (units of segment hist_seg) into the segment's exact accumulator,
-// then its arrival; the arrival that completes the segment writes the codebook.
-__device__ void q2_flush(const Q2Args& a, WSm& ws, uint32_t& nclip_lo, uint32_t& nclip_hi) {
-    const int lane = threadIdx.x & 31;
-    if (ws.hist_seg < 0) return;
-    const uint32_t s = (uint32_t)ws.hist_seg;
-    SegAcc* acc = &a.acc[s];
+    const uint64_t hiel = si.lo + si.len;
+    const float4* xs = reinterpret_cast<const float4*>(a.scratch) + ((int64_t)si.sq0 - (int64_t)si.q0);
+    uint32_t nclip_lo = 0, nclip_hi = 0;
+    const BinParams bpar{c_f, inv_w, lo_up, hi_dn, margin, one_m};
+    for (int ui = 0; ui < (int)si.upw; ++ui) {
+        const uint32_t u = (tile * si.upw + ui) * kWarps + warp;
+        if (u >= si.nunits) break;
+        const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
+        const bool interior = qbase * 4 >= si.lo && (qbase + kUnitSlots) * 4 <= hiel;  // warp-uniform
+        if (FROM_SCRATCH && ui + 1 < (int)si.upw && u + kWarps < si.nunits) {
+            const float4* nx = xs + qbase + (uint64_t)kWarps * kUnitSlots + lane * 8;  // one 128-B line per lane
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(nx));
+        }
+        if (degenerate) {  // sigma == 0: every code is 0 (quant.hpp:49-55)
+            for (int j = 0; j < kSlotsPerLane; ++j) {
+                const uint64_t q = qbase + (uint64_t)j * 32 + lane;
+                for (int e = 0; e < 4; ++e)
+                    if (q * 4 + e >= si.lo && q * 4 + e < hiel)
+                        for (uint32_t d = 0; d < a.ndest; ++d) a.dcodes[d][q * 4 + e] = 0;
+            }
+        } else if (interior) {
+            bin_unit<true, FROM_SCRATCH>(a, sm, si, qbase, hiel, xs, hw, bpar, nclip_lo, nclip_hi);
+        } else {
+            bin_unit<false, FROM_SCRATCH>(a, sm, si, qbase, hiel, xs, hw, bpar, nclip_lo, nclip_hi);
+        }
+    }
+    nclip_lo = warp_sum_u(nclip_lo);
+    nclip_hi = warp_sum_u(nclip_hi);
+    if (lane == 0 && (nclip_lo | nclip_hi)) {
+        atomicAdd(&sm.clip[0], nclip_lo);
+        atomicAdd(&sm.clip[1], nclip_hi);
+    }
+    __syncthreads();
+    {   // tile histogram (exact integers, order-free) into the segment's
+        // accumulator; re-zero the limbs
+        const int b = threadIdx.x;
+        unsigned long long r = 0;
+        uint32_t cn = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int b = lane + 32 * i;
-        const uint32_t A = ws.hist[b][0], B = ws.hist[b][1], Cc = ws.hist[b][2];
-        const unsigned long long r = (unsigned long long)(A & ((1u << kWCntShift) - 1u)) +
-                                     ((unsigned long long)B << kWLoBits) + ((unsigned long long)Cc << kWMidEnd);
-        const uint32_t cn = A >> kWCntShift;
-        ws.hist[b][0] = 0u;
-        ws.hist[b][1] = 0u;
-        ws.hist[b][2] = 0u;
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t A = sm.hist[w][b][0], B = sm.hist[w][b][1], C = sm.hist[w][b][2];
+            r += (unsigned long long)(A & ((1u << kCntShift) - 1u)) + ((unsigned long long)B << kLoBits) +
+                 ((unsigned long long)C << kMidEnd);
+            cn += A >> kCntShift;
+            sm.hist[w][b][0] = 0u;
+            sm.hist[w][b][1] = 0u;
+            sm.hist[w][b][2] = 0u;
+        }
+        SegAcc* acc = &a.acc[s];
         if (cn) {
             atomicAdd(&acc->rlo[b], r & 0xffffffffull);
             if (r >> 32) atomicAdd(&acc->rhi[b], r >> 32);
             atomicAdd(&acc->cnt[b], (unsigned long long)cn);
         }
+        if (b < 2 && sm.clip[b]) atomicAdd(&acc->clip[b], (unsigned long long)sm.clip[b]);
     }
-    const uint32_t clo = warp_sum_u(nclip_lo), chi = warp_sum_u(nclip_hi);
-    nclip_lo = nclip_hi = 0;
-    if (lane == 0) {
-        if (clo) atomicAdd(&acc->clip[0], (unsigned long long)clo);
-        if (chi) atomicAdd(&acc->clip[1], (unsigned long long)chi);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // acq_rel: releases the CTA's atomics; the last tile acquires all
+        sm.flag = atom_add_acq_rel(&a.sync[kSyncReady + 2 * a.nseg + s], 1u) == si.ncta - 1 ? 1u : 0u;
     }
-    if (lane < 3) ws.hist[kBuckets][lane] = 0u;
-    const uint32_t units = ws.hist_units;
-    __syncwarp();
-    uint32_t old = 0;
-    if (lane == 0) {
-        ws.hist_seg = -1;
-        ws.hist_units = 0;
-        // acq_rel: releases the warp's accumulator atomics and code stores (through the warp
-        // barrier above); the arrival that completes the segment acquires all
-        old = atom_add_acq_rel(a.sync + kSyncReady + kSyPerSeg * s + kSyBins, units);
-    }
-    old = bcast(old);
-    __syncwarp();
-    const SegInfo& si = a.segs[s];
-    if (old + units == si.nu8) q2_finalize_codebook(a, s, si);
+    __syncthreads();
+    if (sm.flag) finalize_codebook(a, s, si);
 }
 
-// Run by the warp whose flush completed segment s: the codebook from the exact bucket sums
-// (quant.hpp:78-85); re-zeroes the accumulator; ChunkMsg headers; raises the arrival flags.
-__device__ void q2_finalize_codebook(const Q2Args& a, uint32_t s, const SegInfo& si) {
-    const int lane = threadIdx.x & 31;
+// Run by the last BIN tile of s to finish: the codebook from the exact
+// bucket sums (quant.hpp:78-85); re-zeroes the accumulator for the next launch.
+__device__ void finalize_codebook(const QuantArgs& a, uint32_t s, const SegInfo& si) {
     const SegStat* st = &a.stats[si.slot];
-    SegAcc* acc = &a.acc[s];
-    unsigned long long rl[8], rh[8], total[8];
-    const unsigned long long clip_lo = __ldcg(&acc->clip[0]), clip_hi = __ldcg(&acc->clip[1]);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int b = lane + 32 * i;
-        rl[i] = __ldcg(&acc->rlo[b]);
-        rh[i] = __ldcg(&acc->rhi[b]);
-        const unsigned long long clip = b == 0 ? clip_lo : b == 255 ? clip_hi : 0ull;
-        total[i] = __ldcg(&acc->cnt[b]) + clip;  // clipped members sit in the sink row
-    }
-    __syncwarp();  // every read done before the re-zeroing
     const bool degenerate = (__ldcg(&st->flags) & kFlagDegenerate) != 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int b = lane + 32 * i;
-        acc->rlo[b] = 0ull;
-        acc->rhi[b] = 0ull;
-        acc->cnt[b] = 0ull;
-        const unsigned long long clip = b == 0 ? clip_lo : b == 255 ? clip_hi : 0ull;
-        float v;
-        if (degenerate) v = (float)__ldcg(&st->mu);
-        else if (total[i] == 0)
-            v = (float)__dadd_rn(__ldcg(&st->lo), __dmul_rn(__dadd_rn((double)b, 0.5), __ldcg(&st->width)));
-        else v = codebook_entry(st, b, rl[i], rh[i], total[i], clip);
-        for (uint32_t d = 0; d < a.ndest; ++d) a.dcb[d][(uint64_t)si.slot * kBuckets + b] = v;
+    const int b = threadIdx.x;
+    SegAcc* acc = &a.acc[s];
+    const unsigned long long rl = __ldcg(&acc->rlo[b]), rh = __ldcg(&acc->rhi[b]);
+    const unsigned long long clip = b == 0 ? __ldcg(&acc->clip[0]) : b == 255 ? __ldcg(&acc->clip[1]) : 0ull;
+    const unsigned long long total = __ldcg(&acc->cnt[b]) + clip;  // clipped members sit in the sink row
+    __syncthreads();  // every read done before the re-zeroing
+    acc->rlo[b] = 0ull;
+    acc->rhi[b] = 0ull;
+    acc->cnt[b] = 0ull;
+    if (b < 2) acc->clip[b] = 0ull;
+    float v;
+    if (degenerate) {
+        v = (float)__ldcg(&st->mu);
+    } else if (total == 0) {
+        v = (float)__dadd_rn(__ldcg(&st->lo), __dmul_rn(__dadd_rn((double)b, 0.5), __ldcg(&st->width)));
+    } else {
+        v = codebook_entry(st, b, rl, rh, total, clip);
     }
-    if (lane < 2) acc->clip[lane] = 0ull;
-    __syncwarp();
-    if (lane == 0) {
-        for (uint32_t d = 0; d < a.ndest; ++d)  // the ChunkMsg header of this payload, before its flag
+    for (uint32_t d = 0; d < a.ndest; ++d) a.dcb[d][(uint64_t)si.slot * kBuckets + b] = v;
+    if (threadIdx.x == 0)  // the ChunkMsg header of this payload, before its flag
+        for (uint32_t d = 0; d < a.ndest; ++d)
             if (a.dhdr[d]) write_hdr(a.dhdr[d] + si.slot, a.hdr, si.chunk, (uint32_t)si.len, (uint8_t)a.phase_out);
-        if (a.nflag) {
-            // every unit of s released its stores (gpu scope) to the arrival counter this warp
-            // acquired; the system-scope fence + release extends that chain to the peers
+    if (a.nflag) {
+        // Every tile of s released its stores (gpu scope) to the arrival
+        // counter this CTA acquired; the system-scope fence + release here
+        // extends that causality chain to the peers polling the flags.
+        __syncthreads();
+        if (threadIdx.x == 0) {
             __threadfence_system();
             const uint32_t v = raise_value(a.err, a.epoch);  // poison when this rank's round failed
             for (uint32_t f = 0; f < a.nflag; ++f) st_release_sys(a.sflag[f] + si.slot, v);
         }
     }
-    __syncwarp();
 }
 
-// ---------------------------------------------------------------------------
-// The warp worker
 
-// Batch unit -> segment (binary search over seg_u0; cached in shared memory when it fits).
-__device__ __forceinline__ uint32_t q2_seg_of(const Q2Args& a, const QCta& cta, uint32_t u) {
-    const uint32_t* t = a.nseg <= kMaxSegCache ? cta.seg_u0 : a.seg_u0;
-    uint32_t lo = 0, hi = a.nseg;
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (t[mid] <= u) lo = mid; else hi = mid;
+// Task t of run r -> (kind, segment, tile).
+__device__ __forceinline__ void decode_run(const uint4 r, uint32_t t, uint32_t& kind, uint32_t& s, uint32_t& tile) {
+    const uint32_t off = t - r.x, k = r.y & 3u;
+    if (k == kTaskMixRev || k == kTaskMixFwd) {
+        const uint32_t i = off >> 1;
+        if (off & 1u) {
+            kind = kTaskBin;
+            s = r.y >> 2;
+            tile = k == kTaskMixRev ? (r.w >> 16) - i : (r.w >> 16) + i;
+        } else {
+            kind = kTaskStats;
+            s = r.z;
+            tile = (r.w & 0xffffu) + i;
+        }
+    } else {
+        kind = r.y;
+        s = r.z;
+        tile = (r.w & 0x80000000u) ? (r.w & 0x7fffffffu) - off : r.w + off;
     }
-    return lo;
-}
-
-// STATS: the incoming codebook of segment s (hop add), after the peer flag (warp-level)
-__device__ void q2_stats_lut(const Q2Args& a, WSm& ws, uint32_t s, const SegInfo& si) {
-    const int lane = threadIdx.x & 31;
-    if (a.in_flag) {  // peer transport: the predecessor's payload of s must have landed intact
-        if (lane == 0 && spin_until_ge_sys(a.in_flag + si.in_slot, a.epoch, a.err, a.timeout_ns, a.culprit_in) &&
-            a.in_hdr)
-            check_hdr(a.in_hdr + si.in_slot, a.hdr, si.chunk, (uint32_t)si.len, kPhaseRS, a.err, a.culprit_in);
-        __syncwarp();
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) ws.lut[lane + 32 * i] = __ldcg(a.in_cb + (uint64_t)si.in_slot * kBuckets + lane + 32 * i);
-    if (lane == 0) ws.lut_seg = (int32_t)s;
-    __syncwarp();
 }
 
 template <int SRC>
-__global__ void __launch_bounds__(kQThreads, 1) k_quant(Q2Args a) {
-    extern __shared__ __align__(16) unsigned char qraw[];
-    QCta& cta = *reinterpret_cast<QCta*>(qraw);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WSm& ws = *reinterpret_cast<WSm*>(qraw + ((sizeof(QCta) + 15) & ~size_t(15)) +
-                                      (size_t)warp * ((sizeof(WSm) + 15) & ~size_t(15)));
-    if (warp == 0) {  // the whole tensor memory of this SM (one CTA per SM)
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-            (uint32_t)__cvta_generic_to_shared(&cta.tbase)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+__global__ void __launch_bounds__(kThreads, kQuantMinBlocks) k_quant(QuantArgs a) {
+    extern __shared__ __align__(16) unsigned char qsmem_raw[];
+    QSmem& sm = *reinterpret_cast<QSmem*>(qsmem_raw);  // dynamic: > 48 KB in total
+    uint4* runs_s = reinterpret_cast<uint4*>(qsmem_raw + sizeof(QSmem));
+    SegInfo* segs_s = reinterpret_cast<SegInfo*>(qsmem_raw + sizeof(QSmem) + kMaxRunsSmem * sizeof(uint4));
+    const bool runs_in_smem = a.nruns <= kMaxRunsSmem;
+    const bool segs_in_smem = a.nseg <= kMaxSegsSmem;
+    for (uint32_t i = threadIdx.x; i < kWarps * (kBuckets + 1) * 3; i += kThreads) (&sm.hist[0][0][0])[i] = 0u;
+    if (runs_in_smem)
+        for (uint32_t i = threadIdx.x; i < a.nruns; i += kThreads) runs_s[i] = a.runs[i];
+    if (segs_in_smem)
+        for (uint32_t i = threadIdx.x; i < a.nseg; i += kThreads) segs_s[i] = a.segs[i];
+    uint32_t nxt = 0;  // thread 0: the next task, claimed at the start of the current one
+    if (threadIdx.x == 0) {
+        sm.bin_seg = -1;
+        sm.lut_seg = -1;
+        sm.ready_seg = -1;
+        nxt = atomicAdd(&a.sync[0], 1u);
     }
-    if (a.nseg <= kMaxSegCache)
-        for (uint32_t i = threadIdx.x; i <= a.nseg; i += kQThreads) cta.seg_u0[i] = a.seg_u0[i];
-    for (uint32_t i = lane; i < (kBuckets + 1) * 3; i += 32) (&ws.hist[0][0])[i] = 0u;
-    if (lane == 0) {
-        ws.lut_seg = ws.bin_seg = ws.hist_seg = -1;
-        ws.hist_units = 0;
-        ws.qh = ws.qn = 0;
-        ws.freemask = (1u << kWSlots) - 1u;
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tbase = cta.tbase;
-
-    // claims: quads of units in batch order (one atomic per 4 units), one quad ahead
-    const uint32_t nquads = (a.nunits + kQuad - 1) / kQuad;
-    uint32_t cq = 0, cn = 0;  // current quad's next unit and end (units)
-    uint32_t nq = bcast(lane == 0 ? atomicAdd(a.sync, 1u) : 0u);  // the next claimed quad
-    uint32_t ovf_seg = 0;     // lowest segment that may still hold unclaimed overflow units
-    uint32_t ready_seg = kNone;
-    uint32_t nclip_lo = 0, nclip_hi = 0;
     for (;;) {
-        // ---- STATS unit: the next claimed unit (claim the quad after it now)
-        uint32_t su = kNone;
-        if (cq == cn && nq < nquads) {
-            cq = nq * kQuad;
-            cn = min(cq + kQuad, a.nunits);
-            nq = bcast(lane == 0 ? atomicAdd(a.sync, 1u) : 0u);  // used one quad later
+        if (threadIdx.x == 0) sm.task = nxt;
+        __syncthreads();
+        const uint32_t t = sm.task;
+        if (t >= a.ntasks) return;
+        // claim the following task now: the atomic's latency hides behind this tile
+        if (threadIdx.x == 0) nxt = atomicAdd(&a.sync[0], 1u);
+        uint32_t kind, s, tile;
+        if (runs_in_smem) {  // binary search of the run table (smem)
+            uint32_t lo = 0, hi = a.nruns;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (runs_s[mid].x <= t) lo = mid; else hi = mid;
+            }
+            decode_run(runs_s[lo], t, kind, s, tile);
+        } else {
+            uint32_t lo = 0, hi = a.nruns;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (a.runs[mid].x <= t) lo = mid; else hi = mid;
+            }
+            decode_run(a.runs[lo], t, kind, s, tile);
         }
-        if (cq < cn) su = cq++;
-        // ---- BIN unit: the oldest held unit whose segment is ready, else an overflow unit
-        uint32_t bseg = kNone, bunit = 0, bslot = kSlotGlobal;
-        if (ws.qn > 0) {
-            const QHeld h = ws.q[ws.qh];
-            bool rdy = h.seg == ready_seg;
-            if (!rdy) {
-                uint32_t v = lane == 0 ? ld_relaxed(a.sync + kSyncReady + kSyPerSeg * h.seg + kSyReady) : 0u;
-                rdy = bcast(v) != 0u;
-                if (rdy) { __threadfence(); ready_seg = h.seg; }
+        const SegInfo si = segs_in_smem ? segs_s[s] : a.segs[s];
+        if (kind == kTaskBin && threadIdx.x == 0 && sm.ready_seg != (int32_t)s) {
+            // acquire SegStat(s) (cached per CTA); the CTA owes nothing here
+            uint32_t ns = 32;
+            while (ld_acquire(&a.sync[kSyncReady + s]) == 0u) {
+                __nanosleep(ns);
+                ns = ns < 1024 ? 2 * ns : ns;
             }
-            if (rdy) {
-                bseg = h.seg; bunit = h.unit; bslot = h.slot;
-                __syncwarp();
-                if (lane == 0) { ws.qh = (ws.qh + 1) % kWSlots; ws.qn -= 1; }
-            }
+            sm.ready_seg = (int32_t)s;
         }
-        if (bseg == kNone && (su == kNone || ws.qn == kWSlots)) {
-            // overflow units of ready segments (any warp may bin those)
-            while (ovf_seg < a.nseg) {
-                const SegInfo& so = a.segs[ovf_seg];
-                if (so.nu8 == 0) { ++ovf_seg; continue; }
-                uint32_t got = kNone, more = 0;
-                if (lane == 0) {
-                    uint32_t* sy = a.sync + kSyncReady + kSyPerSeg * ovf_seg;
-                    if (ld_relaxed(sy + kSyReady)) {
-                        __threadfence();
-                        const uint32_t cnt = __ldcg(sy + kSyOvfCount);
-                        more = 1;
-                        if (cnt && __ldcg(sy + kSyOvfClaim) < cnt) {
-                            const uint32_t i = atomicAdd(sy + kSyOvfClaim, 1u);
-                            if (i < cnt) got = __ldcg(a.ovf + so.u0 + i);
-                        }
-                    }
-                }
-                got = bcast(got);
-                more = bcast(more);
-                if (got != kNone) { bseg = ovf_seg; bunit = got; bslot = kSlotGlobal; break; }
-                if (!more) break;  // not ready yet
-                ++ovf_seg;        // ready and exhausted
-            }
-        }
-        if (su == kNone && bseg == kNone) {
-            if (ws.qn == 0 && ovf_seg >= a.nseg && nq >= nquads) break;  // done
-            // nothing runnable: every unit is claimed (by running warps, which complete their
-            // STATS without waiting): wait for the oldest pending segment's statistics
-            const uint32_t s = ws.qn > 0 ? ws.q[ws.qh].seg : ovf_seg;
-            if (lane == 0) {
-                uint32_t ns = 32;
-                while (ld_acquire(a.sync + kSyncReady + kSyPerSeg * s + kSyReady) == 0u) {
-                    __nanosleep(ns);
-                    ns = ns < 1024 ? 2 * ns : ns;
-                }
-            }
-            __syncwarp();
-            ready_seg = s;
-            continue;
-        }
-        // ---- STATS setup (segment, slot, LUT)
-        uint32_t sseg = kNone, sunit = 0, sslot = kSlotGlobal, ovf_i = 0;
-        SegInfo ss{}, sb{};
-        if (su != kNone) {
-            sseg = q2_seg_of(a, cta, su);
-            ss = a.segs[sseg];
-            sunit = su - ss.u0;
-            if ((SRC & kHasIn) && ws.lut_seg != (int32_t)sseg) q2_stats_lut(a, ws, sseg, ss);
-            if (ws.freemask) {
-                sslot = __ffs(ws.freemask) - 1;
-                __syncwarp();
-                if (lane == 0) {
-                    ws.freemask &= ~(1u << sslot);
-                    ws.q[(ws.qh + ws.qn) % kWSlots] = QHeld{sseg, sunit, sslot};
-                    ws.qn += 1;
-                }
-            } else if (lane == 0) {
-                ovf_i = atomicAdd(a.sync + kSyncReady + kSyPerSeg * sseg + kSyOvfCount, 1u);  // used at the end
-            }
-        }
-        // ---- BIN setup (tables, histogram segment)
-        if (bseg != kNone) {
-            sb = a.segs[bseg];
-            if (ws.hist_seg != (int32_t)bseg) {  // a histogram holds one segment: flush the previous one
-                q2_flush(a, ws, nclip_lo, nclip_hi);
-                if (lane == 0) ws.hist_seg = (int32_t)bseg;
-                __syncwarp();
-            }
-            if (ws.bin_seg != (int32_t)bseg) q2_bin_tables(a, ws, bseg, sb);
-        }
-        // ---- the fused unit: STATS loads in flight while the BIN half is computed
-        const bool vs = sseg != kNone, vb = bseg != kNone;
-        const uint64_t hs = ss.lo + ss.len, hb = sb.lo + sb.len;
-        const uint64_t os = ss.o0 + (uint64_t)sunit * kUnitOct, ob = sb.o0 + (uint64_t)bunit * kUnitOct;
-        const bool is = vs && os * 8 >= ss.lo && (os + kUnitOct) * 8 <= hs;
-        const bool ib = vb && ob * 8 >= sb.lo && (ob + kUnitOct) * 8 <= hb;
-        const QSlotRef rs = q2_slot(a, tbase, ws, ss, sslot), rb = q2_slot(a, tbase, ws, sb, bslot);
-        QMoments m{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0u, false};
-        uint32_t* hw = &ws.hist[0][0];
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-            QLoads<SRC> L;
-            if (vs) q2_stats_load<SRC>(a, os, hs, is, h, L);
-            if (vb) {  // bin this half while the loads fly
-                float y[16];
-                q2_get_half(rb, ob, h, y);
-                if (ws.degenerate) {  // sigma == 0: every code is 0 (quant.hpp:49-55)
-                    for (int jj = 0; jj < 2; ++jj) {
-                        const uint64_t o = ob + (uint64_t)(2 * h + jj) * 32 + lane;
-                        for (int e = 0; e < 8; ++e)
-                            if (o * 8 + e >= sb.lo && o * 8 + e < hb)
-                                for (uint32_t d = 0; d < a.ndest; ++d) a.dcodes[d][o * 8 + e] = 0;
-                    }
-                } else if (ib) {
-                    q2_bin_octet<true>(a, ws, &y[0], ob + (uint64_t)(2 * h) * 32 + lane, sb, hw, nclip_lo, nclip_hi);
-                    q2_bin_octet<true>(a, ws, &y[8], ob + (uint64_t)(2 * h + 1) * 32 + lane, sb, hw, nclip_lo, nclip_hi);
-                } else {
-                    q2_bin_octet<false>(a, ws, &y[0], ob + (uint64_t)(2 * h) * 32 + lane, sb, hw, nclip_lo, nclip_hi);
-                    q2_bin_octet<false>(a, ws, &y[8], ob + (uint64_t)(2 * h + 1) * 32 + lane, sb, hw, nclip_lo, nclip_hi);
-                }
-            }
-            if (vs) {
-                q2_stats_finish<SRC>(a, ws, ss, os, is, h, L, m);
-                q2_put_half(rs, os, h, L.a);
-            }
-        }
-        // ---- BIN epilogue: slot free, scratch discard, histogram accounting
-        if (vb) {
-            if (bslot == kSlotGlobal && ib) {
-                // consumed (read exactly once): drop the unit's scratch lines from L2 without write-back
-                const uintptr_t lo_b = reinterpret_cast<uintptr_t>(rb.gp + ob * 8);
-                asm volatile("discard.global.L2 [%0], 128;" ::"l"(lo_b + (uintptr_t)lane * 128) : "memory");
-            }
-            __syncwarp();
-            if (lane == 0) {
-                if (bslot < kWSlots) ws.freemask |= 1u << bslot;
-                ws.hist_units += 1;
-            }
-            __syncwarp();
-            if (ws.hist_units == kWFlushUnits) q2_flush(a, ws, nclip_lo, nclip_hi);
-        }
-        // ---- STATS epilogue: the unit's leaf, overflow registration, arrival
-        if (vs) {
-            StatP p{__dadd_rn(m.s0, m.s1), __dadd_rn(m.q0, m.q1), __dadd_rn(m.d0, m.d1), m.piv, (uint64_t)m.cnt};
-            p = warp_merge(p);
-            if (lane == 0) {
-                a.leaf[ss.u0 + sunit] = p;
-                if (sslot == kSlotGlobal) a.ovf[ss.u0 + ovf_i] = sunit;  // for BIN by any warp (published below)
-                if (!isfinite(p.s) || !isfinite(p.m2)) {  // finite fp32 inputs cannot overflow an fp64 sum
-                    atomicOr(&a.seg_flags[sseg], kFlagNonFinite);
-                    atomicOr(a.err, kErrNonFinite);
-                }
-            }
-            __syncwarp();  // the lanes' scratch stores, then lane 0's release (cumulative)
-            q2_stats_arrive(a, sseg, ss, sunit);
+        __syncthreads();  // everyone has read sm.task; SegStat(s) visible for BIN
+        switch (kind) {
+            case kTaskStats: stats_tile<SRC>(a, sm, s, si, tile); break;
+            default: bin_tile<SRC != kSrcA>(a, sm, s, si, tile); break;
         }
     }
-    q2_flush(a, ws, nclip_lo, nclip_hi);
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
 }
 
-}  // namespace emesh_b200
+constexpr size_t kQuantSmemBytes = sizeof(QSmem) + kMaxRunsSmem * sizeof(uint4) + kMaxSegsSmem * sizeof(SegInfo);
 
+}  // namespace emesh_b200

@@ -46,14 +46,14 @@ def main():
                 store.set(key, uid)
             else:
                 uid = bytes(store.get(key))
-        return E.RingEngine(n, k, rank=plan.self_index, opts=opts, nccl_id=uid, transport=transport)
+        return E.RingEngine(n, k, rank=plan.self_index, opts=opts, nccl_id=uid, transport=transport, plan=plan)
 
     class Mesh:  # the coordinator's view: the crashed rank is evicted at the next epoch
         def __init__(self):
             self.state = E.MeshState(1, list(ids))
 
         def report_failure(self, node):
-            pass
+            reported.append(node)
 
         def wait_epoch_change(self, epoch, timeout):
             self.state = E.MeshState(epoch + 1, [m for m in self.state.ring if m != crashed])
@@ -64,6 +64,7 @@ def main():
 
     me = ids[rank]
     ok = True
+    reported = []
     if me == crashed:
         # build the first engine with everyone (collective), then stop participating
         eng = make_engine(E.RingPlan.from_mesh(E.MeshState(1, list(ids)), me, 1))
@@ -83,6 +84,9 @@ def main():
             ok = False
         if res.participants != world - 1 or res.attempts != 1 or not torch.equal(job.input, before):
             print(f"{me}: participants {res.participants} attempts {res.attempts}", flush=True)
+            ok = False
+        if reported != [crashed]:  # the culprit travels with the failure (allreduce.hpp:341-359, :505-506)
+            print(f"{me}: reported {reported}, expected [{crashed!r}]", flush=True)
             ok = False
         if rank == 0:
             store.set("survivors_done", b"1")
