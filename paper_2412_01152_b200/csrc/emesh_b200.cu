@@ -1194,6 +1194,7 @@ int nccl_settle(emesh_engine* e, ncclResult_t r, const char* what) {
         if (waited * 1e9 > wait_budget_ns(e)) {
             e->failed = true;
             if (e->h_gate) *e->h_gate = 0u;  // nothing of this round may commit
+            if (e->k > 1) e->culprit = (int32_t)((e->rank + e->k - 1) % e->k);  // we wait on the predecessor
             ncclCommAbort(e->comm);
             e->comm = nullptr;
             return fail(EMESH_ERING, "NCCL %s did not complete within step_timeout (%.1f s)", what,
@@ -1204,6 +1205,7 @@ int nccl_settle(emesh_engine* e, ncclResult_t r, const char* what) {
     if (r != ncclSuccess) {
         e->failed = true;
         if (e->h_gate) *e->h_gate = 0u;
+        if (e->k > 1) e->culprit = (int32_t)((e->rank + e->k - 1) % e->k);
         ncclCommAbort(e->comm);
         e->comm = nullptr;
         return fail(EMESH_ENCCL, "NCCL %s: %s", what, ncclGetErrorString(r));
