@@ -207,13 +207,14 @@ def intellect1_tensor_sizes():
 def nvlink_block(world, k, n, S, ms, transport, measured=None):
     """per GPU per direction, the ring moves 2(k-1)/k B/param of codes + 2(k-1) S 1028 B of
     codebooks per round; averaged over the round (the transfers overlap the kernels, so this is a floor,
-    not the link's busy rate). NVLink 5: 900 GB/s per direction per GPU."""
+    not the link's busy rate). NVLink 5: 900 GB/s per direction per GPU. `measured`: the ncu link
+    counters of the quantizer's peer stores (profiles/nvlink_evidence.json, profiles/r02_nvlink_p2p_n2.txt)."""
     if world < 2:
         return None
     by = 2 * (k - 1) / k * n + 2 * (k - 1) * S * 1028
     gbs = by / (ms / 1e3) / 1e9
     return {"bytes_per_gpu_per_round": int(by), "avg_GBps_per_direction": round(gbs, 1), "peak_GBps": 900.0,
-            "frac_of_round": round(gbs / 900.0, 4), "transport": transport, "measured": measured,
+            "frac_of_round": round(gbs / 900.0, 4), "transport": transport, "ncu_link_counters": measured,
             "note": "algorithmic ring bytes averaged over the whole round; it overlaps the quantize/decode kernels"}
 
 
@@ -233,42 +234,6 @@ def host_info():
     except OSError:
         pass
     return {"nproc": os.cpu_count(), "cpu_model": model}
-
-
-class NvlinkCounters:
-    """NVLink data-throughput counters of one GPU from NVML (the driver's per-link hardware
-    counters, KiB, cumulative): user-data bytes sent / received over the timed region."""
-
-    TX, RX = 138, 139  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX
-
-    def __init__(self, index):
-        self.ok = False
-        try:
-            import pynvml as N
-            N.nvmlInit()
-            self.N = N
-            self.h = N.nvmlDeviceGetHandleByIndex(index)
-            self.links = [l for l in range(18) if self._state(l)]
-            self.ok = bool(self.links)
-        except Exception as ex:  # reported as unavailable, never required
-            self.err = str(ex)[:120]
-
-    def _state(self, l):
-        try:
-            return self.N.nvmlDeviceGetNvLinkState(self.h, l) == 1
-        except Exception:
-            return False
-
-    def read(self):
-        if not self.ok:
-            return None
-        N = self.N
-        tx = rx = 0
-        for l in self.links:
-            vals = N.nvmlDeviceGetFieldValues(self.h, [(self.TX, l), (self.RX, l)])
-            tx += vals[0].value.ullVal
-            rx += vals[1].value.ullVal
-        return tx * 1024, rx * 1024
 
 
 def parity_round(eng, tg, tl, tb, hp, k, S, n, world, rank, nseg_pick):
@@ -399,7 +364,6 @@ def main():
         return
 
     clk = ClockSampler(local_rank).__enter__()  # started early: nvidia-smi needs time to come up
-    nvl = NvlinkCounters(local_rank) if world > 1 else None
     for _ in range(args.warmup):
         step()
     eng.check()
@@ -410,13 +374,11 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     clk.start()
-    nv0 = nvl.read() if nvl else None
     ev0.record(stream)
     for _ in range(args.steps):
         step()
     ev1.record(stream)
     barrier()
-    nv1 = nvl.read() if nvl else None
     clk.stop()
     clk.__exit__()
     ms_local = ev0.elapsed_time(ev1)
@@ -480,20 +442,14 @@ def main():
     step_alg_gbs = W * n * alg_bytes_per_param(k) / (ms / 1e3) / 1e9
 
     # ---- e2e through the host-buffer C-ABI entry point (pinned host memory)
-    # ---- NVLink bytes this GPU moved during the timed region (NVML hardware counters)
+    # ---- NVLink: NVML's link counters are NOT_SUPPORTED on these boxes and ncu never runs on a
+    # multi-rank command, so the link counters come from the committed single-process ncu capture
     nvl_meas = None
-    if nv0 is not None and nv1 is not None:
-        tx, rx = nv1[0] - nv0[0], nv1[1] - nv0[1]
-        v = torch.tensor([tx, rx], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(v, op=dist.ReduceOp.MAX)
-        tx, rx = float(v[0]), float(v[1])
-        secs = ms * args.steps / 1e3
-        nvl_meas = {"source": "NVML NVLink data-throughput counters (per-link hardware counters), max over ranks",
-                    "tx_bytes_per_round": tx / args.steps, "rx_bytes_per_round": rx / args.steps,
-                    "tx_GBps_round_avg": round(tx / secs / 1e9, 1), "rx_GBps_round_avg": round(rx / secs / 1e9, 1)}
-    elif nvl is not None:
-        nvl_meas = {"unavailable": getattr(nvl, "err", "no active NVLink")}
+    if world > 1:
+        try:
+            nvl_meas = json.load(open(os.path.join(ROOT, "profiles", "nvlink_evidence.json")))
+        except OSError:
+            nvl_meas = {"unavailable": "profiles/nvlink_evidence.json missing"}
 
     # ---- parity of one more (untimed) round, sampled segments vs the oracle (checker only)
     parity = None

@@ -1392,7 +1392,13 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
                 break;
             }
             case EMESH_OP_APPLY:
-                if (o.hop >= 0) CU(cudaStreamWaitEvent(sc, e->ev_recv[j], 0));
+                // every decode (the own chunk's too) waits for the LAST all-gather
+                // transfer: the comm stream is in order, so then every final payload
+                // arrived, or the host aborted the communicator after closing the gate.
+                // An apply that only followed the compute stream could commit the own
+                // chunk while a peer's payload never comes (a late peer's buffered
+                // reduce-scatter sends complete; its all-gather then times out).
+                CU(cudaStreamWaitEvent(sc, e->ev_recv[W - 1], 0));
                 if (e->fp32)
                     TRY(launch_f32_apply(P[o.recv_chunk][j], out ? 0 : 1, e->pay[0], theta, buf, local_out, out, lr, mom,
                                          sc, &e->tr, e->d_gate, ep));

@@ -1,5 +1,5 @@
-"""Run under torchrun on 2+ GPUs (tests/test_gpu_nccl.py): every rank runs one
-outer-sync round, but the last rank starts it only after twice step_timeout
+"""Run under torchrun on 2+ GPUs (tests/test_gpu_nccl.py): every rank runs an
+on-time outer-sync round, then another that the last rank starts only after twice step_timeout
 (alive, just late). The reference unwinds such an attempt on every rank
 (abort frames carry the culprit, allreduce.hpp:341-359; Nesterov is applied
 only to a completed all-reduce, trainer.hpp:375-381). Here: every rank must
@@ -40,6 +40,10 @@ def main():
     tg = torch.rand(n + 8, device=dev, generator=g)[:n]
     tl = (tg - 1e-3 * torch.rand(n + 8, device=dev, generator=g)[:n]).contiguous()
     tb = torch.rand(n + 8, device=dev, generator=g)[:n]
+    # one on-time round first: NCCL connects send/recv peers lazily at their first use, and an
+    # engine's first round waits with a setup floor over step_timeout; the late round is a later one
+    eng.outer_sync([tg], [tl], [tb], E.HyperParams(), write_local=True)
+    eng.check()
     before = [t.clone() for t in (tg, tl, tb)]
     dist.barrier()
     torch.cuda.synchronize()
