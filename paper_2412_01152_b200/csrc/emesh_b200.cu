@@ -933,8 +933,8 @@ struct emesh_engine {
     uint2* meta = nullptr;        // by slot: {ring chunk, elements}
     // NCCL transport's gate: page-locked host word mapped into the device; the host sets it to
     // the round number when it enqueues a round and to 0 when it aborts the communicator
-    volatile uint32_t* h_gate = nullptr;
-    uint32_t* d_gate = nullptr;
+    volatile uint32_t* h_gate = nullptr;  // NCCL transport: kGateSlots page-locked gate words (one per round in flight)
+    uint32_t* gate_dev = nullptr;         // ... and the device word the decodes read (copied once per round)
     uint32_t plan_epoch = 0;      // RingPlan epoch (ChunkMsg epoch)
     unsigned long long job = 0;   // ReduceJob id of the next round (ChunkMsg job)
     bool job_set = false;
@@ -1184,6 +1184,15 @@ double wait_budget_ns(const emesh_engine* e) {
     return std::max((double)e->tr.timeout_ns, (double)e->setup_floor_ns);
 }
 
+// The NCCL transport's commit gates: page-locked host words the decode
+// kernels read, one per round in flight (the host may enqueue later rounds
+// before the GPU reaches this round's decodes). A failure closes all of them.
+constexpr uint32_t kGateSlots = 256;
+void close_nccl_gates(emesh_engine* e) {
+    if (e->h_gate)
+        for (uint32_t i = 0; i < kGateSlots; ++i) e->h_gate[i] = 0u;
+}
+
 int nccl_settle(emesh_engine* e, ncclResult_t r, const char* what) {
     const auto t0 = std::chrono::steady_clock::now();
     int spins = 0;
@@ -1193,7 +1202,7 @@ int nccl_settle(emesh_engine* e, ncclResult_t r, const char* what) {
         const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (waited * 1e9 > wait_budget_ns(e)) {
             e->failed = true;
-            if (e->h_gate) *e->h_gate = 0u;  // nothing of this round may commit
+            close_nccl_gates(e);  // nothing of this round may commit
             if (e->k > 1) e->culprit = (int32_t)((e->rank + e->k - 1) % e->k);  // we wait on the predecessor
             ncclCommAbort(e->comm);
             e->comm = nullptr;
@@ -1204,7 +1213,7 @@ int nccl_settle(emesh_engine* e, ncclResult_t r, const char* what) {
     }
     if (r != ncclSuccess) {
         e->failed = true;
-        if (e->h_gate) *e->h_gate = 0u;
+        close_nccl_gates(e);
         if (e->k > 1) e->culprit = (int32_t)((e->rank + e->k - 1) % e->k);
         ncclCommAbort(e->comm);
         e->comm = nullptr;
@@ -1243,7 +1252,7 @@ int nccl_drain(emesh_engine* e, std::initializer_list<cudaStream_t> streams, con
         const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (err || waited * 1e9 > wait_budget_ns(e)) {
             e->failed = true;
-            if (e->h_gate) *e->h_gate = 0u;  // the decodes still queued behind the aborted transfers skip
+            close_nccl_gates(e);  // the decodes still queued behind the aborted transfers skip
             e->culprit = (int32_t)((e->rank + e->k - 1) % e->k);  // every receive of the NCCL ring is from the predecessor
             if (e->comm) ncclCommAbort(e->comm);
             e->comm = nullptr;
@@ -1339,7 +1348,12 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
     cudaStream_t sc = e->s_comp, sm = e->s_comm;
     if (!e->comm) return fail(EMESH_ERING, "NCCL communicator was aborted by an earlier ring failure");
     const uint32_t ep = ++e->epoch;
-    *e->h_gate = ep;  // the decodes commit unless the host aborts the communicator (nccl_abort)
+    // the decodes commit unless the host aborts the communicator (nccl_drain / nccl_settle):
+    // this round's host gate word is copied to the device word the decodes read once every
+    // all-gather transfer finished (or was aborted), one DMA per round
+    volatile uint32_t* const h_gate = e->h_gate + ep % kGateSlots;
+    *h_gate = ep;
+    bool gate_loaded = false;
     const auto& P = e->plan.batches;
     const uint32_t W = (uint32_t)P[0].size();
     for (uint32_t c = 1; c < k; ++c)
@@ -1399,15 +1413,20 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
                 // chunk while a peer's payload never comes (a late peer's buffered
                 // reduce-scatter sends complete; its all-gather then times out).
                 CU(cudaStreamWaitEvent(sc, e->ev_recv[W - 1], 0));
+                if (!gate_loaded) {
+                    CU(cudaMemcpyAsync(e->gate_dev, const_cast<const uint32_t*>(h_gate), sizeof(uint32_t),
+                                       cudaMemcpyHostToDevice, sc));
+                    gate_loaded = true;
+                }
                 if (e->fp32)
                     TRY(launch_f32_apply(P[o.recv_chunk][j], out ? 0 : 1, e->pay[0], theta, buf, local_out, out, lr, mom,
-                                         sc, &e->tr, e->d_gate, ep));
+                                         sc, &e->tr, e->gate_dev, ep));
                 else if (out)
                     TRY(launch_apply(P[o.recv_chunk][j], 0, ar.codes, ar.cbs, nullptr, nullptr, nullptr, out, 0.f, 0.f,
-                                     sc, &e->tr, e->d_gate, ep));
+                                     sc, &e->tr, e->gate_dev, ep));
                 else
                     TRY(launch_apply(P[o.recv_chunk][j], 1, ar.codes, ar.cbs, theta, buf, local_out, nullptr, lr, mom,
-                                     sc, &e->tr, e->d_gate, ep));
+                                     sc, &e->tr, e->gate_dev, ep));
                 break;
             default:
                 return fail(EMESH_ECONFIG, "bad schedule op");
@@ -1430,7 +1449,13 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
 // commands' fixed cost would dominate).
 constexpr size_t kMaxDmaRuns = 16;
 constexpr uint64_t kMinDmaElems = (uint64_t)32 << 20;
-bool push_final_payload(const Batch& fb) { return fb.eruns.size() > kMaxDmaRuns || fb.elems < kMinDmaElems; }
+bool push_final_payload(const Batch& fb) {
+#ifdef EMESH_PUSH_FINAL_ALWAYS
+    return true;
+#else
+    return fb.eruns.size() > kMaxDmaRuns || fb.elems < kMinDmaElems;
+#endif
+}
 
 // Owner's final chunk -> every other rank by DMA (see run_p2p), in segment
 // groups: codes (or fp32 means), codebooks and ChunkMsg headers. The owner's
@@ -1938,13 +1963,13 @@ int emesh_engine_create(const emesh_engine_config* cfg, emesh_engine** out) {
         cudaEventCreateWithFlags(&e->ev_recv[j], cudaEventDisableTiming);
     }
     if (!virt && e->k > 1) {
-        {   // the NCCL transport's commit gate: a page-locked host word the decode kernels read
+        {   // the NCCL transport's commit gates: page-locked host words (see run_nccl)
             void* h = nullptr;
-            if (cudaHostAlloc(&h, 64, cudaHostAllocMapped) != cudaSuccess ||
-                cudaHostGetDevicePointer((void**)&e->d_gate, h, 0) != cudaSuccess)
+            if (cudaHostAlloc(&h, kGateSlots * sizeof(uint32_t), cudaHostAllocDefault) != cudaSuccess ||
+                cudaMalloc(&e->gate_dev, sizeof(uint32_t)) != cudaSuccess)
                 return bail(fail(EMESH_ECUDA, "gate word allocation"));
             e->h_gate = static_cast<volatile uint32_t*>(h);
-            *e->h_gate = 0u;
+            close_nccl_gates(e);
         }
         e->schedule = build_schedule(e->plan, e->rank);
         ncclUniqueId id;
@@ -2006,6 +2031,7 @@ int emesh_engine_destroy(emesh_engine* e) {
     nccl_close(e);  // aborts when a round failed: peers may be gone
     for (auto& a : e->arenas) { cudaFree(a.codes); cudaFree(a.cbs); cudaFree(a.stats); }
     if (e->h_gate) cudaFreeHost(const_cast<uint32_t*>(e->h_gate));
+    if (e->gate_dev) cudaFree(e->gate_dev);
     for (auto* p : e->pay) cudaFree(p);
     for (auto* p : e->h_theta) cudaFree(p);
     for (auto* p : e->h_local) cudaFree(p);

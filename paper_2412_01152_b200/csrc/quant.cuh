@@ -87,8 +87,8 @@ __device__ __forceinline__ float4 ld4(const float* p, uint64_t q) {
 
 struct __align__(16) QSmem {
     uint32_t hist[kWarps][kBuckets + 1][3];  // per-warp limbs over the tile (bin), see bin_unit; row 256: sink
-    uint2 bsk[2 * kBuckets];             // per bucket {high word of s, high word of K} (bin), twice:
-                                         // index code | 256 = same bucket (see kInfoWide)
+    double2 bsk[2 * kBuckets];           // per bucket {s, K} (bin), twice: index code | 256 = same bucket
+                                         // (see kInfoWide); whole doubles, so the fma needs no moves
     float thr[kBuckets + 2];             // exact threshold table (bin); [257] = bucket 0's base (lo_up)
     float lut[kBuckets];                 // incoming codebook (stats, hop)
     StatP wp[kWarps];
@@ -98,6 +98,7 @@ struct __align__(16) QSmem {
     uint32_t task;
     int32_t bin_seg, lut_seg, ready_seg;
     uint32_t run_idx;
+    uint32_t cnt_one;  // 1 << kCntShift, read back from smem (an opaque register for lop3_and_or)
 };
 
 // Task order (host-built run table, QuantArgs::runs): the STATS tiles of
@@ -149,7 +150,7 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
         }
     }
     StatP p{0.0, 0.0, 0.0, 0.0, 0};
-    double sum0 = 0.0, sum1 = 0.0, d0 = 0.0, d1 = 0.0, q0 = 0.0, q1 = 0.0;
+    double sum0 = 0.0, sum1 = 0.0, q0 = 0.0, q1 = 0.0;
     double piv = 0.0;
     uint32_t cnt = 0;
     bool have_piv = false;
@@ -204,8 +205,6 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
                     const double v2 = __dsub_rn(x2, piv), v3 = __dsub_rn(x3, piv);
                     sum0 = __dadd_rn(__dadd_rn(sum0, x0), x2);
                     sum1 = __dadd_rn(__dadd_rn(sum1, x1), x3);
-                    d0 = __dadd_rn(__dadd_rn(d0, v0), v2);
-                    d1 = __dadd_rn(__dadd_rn(d1, v1), v3);
                     // sigma is not bit-exact vs the sequential reference anyway:
                     // fused multiply-adds for the squares
                     q0 = __fma_rn(v2, v2, __fma_rn(v0, v0, q0));
@@ -222,7 +221,6 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
                             if (!have_piv) { piv = xd; have_piv = true; }
                             const double dv = __dsub_rn(xd, piv);
                             sum0 = __dadd_rn(sum0, xd);
-                            d0 = __dadd_rn(d0, dv);
                             q0 = __fma_rn(dv, dv, q0);
                             cnt += 1;
                             if (SRC != kSrcA) reinterpret_cast<float*>(xs + q)[e] = x[e];
@@ -233,7 +231,10 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
         }
         if (interior) cnt += kSlotsPerLane * 4;  // per lane
     }
-    p = StatP{__dadd_rn(sum0, sum1), __dadd_rn(q0, q1), __dadd_rn(d0, d1), piv, (uint64_t)cnt};
+    // D = sum (x - p) of the lane, as sum x - n p (sigma's pivot correction, see finalize_stats;
+    // sigma is not reproduced bit-for-bit either way)
+    const double sx = __dadd_rn(sum0, sum1);
+    p = StatP{sx, __dadd_rn(q0, q1), __dsub_rn(sx, __dmul_rn((double)cnt, piv)), piv, (uint64_t)cnt};
     p = warp_merge(p);
     if (lane == 0) {
         sm.wp[warp] = p;
@@ -341,7 +342,16 @@ __device__ void finalize_stats(const QuantArgs& a, QSmem& sm, uint32_t s, const 
 
 struct BinParams {
     float c, inv_w, lo_up, hi_dn, margin, one_m;  // bucket estimate g = fma(x, inv_w, -c)
+    uint32_t cnt_one;                              // 1 << kCntShift, in a register (see lop3_and_or)
 };
+// (a & b) | c in one LOP3: c comes from a register, so ptxas cannot split the
+// two immediates into two instructions.
+template <uint32_t B>
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "n"(B), "r"(c));
+    return d;
+}
 
 // One warp unit of the bin pass (1024 elements; this lane's 32), in groups of
 // 8: bucket estimates for all 8, rare fix-ups (exact table near an edge,
@@ -430,18 +440,20 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
             // fixed point r(x) (see kInfoWide), split into the limbs
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const uint2 sk = sm.bsk[cc[i]];
+                const double2 sk = sm.bsk[cc[i]];
                 // m = x * s + K in [2^52, 2^53): mantissa = r (see kInfoWide)
-                const double sc = __hiloint2double((int)sk.x, 0);
-                const double kk = __hiloint2double((int)sk.y, 0);
-                const double m = __fma_rn((double)xe[i], sc, kk);
+                const double m = __fma_rn((double)xe[i], sk.x, sk.y);
                 const uint32_t rlo = (uint32_t)__double2loint(m);
                 const uint32_t rhi = (uint32_t)__double2hiint(m);
                 uint32_t* hc = hw + 3 * min(cc[i], kBuckets);
-                red_shared_add(hc, (rlo & ((1u << kLoBits) - 1u)) | (1u << kCntShift));
+                red_shared_add(hc, lop3_and_or<(1u << kLoBits) - 1u>(rlo, p.cnt_one));
                 red_shared_add(hc + 1, (rlo >> kLoBits) & ((1u << (kMidEnd - kLoBits)) - 1u));
                 const uint32_t rc = __funnelshift_r(rlo, rhi, kMidEnd) & ((1u << (42 - kMidEnd)) - 1u);
-                if (rc) red_shared_add(hc + 2, rc);
+#ifdef EMESH_Q_RC_ALWAYS
+                red_shared_add(hc + 2, rc);
+#else
+                red_shared_add_nz(hc + 2, rc);  // nonzero mostly in the wide bucket
+#endif
             }
             const uint32_t p0 = __byte_perm(__byte_perm(cc[0], cc[1], 0x0040), __byte_perm(cc[2], cc[3], 0x0040), 0x5410);
             const uint32_t p1 = __byte_perm(__byte_perm(cc[4], cc[5], 0x0040), __byte_perm(cc[6], cc[7], 0x0040), 0x5410);
@@ -500,7 +512,8 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
         const int b = threadIdx.x;
         sm.thr[b] = b == 0 ? -INFINITY : __ldcg(&st->thr[b]);
         const uint32_t info = __ldcg(&st->binfo[b]);
-        const uint2 sk = make_uint2(info & ~kInfoWide, 0x43300000u | ((info & kInfoWide) << 9));  // K = 2^52 (+2^41)
+        const double2 sk = make_double2(__hiloint2double((int)(info & ~kInfoWide), 0),  // K = 2^52 (+2^41)
+                                        __hiloint2double((int)(0x43300000u | ((info & kInfoWide) << 9)), 0));
         sm.bsk[b] = sm.bsk[kBuckets + b] = sk;
 
         if (b == 0) {
@@ -521,7 +534,7 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
     const uint64_t hiel = si.lo + si.len;
     const float4* xs = reinterpret_cast<const float4*>(a.scratch) + ((int64_t)si.sq0 - (int64_t)si.q0);
     uint32_t nclip_lo = 0, nclip_hi = 0;
-    const BinParams bpar{c_f, inv_w, lo_up, hi_dn, margin, one_m};
+    const BinParams bpar{c_f, inv_w, lo_up, hi_dn, margin, one_m, sm.cnt_one};
     for (int ui = 0; ui < (int)si.upw; ++ui) {
         const uint32_t u = (tile * si.upw + ui) * kWarps + warp;
         if (u >= si.nunits) break;
@@ -660,6 +673,7 @@ __global__ void __launch_bounds__(kThreads, kQuantMinBlocks) k_quant(QuantArgs a
         for (uint32_t i = threadIdx.x; i < a.nseg; i += kThreads) segs_s[i] = a.segs[i];
     uint32_t nxt = 0;  // thread 0: the next task, claimed at the start of the current one
     if (threadIdx.x == 0) {
+        sm.cnt_one = 1u << kCntShift;
         sm.bin_seg = -1;
         sm.lut_seg = -1;
         sm.ready_seg = -1;

@@ -58,7 +58,8 @@ def main():
         print(f"{ids[rank]}: RingFailureError (culprit {culprit!r}): {ex}", flush=True)
     torch.cuda.synchronize()
     untouched = all(torch.equal(a, b) for a, b in zip((tg, tl, tb), before))
-    ok = failed and untouched and culprit in (ids[-1], "")
+    # the on-time ranks name the late one (or nobody); the late rank itself sees its peers gone
+    ok = failed and untouched and (rank == world - 1 or culprit in (ids[-1], ""))
     print(f"{ids[rank]}: slow-peer {'OK' if ok else 'FAILED'} [{transport}] failed={failed} untouched={untouched}",
           flush=True)
     store.set(f"done/{rank}", b"1")
