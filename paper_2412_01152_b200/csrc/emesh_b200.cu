@@ -549,8 +549,13 @@ int persistent_grid(const void* fn, uint32_t ntasks) {
         if (!per_sm) {
             if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQuantSmemBytes) != cudaSuccess)
                 return -1;
-            // leave L1 room for the prefetched scratch lines (smem only as large as the CTAs need)
-            cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 64);
+            // the smallest carveout that holds kQuantMinBlocks CTAs (+1 KB reserved each): the rest
+            // of the 256 KB stays L1, which stages the in-flight global loads
+            int smem_sm = 0;
+            cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+            const size_t need = (size_t)kQuantMinBlocks * (kQuantSmemBytes + 1024);
+            int pct = smem_sm > 0 ? (int)((100 * need + smem_sm - 1) / (size_t)smem_sm) : 100;
+            cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, std::min(pct, 100));
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, kQuantSmemBytes) != cudaSuccess)
                 return -1;
             cache.push_back({fn, per_sm});

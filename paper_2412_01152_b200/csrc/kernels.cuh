@@ -169,11 +169,6 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ void red_shared_add(uint32_t* p, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
 }
-// predicated (no branch): adds only when v != 0
-__device__ __forceinline__ void red_shared_add_nz(uint32_t* p, uint32_t v) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q red.shared.add.u32 [%0], %1;\n\t}"
-                 ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
-}
 // Cross-GPU signalling (peer transport): flags live in the receiver's memory.
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
     uint32_t v;

@@ -87,10 +87,10 @@ __device__ __forceinline__ float4 ld4(const float* p, uint64_t q) {
 
 struct __align__(16) QSmem {
     uint32_t hist[kWarps][kBuckets + 1][3];  // per-warp limbs over the tile (bin), see bin_unit; row 256: sink
-    double2 bsk[2 * kBuckets];           // per bucket {s, K} (bin), twice: index code | 256 = same bucket
-                                         // (see kInfoWide); whole doubles, so the fma needs no moves
-    float thr[kBuckets + 2];             // exact threshold table (bin); [257] = bucket 0's base (lo_up)
+    uint32_t binfo[kBuckets];            // bucket encodings (bin, see kInfoWide): one 32-bit lookup per
+                                         // element (a 64/128-bit table measured slower: more smem wavefronts)
     float lut[kBuckets];                 // incoming codebook (stats, hop)
+    float thr[kBuckets + 2];             // exact threshold table (bin); [257] = bucket 0's base (lo_up)
     StatP wp[kWarps];
     double red[2];
     uint32_t clip[2];
@@ -116,8 +116,8 @@ enum : uint32_t { kTaskStats = 0, kTaskBin = 2 };
 // mixed run (alternating STATS / BIN tasks): y = kTaskMix{Rev,Fwd} | bin segment << 2,
 // z = STATS segment, w = first STATS tile | first BIN tile << 16
 constexpr uint32_t kTaskMixRev = 1, kTaskMixFwd = 3;
-constexpr uint32_t kMaxRunsSmem = 512;  // run table cached in smem when it fits (8 KB)
-constexpr uint32_t kMaxSegsSmem = 128;  // SegInfo cached in smem when it fits (6 KB)
+constexpr uint32_t kMaxRunsSmem = 256;  // run table cached in smem when it fits (4 KB)
+constexpr uint32_t kMaxSegsSmem = 128;  // SegInfo cached in smem when it fits
 
 
 
@@ -440,20 +440,20 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
             // fixed point r(x) (see kInfoWide), split into the limbs
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const double2 sk = sm.bsk[cc[i]];
-                // m = x * s + K in [2^52, 2^53): mantissa = r (see kInfoWide)
-                const double m = __fma_rn((double)xe[i], sk.x, sk.y);
+                const uint32_t info = sm.binfo[cc[i] & 0xff];  // sink members: their bucket's entry
+                // m = x * s + K in [2^52, 2^53): mantissa = r (see kInfoWide); s = the entry's
+                // high word, K = 2^52 (+ 2^41 for the wide bucket)
+                const double sc = __hiloint2double((int)(info & ~kInfoWide), 0);
+                const double kk = __hiloint2double((int)(0x43300000u | ((info & kInfoWide) << 9)), 0);
+                const double m = __fma_rn((double)xe[i], sc, kk);
                 const uint32_t rlo = (uint32_t)__double2loint(m);
                 const uint32_t rhi = (uint32_t)__double2hiint(m);
                 uint32_t* hc = hw + 3 * min(cc[i], kBuckets);
                 red_shared_add(hc, lop3_and_or<(1u << kLoBits) - 1u>(rlo, p.cnt_one));
                 red_shared_add(hc + 1, (rlo >> kLoBits) & ((1u << (kMidEnd - kLoBits)) - 1u));
                 const uint32_t rc = __funnelshift_r(rlo, rhi, kMidEnd) & ((1u << (42 - kMidEnd)) - 1u);
-#ifdef EMESH_Q_RC_ALWAYS
-                red_shared_add(hc + 2, rc);
-#else
-                red_shared_add_nz(hc + 2, rc);  // nonzero mostly in the wide bucket
-#endif
+                if (rc) red_shared_add(hc + 2, rc);  // nonzero mostly in the wide bucket (an unconditional
+                                                     // third atomic measured 1.3 % slower)
             }
             const uint32_t p0 = __byte_perm(__byte_perm(cc[0], cc[1], 0x0040), __byte_perm(cc[2], cc[3], 0x0040), 0x5410);
             const uint32_t p1 = __byte_perm(__byte_perm(cc[4], cc[5], 0x0040), __byte_perm(cc[6], cc[7], 0x0040), 0x5410);
@@ -512,9 +512,7 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
         const int b = threadIdx.x;
         sm.thr[b] = b == 0 ? -INFINITY : __ldcg(&st->thr[b]);
         const uint32_t info = __ldcg(&st->binfo[b]);
-        const double2 sk = make_double2(__hiloint2double((int)(info & ~kInfoWide), 0),  // K = 2^52 (+2^41)
-                                        __hiloint2double((int)(0x43300000u | ((info & kInfoWide) << 9)), 0));
-        sm.bsk[b] = sm.bsk[kBuckets + b] = sk;
+        sm.binfo[b] = info;
 
         if (b == 0) {
             sm.thr[kBuckets] = INFINITY;
