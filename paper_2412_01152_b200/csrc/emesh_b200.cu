@@ -602,6 +602,7 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     for (uint32_t f = 0; f < io.nflags; ++f) a.sflag[f] = io.flags[f];
     a.nflag = io.nflags;
     if (a.ndest == 0) return fail(EMESH_ECONFIG, "quantizer without a destination");
+    a.ndest_fail = io.local_out ? 1 : a.ndest;  // a failed owner keeps its final payload local
     a.in_flag = io.in_flag;
     a.epoch = io.epoch;
     a.timeout_ns = tr ? tr->timeout_ns : 30ull * 1000000000ull;
@@ -993,6 +994,7 @@ struct F32IO {
     HdrRef hdr{};
     uint32_t phase_out = kPhaseRS;
     uint32_t culprit_in = kNoCulprit;
+    uint32_t ndest_fail = 0;  // destinations still written after a failure (0: all; see QuantArgs::ndest_fail)
 };
 
 int launch_f32_hop(const Batch& bt, Workspace& ws, const F32IO& io, cudaStream_t st, Tracker* tr) {
@@ -1007,6 +1009,7 @@ int launch_f32_hop(const Batch& bt, Workspace& ws, const F32IO& io, cudaStream_t
     int ex = 0;
     a.inv_divisor = std::frexp(io.k, &ex) == 0.5f ? std::ldexp(1.0f, 1 - ex) : 0.f;
     a.ndest = io.ndest;
+    a.ndest_fail = io.ndest_fail ? std::min(io.ndest_fail, io.ndest) : io.ndest;
     for (uint32_t d = 0; d < io.ndest; ++d) a.dst[d] = io.dst[d];
     a.nflag = io.nflags;
     for (uint32_t f = 0; f < io.nflags; ++f) a.sflag[f] = io.flags[f];
@@ -1193,6 +1196,14 @@ double wait_budget_ns(const emesh_engine* e) {
 // kernels read, one per round in flight (the host may enqueue later rounds
 // before the GPU reaches this round's decodes). A failure closes all of them.
 constexpr uint32_t kGateSlots = 256;
+// The rank a timed-out NCCL wait can name: every receive of the ring is from
+// the predecessor, but past k = 2 a blocked predecessor may itself be waiting
+// on a dead rank further up (NCCL carries no abort frames, allreduce.hpp:341-359),
+// so the culprit is known only with a single peer; -1 = unknown (the
+// membership service's own failure detection evicts the dead rank).
+int32_t nccl_suspect(const emesh_engine* e) {
+    return e->k == 2 ? (int32_t)((e->rank + 1) % 2) : -1;
+}
 void close_nccl_gates(emesh_engine* e) {
     if (e->h_gate)
         for (uint32_t i = 0; i < kGateSlots; ++i) e->h_gate[i] = 0u;
@@ -1208,7 +1219,7 @@ int nccl_settle(emesh_engine* e, ncclResult_t r, const char* what) {
         if (waited * 1e9 > wait_budget_ns(e)) {
             e->failed = true;
             close_nccl_gates(e);  // nothing of this round may commit
-            if (e->k > 1) e->culprit = (int32_t)((e->rank + e->k - 1) % e->k);  // we wait on the predecessor
+            e->culprit = nccl_suspect(e);
             ncclCommAbort(e->comm);
             e->comm = nullptr;
             return fail(EMESH_ERING, "NCCL %s did not complete within step_timeout (%.1f s)", what,
@@ -1219,7 +1230,7 @@ int nccl_settle(emesh_engine* e, ncclResult_t r, const char* what) {
     if (r != ncclSuccess) {
         e->failed = true;
         close_nccl_gates(e);
-        if (e->k > 1) e->culprit = (int32_t)((e->rank + e->k - 1) % e->k);
+        e->culprit = nccl_suspect(e);
         ncclCommAbort(e->comm);
         e->comm = nullptr;
         return fail(EMESH_ENCCL, "NCCL %s: %s", what, ncclGetErrorString(r));
@@ -1258,7 +1269,7 @@ int nccl_drain(emesh_engine* e, std::initializer_list<cudaStream_t> streams, con
         if (err || waited * 1e9 > wait_budget_ns(e)) {
             e->failed = true;
             close_nccl_gates(e);  // the decodes still queued behind the aborted transfers skip
-            e->culprit = (int32_t)((e->rank + e->k - 1) % e->k);  // every receive of the NCCL ring is from the predecessor
+            e->culprit = nccl_suspect(e);
             if (e->comm) ncclCommAbort(e->comm);
             e->comm = nullptr;
             for (cudaStream_t st : streams) cudaStreamSynchronize(st);
@@ -1291,6 +1302,35 @@ int xfer_window(emesh_engine* e, const Batch& snd, const Batch& rcv) {
     for (const auto& r : rcv.eruns) NCS(ncclRecv(ar.codes + r.first, r.second, ncclUint8, pred, e->comm, e->s_comm));
     NCS(ncclRecv(ar.cbs + (size_t)rcv.slot0 * kBuckets, (size_t)rcv.nseg * kBuckets, ncclFloat32, pred, e->comm,
                 e->s_comm));
+    NCS(ncclGroupEnd());
+    return EMESH_OK;
+}
+
+// All-gather of window j on the NCCL transport: every owner broadcasts its
+// final window (k grouped in-place broadcasts; the bytes are the ones the
+// reference's all-gather forwards hop by hop, allreduce.hpp:446-464). NCCL's
+// collective kernels spread a broadcast over all channels, where a send/recv
+// pair gets a couple per peer: the ring forwarding moved ~150 GB/s per
+// window at 4 GPUs.
+int bcast_window(emesh_engine* e, uint32_t j) {
+    const uint32_t k = e->k;
+    auto& ar = e->arenas[0];
+    NCS(ncclGroupStart());
+    for (uint32_t c = 0; c < k; ++c) {
+        const Batch& b = e->plan.batches[c][j];
+        const int root = (int)((c + k - 1) % k);  // owner of chunk c
+        if (e->fp32) {
+            for (const auto& ru : b.eruns)
+                NCS(ncclBroadcast(e->pay[0] + ru.first, e->pay[0] + ru.first, ru.second, ncclFloat32, root, e->comm,
+                                  e->s_comm));
+        } else {
+            for (const auto& ru : b.eruns)
+                NCS(ncclBroadcast(ar.codes + ru.first, ar.codes + ru.first, ru.second, ncclUint8, root, e->comm,
+                                  e->s_comm));
+            float* cb = ar.cbs + (size_t)b.slot0 * kBuckets;
+            NCS(ncclBroadcast(cb, cb, (size_t)b.nseg * kBuckets, ncclFloat32, root, e->comm, e->s_comm));
+        }
+    }
     NCS(ncclGroupEnd());
     return EMESH_OK;
 }
@@ -1392,6 +1432,13 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
                 // forwards the owner's final bytes, later AG hops bytes this
                 // stream itself received
                 if (o.phase == 0 || o.hop == 0) CU(cudaStreamWaitEvent(sm, e->ev_send[j], 0));
+#ifndef EMESH_NCCL_AG_RING
+                if (o.phase == 1) {  // the schedule's k-1 forwarding hops as one broadcast group
+                    if (o.hop == 0) TRY(bcast_window(e, j));
+                    CU(cudaEventRecord(e->ev_recv[j], sm));
+                    break;
+                }
+#endif
                 TRY(xfer_window(e, P[o.send_chunk][j], P[o.recv_chunk][j]));
                 CU(cudaEventRecord(e->ev_recv[j], sm));
                 break;
@@ -1448,70 +1495,15 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
 // hop's quantizer waits segment by segment. The owner's final payload goes
 // to every rank at once, which replaces the all-gather's k-1 forwarding hops
 // (the bytes are identical: AG forwards them verbatim, allreduce.hpp:446-464).
-// The owner's quantizer stores its final payload to every rank itself
-// (instead of the copy engines) when the final chunk has many contiguous runs
-// (multi-tensor plans: one DMA per run and peer) or is small (the DMA
-// commands' fixed cost would dominate).
-constexpr size_t kMaxDmaRuns = 16;
-constexpr uint64_t kMinDmaElems = (uint64_t)32 << 20;
-bool push_final_payload(const Batch& fb) {
-#ifdef EMESH_PUSH_FINAL_ALWAYS
-    return true;
-#else
-    return fb.eruns.size() > kMaxDmaRuns || fb.elems < kMinDmaElems;
-#endif
-}
-
-// Owner's final chunk -> every other rank by DMA (see run_p2p), in segment
-// groups: codes (or fp32 means), codebooks and ChunkMsg headers. The owner's
-// done word follows in stream order (p2p_commit).
-int p2p_allgather(emesh_engine* e, int par) {
-    const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
-    cudaStream_t cm = e->s_comm;
-    const Batch& fb = e->plan.batches[succ][0];
-    const uint32_t groups = std::min<uint32_t>(fb.nseg, 4);
-    for (uint32_t g = 0; g < groups; ++g) {
-        const uint32_t s0 = fb.slot0 + (uint32_t)((uint64_t)fb.nseg * g / groups);
-        const uint32_t s1 = fb.slot0 + (uint32_t)((uint64_t)fb.nseg * (g + 1) / groups);
-        if (s1 == s0) continue;
-        std::vector<std::pair<uint64_t, uint64_t>> runs;  // contiguous element runs of the group
-        for (uint32_t s = s0; s < s1; ++s) {
-            const Seg& sg = e->plan.segs[s];
-            if (!sg.len) continue;
-            if (!runs.empty() && runs.back().first + runs.back().second == sg.lo) runs.back().second += sg.len;
-            else runs.push_back({sg.lo, sg.len});
-        }
-        for (uint32_t d = 1; d < k; ++d) {
-            const uint32_t q = (r + d) % k;
-            if (e->fp32) {
-                for (const auto& ru : runs)
-                    CU(cudaMemcpyAsync(e->peers[q].pay[par] + ru.first, e->peers[r].pay[par] + ru.first,
-                                       ru.second * sizeof(float), cudaMemcpyDeviceToDevice, cm));
-            } else {
-                for (const auto& ru : runs)
-                    CU(cudaMemcpyAsync(e->peers[q].codes[par] + ru.first, e->peers[r].codes[par] + ru.first, ru.second,
-                                       cudaMemcpyDeviceToDevice, cm));
-                CU(cudaMemcpyAsync(e->peers[q].cbs[par] + (size_t)s0 * kBuckets,
-                                   e->peers[r].cbs[par] + (size_t)s0 * kBuckets,
-                                   (size_t)(s1 - s0) * kBuckets * sizeof(float), cudaMemcpyDeviceToDevice, cm));
-            }
-            CU(cudaMemcpyAsync(e->peers[q].hdr[par] + s0, e->peers[r].hdr[par] + s0, (size_t)(s1 - s0) * sizeof(ChunkHdr),
-                               cudaMemcpyDeviceToDevice, cm));
-        }
-    }
-    return EMESH_OK;
-}
-
 // The round's commit (peer transport), after this rank's last quantizer:
 // k_done_value turns this rank's error word into its done value (the round,
-// or poison naming the culprit); the copy engines deliver the owner's final
-// payload (unless the quantizer stored it itself) and then the done word to
-// every peer; k_round_gate waits for every other owner's done word,
-// validates the final payloads' headers and publishes the gate word that
-// every decode kernel of the round checks. A round that failed anywhere
+// or poison naming the culprit); the copy engines deliver it to every peer;
+// k_round_gate waits for every other owner's done word and final-payload
+// flags, validates the final payloads' headers and publishes the gate word
+// that every decode kernel of the round checks. A round that failed anywhere
 // therefore commits nowhere (theta / momentum untouched) and every rank
 // reports it.
-int p2p_commit(emesh_engine* e, int par, uint32_t ep, bool push_final) {
+int p2p_commit(emesh_engine* e, int par, uint32_t ep) {
     const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
     cudaStream_t sc = e->s_comp, cm = e->s_comm;
     k_done_value<<<1, 32, 0, sc>>>(e->ws.err, ep, e->done_src);
@@ -1519,7 +1511,6 @@ int p2p_commit(emesh_engine* e, int par, uint32_t ep, bool push_final) {
     CU(cudaGetLastError());
     CU(cudaEventRecord(e->ev_send[0], sc));
     CU(cudaStreamWaitEvent(cm, e->ev_send[0], 0));
-    if (!push_final) TRY(p2p_allgather(e, par));
     for (uint32_t d = 1; d < k; ++d) {  // after the payload (stream order)
         const uint32_t q = (r + d) % k;
         CU(cudaMemcpyAsync(e->peers[q].done + r, e->done_src, sizeof(uint32_t), cudaMemcpyDeviceToDevice, cm));
@@ -1537,7 +1528,7 @@ int p2p_commit(emesh_engine* e, int par, uint32_t ep, bool push_final) {
     g.nslots = (uint32_t)e->plan.segs.size();
     g.epoch = ep;
     g.timeout_ns = (unsigned long long)wait_budget_ns(e);
-    g.ag_flag = push_final ? e->ag_flag : nullptr;
+    g.ag_flag = e->ag_flag;
     k_round_gate<<<1, kThreads, 0, sc>>>(g);
     e->tr.launches += 1;
     CU(cudaGetLastError());
@@ -1555,7 +1546,6 @@ int run_p2p_f32(emesh_engine* e, const float* A, const float* B, float* theta, f
     const int par = (int)(ep & 1u);
     cudaStream_t sc = e->s_comp;
     const auto& P = e->plan.batches;
-    const bool push_final = push_final_payload(P[succ][0]);
     const HdrRef H = round_hdr(e);
     {
         F32IO io{A, B, nullptr};
@@ -1582,13 +1572,13 @@ int run_p2p_f32(emesh_engine* e, const float* A, const float* B, float* theta, f
             io.dst[0] = e->peers[r].pay[par];
             io.hdr_out[0] = e->peers[r].hdr[par];
             io.phase_out = kPhaseAG;
-            if (push_final)
-                for (uint32_t q = 0; q < k; ++q)
-                    if (q != r) {
-                        io.hdr_out[io.ndest] = e->peers[q].hdr[par];
-                        io.dst[io.ndest++] = e->peers[q].pay[par];
-                        io.flags[io.nflags++] = e->peers[q].ag_flag;
-                    }
+            io.ndest_fail = 1;  // a failed owner keeps its (garbage) final local
+            for (uint32_t q = 0; q < k; ++q)
+                if (q != r) {
+                    io.hdr_out[io.ndest] = e->peers[q].hdr[par];
+                    io.dst[io.ndest++] = e->peers[q].pay[par];
+                    io.flags[io.nflags++] = e->peers[q].ag_flag;
+                }
         } else {
             io.dst[0] = e->peers[succ].pay[par];
             io.hdr_out[0] = e->peers[succ].hdr[par];
@@ -1597,7 +1587,7 @@ int run_p2p_f32(emesh_engine* e, const float* A, const float* B, float* theta, f
         }
         TRY(launch_f32_hop(P[rc][0], e->ws, io, sc, &e->tr));
     }
-    TRY(p2p_commit(e, par, ep, push_final));
+    TRY(p2p_commit(e, par, ep));
     for (uint32_t d = 0; d < k; ++d) {
         const uint32_t c = (succ + k - d) % k;
         TRY(launch_f32_apply(P[c][0], out ? 0 : 1, e->peers[r].pay[par], theta, buf, local_out, out, lr, mom, sc,
@@ -1621,7 +1611,6 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
     e->job_set = false;
     if (e->fp32) return run_p2p_f32(e, A, B, theta, buf, local_out, out, lr, mom);
     const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k, pred = (r + k - 1) % k;
-    const bool push_final = push_final_payload(e->plan.batches[succ][0]);
     const bool pg = B != nullptr;
     const int par = (int)(ep & 1u);
     auto& ar = e->arenas[0];
@@ -1665,19 +1654,18 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
         io.hdr = H;
         if (s + 2 < k) {
             to_succ(io);
-        } else {  // owner: final payload local; the copy engines deliver it to every other rank
+        } else {  // owner: the quantizer stores the final payload locally and into every other rank
             io.local_out = true;
             io.hdr_out[0] = e->peers[r].hdr[par];
             io.phase_out = kPhaseAG;
-            if (push_final)  // many small runs (multi-tensor): the quantizer stores to every rank itself
-                for (uint32_t q = 0; q < k; ++q)
-                    if (q != r) {
-                        io.x_codes[io.nx] = e->peers[q].codes[par];
-                        io.x_cb[io.nx] = e->peers[q].cbs[par];
-                        ++io.nx;
-                        io.hdr_out[io.nx] = e->peers[q].hdr[par];
-                        io.flags[io.nflags++] = e->peers[q].ag_flag;
-                    }
+            for (uint32_t q = 0; q < k; ++q)
+                if (q != r) {
+                    io.x_codes[io.nx] = e->peers[q].codes[par];
+                    io.x_cb[io.nx] = e->peers[q].cbs[par];
+                    ++io.nx;
+                    io.hdr_out[io.nx] = e->peers[q].hdr[par];
+                    io.flags[io.nflags++] = e->peers[q].ag_flag;
+                }
         }
         if (hp) TRY(hp->before_rs(rc));
         mark(EMESH_OP_QUANT, (int)s, true);
@@ -1686,7 +1674,7 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
     }
     // all-gather (the owner's final bytes to every rank, allreduce.hpp:446-464 forwards the same
     // bytes hop by hop) + the commit gate
-    TRY(p2p_commit(e, par, ep, push_final));
+    TRY(p2p_commit(e, par, ep));
     // decode every chunk (own final first); each decode commits only through the gate
     for (uint32_t d = 0; d < k; ++d) {
         const uint32_t c = (succ + k - d) % k;  // succ = own chunk; then chunks owned by r-1, r-2, ...

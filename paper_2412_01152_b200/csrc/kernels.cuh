@@ -563,6 +563,7 @@ struct F32HopArgs {
     float divisor, inv_divisor;  // owner mean: x / k (allreduce.hpp:435-440)
     float* dst[kMaxDest];      // payload destinations (arena-indexed)
     uint32_t ndest;
+    uint32_t ndest_fail;       // destinations still written once this rank's round failed (QuantArgs)
     uint32_t* sflag[kMaxDest];  // peer arrival flags raised per finished segment
     uint32_t nflag;
     uint32_t* seg_done;        // [batch segment] CTA arrival counters (zeroed per launch)
@@ -594,6 +595,7 @@ __global__ void __launch_bounds__(kThreads) k_f32_hop(F32HopArgs a) {
         __syncthreads();
     }
     const uint64_t hiel = si.lo + si.len;
+    const uint32_t nd = (ld_acquire(a.err) & kErrRing) ? a.ndest_fail : a.ndest;
     for (int ui = 0; ui < kApplyUnits; ++ui) {
         const uint32_t u = ((tile - si.cta0) * a.upw + part * kApplyUnits + ui) * kWarps + warp;
         if (u >= si.nunits) break;
@@ -621,7 +623,7 @@ __global__ void __launch_bounds__(kThreads) k_f32_hop(F32HopArgs a) {
                 for (int e = 0; e < 4; ++e)
                     x[e] = a.inv_divisor != 0.f ? __fmul_rn(x[e], a.inv_divisor) : __fdiv_rn(x[e], a.divisor);
             }
-            for (uint32_t d = 0; d < a.ndest; ++d) {
+            for (uint32_t d = 0; d < nd; ++d) {
                 if (full) {
                     __stcs(reinterpret_cast<float4*>(a.dst[d]) + q, make_float4(x[0], x[1], x[2], x[3]));
                 } else {
@@ -638,7 +640,8 @@ __global__ void __launch_bounds__(kThreads) k_f32_hop(F32HopArgs a) {
             last = atom_add_acq_rel(a.seg_done + s, 1u) == si.ncta * a.upw - 1 ? 1u : 0u;
         __syncthreads();
         if (last && threadIdx.x == 0) {
-            for (uint32_t d = 0; d < a.ndest; ++d)
+            const uint32_t ndh = (ld_acquire(a.err) & kErrRing) ? a.ndest_fail : a.ndest;
+            for (uint32_t d = 0; d < ndh; ++d)
                 if (a.dhdr[d]) write_hdr(a.dhdr[d] + si.slot, a.hdr, si.chunk, (uint32_t)si.len, a.phase_out);
             __threadfence_system();
             const uint32_t v = raise_value(a.err, a.epoch);

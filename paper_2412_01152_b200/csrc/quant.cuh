@@ -44,6 +44,9 @@ struct QuantArgs {
     uint8_t* dcodes[kMaxDest];
     float* dcb[kMaxDest];
     uint32_t ndest;
+    uint32_t ndest_fail;       // destinations still written once this rank's round failed: a failed
+                               // owner must not overwrite the peers' arenas with a garbage final payload
+                               // (a late peer may still read its reduce-scatter input from those slots)
     uint32_t* sflag[kMaxDest];
     uint32_t nflag;
     const uint32_t* in_flag;   // peer transport: in_codes / in_cb of slot s valid once in_flag[s] >= epoch
@@ -99,6 +102,7 @@ struct __align__(16) QSmem {
     int32_t bin_seg, lut_seg, ready_seg;
     uint32_t run_idx;
     uint32_t cnt_one;  // 1 << kCntShift, read back from smem (an opaque register for lop3_and_or)
+    uint32_t nd;       // destinations this BIN tile writes (QuantArgs::ndest_fail)
 };
 
 // Task order (host-built run table, QuantArgs::runs): the STATS tiles of
@@ -371,7 +375,7 @@ __device__ __forceinline__ float4 ld_scratch(const float4* p) { return *p; }
 template <bool INTERIOR, bool FROM_SCRATCH>
 __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const SegInfo& si, uint64_t qbase,
                                          uint64_t hiel, const float4* xs, uint32_t* hw, const BinParams& p,
-                                         uint32_t& nclip_lo, uint32_t& nclip_hi) {
+                                         uint32_t nd, uint32_t& nclip_lo, uint32_t& nclip_hi) {
     const int lane = threadIdx.x & 31;
     constexpr int kHalf = kSlotsPerLane / 2;
 #pragma unroll 1
@@ -457,7 +461,7 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
             }
             const uint32_t p0 = __byte_perm(__byte_perm(cc[0], cc[1], 0x0040), __byte_perm(cc[2], cc[3], 0x0040), 0x5410);
             const uint32_t p1 = __byte_perm(__byte_perm(cc[4], cc[5], 0x0040), __byte_perm(cc[6], cc[7], 0x0040), 0x5410);
-            for (uint32_t d = 0; d < a.ndest; ++d) {
+            for (uint32_t d = 0; d < nd; ++d) {
                 uint8_t* oc = a.dcodes[d];
                 if (INTERIOR) {
                     reinterpret_cast<uint32_t*>(oc)[q0] = p0;
@@ -527,7 +531,9 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
     const bool degenerate = (__ldcg(&st->flags) & kFlagDegenerate) != 0;
     uint32_t* hw = &sm.hist[warp][0][0];  // zero on entry (kernel start / previous tile's combine)
     if (threadIdx.x < 2) sm.clip[threadIdx.x] = 0u;
+    if (threadIdx.x == 0) sm.nd = (ld_acquire(a.err) & kErrRing) ? a.ndest_fail : a.ndest;
     __syncthreads();
+    const uint32_t nd = sm.nd;
 
     const uint64_t hiel = si.lo + si.len;
     const float4* xs = reinterpret_cast<const float4*>(a.scratch) + ((int64_t)si.sq0 - (int64_t)si.q0);
@@ -547,12 +553,12 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
                 const uint64_t q = qbase + (uint64_t)j * 32 + lane;
                 for (int e = 0; e < 4; ++e)
                     if (q * 4 + e >= si.lo && q * 4 + e < hiel)
-                        for (uint32_t d = 0; d < a.ndest; ++d) a.dcodes[d][q * 4 + e] = 0;
+                        for (uint32_t d = 0; d < nd; ++d) a.dcodes[d][q * 4 + e] = 0;
             }
         } else if (interior) {
-            bin_unit<true, FROM_SCRATCH>(a, sm, si, qbase, hiel, xs, hw, bpar, nclip_lo, nclip_hi);
+            bin_unit<true, FROM_SCRATCH>(a, sm, si, qbase, hiel, xs, hw, bpar, nd, nclip_lo, nclip_hi);
         } else {
-            bin_unit<false, FROM_SCRATCH>(a, sm, si, qbase, hiel, xs, hw, bpar, nclip_lo, nclip_hi);
+            bin_unit<false, FROM_SCRATCH>(a, sm, si, qbase, hiel, xs, hw, bpar, nd, nclip_lo, nclip_hi);
         }
     }
     nclip_lo = warp_sum_u(nclip_lo);
@@ -617,9 +623,10 @@ __device__ void finalize_codebook(const QuantArgs& a, uint32_t s, const SegInfo&
     } else {
         v = codebook_entry(st, b, rl, rh, total, clip);
     }
-    for (uint32_t d = 0; d < a.ndest; ++d) a.dcb[d][(uint64_t)si.slot * kBuckets + b] = v;
+    const uint32_t nd = (ld_acquire(a.err) & kErrRing) ? a.ndest_fail : a.ndest;
+    for (uint32_t d = 0; d < nd; ++d) a.dcb[d][(uint64_t)si.slot * kBuckets + b] = v;
     if (threadIdx.x == 0)  // the ChunkMsg header of this payload, before its flag
-        for (uint32_t d = 0; d < a.ndest; ++d)
+        for (uint32_t d = 0; d < nd; ++d)
             if (a.dhdr[d]) write_hdr(a.dhdr[d] + si.slot, a.hdr, si.chunk, (uint32_t)si.len, (uint8_t)a.phase_out);
     if (a.nflag) {
         // Every tile of s released its stores (gpu scope) to the arrival

@@ -59,7 +59,7 @@ def main():
     torch.cuda.synchronize()
     untouched = all(torch.equal(a, b) for a, b in zip((tg, tl, tb), before))
     # the on-time ranks name the late one (or nobody); the late rank itself sees its peers gone
-    ok = failed and untouched and (rank == world - 1 or culprit in (ids[-1], ""))
+    ok = failed and untouched and (rank == world - 1 or culprit in (ids[-1], ""))  # "" = unknown
     print(f"{ids[rank]}: slow-peer {'OK' if ok else 'FAILED'} [{transport}] failed={failed} untouched={untouched}",
           flush=True)
     store.set(f"done/{rank}", b"1")
