@@ -897,7 +897,10 @@ struct emesh_engine {
     cudaEvent_t ev_entry = nullptr, ev_done = nullptr, ev_comm_done = nullptr;
     std::vector<cudaEvent_t> ev_send, ev_recv;  // per window
     std::vector<emesh_ring_op> schedule;        // NCCL mode program (build_schedule)
-    uint32_t reserve_sms = 8;                   // SMs the quantizer leaves to NCCL's kernels (NCCL transport)
+#ifndef EMESH_RESERVE_SMS
+#define EMESH_RESERVE_SMS 8
+#endif
+    uint32_t reserve_sms = EMESH_RESERVE_SMS;   // SMs the quantizer leaves to NCCL's kernels (NCCL transport)
     struct Arena {
         uint8_t* codes = nullptr;
         float* cbs = nullptr;
