@@ -475,6 +475,8 @@ struct QuantIO {
     HdrRef hdr{};
     uint32_t phase_out = kPhaseRS;
     uint32_t culprit_in = kNoCulprit;
+    uint32_t* wait_self = nullptr;        // "waiting" words (peer transport, spin_until_ge_sys)
+    const uint32_t* wait_pred = nullptr;
 };
 
 enum ProfKind : int {
@@ -620,6 +622,8 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     a.hdr = io.hdr;
     a.phase_out = io.phase_out;
     a.culprit_in = io.culprit_in;
+    a.wait_self = io.wait_self;
+    a.wait_pred = io.wait_pred;
     CU(cudaMemsetAsync(ws.sync, 0, (kSyncReady + 3 * (size_t)bt.nseg) * sizeof(uint32_t), st));
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
@@ -998,6 +1002,8 @@ struct F32IO {
     uint32_t phase_out = kPhaseRS;
     uint32_t culprit_in = kNoCulprit;
     uint32_t ndest_fail = 0;  // destinations still written after a failure (0: all; see QuantArgs::ndest_fail)
+    uint32_t* wait_self = nullptr;
+    const uint32_t* wait_pred = nullptr;
 };
 
 int launch_f32_hop(const Batch& bt, Workspace& ws, const F32IO& io, cudaStream_t st, Tracker* tr) {
@@ -1027,6 +1033,8 @@ int launch_f32_hop(const Batch& bt, Workspace& ws, const F32IO& io, cudaStream_t
     a.hdr = io.hdr;
     a.phase_out = (uint8_t)io.phase_out;
     a.culprit_in = io.culprit_in;
+    a.wait_self = io.wait_self;
+    a.wait_pred = io.wait_pred;
     if (io.nflags) CU(cudaMemsetAsync(ws.sync + kSyncReady, 0, (size_t)bt.nseg * sizeof(uint32_t), st));
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
@@ -1568,6 +1576,8 @@ int run_p2p_f32(emesh_engine* e, const float* A, const float* B, float* theta, f
         io.in_flag = e->rs_flag;
         io.in_hdr = e->peers[r].hdr[par];
         io.culprit_in = pred;
+        io.wait_self = e->done + kWaitSlot;
+        io.wait_pred = e->peers[pred].done + kWaitSlot;
         io.epoch = ep;
         io.hdr = H;
         io.ndest = 1;
@@ -1653,6 +1663,8 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
         io.in_flag = e->rs_flag;
         io.in_hdr = e->peers[r].hdr[par];
         io.culprit_in = pred;
+        io.wait_self = e->done + kWaitSlot;
+        io.wait_pred = e->peers[pred].done + kWaitSlot;
         io.epoch = ep;
         io.hdr = H;
         if (s + 2 < k) {
@@ -1677,7 +1689,9 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
     }
     // all-gather (the owner's final bytes to every rank, allreduce.hpp:446-464 forwards the same
     // bytes hop by hop) + the commit gate
+    mark(EMESH_OP_XFER, 0, true);  // the commit: done words + gate (timeline only)
     TRY(p2p_commit(e, par, ep));
+    mark(EMESH_OP_XFER, 0, false);
     // decode every chunk (own final first); each decode commits only through the gate
     for (uint32_t d = 0; d < k; ++d) {
         const uint32_t c = (succ + k - d) % k;  // succ = own chunk; then chunks owned by r-1, r-2, ...

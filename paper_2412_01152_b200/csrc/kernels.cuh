@@ -214,10 +214,22 @@ __device__ __forceinline__ uint32_t raise_value(const uint32_t* err, uint32_t ep
 // ones); a poisoned flag fails at once with the culprit it carries; once
 // this rank failed, every other wait gives up at once. Returns true when the
 // flag arrived for this round.
+//
+// Attribution past k = 2 (reduce-scatter waits, wait_self / wait_pred set):
+// a waiter publishes the round it waits in (its "waiting" word, mapped by its
+// successor). When the budget expires and the predecessor is itself waiting
+// in this round, the predecessor is blocked on a rank further up, not dead:
+// the waiter grants it one more budget for its poisoned flag (which names
+// the real culprit) before blaming it. A dead or stalled predecessor is not
+// waiting in this round and is named at once.
 __device__ __forceinline__ bool spin_until_ge_sys(const uint32_t* p, uint32_t epoch, uint32_t* err,
-                                                  unsigned long long timeout_ns, uint32_t culprit) {
+                                                  unsigned long long timeout_ns, uint32_t culprit,
+                                                  uint32_t* wait_self = nullptr,
+                                                  const uint32_t* wait_pred = nullptr) {
     uint32_t ns = 64;
-    const unsigned long long t0 = gtimer();
+    unsigned long long t0 = gtimer();
+    bool extended = false;
+    if (wait_self) *reinterpret_cast<volatile uint32_t*>(wait_self) = epoch;
     for (;;) {
         const uint32_t v = ld_acquire_sys(p);
         if (v & kPoison) {
@@ -227,6 +239,11 @@ __device__ __forceinline__ bool spin_until_ge_sys(const uint32_t* p, uint32_t ep
         if ((int32_t)(v - epoch) >= 0) return true;
         if (ld_acquire(err) & kErrRing) return false;
         if (gtimer() - t0 > timeout_ns) {
+            if (wait_pred && !extended && *reinterpret_cast<const volatile uint32_t*>(wait_pred) == epoch) {
+                extended = true;  // the predecessor is blocked too: wait for its verdict
+                t0 = gtimer();
+                continue;
+            }
             ring_fail(err, kErrRingTimeout, culprit);
             return false;
         }
@@ -234,6 +251,7 @@ __device__ __forceinline__ bool spin_until_ge_sys(const uint32_t* p, uint32_t ep
         ns = ns < 2048 ? 2 * ns : ns;
     }
 }
+constexpr uint32_t kWaitSlot = 63;  // the "waiting" word's index in each rank's mapped done[] array
 
 // ChunkMsg header (allreduce.hpp:66-103) of one segment payload in a peer
 // arena, written by the producer before it raises the segment's flag and
@@ -578,6 +596,8 @@ struct F32HopArgs {
     HdrRef hdr;
     uint8_t phase_out;
     uint32_t culprit_in;       // rank that owes the incoming payload (the predecessor)
+    uint32_t* wait_self;       // this rank's / the predecessor's "waiting" words (spin_until_ge_sys)
+    const uint32_t* wait_pred;
 };
 
 // x = (a - b | a) (+ in) (/ k), the reduce-scatter accumulate
@@ -589,7 +609,9 @@ __global__ void __launch_bounds__(kThreads) k_f32_hop(F32HopArgs a) {
     const uint32_t s = a.cta_seg[tile];
     const SegInfo si = a.segs[s];
     if (HAS_IN && a.in_flag) {
-        if (threadIdx.x == 0 && spin_until_ge_sys(a.in_flag + si.in_slot, a.epoch, a.err, a.timeout_ns, a.culprit_in) &&
+        if (threadIdx.x == 0 &&
+            spin_until_ge_sys(a.in_flag + si.in_slot, a.epoch, a.err, a.timeout_ns, a.culprit_in, a.wait_self,
+                              a.wait_pred) &&
             a.in_hdr)
             check_hdr(a.in_hdr + si.in_slot, a.hdr, si.chunk, (uint32_t)si.len, kPhaseRS, a.err, a.culprit_in);
         __syncthreads();

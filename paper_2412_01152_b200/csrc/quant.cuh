@@ -66,6 +66,8 @@ struct QuantArgs {
     HdrRef hdr;
     uint32_t phase_out;        // kPhaseRS, or kPhaseAG for the owner's final payload
     uint32_t culprit_in;       // rank that owes the incoming payloads (the predecessor)
+    uint32_t* wait_self;       // this rank's / the predecessor's "waiting" words (spin_until_ge_sys)
+    const uint32_t* wait_pred;
 };
 
 
@@ -142,7 +144,8 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
             __syncthreads();
             if (a.in_flag) {  // peer transport: the predecessor's payload of s must have landed intact
                 if (threadIdx.x == 0 &&
-                    spin_until_ge_sys(a.in_flag + si.in_slot, a.epoch, a.err, a.timeout_ns, a.culprit_in) &&
+                    spin_until_ge_sys(a.in_flag + si.in_slot, a.epoch, a.err, a.timeout_ns, a.culprit_in,
+                                      a.wait_self, a.wait_pred) &&
                     a.in_hdr)
                     check_hdr(a.in_hdr + si.in_slot, a.hdr, si.chunk, (uint32_t)si.len, kPhaseRS, a.err,
                               a.culprit_in);
