@@ -901,10 +901,9 @@ struct emesh_engine {
     cudaEvent_t ev_entry = nullptr, ev_done = nullptr, ev_comm_done = nullptr;
     std::vector<cudaEvent_t> ev_send, ev_recv;  // per window
     std::vector<emesh_ring_op> schedule;        // NCCL mode program (build_schedule)
-#ifndef EMESH_RESERVE_SMS
-#define EMESH_RESERVE_SMS 8
-#endif
-    uint32_t reserve_sms = EMESH_RESERVE_SMS;   // SMs the quantizer leaves to NCCL's kernels (NCCL transport)
+    // quantizer CTAs left out of the persistent grid for NCCL's send/recv kernels (NCCL transport;
+    // leaving one CTA slot per SM measured the same at 4 GPUs)
+    uint32_t reserve_sms = 8;
     struct Arena {
         uint8_t* codes = nullptr;
         float* cbs = nullptr;
@@ -1315,6 +1314,7 @@ int xfer_window(emesh_engine* e, const Batch& snd, const Batch& rcv) {
                 e->s_comm));
     NCS(ncclGroupEnd());
     return EMESH_OK;
+
 }
 
 // All-gather of window j on the NCCL transport: every owner broadcasts its
@@ -1443,13 +1443,11 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
                 // forwards the owner's final bytes, later AG hops bytes this
                 // stream itself received
                 if (o.phase == 0 || o.hop == 0) CU(cudaStreamWaitEvent(sm, e->ev_send[j], 0));
-#ifndef EMESH_NCCL_AG_RING
                 if (o.phase == 1) {  // the schedule's k-1 forwarding hops as one broadcast group
                     if (o.hop == 0) TRY(bcast_window(e, j));
                     CU(cudaEventRecord(e->ev_recv[j], sm));
                     break;
                 }
-#endif
                 TRY(xfer_window(e, P[o.send_chunk][j], P[o.recv_chunk][j]));
                 CU(cudaEventRecord(e->ev_recv[j], sm));
                 break;
