@@ -127,6 +127,20 @@ struct Plan {
     size_t max_cta = 0, max_segs = 0, max_slots = 0;
 
     // Appends the device tables for one batch over segments [s0, s1).
+    // One batch over every segment (the peer transport's single decode launch
+    // per round); built after the ring batches, not sized into the quantizer's
+    // workspace (it never quantizes).
+    Batch all;
+    bool has_all = false;
+    void add_all() {
+        const size_t mc = max_cta, ms = max_segs, mx = max_slots;
+        add_batch(0, 0, 0, (uint32_t)segs.size());
+        all = batches[0].back();
+        batches[0].pop_back();
+        max_cta = mc; max_segs = ms; max_slots = mx;
+        has_all = true;
+    }
+
     void add_batch(uint32_t chunk, uint32_t window, uint32_t s0, uint32_t s1) {
         Batch b;
         b.chunk = chunk;
@@ -274,6 +288,7 @@ struct Plan {
         CU(cudaMemcpy(d_tables, host_tables.data(), host_tables.size(), cudaMemcpyHostToDevice));
         for (auto& row : batches)
             for (auto& b : row) b.bind(d_tables);
+        if (has_all) all.bind(d_tables);
         return EMESH_OK;
     }
     void release() {
@@ -330,6 +345,7 @@ Plan make_ring_plan(uint64_t n, uint32_t k, uint32_t S, uint64_t window_elems) {
         for (uint64_t s = first[c]; s < first[c + 1]; s += G, ++w)
             p.add_batch(c, w, (uint32_t)s, (uint32_t)std::min<uint64_t>(first[c + 1], s + G));
     }
+    if (k > 1) p.add_all();
     return p;
 }
 
@@ -380,6 +396,7 @@ Plan make_tensor_ring_plan(const uint64_t* sizes, uint32_t nt, uint32_t k, uint3
             p.add_batch(c, (uint32_t)w, s0, s);
         }
     }
+    if (k > 1) p.add_all();
     return p;
 }
 
@@ -477,6 +494,8 @@ struct QuantIO {
     uint32_t culprit_in = kNoCulprit;
     uint32_t* wait_self = nullptr;        // "waiting" words (peer transport, spin_until_ge_sys)
     const uint32_t* wait_pred = nullptr;
+    uint32_t* done_dst[kMaxDest] = {};    // owner's final quantizer: the peers' done words for this rank
+    uint32_t ndone = 0;
 };
 
 enum ProfKind : int {
@@ -624,6 +643,9 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     a.culprit_in = io.culprit_in;
     a.wait_self = io.wait_self;
     a.wait_pred = io.wait_pred;
+    if (io.ndone > (uint32_t)kMaxDest) return fail(EMESH_ECONFIG, "too many done destinations");
+    a.ndone = io.ndone;
+    for (uint32_t d = 0; d < io.ndone; ++d) a.done_dst[d] = io.done_dst[d];
     CU(cudaMemsetAsync(ws.sync, 0, (kSyncReady + 3 * (size_t)bt.nseg) * sizeof(uint32_t), st));
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
@@ -1512,17 +1534,19 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
 // that every decode kernel of the round checks. A round that failed anywhere
 // therefore commits nowhere (theta / momentum untouched) and every rank
 // reports it.
-int p2p_commit(emesh_engine* e, int par, uint32_t ep) {
+int p2p_commit(emesh_engine* e, int par, uint32_t ep, bool done_sent) {
     const uint32_t k = e->k, r = e->rank, succ = (r + 1) % k;
     cudaStream_t sc = e->s_comp, cm = e->s_comm;
-    k_done_value<<<1, 32, 0, sc>>>(e->ws.err, ep, e->done_src);
-    e->tr.launches += 1;
-    CU(cudaGetLastError());
-    CU(cudaEventRecord(e->ev_send[0], sc));
-    CU(cudaStreamWaitEvent(cm, e->ev_send[0], 0));
-    for (uint32_t d = 1; d < k; ++d) {  // after the payload (stream order)
-        const uint32_t q = (r + d) % k;
-        CU(cudaMemcpyAsync(e->peers[q].done + r, e->done_src, sizeof(uint32_t), cudaMemcpyDeviceToDevice, cm));
+    if (!done_sent) {  // fp32 mode: a one-thread kernel + copy-engine writes of the done word
+        k_done_value<<<1, 32, 0, sc>>>(e->ws.err, ep, e->done_src);
+        e->tr.launches += 1;
+        CU(cudaGetLastError());
+        CU(cudaEventRecord(e->ev_send[0], sc));
+        CU(cudaStreamWaitEvent(cm, e->ev_send[0], 0));
+        for (uint32_t d = 1; d < k; ++d) {  // after the payload (stream order)
+            const uint32_t q = (r + d) % k;
+            CU(cudaMemcpyAsync(e->peers[q].done + r, e->done_src, sizeof(uint32_t), cudaMemcpyDeviceToDevice, cm));
+        }
     }
     GateArgs g{};
     g.done = e->done;
@@ -1598,7 +1622,10 @@ int run_p2p_f32(emesh_engine* e, const float* A, const float* B, float* theta, f
         }
         TRY(launch_f32_hop(P[rc][0], e->ws, io, sc, &e->tr));
     }
-    TRY(p2p_commit(e, par, ep));
+    TRY(p2p_commit(e, par, ep, false));
+    if (e->plan.has_all)  // one decode launch over all segments
+        return launch_f32_apply(e->plan.all, out ? 0 : 1, e->peers[r].pay[par], theta, buf, local_out, out, lr, mom,
+                                sc, &e->tr, e->gate, ep);
     for (uint32_t d = 0; d < k; ++d) {
         const uint32_t c = (succ + k - d) % k;
         TRY(launch_f32_apply(P[c][0], out ? 0 : 1, e->peers[r].pay[par], theta, buf, local_out, out, lr, mom, sc,
@@ -1678,6 +1705,8 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
                     ++io.nx;
                     io.hdr_out[io.nx] = e->peers[q].hdr[par];
                     io.flags[io.nflags++] = e->peers[q].ag_flag;
+                    if (P[rc][0].ncta)  // the commit's done word, from the kernel (an empty chunk runs none)
+                        io.done_dst[io.ndone++] = e->peers[q].done + r;
                 }
         }
         if (hp) TRY(hp->before_rs(rc));
@@ -1687,10 +1716,23 @@ int run_p2p(emesh_engine* e, const float* A, const float* B, float* theta, float
     }
     // all-gather (the owner's final bytes to every rank, allreduce.hpp:446-464 forwards the same
     // bytes hop by hop) + the commit gate
-    mark(EMESH_OP_XFER, 0, true);  // the commit: done words + gate (timeline only)
-    TRY(p2p_commit(e, par, ep));
+    mark(EMESH_OP_XFER, 0, true);  // the commit: the gate (timeline only)
+    TRY(p2p_commit(e, par, ep, P[succ][0].ncta > 0));
     mark(EMESH_OP_XFER, 0, false);
-    // decode every chunk (own final first); each decode commits only through the gate
+    // decode every chunk, committing only through the gate: one launch over all segments (the
+    // per-chunk launches cost ~10-25 us each at small sizes), per chunk when the host pipeline
+    // copies chunks back as they finish (outer_sync_host)
+    if (!hp && e->plan.has_all) {
+        mark(EMESH_OP_APPLY, -1, true);
+        if (out)
+            TRY(launch_apply(e->plan.all, 0, e->peers[r].codes[par], e->peers[r].cbs[par], nullptr, nullptr, nullptr,
+                             out, 0.f, 0.f, sc, &e->tr, e->gate, ep));
+        else
+            TRY(launch_apply(e->plan.all, 1, e->peers[r].codes[par], e->peers[r].cbs[par], theta, buf, local_out,
+                             nullptr, lr, mom, sc, &e->tr, e->gate, ep));
+        mark(EMESH_OP_APPLY, -1, false);
+        return EMESH_OK;
+    }
     for (uint32_t d = 0; d < k; ++d) {
         const uint32_t c = (succ + k - d) % k;  // succ = own chunk; then chunks owned by r-1, r-2, ...
         if (hp) TRY(hp->before_apply(c));

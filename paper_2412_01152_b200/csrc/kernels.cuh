@@ -251,6 +251,7 @@ __device__ __forceinline__ bool spin_until_ge_sys(const uint32_t* p, uint32_t ep
         ns = ns < 2048 ? 2 * ns : ns;
     }
 }
+constexpr uint32_t kSyncExit = 1;   // sync[] word counting the quantizer CTAs that ran out of tasks
 constexpr uint32_t kWaitSlot = 63;  // the "waiting" word's index in each rank's mapped done[] array
 
 // ChunkMsg header (allreduce.hpp:66-103) of one segment payload in a peer

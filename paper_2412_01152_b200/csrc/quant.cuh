@@ -68,6 +68,10 @@ struct QuantArgs {
     uint32_t culprit_in;       // rank that owes the incoming payloads (the predecessor)
     uint32_t* wait_self;       // this rank's / the predecessor's "waiting" words (spin_until_ge_sys)
     const uint32_t* wait_pred;
+    // the owner's final quantizer: once every CTA is done, the last one stores this rank's done
+    // value (the round, or poison naming the culprit) into every peer's done word (p2p_commit)
+    uint32_t* done_dst[kMaxDest];
+    uint32_t ndone;
 };
 
 
@@ -691,7 +695,15 @@ __global__ void __launch_bounds__(kThreads, kQuantMinBlocks) k_quant(QuantArgs a
         if (threadIdx.x == 0) sm.task = nxt;
         __syncthreads();
         const uint32_t t = sm.task;
-        if (t >= a.ntasks) return;
+        if (t >= a.ntasks) {
+            if (a.ndone && threadIdx.x == 0 &&
+                atom_add_acq_rel(&a.sync[kSyncExit], 1u) == gridDim.x - 1) {  // the last CTA out
+                __threadfence_system();
+                const uint32_t v = raise_value(a.err, a.epoch);
+                for (uint32_t d = 0; d < a.ndone; ++d) st_release_sys(a.done_dst[d], v);
+            }
+            return;
+        }
         // claim the following task now: the atomic's latency hides behind this tile
         if (threadIdx.x == 0) nxt = atomicAdd(&a.sync[0], 1u);
         uint32_t kind, s, tile;
