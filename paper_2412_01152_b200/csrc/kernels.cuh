@@ -248,7 +248,7 @@ __device__ __forceinline__ bool spin_until_ge_sys(const uint32_t* p, uint32_t ep
             return false;
         }
         __nanosleep(ns);
-        ns = ns < 2048 ? 2 * ns : ns;
+        ns = ns < 256 ? 2 * ns : ns;  // short cap: a hop's flag latency is on the small-round critical path
     }
 }
 constexpr uint32_t kSyncExit = 1;   // sync[] word counting the quantizer CTAs that ran out of tasks

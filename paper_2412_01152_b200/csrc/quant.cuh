@@ -171,7 +171,11 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
         const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
         const bool interior = qbase * 4 >= si.lo && (qbase + kUnitSlots) * 4 <= hiel;  // warp-uniform
         constexpr int kHalf = kSlotsPerLane / 2;
+#ifdef EMESH_STATS_ROLLED
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
         for (int h = 0; h < 2; ++h) {
             float4 xa[kHalf], xb[kHalf];
             uint32_t c4[kHalf];
@@ -728,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, kQuantMinBlocks) k_quant(QuantArgs a
             uint32_t ns = 32;
             while (ld_acquire(&a.sync[kSyncReady + s]) == 0u) {
                 __nanosleep(ns);
-                ns = ns < 1024 ? 2 * ns : ns;
+                ns = ns < 128 ? 2 * ns : ns;
             }
             sm.ready_seg = (int32_t)s;
         }
