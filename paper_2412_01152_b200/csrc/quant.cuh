@@ -460,20 +460,8 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
                 const uint32_t rlo = (uint32_t)__double2loint(m);
                 const uint32_t rhi = (uint32_t)__double2hiint(m);
                 uint32_t* hc = hw + 3 * min(cc[i], kBuckets);
-#ifdef EMESH_WARP_AGG
-                {   // lanes on the same bucket row add their limbs once (no same-address atomics)
-                    const uint32_t grp = __match_any_sync(0xffffffffu, (uint32_t)min(cc[i], kBuckets));
-                    const uint32_t sa = __reduce_add_sync(grp, lop3_and_or<(1u << kLoBits) - 1u>(rlo, p.cnt_one));
-                    const uint32_t sb = __reduce_add_sync(grp, (rlo >> kLoBits) & ((1u << (kMidEnd - kLoBits)) - 1u));
-                    if ((uint32_t)(__ffs(grp) - 1) == (uint32_t)lane) {
-                        red_shared_add(hc, sa);
-                        red_shared_add(hc + 1, sb);
-                    }
-                }
-#else
                 red_shared_add(hc, lop3_and_or<(1u << kLoBits) - 1u>(rlo, p.cnt_one));
                 red_shared_add(hc + 1, (rlo >> kLoBits) & ((1u << (kMidEnd - kLoBits)) - 1u));
-#endif
                 const uint32_t rc = __funnelshift_r(rlo, rhi, kMidEnd) & ((1u << (42 - kMidEnd)) - 1u);
                 if (rc) red_shared_add(hc + 2, rc);  // nonzero mostly in the wide bucket (an unconditional
                                                      // third atomic measured 1.3 % slower)
