@@ -961,7 +961,7 @@ struct emesh_engine {
     // round commit (peer transport): this rank's done source word, gate word, slot metadata
     ChunkHdr* hdr_alt = nullptr;  // parity-1 headers (parity 0: hdr0)
     ChunkHdr* hdr0 = nullptr;
-    uint32_t* done = nullptr;     // [k], written by the owners' copy engines
+    uint32_t* done = nullptr;     // [k] owners' done words (written by their final quantizers / copy engines); [63] waiting word
     uint32_t* done_src = nullptr; // this rank's done value (k_done_value)
     uint32_t* gate = nullptr;     // the gate word the decode kernels check (k_round_gate)
     uint2* meta = nullptr;        // by slot: {ring chunk, elements}
@@ -1527,8 +1527,9 @@ int run_nccl(emesh_engine* e, const float* A, const float* B, float* theta, floa
 // to every rank at once, which replaces the all-gather's k-1 forwarding hops
 // (the bytes are identical: AG forwards them verbatim, allreduce.hpp:446-464).
 // The round's commit (peer transport), after this rank's last quantizer:
-// k_done_value turns this rank's error word into its done value (the round,
-// or poison naming the culprit); the copy engines deliver it to every peer;
+// this rank's done value (the round, or poison naming the culprit) reaches
+// every peer — stored by the last CTA of the final quantizer (int8), or by
+// k_done_value + copy-engine writes (fp32 mode, an empty final chunk);
 // k_round_gate waits for every other owner's done word and final-payload
 // flags, validates the final payloads' headers and publishes the gate word
 // that every decode kernel of the round checks. A round that failed anywhere

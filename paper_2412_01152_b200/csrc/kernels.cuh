@@ -523,10 +523,10 @@ __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Round commit (peer transport). The owners' final payloads reach every rank
-// by copy engine (or by the owner's quantizer); after its own payloads, each
-// owner q copies a "done" word into every rank's done[q]: the round number,
-// or poison naming a culprit when q's round failed. k_round_gate (one small
+// Round commit (peer transport). Each owner's final quantizer stores its
+// payload into every rank (ag_flag per segment) and then, from its last CTA,
+// a "done" word into every rank's done[q]: the round number, or poison
+// naming a culprit when q's round failed. k_round_gate (one small
 // CTA, after this rank's last quantizer) waits for every other owner's done
 // word, validates the final payloads' ChunkMsg headers and then publishes
 // the gate word the decode kernels check: the round number to commit, 0 to
