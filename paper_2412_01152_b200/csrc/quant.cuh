@@ -133,6 +133,15 @@ constexpr uint32_t kMaxSegsSmem = 128;  // SegInfo cached in smem when it fits
 
 __device__ void finalize_stats(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si);
 
+// Where BIN gets x: the STATS pass's scratch, the input itself (plain
+// quantize), or theta_g - theta_l recomputed (the PG payload: the same 8
+// bytes of DRAM reads as the scratch round trip, without its 4-byte write)
+// (the hops' x = (theta_g - theta_l) + cb_in[code] recomputed in BIN was 12-25 % slower than the scratch:
+// one more byte per element and a second lookup table)
+enum : int { kBinScratch = 0, kBinA = 1, kBinRecompute = 2 };
+template <int SRC> constexpr int kBinSource = SRC == kSrcA ? kBinA : SRC == kSrcAminusB ? kBinRecompute : kBinScratch;
+template <int SRC> constexpr bool kStatsWritesScratch = kBinSource<SRC> == kBinScratch;
+
 // Scratch x (written by STATS, read once by BIN, then discarded).
 __device__ __forceinline__ void st_scratch(float4* p, float4 v) { *p = v; }
 
@@ -220,7 +229,7 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
                     // fused multiply-adds for the squares
                     q0 = __fma_rn(v2, v2, __fma_rn(v0, v0, q0));
                     q1 = __fma_rn(v3, v3, __fma_rn(v1, v1, q1));
-                    if (SRC != kSrcA) st_scratch(xs + q, make_float4(x[0], x[1], x[2], x[3]));
+                    if (kStatsWritesScratch<SRC>) st_scratch(xs + q, make_float4(x[0], x[1], x[2], x[3]));
                 } else {
                     uint32_t vm = 0u;
 #pragma unroll
@@ -234,7 +243,7 @@ __device__ __forceinline__ void stats_tile(const QuantArgs& a, QSmem& sm, uint32
                             sum0 = __dadd_rn(sum0, xd);
                             q0 = __fma_rn(dv, dv, q0);
                             cnt += 1;
-                            if (SRC != kSrcA) reinterpret_cast<float*>(xs + q)[e] = x[e];
+                            if (kStatsWritesScratch<SRC>) reinterpret_cast<float*>(xs + q)[e] = x[e];
                         }
                     }
                 }
@@ -379,7 +388,7 @@ __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t c) {
 // read (or prefetched) after: no stale L1 copy can exist within the launch.
 __device__ __forceinline__ float4 ld_scratch(const float4* p) { return *p; }
 
-template <bool INTERIOR, bool FROM_SCRATCH>
+template <bool INTERIOR, int BSRC, int SRC>
 __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const SegInfo& si, uint64_t qbase,
                                          uint64_t hiel, const float4* xs, uint32_t* hw, const BinParams& p,
                                          uint32_t nd, uint32_t& nclip_lo, uint32_t& nclip_hi) {
@@ -392,7 +401,17 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
         for (int jj = 0; jj < kHalf; ++jj) {
             const uint64_t q = qbase + (uint64_t)(h * kHalf + jj) * 32 + lane;
             const bool in = INTERIOR || q * 4 < hiel;
-            xv[jj] = !in ? make_float4(0.f, 0.f, 0.f, 0.f) : FROM_SCRATCH ? ld_scratch(xs + q) : ld4(a.a, q);
+            if (!in) {
+                xv[jj] = make_float4(0.f, 0.f, 0.f, 0.f);
+            } else if (BSRC == kBinScratch) {
+                xv[jj] = ld_scratch(xs + q);
+            } else if (BSRC == kBinA) {
+                xv[jj] = ld4(a.a, q);
+            } else {  // kBinRecompute (PG payload): x = theta_g - theta_l again, STATS' rounding
+                static_assert(BSRC != kBinRecompute || SRC == kSrcAminusB, "BIN recomputes only the PG payload");
+                const float4 u = ld4_stream(a.a, q), w = ld4_stream(a.b, q);
+                xv[jj] = make_float4(__fsub_rn(u.x, w.x), __fsub_rn(u.y, w.y), __fsub_rn(u.z, w.z), __fsub_rn(u.w, w.w));
+            }
         }
 #pragma unroll
         for (int pr = 0; pr < kHalf / 2; ++pr) {
@@ -490,7 +509,7 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
                 }
             }
         }
-        if (FROM_SCRATCH && INTERIOR) {
+        if (BSRC == kBinScratch && INTERIOR) {
             // this half's 2 KB of scratch x is consumed (each element is read
             // exactly once): drop the 128-B L2 lines wholly inside it without
             // write-back — x was only ever meant as an L2 round trip
@@ -507,11 +526,11 @@ __device__ void finalize_codebook(const QuantArgs& a, uint32_t s, const SegInfo&
 __device__ float codebook_entry(const SegStat* st, int b, unsigned long long rl, unsigned long long rh,
                                 unsigned long long total, unsigned long long clip);
 
-template <bool FROM_SCRATCH>
+template <int BSRC, int SRC>
 __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t s, const SegInfo& si, uint32_t tile) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const SegStat* st = &a.stats[si.slot];
-    if (FROM_SCRATCH) {  // the warp's first unit, while the tables load (the segment's scratch is complete)
+    if (BSRC == kBinScratch) {  // the warp's first unit, while the tables load (the segment's scratch is complete)
         const uint32_t u0 = tile * si.upw * kWarps + warp;
         if (u0 < si.nunits) {
             const float4* p0 = reinterpret_cast<const float4*>(a.scratch) + si.sq0 + (uint64_t)u0 * kUnitSlots + lane * 8;
@@ -551,7 +570,7 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
         if (u >= si.nunits) break;
         const uint64_t qbase = si.q0 + (uint64_t)u * kUnitSlots;
         const bool interior = qbase * 4 >= si.lo && (qbase + kUnitSlots) * 4 <= hiel;  // warp-uniform
-        if (FROM_SCRATCH && ui + 1 < (int)si.upw && u + kWarps < si.nunits) {
+        if (BSRC == kBinScratch && ui + 1 < (int)si.upw && u + kWarps < si.nunits) {
             const float4* nx = xs + qbase + (uint64_t)kWarps * kUnitSlots + lane * 8;  // one 128-B line per lane
             asm volatile("prefetch.global.L1 [%0];" ::"l"(nx));
         }
@@ -563,9 +582,9 @@ __device__ __forceinline__ void bin_tile(const QuantArgs& a, QSmem& sm, uint32_t
                         for (uint32_t d = 0; d < nd; ++d) a.dcodes[d][q * 4 + e] = 0;
             }
         } else if (interior) {
-            bin_unit<true, FROM_SCRATCH>(a, sm, si, qbase, hiel, xs, hw, bpar, nd, nclip_lo, nclip_hi);
+            bin_unit<true, BSRC, SRC>(a, sm, si, qbase, hiel, xs, hw, bpar, nd, nclip_lo, nclip_hi);
         } else {
-            bin_unit<false, FROM_SCRATCH>(a, sm, si, qbase, hiel, xs, hw, bpar, nd, nclip_lo, nclip_hi);
+            bin_unit<false, BSRC, SRC>(a, sm, si, qbase, hiel, xs, hw, bpar, nd, nclip_lo, nclip_hi);
         }
     }
     nclip_lo = warp_sum_u(nclip_lo);
@@ -735,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, kQuantMinBlocks) k_quant(QuantArgs a
         __syncthreads();  // everyone has read sm.task; SegStat(s) visible for BIN
         switch (kind) {
             case kTaskStats: stats_tile<SRC>(a, sm, s, si, tile); break;
-            default: bin_tile<SRC != kSrcA>(a, sm, s, si, tile); break;
+            default: bin_tile<kBinSource<SRC>, SRC>(a, sm, s, si, tile); break;
         }
     }
 }

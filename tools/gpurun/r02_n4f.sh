@@ -11,7 +11,7 @@ B p2p --steps 20 --warmup 3
 B nccl --steps 10 --warmup 3 --transport nccl --no-e2e
 B p2p_10b_S80 --steps 5 --warmup 3 --params 10.211381248e9 --S 80 --no-e2e
 B p2p_cfg5 --steps 5 --warmup 3 --params 10.211381248e9 --S 4 --tensors intellect1 --no-e2e
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=4 --master-addr 127.0.0.1 --master-port 29702 tools/sweep_msg.py 268435456 10 > gpurun_out/r02n4f/sweep_n4.jsonl 2> gpurun_out/r02n4f/sweep_n4.err; echo "sweep rc=$?"
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=4 --master-addr 127.0.0.1 --master-port 29702 tools/sweep_msg.py 1073741824 10 > gpurun_out/r02n4f/sweep_n4.jsonl 2> gpurun_out/r02n4f/sweep_n4.err; echo "sweep rc=$?"
 python -c "
 import json
 for l in open('gpurun_out/r02n4f/sweep_n4.jsonl'):
