@@ -4,7 +4,9 @@ send/recv as the transport and the oracle codec as the compute, and check
 every rank ends bit-identical to the oracle's transport-free ring
 (allreduce.hpp:314-473). This pins the multi-GPU host logic — who sends
 which window of which chunk at which hop, owner finalize, all-gather
-forwarding — without a GPU."""
+forwarding — without a GPU. ag="bcast" executes the all-gather the way
+run_nccl does (emesh_b200.cu bcast_window): at hop 0 of each window, one
+broadcast per chunk from its owner; the later forwarding hops are skipped."""
 import os
 import socket
 
@@ -24,7 +26,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, S, window, q):
+def _worker(rank, world, port, n, S, window, q, ag="hops"):
     import sys
     ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, ROOT)
@@ -55,7 +57,31 @@ def _worker(rank, world, port, n, S, window, q):
         codes[a:a + b] = c
         cbs[i] = cb
 
-    for op in E.ring_schedule(n, k, S, rank, window):
+    ops = E.ring_schedule(n, k, S, rank, window)
+    wins = {}  # (chunk, window) -> (first segment, segments): the batch table run_nccl broadcasts from
+    for op in ops:
+        if op.send_chunk >= 0:
+            wins[(op.send_chunk, op.window)] = (op.send_seg0, op.send_nseg)
+        if op.recv_chunk >= 0:
+            wins[(op.recv_chunk, op.window)] = (op.recv_seg0, op.recv_nseg)
+    for op in ops:
+        if op.kind == _capi.OP_XFER and op.phase == 1 and ag == "bcast":
+            if op.hop == 0:
+                for c in range(k):  # k broadcasts, root = the chunk's owner (allreduce.hpp:428-445)
+                    s0, ns = wins[(c, op.window)]
+                    ss = segs(s0, ns)
+                    buf = torch.from_numpy(np.concatenate([codes[a:a + b] for _, a, b in ss] + [np.zeros(0, np.uint8)]))
+                    bcb = torch.from_numpy(cbs[s0:s0 + ns].copy())
+                    root = (c + k - 1) % k
+                    dist.broadcast(buf, src=root)
+                    dist.broadcast(bcb, src=root)
+                    off = 0
+                    bn = buf.numpy()
+                    for _, a, b in ss:
+                        codes[a:a + b] = bn[off:off + b]
+                        off += b
+                    cbs[s0:s0 + ns] = bcb.numpy()
+            continue
         if op.kind == _capi.OP_OWN:
             for i, a, b in segs(op.recv_seg0, op.recv_nseg):
                 quant_into(i, a, b, delta[a:a + b])
@@ -93,13 +119,15 @@ def _worker(rank, world, port, n, S, window, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,S,window", [(2, 4099, 4, 0), (2, 50_000, 4, 6000), (3, 3001, 3, 1),
-                                             (3, 10, 4, 0), (2, 1, 4, 0)])
-def test_schedule_over_gloo_matches_oracle(world, n, S, window):
+@pytest.mark.parametrize("world,n,S,window,ag", [(2, 4099, 4, 0, "hops"), (2, 50_000, 4, 6000, "hops"),
+                                                (3, 3001, 3, 1, "hops"), (3, 10, 4, 0, "hops"), (2, 1, 4, 0, "hops"),
+                                                (3, 3001, 3, 1, "bcast"), (3, 50_000, 4, 6000, "bcast"),
+                                                (2, 4099, 4, 0, "bcast")])
+def test_schedule_over_gloo_matches_oracle(world, n, S, window, ag):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, S, window, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, S, window, q, ag)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
