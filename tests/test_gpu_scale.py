@@ -1,6 +1,6 @@
 """Bit-exact parity at the sizes the bench runs: whole
-rounds whose segments exceed what one SM keeps on chip (the quantizer's
-overflow path), and the full config-2 round (1B params/worker, 4 workers,
+rounds with 12M-20M-element segments (4-unit tiles, scratch larger than L2),
+and the full config-2 round (1B params/worker, 4 workers,
 S = 16: 64 segments of 15.6M elements), every segment re-derived by the
 oracle's transport-free chain (oracle/parity.py) and compared bit for bit:
 final codes, codebooks, updated theta_g and Nesterov momentum."""
@@ -63,9 +63,9 @@ def _round_and_check(E, oracle, n, k, S, seed=3, picks=None):
 
 
 @pytest.mark.parametrize("n,k,S", [(80_000_000, 4, 1), (48_000_011, 2, 2)])
-def test_segments_beyond_on_chip_capacity(E, oracle, n, k, S):
-    """20M / 12M-element segments: more x than the SMs hold on chip, so tiles overflow to the
-    global scratch and are binned by other CTAs; still bit-exact."""
+def test_large_segments_four_unit_tiles(E, oracle, n, k, S):
+    """20M / 12M-element segments: batches above 16M elements take the 4-unit tiles (32K elements per
+    CTA task) and a scratch round trip larger than L2, like the bench; still bit-exact."""
     rep = _round_and_check(E, oracle, n, k, S)
     assert rep.ok(), rep.as_dict()
     assert rep.checked_segments == k * S
