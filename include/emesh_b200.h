@@ -222,7 +222,10 @@ int emesh_engine_check(emesh_engine* e);
 
 /* The rank the last failed round names as the culprit (the predecessor whose
  * reduce-scatter payload or the owner whose final payload never arrived, or
- * the one a poisoned flag names); -1 when unknown. RingFailureError.failed_node. */
+ * the one a poisoned flag names; a waiter whose predecessor is itself
+ * waiting in the round first gives it one more step_timeout for its verdict);
+ * -1 when unknown — always past k = 2 on the NCCL transport, which has no
+ * abort frames. RingFailureError.failed_node. */
 int emesh_engine_failed_rank(const emesh_engine* e);
 
 /* ReduceJob.id of the engine's next round (ChunkMsg job id; default: the
