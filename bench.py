@@ -218,9 +218,10 @@ def nvlink_block(world, k, n, S, ms, transport, measured=None):
             "note": "algorithmic ring bytes averaged over the whole round; it overlaps the quantize/decode kernels"}
 
 
-def alg_bytes_per_param(k):
-    # A(1) = 20, A(k>=2) = 24 + (2k-1)/k + 1 (theta_l write excluded)
-    return 20.0 if k == 1 else 24.0 + (2 * k - 1) / k + 1.0
+def alg_bytes_per_param(k, local_workers=1):
+    # A(1) = 20, A(k>=2) = 24 + (2k-1)/k + 1 (theta_l write excluded); with several
+    # workers on one GPU (the virtual ring) each final payload's codes are read once for all of them
+    return 20.0 if k == 1 else 24.0 + (2 * k - 1) / k + 1.0 / max(local_workers, 1)
 
 
 def host_info():
@@ -439,7 +440,7 @@ def main():
     kernels = {kname: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,
                        "GB/s_alg": round(v["alg_bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] else None}
                for kname, v in prof.items()}
-    step_alg_gbs = W * n * alg_bytes_per_param(k) / (ms / 1e3) / 1e9
+    step_alg_gbs = W * n * alg_bytes_per_param(k, W) / (ms / 1e3) / 1e9
 
     # ---- e2e through the host-buffer C-ABI entry point (pinned host memory)
     # ---- NVLink: NVML's link counters are NOT_SUPPORTED on these boxes and ncu never runs on a

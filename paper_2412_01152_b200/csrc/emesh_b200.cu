@@ -687,11 +687,32 @@ int launch_quant(const Batch& bt, Workspace& ws, const QuantIO& io, cudaStream_t
     return EMESH_OK;
 }
 
+// Decode (+ Nesterov) of one batch for nw local replicas (thetas / bufs / locals, nw <= kMaxDest).
+int launch_apply_multi(const Batch& bt, int mode, const uint8_t* codes, const float* cb, float* const* thetas,
+                       float* const* bufs, float* const* locals, uint32_t nw, float* out, float lr, float mom,
+                       cudaStream_t st, Tracker* tr, const uint32_t* gate = nullptr, uint32_t epoch = 0);
+
 int launch_apply(const Batch& bt, int mode, const uint8_t* codes, const float* cb, float* theta, float* buf,
                  float* theta_local, float* out, float lr, float mom, cudaStream_t st, Tracker* tr,
                  const uint32_t* gate = nullptr, uint32_t epoch = 0) {
+    return launch_apply_multi(bt, mode, codes, cb, &theta, &buf, &theta_local, 1, out, lr, mom, st, tr, gate, epoch);
+}
+
+int launch_apply_multi(const Batch& bt, int mode, const uint8_t* codes, const float* cb, float* const* thetas,
+                       float* const* bufs, float* const* locals, uint32_t nw, float* out, float lr, float mom,
+                       cudaStream_t st, Tracker* tr, const uint32_t* gate, uint32_t epoch) {
     if (bt.ncta == 0) return EMESH_OK;
+    if (nw == 0 || nw > (uint32_t)kMaxDest) return fail(EMESH_ECONFIG, "decode: bad replica count");
     ApplyArgs a{};
+    a.nw = nw;
+    for (uint32_t w = 0; w < nw; ++w) {
+        a.thetas[w] = thetas[w];
+        a.bufs[w] = bufs[w];
+        a.locals[w] = locals ? locals[w] : nullptr;
+    }
+    float* const theta = thetas[0];
+    float* const buf = bufs[0];
+    float* const theta_local = locals ? locals[0] : nullptr;
     a.gate = gate;
     a.epoch = epoch;
     a.segs = bt.d_segs;
@@ -710,11 +731,12 @@ int launch_apply(const Batch& bt, int mode, const uint8_t* codes, const float* c
     const bool prof = tr && tr->prof;
     cudaEvent_t e0 = prof ? tr->ev(st) : nullptr;
     if (mode == 0) k_apply<0><<<g, blk, 0, st>>>(a);
-    else k_apply<1><<<g, blk, 0, st>>>(a);
+    else if (nw == 1) k_apply<1><<<g, blk, 0, st>>>(a);
+    else k_apply<2><<<g, blk, 0, st>>>(a);
     if (tr) tr->launches += 1;
     if (prof) {
         const double elems = (double)bt.elems;
-        const double by = mode == 0 ? elems * 5.0 : elems * (theta_local ? 21.0 : 17.0);
+        const double by = mode == 0 ? elems * 5.0 : elems * (1.0 + nw * (theta_local ? 20.0 : 16.0));
         tr->recs.push_back({mode == 0 ? kProfDequant : kProfNesterov, e0, tr->ev(st), by + 1024.0 * bt.nseg});
     }
     CU(cudaGetLastError());
@@ -1205,6 +1227,13 @@ int run_virtual(emesh_engine* e, const float* const* A, const float* const* B, f
     if (e->fp32) return run_virtual_f32(e, A, B, theta, buf, local_out, out, lr, mom);
     for (uint32_t c = 0; c < e->k; ++c) {
         TRY(run_virtual_chain(e, c, A, B));
+        if (!out && e->k <= (uint32_t)kMaxDest) {  // one decode of the owner's payload for every local replica
+            const uint32_t owner = (c + e->k - 1) % e->k;
+            for (const Batch& bt : e->plan.batches[c])
+                TRY(launch_apply_multi(bt, 1, e->arenas[owner].codes, e->arenas[owner].cbs, theta, buf, local_out,
+                                       e->k, nullptr, lr, mom, e->s_comp, &e->tr));
+            continue;
+        }
         for (uint32_t w = 0; w < e->k; ++w) TRY(run_virtual_apply(e, c, w, theta, buf, local_out, out, lr, mom));
     }
     return EMESH_OK;

@@ -454,6 +454,12 @@ struct ApplyArgs {
     // untouched and allreduce_with_retry can restart from them
     const volatile uint32_t* gate;
     uint32_t epoch;
+    // k_apply<1>: the workers whose replicas decode this payload (several on one GPU: the virtual
+    // ring decodes each final payload once for all of them); [0] = theta / buf / theta_local
+    uint32_t nw;
+    float* thetas[kMaxDest];
+    float* bufs[kMaxDest];
+    float* locals[kMaxDest];
 };
 // k_apply-family CTAs: a.upw per quantizer tile, one unit per warp (measured
 // best: k_apply 11.3 -> 11.0 ms per round).
@@ -498,7 +504,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
                 for (int e = 0; e < 4; ++e)
                     if (e0 + e >= si.lo && e0 + e < hiel) a.out[e0 + e] = d[e];
             }
-        } else {
+        } else if (MODE == 1) {  // one replica
             float4 th = __ldcs(reinterpret_cast<const float4*>(a.theta) + q);
             float4 bb = __ldcs(reinterpret_cast<const float4*>(a.buf) + q);
             float t4[4] = {th.x, th.y, th.z, th.w}, b4[4] = {bb.x, bb.y, bb.z, bb.w};
@@ -516,6 +522,42 @@ __global__ void __launch_bounds__(kThreads) k_apply(ApplyArgs a) {
                         a.buf[e0 + e] = b4[e];
                         if (a.theta_local) a.theta_local[e0 + e] = t4[e];
                     }
+            }
+        } else {  // MODE 2: several local replicas of one payload (virtual ring)
+            // every replica's loads first (independent streams in flight), then the updates
+            constexpr int kW = 4;  // replicas handled per pass
+            for (uint32_t w0 = 0; w0 < a.nw; w0 += kW) {
+            float4 thv[kW], bbv[kW];
+#pragma unroll
+            for (int i = 0; i < kW; ++i)
+                if (w0 + i < a.nw) {
+                    thv[i] = __ldcs(reinterpret_cast<const float4*>(a.thetas[w0 + i]) + q);
+                    bbv[i] = __ldcs(reinterpret_cast<const float4*>(a.bufs[w0 + i]) + q);
+                }
+#pragma unroll
+            for (int i = 0; i < kW; ++i) {
+                if (w0 + i >= a.nw) break;
+                float* const theta = a.thetas[w0 + i];
+                float* const buf = a.bufs[w0 + i];
+                float* const tloc = a.locals[w0 + i];
+                const float4 th = thv[i], bb = bbv[i];
+                float t4[4] = {th.x, th.y, th.z, th.w}, b4[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) nesterov1(t4[e], b4[e], d[e], a.lr, a.mom);
+                if (full) {
+                    const float4 to = make_float4(t4[0], t4[1], t4[2], t4[3]);
+                    __stcs(reinterpret_cast<float4*>(theta) + q, to);
+                    __stcs(reinterpret_cast<float4*>(buf) + q, make_float4(b4[0], b4[1], b4[2], b4[3]));
+                    if (tloc) __stcs(reinterpret_cast<float4*>(tloc) + q, to);
+                } else {
+                    for (int e = 0; e < 4; ++e)
+                        if (e0 + e >= si.lo && e0 + e < hiel) {
+                            theta[e0 + e] = t4[e];
+                            buf[e0 + e] = b4[e];
+                            if (tloc) tloc[e0 + e] = t4[e];
+                        }
+                }
+            }
             }
         }
     }
