@@ -1,5 +1,5 @@
 """Bit-exact parity at the sizes the bench runs: whole
-rounds with 12M-20M-element segments (4-unit tiles, scratch larger than L2),
+rounds with 12M-20M-element segments (6-unit tiles, scratch larger than L2),
 and the full config-2 round (1B params/worker, 4 workers,
 S = 16: 64 segments of 15.6M elements), every segment re-derived by the
 oracle's transport-free chain (oracle/parity.py) and compared bit for bit:
@@ -80,7 +80,7 @@ def _round_and_check(E, oracle, n, k, S, seed=3, picks=None, gen=_synthetic):
 
 @pytest.mark.parametrize("n,k,S", [(80_000_000, 4, 1), (48_000_011, 2, 2)])
 def test_large_segments_four_unit_tiles(E, oracle, n, k, S):
-    """20M / 12M-element segments: batches above 16M elements take the 4-unit tiles (32K elements per
+    """20M / 12M-element segments: batches above 16M elements take the 6-unit tiles (48K elements per
     CTA task) and a scratch round trip larger than L2, like the bench; still bit-exact."""
     rep = _round_and_check(E, oracle, n, k, S)
     assert rep.ok(), rep.as_dict()
