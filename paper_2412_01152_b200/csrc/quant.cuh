@@ -515,16 +515,6 @@ __device__ __forceinline__ void bin_unit(const QuantArgs& a, QSmem& sm, const Se
                 }
             }
         }
-        if (BSRC == kBinScratch && INTERIOR) {
-            // this half's 2 KB of scratch x is consumed (each element is read
-            // exactly once): drop the 128-B L2 lines wholly inside it without
-            // write-back — x was only ever meant as an L2 round trip
-            const uintptr_t lo_b = reinterpret_cast<uintptr_t>(xs + qbase + (uint64_t)h * kHalf * 32);
-            const uintptr_t hi_b = lo_b + (uintptr_t)kHalf * 32 * 16;
-            const uintptr_t line = ((lo_b + 127) & ~(uintptr_t)127) + (uintptr_t)lane * 128;
-            if (lane < 16 && line + 128 <= hi_b)
-                asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
-        }
     }
 }
 
